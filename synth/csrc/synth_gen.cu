@@ -1,0 +1,29 @@
+/* CUDA synthetic trace generator K0 (INPUT MODULE; not part of the product
+ * library and never timed). Grid-stride over [0, count); request first+j. */
+#include <cuda_runtime.h>
+#include "synth_philox.h"
+
+__global__ void synth_gen_kernel(const uint32_t *__restrict__ luts, const uint8_t *__restrict__ interp,
+                                 const uint32_t *__restrict__ cuts, uint32_t n_comp, uint64_t seed,
+                                 uint64_t first, uint64_t count, uint32_t *__restrict__ out) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride)
+    out[j] = syn_request(luts, interp, cuts, n_comp, seed, first + j);
+}
+
+extern "C" int synth_generate_device(const uint32_t *d_luts, const uint8_t *d_interp,
+                                     const uint32_t *d_cuts, uint32_t n_comp, uint64_t seed,
+                                     uint64_t first, uint64_t count, uint32_t *d_out,
+                                     cudaStream_t stream) {
+  if (n_comp == 0) return 1;
+  if (count == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t blocks = (count + 255) / 256;
+  uint64_t cap = (uint64_t)sms * 16;
+  if (blocks > cap) blocks = cap;
+  synth_gen_kernel<<<(unsigned)blocks, 256, 0, stream>>>(d_luts, d_interp, d_cuts, n_comp, seed,
+                                                         first, count, d_out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}

@@ -1,0 +1,49 @@
+/* Philox4x32-10 and table sampling for the synthetic trace generator.
+ * INPUT MODULE (shared by the host-C and CUDA generators only; the product
+ * library and the oracle do not include this file). See synth/gen.py for the
+ * definition of a trace. */
+#ifndef SYNTH_PHILOX_H
+#define SYNTH_PHILOX_H
+#include <stdint.h>
+
+#ifdef __CUDACC__
+#define SYN_HD __host__ __device__ __forceinline__
+#else
+#define SYN_HD static inline
+#endif
+
+#define SYN_LUT_SIZE 65537u
+
+SYN_HD void syn_philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+  for (int r = 0; r < 10; ++r) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+    k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+  }
+}
+
+SYN_HD uint32_t syn_sample(const uint32_t *q, uint8_t interp, uint32_t w) {
+  uint32_t i = w >> 16;
+  uint32_t a = q[i];
+  if (!interp) return a;
+  uint32_t b = q[i + 1];
+  return a + (uint32_t)((((uint64_t)(b - a)) * (uint64_t)(w & 0xFFFFu)) >> 16);
+}
+
+/* luts: [n_comp][2][SYN_LUT_SIZE]; interp: [n_comp][2]; cuts: [n_comp-1] */
+SYN_HD uint32_t syn_request(const uint32_t *luts, const uint8_t *interp,
+                            const uint32_t *cuts, uint32_t n_comp,
+                            uint64_t seed, uint64_t i) {
+  uint32_t c[4] = {(uint32_t)i, (uint32_t)(i >> 32), 0u, 0u};
+  syn_philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t comp = 0;
+  for (uint32_t k = 0; k + 1 < n_comp; ++k) comp += (c[2] >= cuts[k]) ? 1u : 0u;
+  const uint32_t *qi = luts + (uint64_t)comp * 2u * SYN_LUT_SIZE;
+  const uint32_t *qo = qi + SYN_LUT_SIZE;
+  return syn_sample(qi, interp[2 * comp], c[0]) + syn_sample(qo, interp[2 * comp + 1], c[1]);
+}
+#endif

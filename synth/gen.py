@@ -1,0 +1,151 @@
+"""Trace generation: numpy reference, host-C and CUDA front ends (INPUT MODULE).
+
+A trace is a u32 column of L_total values. Request i of
+a trace with seed s and mixture M is
+
+    w0, w1, w2, _ = Philox4x32-10(ctr=(lo32 i, hi32 i, 0, 0), key=(lo32 s, hi32 s))
+    c      = #{k : w2 >= M.cut[k]}                 (mixture component)
+    L_in   = sample(M.shapes[c].t_in,  w0)
+    L_out  = sample(M.shapes[c].t_out, w1)
+    L_total = L_in + L_out
+
+with `sample` the table rule in shapes.py. No routing or counting here.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from .philox import philox_words
+from .shapes import LUT_SIZE, Mixture, mixture
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_DIR = os.path.join(_HERE, "lib")
+
+
+def _sample(table, w):
+    q = table.q.astype(np.uint64)
+    i = (w >> np.uint32(16)).astype(np.int64)
+    if not table.interp:
+        return q[i]
+    f = (w & np.uint32(0xFFFF)).astype(np.uint64)
+    return q[i] + (((q[i + 1] - q[i]) * f) >> np.uint64(16))
+
+
+def generate_np(mix: Mixture | str, seed: int, first: int, count: int) -> np.ndarray:
+    """Numpy reference generator for indices [first, first+count)."""
+    if isinstance(mix, str):
+        mix = mixture(mix)
+    if count == 0:
+        return np.zeros(0, dtype=np.uint32)
+    w0, w1, w2, _ = philox_words(seed, first, count)
+    comp = np.zeros(count, dtype=np.int64)
+    for c in mix.cut:
+        comp += (w2 >= np.uint32(c)).astype(np.int64)
+    out = np.zeros(count, dtype=np.uint64)
+    for k, sh in enumerate(mix.shapes):
+        m = comp == k
+        if m.any():
+            out[m] = _sample(sh.t_in, w0[m]) + _sample(sh.t_out, w1[m])
+    return out.astype(np.uint32)
+
+
+@dataclass
+class PackedMixture:
+    """Flat arrays handed to the C and CUDA generators."""
+    luts: np.ndarray      # uint32 [n_comp * 2 * LUT_SIZE]  (comp, in/out, level)
+    interp: np.ndarray    # uint8  [n_comp * 2]
+    cuts: np.ndarray      # uint32 [max(n_comp-1, 1)]
+    n_comp: int
+
+
+def pack(mix: Mixture | str) -> PackedMixture:
+    if isinstance(mix, str):
+        mix = mixture(mix)
+    n = len(mix.shapes)
+    luts = np.zeros((n, 2, LUT_SIZE), dtype=np.uint32)
+    interp = np.zeros((n, 2), dtype=np.uint8)
+    for k, sh in enumerate(mix.shapes):
+        luts[k, 0] = sh.t_in.q
+        luts[k, 1] = sh.t_out.q
+        interp[k] = (sh.t_in.interp, sh.t_out.interp)
+    cuts = np.array(mix.cut if mix.cut else (0,), dtype=np.uint32)
+    return PackedMixture(np.ascontiguousarray(luts.ravel()), interp.ravel().copy(), cuts, n)
+
+
+# ---------------------------------------------------------------- host C ----
+_host_lib = None
+
+
+def _load_host():
+    global _host_lib
+    if _host_lib is None:
+        path = os.path.join(LIB_DIR, "libsynth_host.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        lib.synth_generate_host.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
+        lib.synth_generate_host.restype = ctypes.c_int
+        _host_lib = lib
+    return _host_lib
+
+
+def generate_host(mix: Mixture | str, seed: int, first: int, count: int,
+                  out: np.ndarray | None = None) -> np.ndarray:
+    """Host-C generator (OpenMP); same words as generate_np."""
+    p = pack(mix)
+    if out is None:
+        out = np.empty(count, dtype=np.uint32)
+    assert out.dtype == np.uint32 and out.flags.c_contiguous and out.size >= count
+    rc = _load_host().synth_generate_host(
+        p.luts.ctypes.data, p.interp.ctypes.data, p.cuts.ctypes.data, p.n_comp,
+        seed, first, count, out.ctypes.data)
+    if rc != 0:
+        raise RuntimeError(f"synth_generate_host failed rc={rc}")
+    return out
+
+
+# ------------------------------------------------------------------ CUDA ----
+_dev_lib = None
+
+
+def _load_dev():
+    global _dev_lib
+    if _dev_lib is None:
+        path = os.path.join(LIB_DIR, "libsynth_gen.so")
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
+        lib.synth_generate_device.argtypes = [
+            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+            ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p,
+            ctypes.c_void_p]
+        lib.synth_generate_device.restype = ctypes.c_int
+        _dev_lib = lib
+    return _dev_lib
+
+
+def generate_device(mix: Mixture | str, seed: int, first: int, count: int, out=None,
+                    stream=None):
+    """CUDA generator writing into a torch uint32/int32 CUDA tensor (returned)."""
+    import torch
+    p = pack(mix)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    luts = torch.from_numpy(p.luts.view(np.int32)).to(dev)
+    interp = torch.from_numpy(p.interp).to(dev)
+    cuts = torch.from_numpy(p.cuts.view(np.int32)).to(dev)
+    if out is None:
+        out = torch.empty(count, dtype=torch.int32, device=dev)
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    rc = _load_dev().synth_generate_device(
+        luts.data_ptr(), interp.data_ptr(), cuts.data_ptr(), p.n_comp,
+        seed, first, count, out.data_ptr(), ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"synth_generate_device failed rc={rc}")
+    s.synchronize()   # keep the temporary tables alive until the kernel is done
+    return out
