@@ -1,0 +1,265 @@
+/* ===========================================================================
+ * fleet_plan.h -- C ABI of the B200 fleet-sizing sweep
+ * (token-budget pool routing, arxiv 2604.08075).
+ *
+ * The library evaluates the paper's two-pool provisioning method over a whole
+ * request trace on the GPU:
+ *   route_batch      -- Alg. 1 applied to every request
+ *                       of a trace for ONE (B_short, C_S, C_L) split;
+ *   sweep_thresholds -- one HBM pass that routes every request against EVERY
+ *                       candidate split at once (empirical CDF), then
+ *                       sizes every (model, GPU, C_L, C_S, B) candidate with
+ *                       Eq. (1)-(2), the Sec. 3 pool sizing
+ *                       G = ceil(lambda/mu), Eq. `savings`
+ *                        and annual cost;
+ *   best_split       -- the per-model cheapest feasible candidate.
+ * Readings of points where the paper is silent are DESIGN.md R1..R20.
+ *
+ * Conventions (all entry points):
+ *   - Plain C types only. Device pointers (d_*) are CUDA device addresses on
+ *     the plan's device; host pointers (h_*) are CPU addresses.
+ *   - Return codes only: no exceptions cross the ABI, nothing aborts. The
+ *     per-plan message of the last failure is fp_last_error(plan).
+ *   - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t
+ *     passed as void*, NULL = legacy default stream), EXCEPT: a non-NULL host
+ *     output pointer makes the call synchronize `stream` before returning,
+ *     and best_split always synchronizes.
+ *   - The caller owns every buffer it passes and must not modify d_len /
+ *     d_decision until the stream has passed the call. The plan owns its
+ *     scratch memory, NCCL communicator and streams; fleet_plan_destroy frees
+ *     them.
+ *   - A plan is not thread-safe; distinct plans are independent.
+ *   - Multi-GPU (world > 1): every rank must issue the same sequence of
+ *     route_batch / sweep_thresholds / best_split calls with the same
+ *     descriptor (NCCL collective semantics).
+ *   - There is no CPU fallback: without a usable CUDA device every compute
+ *     call fails with FP_ERR_CUDA.
+ * ======================================================================== */
+#ifndef FLEET_PLAN_H
+#define FLEET_PLAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP_ABI_VERSION 1u
+#define FP_NAME_LEN 32
+
+typedef enum fp_status {
+  FP_OK = 0,
+  FP_ERR_INVALID_ARG = 1, /* NULL where not allowed, invalid split, bad sizes      */
+  FP_ERR_CONFIG = 2,      /* descriptor violates a documented constraint           */
+  FP_ERR_EMPTY_TRACE = 3, /* sweep over zero requests (alpha undefined)     */
+  FP_ERR_ALIGNMENT = 4,   /* reserved (misaligned d_len is handled, not rejected)  */
+  FP_ERR_OOM = 5,         /* device or pinned-host allocation failed               */
+  FP_ERR_CUDA = 6,        /* CUDA runtime/launch error, or no device               */
+  FP_ERR_NCCL = 7,        /* NCCL unavailable or a collective failed               */
+  FP_ERR_STATE = 8        /* call out of order (e.g. best_split before a sweep)    */
+} fp_status;
+
+/* ---- descriptor ----------------------------------------------------------- */
+
+/* Model: the symbols of Eq. (1) `eq:kv-per-seq`. */
+typedef struct fp_model {
+  char name[FP_NAME_LEN];
+  uint32_t n_layers;      /* n_l                                             */
+  uint32_t n_kv_heads;    /* n_h (KV heads)                                  */
+  uint32_t head_dim;      /* d_h                                             */
+  uint32_t kv_elem_bytes; /* b_dtype (1, 2 or 4)                             */
+} fp_model;
+
+/* GPU: the symbols of Eq. (2) `eq:max-seqs` plus the activation
+ * reserve of the Sec. 4.7 budget and a price. */
+typedef struct fp_gpu {
+  char name[FP_NAME_LEN];
+  uint64_t hbm_bytes;                /* M_gpu                               */
+  uint32_t util_num, util_den;       /* u = util_num / util_den, 0 < u <= 1 */
+  uint64_t activation_reserve_bytes; /* subtracted from M_gpu * u           */
+  double price_per_gpu_hour;         /* $ per GPU-hour, >= 0                */
+} fp_gpu;
+
+/* Deployment of model m on GPU g (row-major [n_models][n_gpus]). */
+typedef struct fp_deploy {
+  uint32_t tp_degree;            /* KV is split over tp GPUs: per-GPU M_seq = M_seq / tp */
+  uint32_t gpus_per_instance;    /* GPUs counted per instance (DESIGN R6), >= 1          */
+  uint64_t weight_bytes_per_gpu; /* M_model                                              */
+} fp_deploy;
+
+/* Candidate grid. Flat candidate index order (m, g, C_L, C_S, B), B fastest:
+ *   index = (((m * n_gpus + g) * n_cl + l) * n_cs' + s) * n_b + k,
+ *   n_cs' = max(n_cs, 1). n_cs == 0 ties C_S = B (Fig. 6 convention, R16).
+ * A candidate is valid iff B <= C_S <= C_L. Every value >= 1.  */
+typedef struct fp_grid {
+  const uint32_t *b_short; uint32_t n_b;  /* thresholds B_short (tokens)      */
+  const uint32_t *c_short; uint32_t n_cs; /* short-pool windows C_S, or none  */
+  const uint32_t *c_long;  uint32_t n_cl; /* long-pool windows C_L (= C_H)    */
+} fp_grid;
+
+#define FP_FLAG_NO_MASS 0x1u         /* skip token-mass sums (occupancy = 0)          */
+#define FP_FLAG_REPLICATED_GRID 0x2u /* world > 1: every rank evaluates all candidates */
+#define FP_FLAG_KERNEL_TIMING 0x4u   /* record CUDA events around every kernel launch   */
+
+typedef struct fp_plan_desc {
+  uint32_t abi_version;           /* FP_ABI_VERSION                                 */
+  uint32_t flags;                 /* FP_FLAG_*                                      */
+  const fp_model *models; uint32_t n_models;
+  const fp_gpu *gpus;     uint32_t n_gpus;
+  const fp_deploy *deploy;        /* [n_models][n_gpus]                             */
+  fp_grid grid;
+  const uint32_t *windows; uint32_t n_windows; /* strictly increasing list of every
+                                     pool window a candidate uses (each C_S, C_L,
+                                     and each B when n_cs == 0)                      */
+  const double *mu_table;         /* [n_models][n_gpus][n_windows] profiled
+                                     throughput mu, requests/s per instance (R5);
+                                     finite, >= 0                                   */
+  double hours_per_year;          /* cost horizon (R7), > 0                          */
+  int32_t device;                 /* CUDA device ordinal for this rank               */
+  int32_t rank, world;            /* 0 <= rank < world                               */
+  const void *nccl_unique_id;     /* 128-byte ncclUniqueId, same on all ranks;
+                                     NULL iff world == 1                             */
+} fp_plan_desc;
+
+/* ---- outputs -------------------------------------------------------------- */
+
+typedef struct fp_route_counts {
+  uint64_t n_short, n_long, n_reject; /* requests per outcome (sum = N)       */
+  uint64_t mass_short, mass_long;     /* sum of L_total per served pool       */
+} fp_route_counts;
+
+#define FP_CAND_VALID 1u         /* B <= C_S <= C_L                                     */
+#define FP_CAND_FEASIBLE 2u      /* both pools buildable (R13); only these enter argmin */
+#define FP_CAND_HOMO_FEASIBLE 4u /* the homogeneous C_H = C_L fleet is buildable        */
+
+/* One evaluated candidate (192 bytes). Invalid candidates carry zeros and
+ * infinite costs; infeasible pools carry zero instances and infinite cost. */
+typedef struct fp_candidate {
+  uint32_t index, model, gpu;          /* flat index and (m, g)                   */
+  uint32_t b_short, c_short, c_long;   /* the split                               */
+  uint32_t flags, _pad;                /* FP_CAND_*                               */
+  uint64_t nseq_short, nseq_long;      /* Eq. (2) N_seq at C_S and C_L            */
+  uint64_t n_short, n_long, n_reject;  /* routed requests (global)                */
+  uint64_t mass_short, mass_long;      /* token mass per pool                     */
+  uint64_t inst_short, inst_long, inst_homo; /* ceil(lambda_p / mu_p)            */
+  uint64_t gpus_dual, gpus_homo;       /* gpus_per_instance x instances           */
+  double alpha;                        /* n_short / N                     */
+  double rho;                          /* mu(C_S) / mu(C_L)               */
+  double predicted_savings;            /* alpha (1 - 1/rho), Eq. `savings`        */
+  double savings;                      /* (G_homo - G_dual) / G_homo              */
+  double cost_dual, cost_homo;         /* GPUs x price x hours_per_year           */
+  double occupancy_short, occupancy_long; /* mass / (n x C) (R20)     */
+} fp_candidate;
+
+typedef struct fp_plan_info {
+  uint64_t n_candidates;        /* whole grid                                     */
+  uint64_t cand_first, cand_count; /* this rank's slice of the grid             */
+  uint32_t n_edges;             /* |E|, E = sortuniq(B u C_L)                     */
+  uint32_t lut_shift;           /* s: every edge is a multiple of 2^s             */
+  uint32_t lut_cells;           /* cells in the bin LUT (0 = binary-search mode)  */
+  uint32_t n_windows;
+  int32_t device, rank, world;
+  uint32_t sm_count;
+  uint32_t k1_grid, k1_block;   /* trace-pass launch configuration                */
+} fp_plan_info;
+
+typedef struct fp_plan fp_plan; /* opaque */
+
+/* ---- entry points ----------------------------------------------------------- */
+
+/* Validate `desc`, build the edge set and bin LUT, allocate device scratch on
+ * desc->device, and (world > 1) initialise the NCCL communicator from
+ * desc->nccl_unique_id. The descriptor's arrays are copied; the caller may
+ * free them afterwards. On failure *out = NULL and a status is returned.
+ * Errors: FP_ERR_INVALID_ARG (NULL), FP_ERR_CONFIG (constraint violated),
+ * FP_ERR_CUDA, FP_ERR_OOM, FP_ERR_NCCL. */
+fp_status fleet_plan_create(const fp_plan_desc *desc, fp_plan **out);
+
+/* Alg. 1 for one split over this rank's n_local requests
+ * d_len[0..n_local) (u32 L_total, any alignment). Per request writes
+ * d_decision[i] = pool | stage << 2 (pool 0 short, 1 long, 2 rejected; stage 0
+ * budget step, 1 feasibility step, 2 safety check, 3 rejection) when
+ * d_decision != NULL. If h_counts != NULL, writes the GLOBAL counts (summed
+ * over ranks) and synchronizes. Requires 1 <= B <= C_S <= C_L
+ * (else FP_ERR_INVALID_ARG). n_local == 0 is a valid no-op.
+ * d_len may also be a HOST pointer (pinned or pageable): it is then streamed
+ * to the device in chunks inside the call; d_decision must be device memory. */
+fp_status route_batch(fp_plan *plan, const uint32_t *d_len, uint64_t n_local, uint32_t b_short,
+                      uint32_t c_short, uint32_t c_long, uint8_t *d_decision,
+                      fp_route_counts *h_counts, void *stream);
+
+/* The fleet-sizing sweep over this rank's shard d_len[0..n_local) at arrival
+ * rate rate_rps (lambda, > 0, R17). Enqueues: trace pass + histogram,
+ * (world > 1) NCCL all-reduce of the histogram, prefix scan + candidate
+ * evaluation + per-model argmin over this rank's candidate slice, and
+ * (world > 1, not replicated) an all-gather of the per-rank best records.
+ * d_len may be a device pointer or a HOST pointer (streamed in chunks, as in
+ * route_batch). If h_results != NULL it receives this rank's candidate slice
+ * (fp_plan_info.cand_count records, in index order) and the call synchronizes.
+ * Errors: FP_ERR_INVALID_ARG, FP_ERR_EMPTY_TRACE (world == 1 and n_local == 0;
+ * with world > 1 an empty global trace is reported by best_split). */
+fp_status sweep_thresholds(fp_plan *plan, const uint32_t *d_len, uint64_t n_local,
+                           double rate_rps, fp_candidate *h_results, void *stream);
+
+/* Per-model best split of the last sweep: h_best[m] for m < n_models (index =
+ * UINT32_MAX and flags = 0 when model m has no feasible candidate).
+ * Synchronizes the stream of the last sweep. Deterministic for any world size.
+ * Errors: FP_ERR_STATE (no sweep yet), FP_ERR_EMPTY_TRACE (global N == 0). */
+fp_status best_split(fp_plan *plan, fp_candidate *h_best);
+
+/* Global per-bin histogram of the last sweep (K1 output after the cross-rank
+ * sum; synchronizes). With E = sortuniq(B u C_L) ascending (|E| = n_edges of
+ * fleet_plan_info): h_edges[j] = e_j for j < |E|; bin j < |E| holds the
+ * requests with e_{j-1} < L <= e_j (e_{-1} = -inf) and bin |E| those above
+ * every edge. h_bin_cnt[j] = requests in bin j; h_bin_mass[j] = sum of their
+ * L (0 for bin |E|, whose mass no candidate uses; also 0 with
+ * FP_FLAG_NO_MASS). Any pointer may be NULL. */
+fp_status sweep_histogram(fp_plan *plan, uint32_t *h_edges, uint64_t *h_bin_cnt, uint64_t *h_bin_mass);
+
+/* Writes a fresh 128-byte ncclUniqueId (for rank 0 to broadcast before
+ * fleet_plan_create with world > 1). FP_ERR_NCCL if NCCL cannot be loaded. */
+fp_status fp_nccl_get_unique_id(void *out128);
+
+fp_status fleet_plan_info(const fp_plan *plan, fp_plan_info *out);
+
+/* Number of kernels this library launched on the plan since creation. */
+uint64_t fp_kernel_launches(const fp_plan *plan);
+
+/* Kernel kinds for fp_kernel_time. */
+#define FP_KERNEL_TRACE 0 /* K1: sweep trace pass (one launch per chunk)   */
+#define FP_KERNEL_EVAL 1  /* K3: scan + candidate evaluation + argmin      */
+#define FP_KERNEL_ROUTE 2 /* K4: route_batch                               */
+
+/* With FP_FLAG_KERNEL_TIMING: total device time (ms, CUDA events recorded on
+ * the launch stream around each launch) and launch count of kernel `kind`
+ * since the last fp_kernel_time_reset (or creation). Synchronizes those
+ * events. FP_ERR_STATE without the flag. */
+fp_status fp_kernel_time(fp_plan *plan, int32_t kind, double *total_ms, uint64_t *launches);
+fp_status fp_kernel_time_reset(fp_plan *plan);
+
+void fleet_plan_destroy(fp_plan *plan);
+
+const char *fp_status_string(fp_status s);
+const char *fp_last_error(const fp_plan *plan);
+
+/* ---- host-side partition helpers (no device work; used by the library and
+ * by multi-rank tests) -------------------------------------------------------- */
+
+/* Contiguous shard of a global trace for `rank`: [*first, *first + *count),
+ * boundaries rounded to 32 requests (128 B). */
+void fp_shard_range(uint64_t n_total, int32_t rank, int32_t world, uint64_t *first,
+                    uint64_t *count);
+
+/* Contiguous slice of the candidate grid for `rank` (same rule, unrounded). */
+void fp_candidate_range(uint64_t n_candidates, int32_t rank, int32_t world, uint64_t *first,
+                        uint64_t *count);
+
+/* Deterministic merge of per-rank bests: recs[r * n_models + m] is rank r's
+ * best for model m; writes out[m] = the record with the smallest cost_dual
+ * among feasible ones, ties to the lowest index. */
+void fp_merge_best(const fp_candidate *recs, int32_t world, uint32_t n_models, fp_candidate *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEET_PLAN_H */

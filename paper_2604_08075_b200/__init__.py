@@ -1,0 +1,14 @@
+"""B200-native fleet-sizing sweep for token-budget pool routing (arxiv 2604.08075).
+
+The product is the C-ABI library lib/libfleetplan.so (include/fleet_plan.h,
+hand-written sm_100a CUDA in csrc/); this package is its thin ctypes binding.
+Importing it without the built library raises: there is no CPU fallback.
+"""
+from ._abi import (  # noqa: F401
+    EXPORTED, FP_CANDIDATE, FP_CAND_FEASIBLE, FP_CAND_HOMO_FEASIBLE, FP_CAND_VALID,
+    FP_FLAG_KERNEL_TIMING, FP_FLAG_NO_MASS, FP_FLAG_REPLICATED_GRID,
+    FP_KERNEL_EVAL, FP_KERNEL_ROUTE, FP_KERNEL_TRACE, fp_kernel_time, fp_kernel_time_reset, FleetPlan, FleetPlanError, LIB_PATH,
+    best_split, desc_from_config, fleet_plan_create, fleet_plan_destroy, fleet_plan_info,
+    fp_candidate_range, fp_kernel_launches, fp_merge_best, fp_nccl_get_unique_id,
+    fp_shard_range, fp_status_string, route_batch, sweep_histogram, sweep_thresholds,
+)

@@ -1,0 +1,74 @@
+// Internal declarations shared by the library's translation units (not part of
+// the ABI). See include/fleet_plan.h for the public contract and DESIGN.md §5
+// for the kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "fleet_plan.h"
+
+namespace fp {
+
+constexpr int kMaxEdges = 4096;          // |E| limit (K3 scans |E|+1 bins in smem)
+constexpr int kLutMaxCells = 16384;      // above this: binary search over E
+
+// ---- K1: trace pass (route every request against every edge + histogram) ----
+struct TraceArgs {
+  const uint32_t *len;      // device, this chunk
+  uint64_t n;               // elements in this chunk
+  const void *lut;          // device: u8 or u16 [lut_cells] bin of each fine cell
+  const uint32_t *edges;    // device: E ascending [n_edges] (binary-search mode)
+  uint32_t lut_cells;       // 0 => binary search mode
+  uint32_t lut_u8;          // LUT element width
+  uint32_t shift;           // s
+  uint32_t n_edges;         // |E|
+  uint32_t max_edge;        // e_max (mass is accumulated only for L <= e_max)
+  uint32_t flush_iters;     // lane-slot mass flush period (iterations), >= 1
+  uint32_t want_mass;
+  unsigned long long *g_cnt;   // [n_edges + 1] global accumulators (bins)
+  unsigned long long *g_mass;  // [n_edges + 1]
+};
+cudaError_t launch_trace(const TraceArgs &a, int grid, int block, size_t smem, cudaStream_t s);
+size_t trace_smem_bytes(const TraceArgs &a, int block);
+cudaError_t trace_occupancy(const TraceArgs &a, int block, size_t smem, int *per_sm);
+
+// ---- K4: route_batch --------------------------------------------------------
+struct RouteArgs {
+  const uint32_t *len;
+  uint8_t *decision;          // nullable
+  uint64_t n;
+  uint32_t b, cs, cl;
+  unsigned long long *g_counts;  // [5]
+};
+cudaError_t launch_route(const RouteArgs &a, int grid, int block, cudaStream_t s);
+
+// ---- K3: candidate evaluation + argmin ---------------------------------------
+struct BlockBest { double cost; uint32_t index; uint32_t valid; };
+
+struct EvalArgs {
+  const unsigned long long *hist_cnt;   // [nbins] per-bin counts (global, all ranks)
+  const unsigned long long *hist_mass;  // [nbins]
+  uint32_t nbins;                       // |E| + 1
+  const uint32_t *b, *cs, *cl;          // grid values
+  const uint16_t *b_edge, *cl_edge;     // index in E of each B / C_L
+  const uint16_t *b_win, *cs_win, *cl_win;  // index in windows of each B / C_S / C_L
+  uint32_t n_b, n_cs, n_cl, n_cs_eff;
+  uint32_t n_models, n_gpus, n_windows;
+  const uint32_t *model_arch;           // [m][4] n_l, n_h, d_h, b
+  const unsigned long long *gpu_u64;    // [g][4] hbm, u_num, u_den, act
+  const double *price;                  // [g]
+  const unsigned long long *deploy;     // [m][g][3] tp, gpus_per_instance, weights
+  const uint32_t *windows;              // [n_windows]
+  const double *mu;                     // [m][g][w]
+  double rate, hours;
+  uint64_t per_model;                   // candidates per model
+  uint64_t cand_first, cand_count;      // this rank's slice
+  fp_candidate *results;                // nullable [cand_count]
+  fp_candidate *best_out;               // [n_models] (this rank's)
+  BlockBest *block_best;                // [n_models][grid_x]
+  unsigned int *done;                   // [n_models] last-block-done counters (self-resetting)
+};
+cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
+size_t eval_smem_bytes(const EvalArgs &a, int block);
+cudaError_t eval_prepare();
+
+}  // namespace fp

@@ -1,0 +1,282 @@
+// K2 + K3: prefix scan of the trace histogram, candidate-grid evaluation and
+// per-model argmin.
+//
+// One thread per candidate; blockIdx.y = model. Prologue (per block): the
+// |E|+1-bin histogram is scanned into cnt_le / mass_le (K2, P:589 alpha =
+// F(B)) and the capacity table N_seq[g][w] (Eq. 1-2) and mu[g][w]
+// are staged in shared memory. Each thread then sizes its candidate with the
+// Sec. 3 formulas in IEEE binary64 with explicit round-to-nearest
+// intrinsics and no contraction (DESIGN R14; the library is also built with
+// --fmad=false), and the block reduces (cost, index) with warp shuffles. The
+// last block of each model (self-resetting arrival counter) reduces the
+// per-block winners and re-evaluates the winning index into a full record.
+#include <cfloat>
+#include <cmath>
+#include "internal.cuh"
+
+namespace fp {
+
+namespace {
+
+struct Shared {
+  unsigned long long *cnt_le;   // [nbins]
+  unsigned long long *mass_le;  // [nbins]
+  unsigned long long *nseq;     // [n_gpus][n_windows]
+  double *mu;                   // [n_gpus][n_windows]
+};
+
+__device__ __forceinline__ double u2d(unsigned long long x) { return __ull2double_rn(x); }
+
+// Eq. (2): N_seq = floor(budget * tp / M_seq), M_seq = 2 n_l n_h d_h b C (Eq. 1).
+// Bounds validated at plan creation keep every product below 2^64.
+__device__ __forceinline__ unsigned long long max_seqs(unsigned long long budget, uint32_t tp,
+                                                       const uint32_t *arch, uint32_t c) {
+  unsigned long long mseq = 2ull * arch[0] * arch[1] * arch[2] * arch[3] * (unsigned long long)c;
+  if (mseq == 0) return 0;
+  return (budget * tp) / mseq;
+}
+
+// budget = floor(M_gpu * u) - M_model - M_act, clamped at 0.
+__device__ __forceinline__ unsigned long long kv_budget(const unsigned long long *gu,
+                                                        unsigned long long weights) {
+  unsigned long long usable = (gu[0] * gu[1]) / gu[2];
+  unsigned long long need = weights + gu[3];
+  return usable > need ? usable - need : 0ull;
+}
+
+// One pool: I = ceil(lambda / mu); lambda == 0 -> 0; no capacity -> infeasible (R13).
+__device__ __forceinline__ bool pool_instances(double lam, double mu, uint64_t nseq,
+                                               uint64_t *inst) {
+  *inst = 0;
+  if (lam == 0.0) return true;
+  if (nseq == 0 || !(mu > 0.0)) return false;
+  double x = __ddiv_rn(lam, mu);
+  if (!(x <= 9007199254740992.0)) return false;
+  *inst = (unsigned long long)ceil(x);
+  return true;
+}
+
+__device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
+                         fp_candidate &c) {
+  // decompose idx = (((m * G + g) * n_cl + l) * n_cs' + s) * n_b + k
+  uint64_t r = idx;
+  uint32_t k = (uint32_t)(r % a.n_b); r /= a.n_b;
+  uint32_t s = (uint32_t)(r % a.n_cs_eff); r /= a.n_cs_eff;
+  uint32_t l = (uint32_t)(r % a.n_cl); r /= a.n_cl;
+  uint32_t g = (uint32_t)(r % a.n_gpus);
+  uint32_t B = a.b[k], CL = a.cl[l];
+  uint32_t CS = a.n_cs ? a.cs[s] : B;
+  c.index = (uint32_t)idx; c.model = m; c.gpu = g;
+  c.b_short = B; c.c_short = CS; c.c_long = CL; c.flags = 0; c._pad = 0;
+  c.nseq_short = c.nseq_long = 0;
+  c.n_short = c.n_long = c.n_reject = c.mass_short = c.mass_long = 0;
+  c.inst_short = c.inst_long = c.inst_homo = c.gpus_dual = c.gpus_homo = 0;
+  c.alpha = c.rho = c.predicted_savings = c.savings = 0.0;
+  c.cost_dual = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  c.occupancy_short = c.occupancy_long = 0.0;
+  if (!(B <= CS && CS <= CL)) return;  // invalid split
+
+  const unsigned long long N = sh.cnt_le[a.nbins - 1];
+  const uint32_t eb = a.b_edge[k], el = a.cl_edge[l];
+  const unsigned long long n_s = sh.cnt_le[eb], n_sl = sh.cnt_le[el];
+  c.n_short = n_s;
+  c.n_long = n_sl - n_s;
+  c.n_reject = N - n_sl;
+  c.mass_short = sh.mass_le[eb];
+  c.mass_long = sh.mass_le[el] - sh.mass_le[eb];
+
+  const uint32_t ws = a.n_cs ? a.cs_win[s] : a.b_win[k];
+  const uint32_t wl = a.cl_win[l];
+  const uint32_t gw = g * a.n_windows;
+  c.nseq_short = sh.nseq[gw + ws];
+  c.nseq_long = sh.nseq[gw + wl];
+  const double mu_s = sh.mu[gw + ws], mu_l = sh.mu[gw + wl];
+
+  const double dN = u2d(N);
+  c.alpha = __ddiv_rn(u2d(n_s), dN);
+  const double lam_s = __dmul_rn(c.alpha, a.rate);
+  const double lam_l = __dmul_rn(__ddiv_rn(u2d(c.n_long), dN), a.rate);
+  const double lam_h = __dmul_rn(__ddiv_rn(u2d(n_sl), dN), a.rate);
+
+  const bool ok_s = pool_instances(lam_s, mu_s, c.nseq_short, &c.inst_short);
+  const bool ok_l = pool_instances(lam_l, mu_l, c.nseq_long, &c.inst_long);
+  const bool ok_h = pool_instances(lam_h, mu_l, c.nseq_long, &c.inst_homo);
+  const bool ok_d = ok_s && ok_l;
+  if (!ok_d) { c.inst_short = 0; c.inst_long = 0; }
+  const unsigned long long gpi = a.deploy[((uint64_t)m * a.n_gpus + g) * 3 + 1];
+  c.gpus_dual = gpi * (c.inst_short + c.inst_long);
+  c.gpus_homo = gpi * c.inst_homo;
+  const double price = a.price[g];
+  if (ok_d) c.cost_dual = __dmul_rn(__dmul_rn(u2d(c.gpus_dual), price), a.hours);
+  if (ok_h) c.cost_homo = __dmul_rn(__dmul_rn(u2d(c.gpus_homo), price), a.hours);
+  if (ok_d && ok_h && c.gpus_homo > 0)
+    c.savings = __ddiv_rn(__dsub_rn(u2d(c.gpus_homo), u2d(c.gpus_dual)), u2d(c.gpus_homo));
+  if (mu_s > 0.0 && mu_l > 0.0) {
+    c.rho = __ddiv_rn(mu_s, mu_l);
+    c.predicted_savings = __dmul_rn(c.alpha, __dsub_rn(1.0, __ddiv_rn(1.0, c.rho)));
+  }
+  if (c.n_short)
+    c.occupancy_short = __ddiv_rn(u2d(c.mass_short), __dmul_rn(u2d(c.n_short), u2d(CS)));
+  if (c.n_long)
+    c.occupancy_long = __ddiv_rn(u2d(c.mass_long), __dmul_rn(u2d(c.n_long), u2d(CL)));
+  c.flags = FP_CAND_VALID | (ok_d ? FP_CAND_FEASIBLE : 0u) | (ok_h ? FP_CAND_HOMO_FEASIBLE : 0u);
+}
+
+// (cost, index) lexicographic min; non-candidates carry valid = 0.
+__device__ __forceinline__ void better(double &c0, uint32_t &i0, uint32_t &v0, double c1, uint32_t i1,
+                                       uint32_t v1) {
+  bool take = v1 && (!v0 || c1 < c0 || (c1 == c0 && i1 < i0));
+  if (take) { c0 = c1; i0 = i1; v0 = v1; }
+}
+
+__device__ __forceinline__ void warp_argmin(double &c, uint32_t &i, uint32_t &v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    double c1 = __shfl_down_sync(0xffffffffu, c, o);
+    uint32_t i1 = __shfl_down_sync(0xffffffffu, i, o);
+    uint32_t v1 = __shfl_down_sync(0xffffffffu, v, o);
+    better(c, i, v, c1, i1, v1);
+  }
+}
+
+// Block-wide exclusive/inclusive scan helper: inclusive prefix of x over the block.
+__device__ void block_scan_inclusive(unsigned long long *data, uint32_t n,
+                                     unsigned long long *warp_tot) {
+  // each thread owns a contiguous run of ceil(n / blockDim) elements
+  const uint32_t T = blockDim.x, t = threadIdx.x;
+  const uint32_t per = (n + T - 1) / T;
+  const uint32_t lo = min(n, t * per), hi = min(n, lo + per);
+  unsigned long long run = 0;
+  for (uint32_t j = lo; j < hi; ++j) run += data[j];
+  // inclusive warp scan of run
+  unsigned long long x = run;
+  const int lane = t & 31, w = t >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_tot[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (T + 31) >> 5;
+    unsigned long long z = lane < nw ? warp_tot[lane] : 0ull;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    if (lane < nw) warp_tot[lane] = z;
+  }
+  __syncthreads();
+  unsigned long long off = (x - run) + (w ? warp_tot[w - 1] : 0ull);
+  for (uint32_t j = lo; j < hi; ++j) { off += data[j]; data[j] = off; }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ unsigned long long warp_tot[32];
+  __shared__ double red_c[32];
+  __shared__ uint32_t red_i[32], red_v[32];
+  __shared__ bool is_last;
+  const uint32_t m = blockIdx.y;
+
+  Shared sh;
+  sh.cnt_le = reinterpret_cast<unsigned long long *>(smem);
+  sh.mass_le = sh.cnt_le + a.nbins;
+  sh.nseq = sh.mass_le + a.nbins;
+  sh.mu = reinterpret_cast<double *>(sh.nseq + (size_t)a.n_gpus * a.n_windows);
+
+  // ---- prologue: K2 scan + capacity table for model m ----
+  for (uint32_t j = threadIdx.x; j < a.nbins; j += blockDim.x) {
+    sh.cnt_le[j] = a.hist_cnt[j];
+    sh.mass_le[j] = a.hist_mass[j];
+  }
+  const uint32_t *arch = a.model_arch + 4 * m;
+  for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
+    const uint32_t g = j / a.n_windows, w = j % a.n_windows;
+    const unsigned long long *dp = a.deploy + ((uint64_t)m * a.n_gpus + g) * 3;
+    const unsigned long long budget = kv_budget(a.gpu_u64 + 4 * g, dp[2]);
+    sh.nseq[j] = max_seqs(budget, (uint32_t)dp[0], arch, a.windows[w]);
+    sh.mu[j] = a.mu[((uint64_t)m * a.n_gpus + g) * a.n_windows + w];
+  }
+  __syncthreads();
+  block_scan_inclusive(sh.cnt_le, a.nbins, warp_tot);
+  block_scan_inclusive(sh.mass_le, a.nbins, warp_tot);
+
+  // ---- this block's candidates: model m's part of the rank slice ----
+  const uint64_t m_lo = (uint64_t)m * a.per_model, m_hi = m_lo + a.per_model;
+  const uint64_t lo = max(m_lo, a.cand_first), hi = min(m_hi, a.cand_first + a.cand_count);
+  const uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double bc = 0.0;
+  uint32_t bi = 0xffffffffu, bv = 0;
+  if (idx < hi) {
+    fp_candidate c;
+    evaluate(a, sh, m, idx, c);
+    if (a.results) a.results[idx - a.cand_first] = c;
+    if (c.flags & FP_CAND_FEASIBLE) { bc = c.cost_dual; bi = c.index; bv = 1; }
+  }
+  warp_argmin(bc, bi, bv);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) { red_c[w] = bc; red_i[w] = bi; red_v[w] = bv; }
+  __syncthreads();
+  if (w == 0) {
+    bc = lane < nw ? red_c[lane] : 0.0;
+    bi = lane < nw ? red_i[lane] : 0xffffffffu;
+    bv = lane < nw ? red_v[lane] : 0u;
+    warp_argmin(bc, bi, bv);
+    if (lane == 0) {
+      BlockBest *bb = a.block_best + (size_t)m * gridDim.x + blockIdx.x;
+      bb->cost = bc; bb->index = bi; bb->valid = bv;
+      __threadfence();
+      unsigned int prev = atomicAdd(a.done + m, 1u);
+      is_last = (prev == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!is_last) return;
+
+  // ---- last block of model m: reduce the per-block winners, emit the record ----
+  __threadfence();
+  bc = 0.0; bi = 0xffffffffu; bv = 0;
+  for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+    const volatile BlockBest *bb = a.block_best + (size_t)m * gridDim.x + j;
+    better(bc, bi, bv, bb->cost, bb->index, bb->valid);
+  }
+  warp_argmin(bc, bi, bv);
+  if (lane == 0) { red_c[w] = bc; red_i[w] = bi; red_v[w] = bv; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < nw; ++j) better(bc, bi, bv, red_c[j], red_i[j], red_v[j]);
+    fp_candidate c;
+    if (bv) {
+      evaluate(a, sh, m, bi, c);
+    } else {
+      memset(&c, 0, sizeof c);
+      c.index = 0xffffffffu;
+      c.model = m;
+      c.cost_dual = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
+    }
+    a.best_out[m] = c;
+    a.done[m] = 0;  // self-reset for the next launch / graph replay
+  }
+}
+
+}  // namespace
+
+size_t eval_smem_bytes(const EvalArgs &a, int) {
+  return (size_t)a.nbins * 16 + (size_t)a.n_gpus * a.n_windows * 16;
+}
+
+cudaError_t eval_prepare() {
+  return cudaFuncSetAttribute(k3_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {
+  dim3 grid(grid_x, a.n_models);
+  k3_eval<<<grid, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

@@ -1,0 +1,821 @@
+// Plan runtime and C ABI (include/fleet_plan.h).
+//
+// fleet_plan_create validates the descriptor, builds the routing edge set
+// E = sortuniq(B u C_L) and its fine-cell bin LUT, copies
+// every table to one device blob, and (world > 1) initialises NCCL from the
+// caller's unique id (NCCL is dlopen'ed: single-GPU plans never touch it).
+// The compute entry points enqueue the kernels of k_trace.cu / k_eval.cu on
+// the caller's stream; host-resident traces are streamed through two
+// plan-owned device staging buffers on a copy stream, overlapping the
+// host-to-device DMA of chunk i+1 with the trace pass over chunk i.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace fp;
+
+// ---- minimal NCCL surface (types per nccl.h; functions resolved at runtime) ----
+namespace {
+typedef struct { char internal[128]; } NcclUniqueId;
+typedef void *NcclComm;
+enum { kNcclUint8 = 1, kNcclUint64 = 5 };
+enum { kNcclSum = 0 };
+struct NcclApi {
+  void *h = nullptr;
+  int (*GetUniqueId)(NcclUniqueId *) = nullptr;
+  int (*CommInitRank)(NcclComm *, int, NcclUniqueId, int) = nullptr;
+  int (*AllReduce)(const void *, void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+  int (*AllGather)(const void *, void *, size_t, int, NcclComm, cudaStream_t) = nullptr;
+  int (*CommDestroy)(NcclComm) = nullptr;
+  const char *(*GetErrorString)(int) = nullptr;
+};
+
+bool load_nccl(NcclApi &api, std::string &err) {
+  if (api.h) return true;
+  const char *names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char *n : names) {
+    api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) break;
+  }
+  if (!api.h) { err = std::string("dlopen libnccl failed: ") + dlerror(); return false; }
+#define FP_SYM(field, name)                                                   \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(api.h, name));     \
+  if (!api.field) { err = "missing NCCL symbol " name; return false; }
+  FP_SYM(GetUniqueId, "ncclGetUniqueId");
+  FP_SYM(CommInitRank, "ncclCommInitRank");
+  FP_SYM(AllReduce, "ncclAllReduce");
+  FP_SYM(AllGather, "ncclAllGather");
+  FP_SYM(CommDestroy, "ncclCommDestroy");
+  FP_SYM(GetErrorString, "ncclGetErrorString");
+#undef FP_SYM
+  return true;
+}
+NcclApi g_nccl;
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+constexpr uint64_t kChunkElems = 32ull << 20;  // host streaming: 128 MB per chunk
+}  // namespace
+
+struct fp_plan {
+  // descriptor copy
+  std::vector<fp_model> models;
+  std::vector<fp_gpu> gpus;
+  std::vector<fp_deploy> deploy;
+  std::vector<uint32_t> b, cs, cl, windows;
+  std::vector<double> mu;
+  double hours = 8760.0;
+  uint32_t flags = 0;
+  int device = 0, rank = 0, world = 1;
+  // derived
+  std::vector<uint32_t> edges;
+  uint32_t shift = 0, lut_cells = 0, lut_u8 = 0, max_edge = 0, nbins = 0;
+  uint64_t n_cand = 0, per_model = 0, cand_first = 0, cand_count = 0;
+  uint32_t n_cs_eff = 1;
+  int sm_count = 148, k1_grid = 0, k1_block = 512, k4_grid = 0, k4_block = 256;
+  size_t k1_smem = 0, k3_smem = 0;
+  // device
+  unsigned char *d_blob = nullptr;
+  size_t blob_bytes = 0;
+  TraceArgs ta{};
+  EvalArgs ea{};
+  unsigned long long *d_hist = nullptr;    // [2][nbins]
+  unsigned long long *d_rcounts = nullptr; // [5]
+  fp_candidate *d_best = nullptr;          // [world][n_models]
+  fp_candidate *d_results = nullptr;       // [cand_count] (lazy)
+  BlockBest *d_block_best = nullptr;
+  unsigned int *d_done = nullptr;
+  int k3_grid_x = 1;
+  // host streaming
+  uint32_t *d_stage[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  // NCCL
+  NcclComm comm = nullptr;
+  // per-kernel event timing (FP_FLAG_KERNEL_TIMING)
+  struct Timer {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    size_t used = 0;
+  } timers[3];
+  // state
+  bool have_sweep = false;
+  cudaStream_t last_stream = nullptr;
+  uint64_t launches = 0;
+  std::string err;
+};
+
+namespace {
+
+fp_status fail(fp_plan *p, fp_status s, const char *fmt, ...) {
+  if (p) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    p->err = buf;
+  }
+  return s;
+}
+
+fp_status cuda_fail(fp_plan *p, cudaError_t e, const char *what) {
+  cudaGetLastError();
+  return fail(p, e == cudaErrorMemoryAllocation ? FP_ERR_OOM : FP_ERR_CUDA, "%s: %s", what,
+              cudaGetErrorString(e));
+}
+
+#define CUDA_TRY(p, expr, what)                              \
+  do {                                                       \
+    cudaError_t e_ = (expr);                                 \
+    if (e_ != cudaSuccess) return cuda_fail((p), e_, what);  \
+  } while (0)
+
+fp_status nccl_check(fp_plan *p, int r, const char *what) {
+  if (r == 0) return FP_OK;
+  return fail(p, FP_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+}
+
+uint32_t index_of(const std::vector<uint32_t> &v, uint32_t x) {
+  auto it = std::lower_bound(v.begin(), v.end(), x);
+  return (it != v.end() && *it == x) ? (uint32_t)(it - v.begin()) : UINT32_MAX;
+}
+
+bool is_host_pointer(const void *ptr) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+fp_status validate_and_copy(fp_plan *p, const fp_plan_desc *d) {
+  if (d->abi_version != FP_ABI_VERSION)
+    return fail(p, FP_ERR_CONFIG, "abi_version %u != %u", d->abi_version, FP_ABI_VERSION);
+  if (!d->models || !d->gpus || !d->deploy || !d->windows || !d->mu_table || !d->grid.b_short ||
+      !d->grid.c_long || (d->grid.n_cs && !d->grid.c_short))
+    return fail(p, FP_ERR_INVALID_ARG, "NULL array in descriptor");
+  if (d->n_models == 0 || d->n_gpus == 0 || d->grid.n_b == 0 || d->grid.n_cl == 0 || d->n_windows == 0)
+    return fail(p, FP_ERR_CONFIG, "empty models/gpus/grid/windows");
+  if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
+    return fail(p, FP_ERR_CONFIG, "rank %d world %d", d->rank, d->world);
+  if ((d->world > 1) != (d->nccl_unique_id != nullptr))
+    return fail(p, FP_ERR_CONFIG, "nccl_unique_id must be set iff world > 1");
+  if (!(d->hours_per_year > 0.0) || !std::isfinite(d->hours_per_year))
+    return fail(p, FP_ERR_CONFIG, "hours_per_year must be finite and > 0");
+  p->models.assign(d->models, d->models + d->n_models);
+  p->gpus.assign(d->gpus, d->gpus + d->n_gpus);
+  p->deploy.assign(d->deploy, d->deploy + (size_t)d->n_models * d->n_gpus);
+  p->b.assign(d->grid.b_short, d->grid.b_short + d->grid.n_b);
+  if (d->grid.n_cs) p->cs.assign(d->grid.c_short, d->grid.c_short + d->grid.n_cs);
+  p->cl.assign(d->grid.c_long, d->grid.c_long + d->grid.n_cl);
+  p->windows.assign(d->windows, d->windows + d->n_windows);
+  p->mu.assign(d->mu_table, d->mu_table + (size_t)d->n_models * d->n_gpus * d->n_windows);
+  p->hours = d->hours_per_year;
+  p->flags = d->flags;
+  p->device = d->device;
+  p->rank = d->rank;
+  p->world = d->world;
+
+  for (auto &m : p->models) {
+    if (!m.n_layers || !m.n_kv_heads || !m.head_dim ||
+        !(m.kv_elem_bytes == 1 || m.kv_elem_bytes == 2 || m.kv_elem_bytes == 4))
+      return fail(p, FP_ERR_CONFIG, "model %.32s: counts must be >= 1 and b in {1,2,4}", m.name);
+  }
+  for (auto &g : p->gpus) {
+    if (g.hbm_bytes == 0 || g.hbm_bytes >= (1ull << 50))
+      return fail(p, FP_ERR_CONFIG, "gpu %.32s: hbm_bytes must be in [1, 2^50)", g.name);
+    if (g.util_num == 0 || g.util_den == 0 || g.util_num > g.util_den || g.util_den > 8192)
+      return fail(p, FP_ERR_CONFIG, "gpu %.32s: need 0 < util_num <= util_den <= 8192", g.name);
+    if (!(g.price_per_gpu_hour >= 0.0) || !std::isfinite(g.price_per_gpu_hour))
+      return fail(p, FP_ERR_CONFIG, "gpu %.32s: price must be finite and >= 0", g.name);
+  }
+  for (auto &dp : p->deploy) {
+    if (dp.tp_degree < 1 || dp.tp_degree > 8192)
+      return fail(p, FP_ERR_CONFIG, "tp_degree must be in [1, 8192]");
+    if (dp.gpus_per_instance < 1 || dp.gpus_per_instance > 512)
+      return fail(p, FP_ERR_CONFIG, "gpus_per_instance must be in [1, 512]");
+  }
+  for (size_t i = 0; i < p->windows.size(); ++i)
+    if (p->windows[i] == 0 || (i && p->windows[i] <= p->windows[i - 1]))
+      return fail(p, FP_ERR_CONFIG, "windows must be >= 1 and strictly increasing");
+  for (double v : p->mu)
+    if (!(v >= 0.0) || !std::isfinite(v)) return fail(p, FP_ERR_CONFIG, "mu must be finite and >= 0");
+  for (uint32_t v : p->b) if (!v) return fail(p, FP_ERR_CONFIG, "B_short values must be >= 1");
+  for (uint32_t v : p->cs) if (!v) return fail(p, FP_ERR_CONFIG, "C_S values must be >= 1");
+  for (uint32_t v : p->cl) if (!v) return fail(p, FP_ERR_CONFIG, "C_L values must be >= 1");
+  // Eq. (1) products stay below 2^63 for every (model, window)
+  for (auto &m : p->models) {
+    unsigned __int128 per_tok = (unsigned __int128)2 * m.n_layers * m.n_kv_heads * m.head_dim * m.kv_elem_bytes;
+    if (per_tok * p->windows.back() >= ((unsigned __int128)1 << 63))
+      return fail(p, FP_ERR_CONFIG, "model %.32s: M_seq overflows 64 bits", m.name);
+  }
+  return FP_OK;
+}
+
+fp_status build_tables(fp_plan *p) {
+  // edge set E = sortuniq(B u C_L): C_S never adds an edge since B <= C_S (R16)
+  p->edges = p->b;
+  p->edges.insert(p->edges.end(), p->cl.begin(), p->cl.end());
+  std::sort(p->edges.begin(), p->edges.end());
+  p->edges.erase(std::unique(p->edges.begin(), p->edges.end()), p->edges.end());
+  if (p->edges.size() > (size_t)kMaxEdges)
+    return fail(p, FP_ERR_CONFIG, "|E| = %zu exceeds %d", p->edges.size(), kMaxEdges);
+  p->nbins = (uint32_t)p->edges.size() + 1;
+  p->max_edge = p->edges.back();
+  // fine cells: s = largest k with 2^k | every edge; cell(L) = ceil(L / 2^s)
+  uint32_t s = 31;
+  for (uint32_t e : p->edges) s = std::min<uint32_t>(s, (uint32_t)__builtin_ctz(e));
+  p->shift = s;
+  uint64_t cell_max = p->max_edge >> s;
+  p->lut_cells = (cell_max + 2 <= (uint64_t)kLutMaxCells) ? (uint32_t)(cell_max + 2) : 0;
+  p->lut_u8 = p->nbins <= 256;
+  // window / edge index maps
+  p->n_cs_eff = p->cs.empty() ? 1 : (uint32_t)p->cs.size();
+  for (uint32_t v : p->b)
+    if (p->cs.empty() && index_of(p->windows, v) == UINT32_MAX)
+      return fail(p, FP_ERR_CONFIG, "window %u (B with n_cs = 0) missing from windows", v);
+  for (uint32_t v : p->cs)
+    if (index_of(p->windows, v) == UINT32_MAX) return fail(p, FP_ERR_CONFIG, "C_S %u missing from windows", v);
+  for (uint32_t v : p->cl)
+    if (index_of(p->windows, v) == UINT32_MAX) return fail(p, FP_ERR_CONFIG, "C_L %u missing from windows", v);
+  p->per_model = (uint64_t)p->gpus.size() * p->cl.size() * p->n_cs_eff * p->b.size();
+  p->n_cand = p->per_model * p->models.size();
+  if (p->n_cand >= 0xffffffffull) return fail(p, FP_ERR_CONFIG, "grid has >= 2^32 - 1 candidates");
+  if (p->flags & FP_FLAG_REPLICATED_GRID || p->world == 1) {
+    p->cand_first = 0;
+    p->cand_count = p->n_cand;
+  } else {
+    fp_candidate_range(p->n_cand, p->rank, p->world, &p->cand_first, &p->cand_count);
+  }
+  return FP_OK;
+}
+
+// Copy every table into one device blob and fill ta / ea pointers.
+fp_status upload(fp_plan *p) {
+  const uint32_t G = (uint32_t)p->gpus.size(), M = (uint32_t)p->models.size();
+  const uint32_t W = (uint32_t)p->windows.size();
+  std::vector<unsigned char> blob;
+  auto put = [&](const void *src, size_t bytes) {
+    size_t off = (blob.size() + 15) & ~size_t(15);
+    blob.resize(off + bytes);
+    if (bytes) memcpy(blob.data() + off, src, bytes);
+    return off;
+  };
+  // LUT: lut[c] = #{e in E : e < c * 2^s}
+  std::vector<uint8_t> lut8;
+  std::vector<uint16_t> lut16;
+  size_t off_lut = 0;
+  if (p->lut_cells) {
+    std::vector<uint32_t> lut(p->lut_cells);
+    size_t j = 0;
+    for (uint32_t c = 0; c < p->lut_cells; ++c) {
+      uint64_t bound = (uint64_t)c << p->shift;
+      while (j < p->edges.size() && (uint64_t)p->edges[j] < bound) ++j;
+      lut[c] = (uint32_t)j;
+    }
+    if (p->lut_u8) {
+      lut8.assign(lut.begin(), lut.end());
+      off_lut = put(lut8.data(), lut8.size());
+    } else {
+      lut16.assign(lut.begin(), lut.end());
+      off_lut = put(lut16.data(), lut16.size() * 2);
+    }
+  }
+  size_t off_edges = put(p->edges.data(), p->edges.size() * 4);
+  size_t off_b = put(p->b.data(), p->b.size() * 4);
+  size_t off_cs = put(p->cs.data(), p->cs.size() * 4);
+  size_t off_cl = put(p->cl.data(), p->cl.size() * 4);
+  std::vector<uint16_t> b_edge, cl_edge, b_win, cs_win, cl_win;
+  for (uint32_t v : p->b) {
+    b_edge.push_back((uint16_t)index_of(p->edges, v));
+    b_win.push_back(p->cs.empty() ? (uint16_t)index_of(p->windows, v) : 0);
+  }
+  for (uint32_t v : p->cs) cs_win.push_back((uint16_t)index_of(p->windows, v));
+  for (uint32_t v : p->cl) {
+    cl_edge.push_back((uint16_t)index_of(p->edges, v));
+    cl_win.push_back((uint16_t)index_of(p->windows, v));
+  }
+  if (p->windows.size() > 65535) return fail(p, FP_ERR_CONFIG, "too many windows");
+  size_t off_be = put(b_edge.data(), b_edge.size() * 2);
+  size_t off_ce = put(cl_edge.data(), cl_edge.size() * 2);
+  size_t off_bw = put(b_win.data(), b_win.size() * 2);
+  size_t off_sw = put(cs_win.data(), cs_win.size() * 2);
+  size_t off_lw = put(cl_win.data(), cl_win.size() * 2);
+  std::vector<uint32_t> arch;
+  for (auto &m : p->models) {
+    arch.push_back(m.n_layers); arch.push_back(m.n_kv_heads);
+    arch.push_back(m.head_dim); arch.push_back(m.kv_elem_bytes);
+  }
+  size_t off_arch = put(arch.data(), arch.size() * 4);
+  std::vector<unsigned long long> gu;
+  std::vector<double> price;
+  for (auto &g : p->gpus) {
+    gu.push_back(g.hbm_bytes); gu.push_back(g.util_num); gu.push_back(g.util_den);
+    gu.push_back(g.activation_reserve_bytes);
+    price.push_back(g.price_per_gpu_hour);
+  }
+  size_t off_gu = put(gu.data(), gu.size() * 8);
+  size_t off_price = put(price.data(), price.size() * 8);
+  std::vector<unsigned long long> dep;
+  for (auto &d : p->deploy) {
+    dep.push_back(d.tp_degree); dep.push_back(d.gpus_per_instance); dep.push_back(d.weight_bytes_per_gpu);
+  }
+  size_t off_dep = put(dep.data(), dep.size() * 8);
+  size_t off_win = put(p->windows.data(), p->windows.size() * 4);
+  size_t off_mu = put(p->mu.data(), p->mu.size() * 8);
+
+  p->blob_bytes = blob.size();
+  CUDA_TRY(p, cudaMalloc(&p->d_blob, p->blob_bytes), "cudaMalloc tables");
+  CUDA_TRY(p, cudaMemcpy(p->d_blob, blob.data(), p->blob_bytes, cudaMemcpyHostToDevice), "upload tables");
+  CUDA_TRY(p, cudaMalloc(&p->d_hist, 2ull * p->nbins * 8), "cudaMalloc hist");
+  CUDA_TRY(p, cudaMemset(p->d_hist, 0, 2ull * p->nbins * 8), "memset hist");
+  CUDA_TRY(p, cudaMalloc(&p->d_rcounts, 5 * 8), "cudaMalloc counts");
+  CUDA_TRY(p, cudaMalloc(&p->d_best, (size_t)p->world * M * sizeof(fp_candidate)), "cudaMalloc best");
+  CUDA_TRY(p, cudaMemset(p->d_best, 0, (size_t)p->world * M * sizeof(fp_candidate)), "memset best");
+
+  unsigned char *B0 = p->d_blob;
+  TraceArgs &ta = p->ta;
+  ta.lut = p->lut_cells ? (const void *)(B0 + off_lut) : nullptr;
+  ta.edges = reinterpret_cast<const uint32_t *>(B0 + off_edges);
+  ta.lut_cells = p->lut_cells;
+  ta.lut_u8 = p->lut_u8;
+  ta.shift = p->shift;
+  ta.n_edges = (uint32_t)p->edges.size();
+  ta.max_edge = p->max_edge;
+  ta.want_mass = !(p->flags & FP_FLAG_NO_MASS);
+  ta.g_cnt = p->d_hist;
+  ta.g_mass = p->d_hist + p->nbins;
+
+  EvalArgs &ea = p->ea;
+  ea.hist_cnt = p->d_hist;
+  ea.hist_mass = p->d_hist + p->nbins;
+  ea.nbins = p->nbins;
+  ea.b = reinterpret_cast<const uint32_t *>(B0 + off_b);
+  ea.cs = reinterpret_cast<const uint32_t *>(B0 + off_cs);
+  ea.cl = reinterpret_cast<const uint32_t *>(B0 + off_cl);
+  ea.b_edge = reinterpret_cast<const uint16_t *>(B0 + off_be);
+  ea.cl_edge = reinterpret_cast<const uint16_t *>(B0 + off_ce);
+  ea.b_win = reinterpret_cast<const uint16_t *>(B0 + off_bw);
+  ea.cs_win = reinterpret_cast<const uint16_t *>(B0 + off_sw);
+  ea.cl_win = reinterpret_cast<const uint16_t *>(B0 + off_lw);
+  ea.n_b = (uint32_t)p->b.size();
+  ea.n_cs = (uint32_t)p->cs.size();
+  ea.n_cl = (uint32_t)p->cl.size();
+  ea.n_cs_eff = p->n_cs_eff;
+  ea.n_models = M;
+  ea.n_gpus = G;
+  ea.n_windows = W;
+  ea.model_arch = reinterpret_cast<const uint32_t *>(B0 + off_arch);
+  ea.gpu_u64 = reinterpret_cast<const unsigned long long *>(B0 + off_gu);
+  ea.price = reinterpret_cast<const double *>(B0 + off_price);
+  ea.deploy = reinterpret_cast<const unsigned long long *>(B0 + off_dep);
+  ea.windows = reinterpret_cast<const uint32_t *>(B0 + off_win);
+  ea.mu = reinterpret_cast<const double *>(B0 + off_mu);
+  ea.hours = p->hours;
+  ea.per_model = p->per_model;
+  ea.cand_first = p->cand_first;
+  ea.cand_count = p->cand_count;
+  ea.best_out = p->d_best + (size_t)((p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->rank : 0) * M;
+
+  // K3 grid: enough blocks for the largest per-model part of this rank's slice
+  uint64_t widest = 0;
+  for (uint32_t m = 0; m < M; ++m) {
+    uint64_t lo = std::max<uint64_t>((uint64_t)m * p->per_model, p->cand_first);
+    uint64_t hi = std::min<uint64_t>((uint64_t)(m + 1) * p->per_model, p->cand_first + p->cand_count);
+    if (hi > lo) widest = std::max(widest, hi - lo);
+  }
+  p->k3_grid_x = (int)std::max<uint64_t>(1, (widest + 255) / 256);
+  if (p->k3_grid_x > 65535 * 64) return fail(p, FP_ERR_CONFIG, "candidate grid too large for one launch");
+  CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * p->k3_grid_x * sizeof(BlockBest)), "cudaMalloc block_best");
+  CUDA_TRY(p, cudaMalloc(&p->d_done, M * sizeof(unsigned int)), "cudaMalloc done");
+  CUDA_TRY(p, cudaMemset(p->d_done, 0, M * sizeof(unsigned int)), "memset done");
+  ea.block_best = p->d_block_best;
+  ea.done = p->d_done;
+  p->k3_smem = eval_smem_bytes(ea, 256);
+  if (p->k3_smem > 190 * 1024)
+    return fail(p, FP_ERR_CONFIG, "histogram + capacity table need %zu B of shared memory", p->k3_smem);
+  return FP_OK;
+}
+
+fp_status configure_launch(fp_plan *p) {
+  CUDA_TRY(p, cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device), "attr");
+  p->ta.flush_iters = 1;  // set per launch by launch_trace's smem config
+  p->k1_block = 512;
+  p->k1_smem = trace_smem_bytes(p->ta, p->k1_block);
+  if (p->k1_smem > 200 * 1024)
+    return fail(p, FP_ERR_CONFIG, "trace-pass shared memory %zu B too large", p->k1_smem);
+  int per_sm = 0;
+  CUDA_TRY(p, trace_occupancy(p->ta, p->k1_block, p->k1_smem, &per_sm), "occupancy");
+  p->k1_grid = p->sm_count * std::max(1, per_sm);
+  p->k4_block = 256;
+  p->k4_grid = p->sm_count * 8;
+  CUDA_TRY(p, eval_prepare(), "k3 attributes");
+  return FP_OK;
+}
+
+// Record an event pair around one launch of kernel `kind` (timing flag only).
+struct LaunchTimer {
+  fp_plan *p;
+  cudaStream_t s;
+  cudaEvent_t stop = nullptr;
+  LaunchTimer(fp_plan *p_, int kind, cudaStream_t s_) : p(p_), s(s_) {
+    if (!(p->flags & FP_FLAG_KERNEL_TIMING)) return;
+    auto &t = p->timers[kind];
+    if (t.used == t.ev.size()) {
+      cudaEvent_t a, b;
+      if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { cudaGetLastError(); return; }
+      t.ev.emplace_back(a, b);
+    }
+    auto &pr = t.ev[t.used++];
+    cudaEventRecord(pr.first, s);
+    stop = pr.second;
+  }
+  ~LaunchTimer() {
+    if (stop) cudaEventRecord(stop, s);
+  }
+};
+
+fp_status ensure_staging(fp_plan *p) {
+  if (p->d_stage[0]) return FP_OK;
+  for (int i = 0; i < 2; ++i) {
+    CUDA_TRY(p, cudaMalloc(&p->d_stage[i], kChunkElems * 4), "cudaMalloc staging");
+    CUDA_TRY(p, cudaEventCreateWithFlags(&p->ev_copied[i], cudaEventDisableTiming), "event");
+    CUDA_TRY(p, cudaEventCreateWithFlags(&p->ev_used[i], cudaEventDisableTiming), "event");
+  }
+  CUDA_TRY(p, cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking), "copy stream");
+  return FP_OK;
+}
+
+// Run `body(dev_ptr, n, offset)` over a trace that may live on the host: device
+// traces go straight through, host traces are DMA'd chunk by chunk into two
+// staging buffers on the copy stream (double-buffered, event-ordered).
+template <class F>
+fp_status over_trace(fp_plan *p, const uint32_t *len, uint64_t n, cudaStream_t s, F body) {
+  if (n == 0) return FP_OK;
+  if (!is_host_pointer(len)) return body(len, n, 0ull);
+  fp_status st = ensure_staging(p);
+  if (st != FP_OK) return st;
+  // the copy stream must not run ahead of work already queued on s
+  cudaEvent_t start;
+  CUDA_TRY(p, cudaEventCreateWithFlags(&start, cudaEventDisableTiming), "event");
+  cudaEventRecord(start, s);
+  cudaStreamWaitEvent(p->copy_stream, start, 0);
+  cudaEventDestroy(start);
+  for (uint64_t off = 0, i = 0; off < n; off += kChunkElems, ++i) {
+    const int k = (int)(i & 1);
+    const uint64_t cnt = std::min<uint64_t>(kChunkElems, n - off);
+    if (i >= 2) CUDA_TRY(p, cudaStreamWaitEvent(p->copy_stream, p->ev_used[k], 0), "wait used");
+    CUDA_TRY(p, cudaMemcpyAsync(p->d_stage[k], len + off, cnt * 4, cudaMemcpyHostToDevice, p->copy_stream),
+             "H2D chunk");
+    CUDA_TRY(p, cudaEventRecord(p->ev_copied[k], p->copy_stream), "record copied");
+    CUDA_TRY(p, cudaStreamWaitEvent(s, p->ev_copied[k], 0), "wait copied");
+    st = body(p->d_stage[k], cnt, off);
+    if (st != FP_OK) return st;
+    CUDA_TRY(p, cudaEventRecord(p->ev_used[k], s), "record used");
+  }
+  return FP_OK;
+}
+
+}  // namespace
+
+// ============================== ABI ==========================================
+
+extern "C" {
+
+const char *fp_status_string(fp_status s) {
+  switch (s) {
+    case FP_OK: return "ok";
+    case FP_ERR_INVALID_ARG: return "invalid argument";
+    case FP_ERR_CONFIG: return "invalid configuration";
+    case FP_ERR_EMPTY_TRACE: return "empty trace";
+    case FP_ERR_ALIGNMENT: return "misaligned buffer";
+    case FP_ERR_OOM: return "out of memory";
+    case FP_ERR_CUDA: return "CUDA error";
+    case FP_ERR_NCCL: return "NCCL error";
+    case FP_ERR_STATE: return "invalid call order";
+  }
+  return "unknown status";
+}
+
+const char *fp_last_error(const fp_plan *plan) { return plan ? plan->err.c_str() : "no plan"; }
+
+void fp_shard_range(uint64_t n_total, int32_t rank, int32_t world, uint64_t *first, uint64_t *count) {
+  if (world < 1) world = 1;
+  uint64_t per = (n_total + (uint64_t)world - 1) / (uint64_t)world;
+  per = (per + 31) / 32 * 32;
+  uint64_t lo = std::min<uint64_t>(n_total, (uint64_t)rank * per);
+  uint64_t hi = std::min<uint64_t>(n_total, lo + per);
+  *first = lo;
+  *count = hi - lo;
+}
+
+void fp_candidate_range(uint64_t n_candidates, int32_t rank, int32_t world, uint64_t *first, uint64_t *count) {
+  if (world < 1) world = 1;
+  uint64_t per = (n_candidates + (uint64_t)world - 1) / (uint64_t)world;
+  uint64_t lo = std::min<uint64_t>(n_candidates, (uint64_t)rank * per);
+  uint64_t hi = std::min<uint64_t>(n_candidates, lo + per);
+  *first = lo;
+  *count = hi - lo;
+}
+
+void fp_merge_best(const fp_candidate *recs, int32_t world, uint32_t n_models, fp_candidate *out) {
+  for (uint32_t m = 0; m < n_models; ++m) {
+    const fp_candidate *best = nullptr;
+    for (int32_t r = 0; r < world; ++r) {
+      const fp_candidate *c = recs + (size_t)r * n_models + m;
+      if (!(c->flags & FP_CAND_FEASIBLE)) continue;
+      if (!best || c->cost_dual < best->cost_dual ||
+          (c->cost_dual == best->cost_dual && c->index < best->index))
+        best = c;
+    }
+    if (best) {
+      out[m] = *best;
+    } else {
+      memset(&out[m], 0, sizeof(fp_candidate));
+      out[m].index = 0xffffffffu;
+      out[m].model = m;
+      out[m].cost_dual = out[m].cost_homo = INFINITY;
+    }
+  }
+}
+
+fp_status fp_nccl_get_unique_id(void *out128) {
+  if (!out128) return FP_ERR_INVALID_ARG;
+  std::string err;
+  if (!load_nccl(g_nccl, err)) return FP_ERR_NCCL;
+  NcclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != 0) return FP_ERR_NCCL;
+  memcpy(out128, &id, sizeof id);
+  return FP_OK;
+}
+
+fp_status fleet_plan_create(const fp_plan_desc *desc, fp_plan **out) {
+  if (!out) return FP_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!desc) return FP_ERR_INVALID_ARG;
+  fp_plan *p = new fp_plan();
+  fp_status st = validate_and_copy(p, desc);
+  if (st == FP_OK) st = build_tables(p);
+  if (st == FP_OK) {
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      st = fail(p, FP_ERR_CUDA, "no CUDA device (%s)", cudaGetErrorString(e));
+    } else if (p->device < 0 || p->device >= ndev) {
+      st = fail(p, FP_ERR_CONFIG, "device %d out of range (%d devices)", p->device, ndev);
+    }
+  }
+  if (st == FP_OK) {
+    DeviceGuard g(p->device);
+    st = upload(p);
+    if (st == FP_OK) st = configure_launch(p);
+    if (st == FP_OK && p->world > 1) {
+      std::string err;
+      if (!load_nccl(g_nccl, err)) {
+        st = fail(p, FP_ERR_NCCL, "%s", err.c_str());
+      } else {
+        NcclUniqueId id;
+        memcpy(&id, desc->nccl_unique_id, sizeof id);
+        st = nccl_check(p, g_nccl.CommInitRank(&p->comm, p->world, id, p->rank), "ncclCommInitRank");
+      }
+    }
+  }
+  if (st != FP_OK) {
+    fprintf(stderr, "fleet_plan_create: %s: %s\n", fp_status_string(st), p->err.c_str());
+    fleet_plan_destroy(p);
+    return st;
+  }
+  *out = p;
+  return FP_OK;
+}
+
+void fleet_plan_destroy(fp_plan *p) {
+  if (!p) return;
+  {
+    DeviceGuard g(p->device);
+    if (p->last_stream || p->have_sweep) cudaDeviceSynchronize();
+    if (p->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(p->comm);
+    cudaFree(p->d_blob);
+    cudaFree(p->d_hist);
+    cudaFree(p->d_rcounts);
+    cudaFree(p->d_best);
+    cudaFree(p->d_results);
+    cudaFree(p->d_block_best);
+    cudaFree(p->d_done);
+    for (int i = 0; i < 2; ++i) {
+      cudaFree(p->d_stage[i]);
+      if (p->ev_copied[i]) cudaEventDestroy(p->ev_copied[i]);
+      if (p->ev_used[i]) cudaEventDestroy(p->ev_used[i]);
+    }
+    if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+    for (auto &t : p->timers)
+      for (auto &pr : t.ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    cudaGetLastError();
+  }
+  delete p;
+}
+
+fp_status fleet_plan_info(const fp_plan *p, fp_plan_info *o) {
+  if (!p || !o) return FP_ERR_INVALID_ARG;
+  o->n_candidates = p->n_cand;
+  o->cand_first = p->cand_first;
+  o->cand_count = p->cand_count;
+  o->n_edges = (uint32_t)p->edges.size();
+  o->lut_shift = p->shift;
+  o->lut_cells = p->lut_cells;
+  o->n_windows = (uint32_t)p->windows.size();
+  o->device = p->device;
+  o->rank = p->rank;
+  o->world = p->world;
+  o->sm_count = (uint32_t)p->sm_count;
+  o->k1_grid = (uint32_t)p->k1_grid;
+  o->k1_block = (uint32_t)p->k1_block;
+  return FP_OK;
+}
+
+uint64_t fp_kernel_launches(const fp_plan *p) { return p ? p->launches : 0; }
+
+fp_status fp_kernel_time(fp_plan *p, int32_t kind, double *total_ms, uint64_t *launches) {
+  if (!p || kind < 0 || kind > 2) return FP_ERR_INVALID_ARG;
+  if (!(p->flags & FP_FLAG_KERNEL_TIMING)) return fail(p, FP_ERR_STATE, "plan created without FP_FLAG_KERNEL_TIMING");
+  DeviceGuard g(p->device);
+  auto &t = p->timers[kind];
+  double tot = 0.0;
+  for (size_t i = 0; i < t.used; ++i) {
+    CUDA_TRY(p, cudaEventSynchronize(t.ev[i].second), "event sync");
+    float ms = 0.f;
+    CUDA_TRY(p, cudaEventElapsedTime(&ms, t.ev[i].first, t.ev[i].second), "event elapsed");
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = t.used;
+  return FP_OK;
+}
+
+fp_status fp_kernel_time_reset(fp_plan *p) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  for (auto &t : p->timers) t.used = 0;
+  return FP_OK;
+}
+
+fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint32_t b_short,
+                      uint32_t c_short, uint32_t c_long, uint8_t *d_decision, fp_route_counts *h_counts,
+                      void *stream) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (n_local && !d_len) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
+  if (!(b_short >= 1 && b_short <= c_short && c_short <= c_long))
+    return fail(p, FP_ERR_INVALID_ARG, "need 1 <= B_short <= C_S <= C_L (S:316-321)");
+  if (d_decision && n_local && is_host_pointer(d_decision))
+    return fail(p, FP_ERR_INVALID_ARG, "d_decision must be device memory");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(p, cudaMemsetAsync(p->d_rcounts, 0, 5 * 8, s), "memset counts");
+  RouteArgs ra{};
+  ra.b = b_short;
+  ra.cs = c_short;
+  ra.cl = c_long;
+  ra.g_counts = p->d_rcounts;
+  fp_status st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t off) {
+    RouteArgs r = ra;
+    r.len = ptr;
+    r.n = n;
+    r.decision = d_decision ? d_decision + off : nullptr;
+    LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
+    cudaError_t e = launch_route(r, p->k4_grid, p->k4_block, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "route_batch launch");
+    ++p->launches;
+    return FP_OK;
+  });
+  if (st != FP_OK) return st;
+  if (p->world > 1) {
+    st = nccl_check(p, g_nccl.AllReduce(p->d_rcounts, p->d_rcounts, 5, kNcclUint64, kNcclSum, p->comm, s),
+                    "ncclAllReduce(route counts)");
+    if (st != FP_OK) return st;
+  }
+  p->last_stream = s;
+  if (h_counts) {
+    unsigned long long c[5];
+    CUDA_TRY(p, cudaMemcpyAsync(c, p->d_rcounts, sizeof c, cudaMemcpyDeviceToHost, s), "D2H counts");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    h_counts->n_short = c[0];
+    h_counts->n_long = c[1];
+    h_counts->n_reject = c[2];
+    h_counts->mass_short = c[3];
+    h_counts->mass_long = c[4];
+  }
+  return FP_OK;
+}
+
+fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
+                           fp_candidate *h_results, void *stream) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (n_local && !d_len) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
+  if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
+    return fail(p, FP_ERR_INVALID_ARG, "rate_rps must be finite and > 0");
+  if (p->world == 1 && n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace (S:170)");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // K1: trace pass into the global bin histogram
+  CUDA_TRY(p, cudaMemsetAsync(p->d_hist, 0, 2ull * p->nbins * 8, s), "memset hist");
+  fp_status st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t) {
+    TraceArgs t = p->ta;
+    t.len = ptr;
+    t.n = n;
+    LaunchTimer lt(p, FP_KERNEL_TRACE, s);
+    cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");
+    ++p->launches;
+    return FP_OK;
+  });
+  if (st != FP_OK) return st;
+  // C1: sum the per-rank histograms
+  if (p->world > 1) {
+    st = nccl_check(p, g_nccl.AllReduce(p->d_hist, p->d_hist, 2ull * p->nbins, kNcclUint64, kNcclSum,
+                                        p->comm, s),
+                    "ncclAllReduce(histogram)");
+    if (st != FP_OK) return st;
+  }
+  // K2 + K3: scan, evaluate this rank's candidates, per-model argmin
+  if (h_results && !p->d_results && p->cand_count)
+    CUDA_TRY(p, cudaMalloc(&p->d_results, p->cand_count * sizeof(fp_candidate)), "cudaMalloc results");
+  EvalArgs ea = p->ea;
+  ea.rate = rate_rps;
+  ea.results = h_results ? p->d_results : nullptr;
+  cudaError_t e;
+  {
+    LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+    e = launch_eval(ea, p->k3_grid_x, 256, p->k3_smem, s);
+  }
+  if (e != cudaSuccess) return cuda_fail(p, e, "candidate evaluation launch");
+  ++p->launches;
+  // C2: gather every rank's per-model best
+  if (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) {
+    const size_t bytes = p->models.size() * sizeof(fp_candidate);
+    st = nccl_check(p, g_nccl.AllGather(p->d_best + (size_t)p->rank * p->models.size(), p->d_best, bytes,
+                                        kNcclUint8, p->comm, s),
+                    "ncclAllGather(best)");
+    if (st != FP_OK) return st;
+  }
+  p->have_sweep = true;
+  p->last_stream = s;
+  if (h_results && p->cand_count) {
+    CUDA_TRY(p, cudaMemcpyAsync(h_results, p->d_results, p->cand_count * sizeof(fp_candidate),
+                                cudaMemcpyDeviceToHost, s),
+             "D2H results");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  }
+  return FP_OK;
+}
+
+fp_status best_split(fp_plan *p, fp_candidate *h_best) {
+  if (!p || !h_best) return FP_ERR_INVALID_ARG;
+  if (!p->have_sweep) return fail(p, FP_ERR_STATE, "best_split before sweep_thresholds");
+  DeviceGuard g(p->device);
+  const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
+  const size_t M = p->models.size();
+  std::vector<fp_candidate> recs((size_t)ranks * M);
+  unsigned long long total = 0;
+  CUDA_TRY(p, cudaStreamSynchronize(p->last_stream), "sync");
+  CUDA_TRY(p, cudaMemcpy(recs.data(), p->d_best, recs.size() * sizeof(fp_candidate), cudaMemcpyDeviceToHost),
+           "D2H best");
+  std::vector<unsigned long long> cnt(p->nbins);
+  CUDA_TRY(p, cudaMemcpy(cnt.data(), p->d_hist, p->nbins * 8, cudaMemcpyDeviceToHost), "D2H hist");
+  for (auto c : cnt) total += c;
+  if (total == 0) return fail(p, FP_ERR_EMPTY_TRACE, "global trace is empty");
+  fp_merge_best(recs.data(), ranks, (uint32_t)M, h_best);
+  return FP_OK;
+}
+
+fp_status sweep_histogram(fp_plan *p, uint32_t *h_edges, uint64_t *h_bin_cnt, uint64_t *h_bin_mass) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (!p->have_sweep) return fail(p, FP_ERR_STATE, "sweep_histogram before sweep_thresholds");
+  DeviceGuard g(p->device);
+  CUDA_TRY(p, cudaStreamSynchronize(p->last_stream), "sync");
+  if (h_edges) memcpy(h_edges, p->edges.data(), p->edges.size() * 4);
+  if (h_bin_cnt) CUDA_TRY(p, cudaMemcpy(h_bin_cnt, p->d_hist, p->nbins * 8, cudaMemcpyDeviceToHost), "D2H hist");
+  if (h_bin_mass)
+    CUDA_TRY(p, cudaMemcpy(h_bin_mass, p->d_hist + p->nbins, p->nbins * 8, cudaMemcpyDeviceToHost), "D2H hist");
+  return FP_OK;
+}
+
+}  // extern "C"

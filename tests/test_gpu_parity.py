@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bit-exact for every integer (routing counts, histogram, N_seq, instances,
+GPUs, argmin index) and for the fp64 fields as well: both sides evaluate
+the same IEEE binary64 operations in the same order without contraction
+(R14), so the records must agree byte for byte. The north-star
+tolerance (|d| <= 1e-9 relative) is asserted too, as the documented bound.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2604_08075_b200 as fp  # noqa: E402
+from synth import configs  # noqa: E402
+from synth.configs import make_config  # noqa: E402
+from synth.gen import generate_device, generate_host  # noqa: E402
+
+FLOAT_FIELDS = ["alpha", "rho", "predicted_savings", "savings", "cost_dual", "cost_homo",
+                "occupancy_short", "occupancy_long"]
+INT_FIELDS = [n for n in fp.FP_CANDIDATE.names if n not in FLOAT_FIELDS and n != "_pad"]
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+def _compare_records(gpu, ref, what=""):
+    assert gpu.shape == ref.shape, what
+    for f in INT_FIELDS:
+        bad = np.nonzero(gpu[f] != ref[f])[0]
+        assert bad.size == 0, f"{what}: field {f} differs at {bad[:5]}: {gpu[f][bad[:5]]} vs {ref[f][bad[:5]]}"
+    for f in FLOAT_FIELDS:
+        g, r = gpu[f], ref[f]
+        both_inf = np.isinf(g) & np.isinf(r) & (np.sign(g) == np.sign(r))
+        with np.errstate(invalid="ignore"):
+            rel = np.where(both_inf, 0.0, np.abs(g - r) / np.maximum(np.abs(r), 1e-300))
+        assert np.all(both_inf | (rel <= 1e-9)), f"{what}: {f} beyond 1e-9"
+        assert np.array_equal(g.view(np.uint64), r.view(np.uint64)), f"{what}: {f} not bit-exact"
+
+
+def _plan(cfg, **kw):
+    return fp.fleet_plan_create(**fp.desc_from_config(cfg), **kw)
+
+
+def _run_config(cfg, L_host):
+    plan = _plan(cfg)
+    res = fp.sweep_thresholds(plan, _dev(L_host), cfg.rate_rps, want_results=True)
+    best = fp.best_split(plan)
+    allc, obest = oracle.sweep(cfg, L_host)
+    return plan, res, best, allc, obest
+
+
+@pytest.mark.parametrize("name,n", [("C1", 1000), ("C2", 1_000_003), ("C3", 200_001), ("C4", 1_000_001),
+                                    ("C5", 1_000_007)])
+def test_config_parity(name, n):
+    cfg = configs.CONFIGS[name]().with_n(n)
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    plan, res, best, allc, obest = _run_config(cfg, L)
+    _compare_records(res, allc.view(fp.FP_CANDIDATE), name)
+    _compare_records(best, obest.view(fp.FP_CANDIDATE), name + " best")
+    # histogram = the empirical CDF by definition at every edge
+    edges, cnt, mass = fp.sweep_histogram(plan)
+    ocnt, omass = oracle.count_le(L, edges)
+    assert np.array_equal(np.cumsum(cnt)[:-1], ocnt) and int(cnt.sum()) == n
+    assert np.array_equal(np.cumsum(mass)[:-1], omass) and mass[-1] == 0
+
+
+def test_c1_paper_numbers():
+    cfg = configs.c1()
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    fp.sweep_thresholds(plan, _dev(L), cfg.rate_rps)
+    b = fp.best_split(plan)[0]
+    assert (b["nseq_short"], b["nseq_long"]) == (128, 16)                    # P:40-43 (R10)
+    served = (b["n_short"] + b["n_long"]) / cfg.n_requests
+    assert b["inst_homo"] == int(np.ceil(served * 1000.0 / 2.8))            # Table 2 rule
+    assert b["rho"] == 4.0
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 15, 16, 17, 31, 33, 4095, 32768, 32769, 65536 * 4 + 7])
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_ragged_and_misaligned(n, offset):
+    cfg = configs.c3(n)
+    full = generate_host(cfg.shape, cfg.seed, 0, n + offset)
+    L = full[offset:]
+    d = _dev(full)[offset:]
+    plan = _plan(cfg)
+    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    allc, _ = oracle.sweep(cfg, L)
+    _compare_records(res, allc.view(fp.FP_CANDIDATE), f"n={n} off={offset}")
+
+
+def test_edge_values_and_skew():
+    cfg = make_config("edge", "AZ", 1, 0, 1000.0, ["llama3-70b"], ["b200-180g"],
+                      [1, 256, 8192, 65536], [], [65536, 131072])
+    rng = np.random.default_rng(0)
+    L = np.concatenate([np.zeros(1000, np.uint32), np.full(5000, 8192, np.uint32),
+                        np.full(3000, 8193, np.uint32), np.full(17, 2**32 - 1, np.uint32),
+                        np.full(100_000, 300, np.uint32),            # all lanes in one bin
+                        rng.integers(0, 200_000, 50_000).astype(np.uint32)])
+    rng.shuffle(L)
+    plan, res, best, allc, obest = _run_config(cfg.with_n(L.size), L)
+    _compare_records(res, allc.view(fp.FP_CANDIDATE), "edge")
+    _compare_records(best, obest.view(fp.FP_CANDIDATE), "edge best")
+
+
+def test_large_edge_values_split_mass_and_binary_search():
+    # edges up to 2^31 with s = 0 -> LUT too large -> binary-search bins; mass in 16-bit halves
+    cfg = make_config("big", "AZ", 1, 0, 1000.0, ["llama3-8b"], ["b200-180g"],
+                      [1, 3, 1000, 77777, 2**20 + 1], [], [2**31 - 1, 2**31])
+    rng = np.random.default_rng(1)
+    L = rng.integers(0, 2**32 - 1, 300_000, dtype=np.uint64).astype(np.uint32)
+    L[:100_000] = rng.integers(0, 2**21, 100_000).astype(np.uint32)
+    plan, res, best, allc, obest = _run_config(cfg.with_n(L.size), L)
+    assert fp.fleet_plan_info(plan)["lut_cells"] == 0
+    _compare_records(res, allc.view(fp.FP_CANDIDATE), "big")
+
+
+def test_many_edges_u16_lut():
+    # > 255 bins -> u16 LUT; > ~100 KB lane-private histogram -> shared replica
+    b = list(range(16, 16 * 1500, 16))
+    cfg = make_config("many", "AZ", 1, 0, 1000.0, ["llama3-8b"], ["b200-180g"], b, [], [65536])
+    L = generate_host("AZ", 5, 0, 500_000)
+    plan, res, best, allc, obest = _run_config(cfg.with_n(L.size), L)
+    _compare_records(res, allc.view(fp.FP_CANDIDATE), "many")
+    _compare_records(best, obest.view(fp.FP_CANDIDATE), "many best")
+
+
+def test_no_mass_flag():
+    cfg = configs.c2().with_n(100_000)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg, flags=fp.FP_FLAG_NO_MASS)
+    res = fp.sweep_thresholds(plan, _dev(L), cfg.rate_rps, want_results=True)
+    allc, _ = oracle.sweep(cfg, L)
+    ref = allc.view(fp.FP_CANDIDATE)
+    for f in ["n_short", "n_long", "n_reject", "inst_short", "inst_long", "inst_homo", "cost_dual", "flags"]:
+        assert np.array_equal(res[f], ref[f])
+    assert np.all(res["mass_short"] == 0)
+
+
+def test_host_pointer_path_matches_device():
+    cfg = configs.c5().with_n(3_000_017)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    a = fp.sweep_thresholds(plan, _dev(L), cfg.rate_rps, want_results=True)
+    b = fp.sweep_thresholds(plan, L, cfg.rate_rps, want_results=True)                 # pageable host
+    pinned = torch.from_numpy(L.view(np.int32)).pin_memory()
+    c = fp.sweep_thresholds(plan, pinned, cfg.rate_rps, want_results=True)            # pinned host
+    assert a.tobytes() == b.tobytes() == c.tobytes()
+
+
+def test_empty_trace_and_invalid_args():
+    cfg = configs.c1()
+    plan = _plan(cfg)
+    with pytest.raises(fp.FleetPlanError) as e:
+        fp.sweep_thresholds(plan, torch.zeros(0, dtype=torch.int32, device="cuda"), 1000.0)
+    assert e.value.status == 3
+    with pytest.raises(fp.FleetPlanError):
+        fp.best_split(plan)                                                              # no sweep yet
+    with pytest.raises(fp.FleetPlanError):
+        fp.route_batch(plan, torch.ones(4, dtype=torch.int32, device="cuda"), 9000, 8192, 65536)
+    with pytest.raises(fp.FleetPlanError):
+        fp.sweep_thresholds(plan, torch.ones(4, dtype=torch.int32, device="cuda"), 0.0)
+
+
+def test_determinism_and_launch_count():
+    cfg = configs.c4().with_n(2_000_000)
+    d = generate_device(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    l0 = fp.fp_kernel_launches(plan)
+    r1 = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    r2 = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    assert r1.tobytes() == r2.tobytes()
+    assert fp.fp_kernel_launches(plan) - l0 == 4      # K1 + K3 per sweep
+
+
+@pytest.mark.parametrize("split", [(8192, 8192, 65536), (1024, 4096, 131072), (1, 1, 1), (300, 300, 300)])
+@pytest.mark.parametrize("n,off,doff", [(1, 0, 0), (17, 1, 3), (100_003, 3, 5), (1_000_000, 0, 0)])
+def test_route_batch_parity(split, n, off, doff):
+    B, CS, CL = split
+    full = generate_host("SG", 9, 0, n + off)
+    L = full[off:]
+    dec = torch.zeros(n + doff + 16, dtype=torch.uint8, device="cuda")
+    cfg = configs.c1()
+    plan = _plan(cfg)
+    counts = fp.route_batch(plan, _dev(full)[off:], B, CS, CL, decision=dec[doff:doff + n])
+    odec, ocnt = oracle.route_batch(L, B, CS, CL)
+    assert np.array_equal(dec[doff:doff + n].cpu().numpy(), odec)
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in ocnt]
+    # the host-trace path gives the same counts
+    assert fp.route_batch(plan, L, B, CS, CL) == counts
+
+
+@pytest.mark.slow
+def test_full_size_c5_sampled():
+    """C5 at its full size (1e9 requests) in the bench's launch configuration:
+    the CUDA generator's trace equals the host generator's on sampled windows,
+    the global histogram satisfies the invariants, and sub-ranges of the same
+    device trace swept by the same kernels match the oracle exactly."""
+    cfg = configs.c5()
+    n = cfg.n_requests
+    d = generate_device(cfg.shape, cfg.seed, 0, n)
+    rng = np.random.default_rng(0)
+    for first in rng.integers(0, n - (1 << 20), 3):
+        h = generate_host(cfg.shape, cfg.seed, int(first), 1 << 20)
+        assert np.array_equal(d[int(first):int(first) + (1 << 20)].cpu().numpy().view(np.uint32), h)
+    plan = _plan(cfg)
+    fp.sweep_thresholds(plan, d, cfg.rate_rps)
+    best = fp.best_split(plan)
+    edges, cnt, mass = fp.sweep_histogram(plan)
+    assert int(cnt.sum()) == n
+    assert np.all(best["n_short"] + best["n_long"] + best["n_reject"] == n)
+    for first in rng.integers(0, n - (1 << 24), 2):
+        first = int(first) | 1                                       # misaligned on purpose
+        L = generate_host(cfg.shape, cfg.seed, first, 1 << 24)
+        res = fp.sweep_thresholds(plan, d[first:first + (1 << 24)], cfg.rate_rps, want_results=True)
+        allc, _ = oracle.sweep(cfg.with_n(1 << 24), L)
+        _compare_records(res, allc.view(fp.FP_CANDIDATE), f"C5 window @{first}")
