@@ -1,0 +1,345 @@
+"""Benchmark of the fleet-sizing sweep (the north-star hot path) on B200.
+
+One step = the whole hot path of SURVEY.md §8(a) over one batch (the trace):
+  sweep_thresholds  (K1 trace pass + histogram, [C1 all-reduce], K3 scan +
+                     candidate evaluation + argmin, [C2 all-gather])
+  best_split        (per-model best split -> host)
+  route_batch       (K4: Alg. 1 for model 0's best split, decision byte per
+                     request + global counts -> host)
+Default workload: C5 (1e9-request MIX trace per GPU, 4,096 candidates) --
+the configuration BASELINE.json's "at 1/2/4/8 B200" metric is quoted on and
+the largest single-GPU one. Multi-GPU (torchrun): weak scaling, 1e9 requests
+per rank (global index shards of one trace), NCCL inside the library.
+
+`--impl reference` times the CPU oracle (oracle/, as it stands) on bounded
+samples of the same workload (the reference arm of this tier).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace requests routed/s and fleet-sizing candidates/s at 1/2/4/8 B200"
+UNIT = "requests/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _traffic(workload, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(workload, {}).get(kernel)
+        return float(e["dram_bytes_per_launch"]) if e else None
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index, period_s=0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period = period_s
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": getattr(self, "err", "")}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _workload(cfg, n_per_rank, world):
+    return {"workload": f"{cfg.name}: {cfg.description}", "name": cfg.name,
+            "trace": cfg.shape, "seed": cfg.seed, "n_requests_per_gpu": n_per_rank,
+            "n_requests_total": n_per_rank * world, "n_candidates": cfg.n_candidates(),
+            "rate_rps": cfg.rate_rps, "l2": "inputs larger than L2 (4 B x 1e9 = 4 GB per GPU > 126 MB)",
+            "parallelism": f"dp{world} (trace sharded by global request index)"}
+
+
+# ------------------------------------------------------------------ CPU oracle ----
+def oracle_step(cfg, L):
+    """The hot path on the CPU oracle: sweep + argmin + Alg. 1 route of the
+    sample with model 0's best split (same work as one GPU step)."""
+    import oracle
+    _, best = oracle.sweep(cfg, L, want_all=False)
+    b = best[0]
+    if b["index"] != 0xFFFFFFFF:
+        oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    return best
+
+
+def cpu_baseline(cfg, target_s=12.0):
+    import oracle
+    from synth.gen import generate_host
+    n0 = 1 << 20
+    L = generate_host(cfg.shape, cfg.seed, 0, n0)
+    t = time.perf_counter()
+    oracle_step(cfg.with_n(n0), L)
+    dt = max(time.perf_counter() - t, 1e-3)
+    n = int(min(cfg.n_requests, max(n0, n0 * target_s / dt)))
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    t = time.perf_counter()
+    oracle_step(cfg.with_n(n), L)
+    dt = time.perf_counter() - t
+    return {"value": n / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"first {n:,} requests of the {cfg.name} trace (one oracle step: sweep of all "
+                      f"{cfg.n_candidates()} candidates + argmin + Alg. 1 route), {dt:.1f} s"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    from synth.gen import generate_host
+    n = args.ref_sample
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    c = cfg.with_n(n)
+    for _ in range(args.warmup):
+        oracle_step(c, L)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        oracle_step(c, L)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * sum(times) / len(times)
+    value = n / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32/f64", "data": "synthetic",
+            "config": _workload(cfg, cfg.n_requests, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                             "sample": f"each step: first {n:,} requests of the {cfg.name} trace"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU path ----
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_08075_b200 as fp
+    from synth.gen import generate_device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = args.n or cfg.n_requests
+    cfg = cfg.with_n(n)
+
+    uid = None
+    if world > 1:
+        obj = [fp.fp_nccl_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
+                                nccl_unique_id=uid, flags=fp.FP_FLAG_KERNEL_TIMING)
+    info = fp.fleet_plan_info(plan)
+    # this rank's shard of the global trace: requests [rank*n, (rank+1)*n)
+    d_len = generate_device(cfg.shape, cfg.seed, rank * n, n)
+    d_dec = torch.empty(n, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(lengths):
+        fp.sweep_thresholds(plan, lengths, cfg.rate_rps, stream=stream)
+        best = fp.best_split(plan)
+        b = best[0]
+        if b["index"] == 0xFFFFFFFF:
+            raise RuntimeError("model 0 has no feasible split")
+        counts = fp.route_batch(plan, lengths, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]),
+                                decision=d_dec, stream=stream)
+        return best, counts
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step(d_len)
+    barrier()
+    fp.fp_kernel_time_reset(plan)
+    l0 = fp.fp_kernel_launches(plan)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            best, counts = step(d_len)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = fp.fp_kernel_launches(plan) - l0
+    ms_local = e0.elapsed_time(e1)
+    ktime = {k: fp.fp_kernel_time(plan, kind) for k, kind in
+             (("trace", fp.FP_KERNEL_TRACE), ("eval", fp.FP_KERNEL_EVAL), ("route", fp.FP_KERNEL_ROUTE))}
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    total_requests = n * world
+    value = total_requests / (ms_step / 1e3)
+
+    # ---- e2e: the same step through the C ABI with HOST (pinned) buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        h_len = d_len.cpu().pin_memory()
+        step(h_len)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            step(h_len)
+        barrier()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_requests * args.e2e_steps / float(dt.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 2 * 4 * n,   # sweep + route each stream the pinned trace
+               "d2h_bytes_per_step": best.nbytes + 5 * 8,
+               "note": "pinned host trace streamed H2D inside sweep_thresholds and route_batch "
+                       "(128 MB chunks, copy/compute overlapped); best records + route counts to host"}
+        del h_len
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel ----
+    peak, peak_src = _peaks()
+    shares = {k: v[0] for k, v in ktime.items()}
+    dom = max(shares, key=shares.get)
+    algo_bytes = {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0}
+    kms, kcount = ktime[dom]
+    per_launch_ms = kms / max(kcount, 1)
+    per_launch_bytes = algo_bytes[dom] / max(1.0, kcount / args.steps)   # bytes per step / launches per step
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    k_gbs = {k: (algo_bytes[k] * args.steps / (ktime[k][0] / 1e3) / 1e9 if ktime[k][0] and algo_bytes[k] else None)
+             for k in ktime}
+    roof = {"bound": "hbm", "kernel": {"trace": "K1 k1_trace", "route": "K4 k4_route"}.get(dom, dom),
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": _traffic(cfg.name, dom), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": per_launch_bytes,
+            "per_kernel_GBps": k_gbs,
+            "step_share": {k: v / ms_total for k, v in shares.items()}}
+    cand_per_s = cfg.n_candidates() * args.steps / (ktime["eval"][0] / 1e3) if ktime["eval"][0] else None
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32/f64",
+            "data": "synthetic (seeded Philox MIX trace, generated on device; not timed)",
+            "config": _workload(cfg, n, world),
+            "candidates_per_s": cand_per_s,
+            "candidates_per_s_step": cfg.n_candidates() / (ms_step / 1e3),
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktime.items()},
+            "roofline": roof,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "best_split_model0": {k: (int(best[0][k]) if k not in ("cost_dual", "savings", "predicted_savings")
+                                      else float(best[0][k]))
+                                  for k in ("index", "b_short", "c_short", "c_long", "gpus_dual", "gpus_homo",
+                                            "cost_dual", "savings", "predicted_savings")},
+            "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=10_000_000,
+                    help="requests per reference (oracle) step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    from synth import configs
+    cfg = configs.CONFIGS[args.config]()
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()
