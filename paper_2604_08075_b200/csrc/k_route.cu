@@ -1,0 +1,207 @@
+// K4: route_batch -- Alg. 1 for one (B, C_S, C_L) over a trace.
+//
+// With 1 <= B <= C_S <= C_L (validated by the host) and a = L > B,
+// b = L > C_S, c = L > C_L (c => b => a) the outcome of Alg. 1 is
+//   L <= B          -> short, step 2 (budget)        decision 0
+//   B < L <= C_S    -> long,  step 2 (budget)        decision 1
+//   C_S < L <= C_L  -> long,  step 1 (feasibility)   decision 1 | 1 << 2 = 5
+//   L > C_L         -> rejected (R3)      decision 2 | 3 << 2 = 14
+// i.e. decision = a + 4 b + 9 c, branch-free. (The final safety check of
+// Alg. 1 can only fire after a spillover, which a static trace does not
+// have; under B <= C_S its condition is never true.)
+//
+// Memory pattern as K1: per block and step a contiguous tile of blockDim x 4
+// uint4 (coalesced: lane i reads the i-th 16 B of each warp's 512 B), and per
+// uint4 one 32-bit store of its 4 decision bytes (a warp stores 128 B
+// contiguous). Counts live in registers (short = !a, served = !c), masses
+// are summed per tile in u32 (16 requests x L <= C_L < 2^28: exact) and
+// then in u64; one warp/block reduction and 5 global atomics per block.
+#include <algorithm>
+#include "internal.cuh"
+
+namespace fp {
+
+namespace {
+
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// One request: counters + decision byte, as predicated PTX (3 compares +
+// 7 predicated ops; nvcc otherwise emits VIADD + predicated MOV pairs).
+__device__ __forceinline__ uint32_t route_u32(uint32_t L, uint32_t B, uint32_t CS, uint32_t CL, uint32_t &ns,
+                                              uint32_t &nsv, uint32_t &ms, uint32_t &msv) {
+  uint32_t d;
+  asm("{\n\t.reg .pred pa, pb, pc;\n\t"
+      "setp.gt.u32 pa, %5, %6;\n\t"
+      "setp.gt.u32 pb, %5, %7;\n\t"
+      "setp.gt.u32 pc, %5, %8;\n\t"
+      "selp.u32 %0, 1, 0, pa;\n\t"
+      "@pb add.u32 %0, %0, 4;\n\t"
+      "@pc add.u32 %0, %0, 9;\n\t"
+      "@!pa add.u32 %1, %1, 1;\n\t"
+      "@!pa add.u32 %3, %3, %5;\n\t"
+      "@!pc add.u32 %2, %2, 1;\n\t"
+      "@!pc add.u32 %4, %4, %5;\n\t"
+      "}"
+      : "=r"(d), "+r"(ns), "+r"(nsv), "+r"(ms), "+r"(msv)
+      : "r"(L), "r"(B), "r"(CS), "r"(CL));
+  return d;
+}
+
+struct Acc {
+  uint32_t ns = 0, nsv = 0, n = 0;          // short, served (<= C_L), routed by this thread
+  unsigned long long ms = 0, msv = 0;       // mass short, mass served
+};
+
+// generic (u64 mass) single request
+__device__ __forceinline__ uint32_t route_u64(uint32_t L, uint32_t B, uint32_t CS, uint32_t CL, Acc &a) {
+  const bool pa = L > B, pb = L > CS, pc = L > CL;
+  if (!pa) { ++a.ns; a.ms += L; }
+  if (!pc) { ++a.nsv; a.msv += L; }
+  ++a.n;
+  return (pa ? 1u : 0u) + (pb ? 4u : 0u) + (pc ? 9u : 0u);
+}
+
+template <bool SMALL>
+__device__ __forceinline__ uint32_t route4(const uint4 &v, uint32_t B, uint32_t CS, uint32_t CL, Acc &a,
+                                           uint32_t &gms, uint32_t &gmsv) {
+  if constexpr (SMALL) {
+    const uint32_t d0 = route_u32(v.x, B, CS, CL, a.ns, a.nsv, gms, gmsv);
+    const uint32_t d1 = route_u32(v.y, B, CS, CL, a.ns, a.nsv, gms, gmsv);
+    const uint32_t d2 = route_u32(v.z, B, CS, CL, a.ns, a.nsv, gms, gmsv);
+    const uint32_t d3 = route_u32(v.w, B, CS, CL, a.ns, a.nsv, gms, gmsv);
+    a.n += 4;
+    return d0 | (d1 << 8) | (d2 << 16) | (d3 << 24);
+  } else {
+    const uint32_t d0 = route_u64(v.x, B, CS, CL, a);
+    const uint32_t d1 = route_u64(v.y, B, CS, CL, a);
+    const uint32_t d2 = route_u64(v.z, B, CS, CL, a);
+    const uint32_t d3 = route_u64(v.w, B, CS, CL, a);
+    return d0 | (d1 << 8) | (d2 << 16) | (d3 << 24);
+  }
+}
+
+template <bool DEC, bool DVEC>
+__device__ __forceinline__ void store4(uint8_t *dec, uint32_t w) {
+  if constexpr (DEC) {
+    if constexpr (DVEC) {
+      *reinterpret_cast<uint32_t *>(dec) = w;
+    } else {
+      dec[0] = (uint8_t)w; dec[1] = (uint8_t)(w >> 8); dec[2] = (uint8_t)(w >> 16); dec[3] = (uint8_t)(w >> 24);
+    }
+  }
+}
+
+// DEC: write decisions; SMALL: C_L < 2^28 (u32 tile masses); DVEC: the
+// decision address of every uint4 of the body is 4-byte aligned.
+template <bool DEC, bool SMALL, bool DVEC>
+__global__ void __launch_bounds__(512) k4_route(RouteArgs a) {
+  const uint32_t B = a.b, CS = a.cs, CL = a.cl;
+  Acc acc;
+  const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.len) & 15u) >> 2);
+  const uint64_t head = mis ? (a.n < 4u - mis ? a.n : 4u - mis) : 0u;
+  const uint64_t n4 = (a.n - head) >> 2;
+  const uint64_t tail_first = head + (n4 << 2);
+  if (blockIdx.x == 0 && threadIdx.x < head) {
+    const uint32_t d = route_u64(a.len[threadIdx.x], B, CS, CL, acc);
+    if (DEC) a.decision[threadIdx.x] = (uint8_t)d;
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
+    const uint64_t i = tail_first + threadIdx.x;
+    const uint32_t d = route_u64(a.len[i], B, CS, CL, acc);
+    if (DEC) a.decision[i] = (uint8_t)d;
+  }
+  const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
+  uint8_t *dbody = DEC ? a.decision + head : nullptr;
+  const uint64_t tile4 = (uint64_t)blockDim.x * kUnroll;
+  const uint64_t full_tiles = n4 / tile4;
+  const uint64_t ntiles = (n4 + tile4 - 1) / tile4;
+  for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const uint64_t base = t * tile4 + threadIdx.x;
+    uint32_t gms = 0, gmsv = 0;
+    if (t < full_tiles) {
+      uint4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) v[u] = ldg_stream(body + base + (uint64_t)u * blockDim.x);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t w = route4<SMALL>(v[u], B, CS, CL, acc, gms, gmsv);
+        store4<DEC, DVEC>(dbody + 4 * (base + (uint64_t)u * blockDim.x), w);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint64_t i = base + (uint64_t)u * blockDim.x;
+        if (i < n4) {
+          const uint32_t w = route4<SMALL>(ldg_stream(body + i), B, CS, CL, acc, gms, gmsv);
+          store4<DEC, DVEC>(dbody + 4 * i, w);
+        }
+      }
+    }
+    if constexpr (SMALL) {
+      acc.ms += gms;
+      acc.msv += gmsv;
+    }
+  }
+  // reduce: warp shuffles, then one atomic per block per counter
+  unsigned long long v[5] = {acc.ns, (unsigned long long)acc.nsv - acc.ns, (unsigned long long)acc.n - acc.nsv,
+                             acc.ms, acc.msv - acc.ms};
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  __shared__ unsigned long long red[5][16];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) red[k][w] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    unsigned long long t = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += red[threadIdx.x][j];
+    if (t) atomicAdd(a.g_counts + threadIdx.x, t);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_route(const RouteArgs &a0, int grid, int block, cudaStream_t s) {
+  if (a0.n == 0) return cudaSuccess;
+  if (block > 512 || (block & 31)) return cudaErrorInvalidValue;
+  const bool small = a0.cl < (1u << 28);
+  // u32 per-thread counters: at most 2^31 requests per thread per launch
+  const uint64_t cap = (uint64_t)grid * block * (1ull << 31);
+  RouteArgs a = a0;
+  for (uint64_t off = 0; off < a0.n; off += cap) {
+    a.len = a0.len + off;
+    a.decision = a0.decision ? a0.decision + off : nullptr;
+    a.n = std::min<uint64_t>(cap, a0.n - off);
+    const uint64_t tiles = (a.n / 4 + (uint64_t)block * kUnroll - 1) / ((uint64_t)block * kUnroll);
+    const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, tiles));
+    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.len) & 15u) >> 2);
+    const uint64_t head = mis ? std::min<uint64_t>(a.n, 4u - mis) : 0u;
+    const bool dvec = a.decision && ((reinterpret_cast<uintptr_t>(a.decision + head) & 3u) == 0u);
+#define FP_K4(D, S, V) k4_route<D, S, V><<<g, block, 0, s>>>(a)
+    if (a.decision) {
+      if (small) { if (dvec) FP_K4(true, true, true); else FP_K4(true, true, false); }
+      else { if (dvec) FP_K4(true, false, true); else FP_K4(true, false, false); }
+    } else {
+      if (small) FP_K4(false, true, false); else FP_K4(false, false, false);
+    }
+#undef FP_K4
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace fp

@@ -1,23 +1,30 @@
-// K1: the trace pass of sweep_thresholds, and K4: route_batch.
+// K1: the trace pass of sweep_thresholds (K4, route_batch, is in k_route.cu).
 //
 // K1 streams the u32 L_total column once (128-bit loads, one contiguous
-// 32 KB tile per block per step, several tiles in flight per SM) and routes
-// every request against EVERY candidate at once: its bin
+// tile of blockDim x 64 B per block per step, 4 loads in flight per thread)
+// and routes every request against EVERY candidate at once: its bin
 //     b(L) = #{e in E : e < L}          (E = sortuniq(B u C_L), "<=")
-// is read from a fine-cell LUT in shared memory (cell = ceil(L / 2^s); every
-// edge is a multiple of 2^s, so the LUT is exact), and the request adds 1 to
-// cnt[b] and L to mass[b]. A request in bin b is short for every candidate
-// with B >= e_b, long for B < L <= C_L and rejected for L > C_L, so the scan
-// of this histogram (K3 prologue) gives every candidate's routing outcome of
-// Alg. 1 with bit-exact integer counts.
+// is read from a fine-cell LUT in shared memory (cell = ceil(min(L, e_max+1)
+// / 2^s); every edge is a multiple of 2^s, so the LUT is exact), and the
+// request adds 1 to cnt[b] and L to mass[b]. A request in bin b is short for
+// every candidate with B >= e_b, long for B < L <= C_L and rejected for
+// L > C_L, so the scan of this histogram (K3 prologue) gives every
+// candidate's routing outcome of Alg. 1 with bit-exact counts.
 //
 // Histogram layout: R replicas x (|E|+1) bins of u32 counters in shared
 // memory; with R = 32 every lane owns a replica ("lane-private"), so the 32
 // atomics of one warp instruction hit 32 distinct banks whatever the length
 // distribution (no same-address serialisation on skewed traces). Mass uses
 // u32 slots flushed into a u64 per-bin accumulator before they can overflow
-// (64-bit shared atomics are a CAS loop on sm_100a: ATOMS.CAST.SPIN.64).
-// When L can exceed the u32 flush bound the mass is split into 16-bit halves.
+// (64-bit shared atomics are a CAS loop on sm_100a: ATOMS.CAST.SPIN.64). The
+// bin above the last edge also receives its L (so the hot loop has no
+// branch); that slot may wrap and is never published -- no candidate uses
+// the mass of requests above every edge. When e_max is too large for the
+// u32 flush bound the mass is split into 16-bit halves.
+//
+// The kernel is issue-bound unless the per-request instruction count is
+// small (ncu r01: 21 instr/request -> 82% issue-active at 5.5 TB/s), so the
+// hot loop is: VIMNMX, IADD, SHF (cell), LDS.U8 (bin), LEA (slot), ATOMS x2.
 #include <algorithm>
 #include <cstdio>
 #include "internal.cuh"
@@ -38,17 +45,42 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
   return r;
 }
 
+struct K1Ctx {
+  const unsigned char *lut;  // LUT bytes (or the edge list in binary-search mode)
+  unsigned char *hist;       // R = 32: [nbins][W][32] u32 (W = 1 cnt, 2 cnt|mass, 3 cnt|lo|hi)
+                             // R = 1:  [nbins][W] u32
+  unsigned long long *acc;   // [nbins] u64 mass accumulator
+  uint32_t clampv;           // e_max + 1
+  uint32_t round;            // 2^s - 1
+  uint32_t shift;            // s
+  uint32_t n_edges;
+  uint32_t lane4;            // lane * 4 (R = 32) or 0
+};
+
+template <int R, bool SPLIT, bool MASS>
+struct Layout {
+  static constexpr uint32_t W = MASS ? (SPLIT ? 3u : 2u) : 1u;   // u32 words per slot kind
+  static constexpr uint32_t kStride = (R == 32) ? 128u : 4u;     // bytes between kinds
+  static_assert(kStride == 128u || kStride == 4u, "");
+  static constexpr uint32_t kBinShift = (R == 32) ? (W == 1 ? 7 : W == 2 ? 8 : 0) : (W == 1 ? 2 : W == 2 ? 3 : 0);
+  __device__ static __forceinline__ uint32_t bin_off(uint32_t b) {
+    if constexpr (kBinShift) return b << kBinShift;
+    else return b * (W * kStride);
+  }
+};
+
 // bin = #{e in E : e < L}
 template <int LUTW>
-__device__ __forceinline__ uint32_t bin_of(uint32_t L, const unsigned char *lut, const uint32_t *edges,
-                                           uint32_t shift, uint32_t cell_last, uint32_t n_edges) {
-  if (LUTW == 1 || LUTW == 2) {
-    uint32_t cell = (L >> shift) + ((L & ((1u << shift) - 1u)) != 0u);   // ceil(L / 2^s), no overflow
-    cell = min(cell, cell_last);
-    return LUTW == 1 ? (uint32_t)lut[cell] : (uint32_t)reinterpret_cast<const uint16_t *>(lut)[cell];
+__device__ __forceinline__ uint32_t bin_of(const K1Ctx &c, uint32_t L) {
+  if constexpr (LUTW == 1 || LUTW == 2) {
+    // plan guarantees e_max + 2^s <= 2^32 - 1, so this cannot overflow
+    const uint32_t cell = (min(L, c.clampv) + c.round) >> c.shift;
+    if constexpr (LUTW == 1) return (uint32_t)c.lut[cell];
+    else return (uint32_t)reinterpret_cast<const uint16_t *>(c.lut)[cell];
   } else {
     // binary search (large or irregular edge sets): lower_bound of L in E
-    uint32_t lo = 0, n = n_edges;
+    const uint32_t *edges = reinterpret_cast<const uint32_t *>(c.lut);
+    uint32_t lo = 0, n = c.n_edges;
     while (n > 0) {
       uint32_t half = n >> 1;
       if (edges[lo + half] < L) { lo += half + 1; n -= half + 1; } else { n = half; }
@@ -57,50 +89,58 @@ __device__ __forceinline__ uint32_t bin_of(uint32_t L, const unsigned char *lut,
   }
 }
 
-struct K1Smem {
-  unsigned char *lut;     // LUT bytes (or edges in binary-search mode)
-  uint32_t *cnt;          // [nbins * R]
-  uint32_t *m_lo;         // [nbins * R]
-  uint32_t *m_hi;         // [nbins * R] (split mode)
-  unsigned long long *acc;  // [nbins] u64 mass accumulator
-};
-
-template <int R, bool SPLIT>
-__device__ __forceinline__ void flush_mass(const K1Smem &s, uint32_t nbins) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  if (R == 32) {
-    for (uint32_t j = warp; j < nbins; j += nw) {
-      unsigned long long v = s.m_lo[j * 32 + lane];
-      if (SPLIT) v += (unsigned long long)s.m_hi[j * 32 + lane] << 16;
-      s.m_lo[j * 32 + lane] = 0;
-      if (SPLIT) s.m_hi[j * 32 + lane] = 0;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) s.acc[j] += v;
-    }
-  } else {
-    for (uint32_t j = threadIdx.x; j < nbins; j += blockDim.x) {
-      unsigned long long v = s.m_lo[j];
-      if (SPLIT) v += (unsigned long long)s.m_hi[j] << 16;
-      s.m_lo[j] = 0;
-      if (SPLIT) s.m_hi[j] = 0;
-      s.acc[j] += v;
+template <int LUTW, int R, bool SPLIT, bool MASS>
+__device__ __forceinline__ void add_one(const K1Ctx &c, uint32_t L) {
+  using Ly = Layout<R, SPLIT, MASS>;
+  const uint32_t b = bin_of<LUTW>(c, L);
+  unsigned char *slot = c.hist + Ly::bin_off(b) + c.lane4;
+  atomicAdd(reinterpret_cast<uint32_t *>(slot), 1u);
+  if constexpr (MASS) {
+    if constexpr (SPLIT) {
+      atomicAdd(reinterpret_cast<uint32_t *>(slot + Ly::kStride), L & 0xFFFFu);
+      atomicAdd(reinterpret_cast<uint32_t *>(slot + 2 * Ly::kStride), L >> 16);
+    } else {
+      atomicAdd(reinterpret_cast<uint32_t *>(slot + Ly::kStride), L);
     }
   }
 }
 
 template <int LUTW, int R, bool SPLIT, bool MASS>
-__device__ __forceinline__ void add_one(const K1Smem &s, uint32_t L, uint32_t lane, uint32_t shift,
-                                        uint32_t cell_last, uint32_t n_edges, const uint32_t *edges) {
-  const uint32_t b = bin_of<LUTW>(L, s.lut, edges, shift, cell_last, n_edges);
-  const uint32_t slot = (R == 32) ? b * 32 + lane : b;
-  atomicAdd(&s.cnt[slot], 1u);
-  if (MASS && b < n_edges) {     // mass above the last edge is never used
-    if (SPLIT) {
-      atomicAdd(&s.m_lo[slot], L & 0xFFFFu);
-      atomicAdd(&s.m_hi[slot], L >> 16);
-    } else {
-      atomicAdd(&s.m_lo[slot], L);
+__device__ __forceinline__ void add_four(const K1Ctx &c, const uint4 &v) {
+  add_one<LUTW, R, SPLIT, MASS>(c, v.x);
+  add_one<LUTW, R, SPLIT, MASS>(c, v.y);
+  add_one<LUTW, R, SPLIT, MASS>(c, v.z);
+  add_one<LUTW, R, SPLIT, MASS>(c, v.w);
+}
+
+template <int R, bool SPLIT>
+__device__ __forceinline__ void flush_mass(const K1Ctx &c, uint32_t nbins) {
+  using Ly = Layout<R, SPLIT, true>;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if constexpr (R == 32) {
+    for (uint32_t j = warp; j < nbins; j += nw) {
+      uint32_t *lo = reinterpret_cast<uint32_t *>(c.hist + Ly::bin_off(j) + Ly::kStride) + lane;
+      unsigned long long v = *lo;
+      *lo = 0;
+      if constexpr (SPLIT) {
+        uint32_t *hi = lo + 32;
+        v += (unsigned long long)*hi << 16;
+        *hi = 0;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) c.acc[j] += v;
+    }
+  } else {
+    for (uint32_t j = threadIdx.x; j < nbins; j += blockDim.x) {
+      uint32_t *lo = reinterpret_cast<uint32_t *>(c.hist + Ly::bin_off(j) + Ly::kStride);
+      unsigned long long v = *lo;
+      *lo = 0;
+      if constexpr (SPLIT) {
+        v += (unsigned long long)lo[1] << 16;
+        lo[1] = 0;
+      }
+      c.acc[j] += v;
     }
   }
 }
@@ -109,93 +149,90 @@ template <int LUTW, int R, bool SPLIT, bool MASS>
 __global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
-  K1Smem s;
-  uint32_t lut_bytes;
-  if (LUTW == 0) lut_bytes = a.n_edges * 4;
-  else lut_bytes = a.lut_cells * LUTW;
+  uint32_t lut_bytes = (LUTW == 0) ? a.n_edges * 4 : a.lut_cells * LUTW;
   lut_bytes = (lut_bytes + 15u) & ~15u;
-  s.lut = smem;
-  s.acc = reinterpret_cast<unsigned long long *>(smem + lut_bytes);
-  s.cnt = reinterpret_cast<uint32_t *>(s.acc + nbins);
-  s.m_lo = s.cnt + nbins * R;
-  s.m_hi = s.m_lo + nbins * R;
+  K1Ctx c;
+  c.lut = smem;
+  c.acc = reinterpret_cast<unsigned long long *>(smem + lut_bytes);
+  c.hist = reinterpret_cast<unsigned char *>(c.acc + nbins);
+  c.clampv = a.max_edge + 1u;
+  c.round = (1u << a.shift) - 1u;
+  c.shift = a.shift;
+  c.n_edges = a.n_edges;
+  c.lane4 = (R == 32) ? (threadIdx.x & 31u) * 4u : 0u;
 
   // stage the LUT (or the edge list) and clear the histogram
   {
     const uint32_t *src = (LUTW == 0) ? a.edges : reinterpret_cast<const uint32_t *>(a.lut);
-    uint32_t *dst = reinterpret_cast<uint32_t *>(s.lut);
-    for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) {
-      // the device LUT allocation is padded to 16 B inside the table blob
-      dst[i] = src[i];
-    }
-    for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) s.acc[i] = 0ull;
+    uint32_t *dst = reinterpret_cast<uint32_t *>(smem);
+    // the device tables are padded to 16 B inside the plan's table blob
+    for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) dst[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) c.acc[i] = 0ull;
     const uint32_t words = nbins * R * (MASS ? (SPLIT ? 3u : 2u) : 1u);
-    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) s.cnt[i] = 0u;
+    uint32_t *h = reinterpret_cast<uint32_t *>(c.hist);
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) h[i] = 0u;
   }
   __syncthreads();
-  const uint32_t *edges = reinterpret_cast<const uint32_t *>(s.lut);
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t shift = a.shift, cell_last = a.lut_cells ? a.lut_cells - 1 : 0, ne = a.n_edges;
 
   // misaligned head (< 4 elements) and the aligned uint4 body
   const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.len) & 15u) >> 2);
   const uint64_t head = mis ? umin64(a.n, 4u - mis) : 0u;
   const uint64_t n4 = (a.n - head) >> 2;                       // uint4 count of the body
   const uint64_t tail_first = head + (n4 << 2);
-  if (blockIdx.x == 0 && threadIdx.x < head)
-    add_one<LUTW, R, SPLIT, MASS>(s, a.len[threadIdx.x], lane, shift, cell_last, ne, edges);
+  if (blockIdx.x == 0 && threadIdx.x < head) add_one<LUTW, R, SPLIT, MASS>(c, a.len[threadIdx.x]);
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first)
-    add_one<LUTW, R, SPLIT, MASS>(s, a.len[tail_first + threadIdx.x], lane, shift, cell_last, ne, edges);
+    add_one<LUTW, R, SPLIT, MASS>(c, a.len[tail_first + threadIdx.x]);
 
   const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
   const uint64_t tile4 = (uint64_t)blockDim.x * kUnroll;     // uint4 per tile
+  const uint64_t full_tiles = n4 / tile4;
   const uint64_t ntiles = (n4 + tile4 - 1) / tile4;
   uint32_t since_flush = 0;
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const uint64_t base = t * tile4 + threadIdx.x;
-    uint4 v[kUnroll];
+    const uint4 *p = body + t * tile4 + threadIdx.x;
+    if (t < full_tiles) {
+      uint4 v[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t i = base + (uint64_t)u * blockDim.x;
-      v[u] = i < n4 ? ldg_stream(body + i) : make_uint4(0u, 0u, 0u, 0u);
-    }
+      for (int u = 0; u < kUnroll; ++u) v[u] = ldg_stream(p + u * blockDim.x);
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (base + (uint64_t)u * blockDim.x < n4) {
-        add_one<LUTW, R, SPLIT, MASS>(s, v[u].x, lane, shift, cell_last, ne, edges);
-        add_one<LUTW, R, SPLIT, MASS>(s, v[u].y, lane, shift, cell_last, ne, edges);
-        add_one<LUTW, R, SPLIT, MASS>(s, v[u].z, lane, shift, cell_last, ne, edges);
-        add_one<LUTW, R, SPLIT, MASS>(s, v[u].w, lane, shift, cell_last, ne, edges);
-      }
+      for (int u = 0; u < kUnroll; ++u) add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
+    } else {
+      const uint64_t base = t * tile4 + threadIdx.x;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+        if (base + (uint64_t)u * blockDim.x < n4) add_four<LUTW, R, SPLIT, MASS>(c, ldg_stream(p + u * blockDim.x));
     }
     if (MASS && ++since_flush == a.flush_iters) {
       since_flush = 0;
       __syncthreads();
-      flush_mass<R, SPLIT>(s, nbins);
+      flush_mass<R, SPLIT>(c, nbins);
       __syncthreads();
     }
   }
   __syncthreads();
   if (MASS) {
-    flush_mass<R, SPLIT>(s, nbins);
+    flush_mass<R, SPLIT>(c, nbins);
     __syncthreads();
   }
-  // fold replicas and publish this block's histogram
-  if (R == 32) {
-    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // fold replicas and publish this block's histogram (mass of the last bin,
+  // above every edge, is not part of the result)
+  using Ly = Layout<R, SPLIT, MASS>;
+  if constexpr (R == 32) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (uint32_t j = warp; j < nbins; j += nw) {
-      unsigned long long c = s.cnt[j * 32 + lane];
+      unsigned long long v = reinterpret_cast<const uint32_t *>(c.hist + Ly::bin_off(j))[lane];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0) {
-        if (c) atomicAdd(a.g_cnt + j, c);
-        if (MASS && s.acc[j]) atomicAdd(a.g_mass + j, s.acc[j]);
+        if (v) atomicAdd(a.g_cnt + j, v);
+        if (MASS && j < a.n_edges && c.acc[j]) atomicAdd(a.g_mass + j, c.acc[j]);
       }
     }
   } else {
     for (uint32_t j = threadIdx.x; j < nbins; j += blockDim.x) {
-      if (s.cnt[j]) atomicAdd(a.g_cnt + j, (unsigned long long)s.cnt[j]);
-      if (MASS && s.acc[j]) atomicAdd(a.g_mass + j, s.acc[j]);
+      const uint32_t v = *reinterpret_cast<const uint32_t *>(c.hist + Ly::bin_off(j));
+      if (v) atomicAdd(a.g_cnt + j, (unsigned long long)v);
+      if (MASS && j < a.n_edges && c.acc[j]) atomicAdd(a.g_mass + j, c.acc[j]);
     }
   }
 }
@@ -289,113 +326,6 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
-}
-
-// ============================== K4: route_batch ===================================
-// Alg. 1 for one (B, C_S, C_L): 16 requests per thread per step
-// (4 x 128-bit loads in, one 128-bit store of 16 decision bytes out), counts in
-// registers, one warp/block reduction and 5 global atomics per block.
-namespace {
-
-__device__ __forceinline__ uint32_t decide(uint32_t L, uint32_t B, uint32_t CS, uint32_t CL) {
-  if (L > CL) return 2u | (3u << 2);          // rejected (R3)
-  if (L > CS) return 1u | (1u << 2);          // step 1: feasibility
-  uint32_t p = (L <= B) ? 0u : 1u;            // step 2: budget
-  // step 3 (spillover) is out of scope; final safety check:
-  if (L > (p == 0u ? CS : CL)) return 1u | (2u << 2);
-  return p;
-}
-
-struct RouteAcc {
-  uint32_t ns = 0, nl = 0, nr = 0;
-  unsigned long long ms = 0, ml = 0;
-  __device__ __forceinline__ uint32_t add(uint32_t L, uint32_t B, uint32_t CS, uint32_t CL) {
-    uint32_t d = decide(L, B, CS, CL);
-    uint32_t p = d & 3u;
-    ns += p == 0u;
-    nl += p == 1u;
-    nr += p == 2u;
-    ms += p == 0u ? L : 0u;
-    ml += p == 1u ? L : 0u;
-    return d;
-  }
-};
-
-template <bool DEC>
-__global__ void __launch_bounds__(256) k4_route(RouteArgs a) {
-  RouteAcc acc;
-  // align the 16-element groups to the decision buffer (or to len without one)
-  const uintptr_t anchor = DEC ? reinterpret_cast<uintptr_t>(a.decision) : reinterpret_cast<uintptr_t>(a.len) >> 2;
-  const uint64_t head = umin64(a.n, (16u - (uint32_t)(anchor & 15u)) & 15u);
-  const uint64_t groups = (a.n - head) >> 4;
-  const uint64_t tail_first = head + (groups << 4);
-  const bool vec_in = ((reinterpret_cast<uintptr_t>(a.len + head)) & 15u) == 0u;
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t nthr = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t g = tid; g < groups; g += nthr) {
-    const uint64_t e0 = head + (g << 4);
-    uint32_t L[16];
-    if (vec_in) {
-      const uint4 *p = reinterpret_cast<const uint4 *>(a.len + e0);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 v = ldg_stream(p + q);
-        L[4 * q] = v.x; L[4 * q + 1] = v.y; L[4 * q + 2] = v.z; L[4 * q + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 16; ++q) L[q] = __ldg(a.len + e0 + q);
-    }
-    uint32_t w[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      w[q] = 0;
-#pragma unroll
-      for (int r = 0; r < 4; ++r) w[q] |= acc.add(L[4 * q + r], a.b, a.cs, a.cl) << (8 * r);
-    }
-    if (DEC) *reinterpret_cast<uint4 *>(a.decision + e0) = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-  // head and tail (< 16 each)
-  if (tid < head) {
-    uint32_t d = acc.add(a.len[tid], a.b, a.cs, a.cl);
-    if (DEC) a.decision[tid] = (uint8_t)d;
-  }
-  if (tid < a.n - tail_first) {
-    const uint64_t i = tail_first + tid;
-    uint32_t d = acc.add(a.len[i], a.b, a.cs, a.cl);
-    if (DEC) a.decision[i] = (uint8_t)d;
-  }
-  // reduce: warp shuffles, then one atomic per warp
-  unsigned long long v[5] = {acc.ns, acc.nl, acc.nr, acc.ms, acc.ml};
-#pragma unroll
-  for (int k = 0; k < 5; ++k) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
-  }
-  __shared__ unsigned long long red[5][8];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < 5; ++k) red[k][w] = v[k];
-  }
-  __syncthreads();
-  if (threadIdx.x < 5) {
-    unsigned long long t = 0;
-    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += red[threadIdx.x][j];
-    if (t) atomicAdd(a.g_counts + threadIdx.x, t);
-  }
-}
-
-}  // namespace
-
-cudaError_t launch_route(const RouteArgs &a, int grid, int block, cudaStream_t s) {
-  if (a.n == 0) return cudaSuccess;
-  const uint64_t groups = a.n / 16 + 1;
-  const uint64_t need = (groups + block - 1) / block;
-  const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
-  if (a.decision) k4_route<true><<<g, block, 0, s>>>(a);
-  else k4_route<false><<<g, block, 0, s>>>(a);
-  return cudaGetLastError();
 }
 
 }  // namespace fp

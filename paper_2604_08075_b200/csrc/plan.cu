@@ -246,7 +246,11 @@ fp_status build_tables(fp_plan *p) {
   for (uint32_t e : p->edges) s = std::min<uint32_t>(s, (uint32_t)__builtin_ctz(e));
   p->shift = s;
   uint64_t cell_max = p->max_edge >> s;
-  p->lut_cells = (cell_max + 2 <= (uint64_t)kLutMaxCells) ? (uint32_t)(cell_max + 2) : 0;
+  // LUT mode needs a small table and e_max + 2^s < 2^32 (K1 computes
+  // ceil(min(L, e_max + 1) / 2^s) in 32 bits); otherwise binary search over E
+  const bool lut_ok = cell_max + 2 <= (uint64_t)kLutMaxCells &&
+                      (uint64_t)p->max_edge + (1ull << s) <= 0xFFFFFFFFull;
+  p->lut_cells = lut_ok ? (uint32_t)(cell_max + 2) : 0;
   p->lut_u8 = p->nbins <= 256;
   // window / edge index maps
   p->n_cs_eff = p->cs.empty() ? 1 : (uint32_t)p->cs.size();
@@ -426,8 +430,8 @@ fp_status configure_launch(fp_plan *p) {
   int per_sm = 0;
   CUDA_TRY(p, trace_occupancy(p->ta, p->k1_block, p->k1_smem, &per_sm), "occupancy");
   p->k1_grid = p->sm_count * std::max(1, per_sm);
-  p->k4_block = 256;
-  p->k4_grid = p->sm_count * 8;
+  p->k4_block = 512;
+  p->k4_grid = p->sm_count * 4;   // 2,048 threads per SM, 64 B in flight per thread
   CUDA_TRY(p, eval_prepare(), "k3 attributes");
   return FP_OK;
 }
