@@ -10,12 +10,12 @@
 // Alg. 1 can only fire after a spillover, which a static trace does not
 // have; under B <= C_S its condition is never true.)
 //
-// Memory pattern as K1: per block and step a contiguous tile of blockDim x 4
-// uint4 (coalesced: lane i reads the i-th 16 B of each warp's 512 B), and per
-// uint4 one 32-bit store of its 4 decision bytes (a warp stores 128 B
-// contiguous). Counts live in registers (short = !a, served = !c), masses
-// are summed per tile in u32 (16 requests x L <= C_L < 2^28: exact) and
-// then in u64; one warp/block reduction and 5 global atomics per block.
+// Memory pattern: per-block tiles of 128-bit loads (coalesced: lane i reads
+// the i-th 16 B of each warp's 512 B), and per uint4 one streaming
+// 32-bit store of its 4 decision bytes (a warp stores 128 B contiguous).
+// Counts live in registers (short = !a, served = !c), masses are summed per
+// step in u32 (16 requests x L <= C_L < 2^28: exact) and then in u64; one
+// warp/block reduction and 5 global atomics per block.
 #include <algorithm>
 #include "internal.cuh"
 
@@ -92,7 +92,9 @@ template <bool DEC, bool DVEC>
 __device__ __forceinline__ void store4(uint8_t *dec, uint32_t w) {
   if constexpr (DEC) {
     if constexpr (DVEC) {
-      *reinterpret_cast<uint32_t *>(dec) = w;
+      // streaming store (evict-first): 6.9 vs 6.4 TB/s for this 4:1 mix
+      // (profiles/r01_microbench_route_variants.txt)
+      asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(dec), "r"(w) : "memory");
     } else {
       dec[0] = (uint8_t)w; dec[1] = (uint8_t)(w >> 8); dec[2] = (uint8_t)(w >> 16); dec[3] = (uint8_t)(w >> 24);
     }
@@ -120,6 +122,9 @@ __global__ void __launch_bounds__(512) k4_route(RouteArgs a) {
   }
   const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
   uint8_t *dbody = DEC ? a.decision + head : nullptr;
+  // per-block contiguous tiles of blockDim x kUnroll uint4 (for this 4:1
+  // read/write mix tiles beat grid-stride stripes: 0.89 vs 0.97 ms on C5,
+  // profiles/r01_tune_launch_*.txt)
   const uint64_t tile4 = (uint64_t)blockDim.x * kUnroll;
   const uint64_t full_tiles = n4 / tile4;
   const uint64_t ntiles = (n4 + tile4 - 1) / tile4;

@@ -108,6 +108,9 @@ struct fp_plan {
   uint32_t *d_stage[2] = {nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  // pinned host mirrors
+  fp_candidate *h_best = nullptr;          // [world][n_models]
+  unsigned long long *h_small = nullptr;   // [2 * nbins + 8]: hist, route counts
   // NCCL
   NcclComm comm = nullptr;
   // per-kernel event timing (FP_FLAG_KERNEL_TIMING)
@@ -422,17 +425,35 @@ fp_status upload(fp_plan *p) {
 
 fp_status configure_launch(fp_plan *p) {
   CUDA_TRY(p, cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device), "attr");
+  // tuning knobs (measurement only; defaults are the measured best on B200)
+  auto env_int = [](const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+  };
   p->ta.flush_iters = 1;  // set per launch by launch_trace's smem config
-  p->k1_block = 512;
+  p->k1_block = env_int("FP_K1_BLOCK", 512);
+  if (p->k1_block < 64 || p->k1_block > 512 || (p->k1_block & 31))
+    return fail(p, FP_ERR_CONFIG, "FP_K1_BLOCK must be a multiple of 32 in [64, 512]");
   p->k1_smem = trace_smem_bytes(p->ta, p->k1_block);
   if (p->k1_smem > 200 * 1024)
     return fail(p, FP_ERR_CONFIG, "trace-pass shared memory %zu B too large", p->k1_smem);
   int per_sm = 0;
   CUDA_TRY(p, trace_occupancy(p->ta, p->k1_block, p->k1_smem, &per_sm), "occupancy");
+  // 3 x 512 threads per SM measured best for the grid-stride trace pass
+  // (C5: 0.592 ms at 3, 0.605 at 4, 0.667 at 2; profiles/r01_tune_launch_*)
+  const int k1_bps = env_int("FP_K1_BLOCKS_PER_SM", 3);
+  if (k1_bps > 0) per_sm = std::min(per_sm, k1_bps);
   p->k1_grid = p->sm_count * std::max(1, per_sm);
-  p->k4_block = 512;
-  p->k4_grid = p->sm_count * 4;   // 2,048 threads per SM, 64 B in flight per thread
+  p->k4_block = env_int("FP_K4_BLOCK", 512);
+  if (p->k4_block < 64 || p->k4_block > 512 || (p->k4_block & 31))
+    return fail(p, FP_ERR_CONFIG, "FP_K4_BLOCK must be a multiple of 32 in [64, 512]");
+  // default: 2,048 threads per SM, 64 B in flight per thread
+  p->k4_grid = p->sm_count * env_int("FP_K4_BLOCKS_PER_SM", 2048 / p->k4_block);
   CUDA_TRY(p, eval_prepare(), "k3 attributes");
+  // pinned host mirrors for the small synchronous results
+  CUDA_TRY(p, cudaMallocHost(&p->h_best, (size_t)p->world * p->models.size() * sizeof(fp_candidate)),
+           "cudaMallocHost best");
+  CUDA_TRY(p, cudaMallocHost(&p->h_small, (2ull * p->nbins + 8) * 8), "cudaMallocHost small");
   return FP_OK;
 }
 
@@ -632,6 +653,8 @@ void fleet_plan_destroy(fp_plan *p) {
       if (p->ev_used[i]) cudaEventDestroy(p->ev_used[i]);
     }
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+    if (p->h_best) cudaFreeHost(p->h_best);
+    if (p->h_small) cudaFreeHost(p->h_small);
     for (auto &t : p->timers)
       for (auto &pr : t.ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     cudaGetLastError();
@@ -718,8 +741,8 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
   }
   p->last_stream = s;
   if (h_counts) {
-    unsigned long long c[5];
-    CUDA_TRY(p, cudaMemcpyAsync(c, p->d_rcounts, sizeof c, cudaMemcpyDeviceToHost, s), "D2H counts");
+    unsigned long long *c = p->h_small + 2ull * p->nbins;
+    CUDA_TRY(p, cudaMemcpyAsync(c, p->d_rcounts, 5 * 8, cudaMemcpyDeviceToHost, s), "D2H counts");
     CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
     h_counts->n_short = c[0];
     h_counts->n_long = c[1];
@@ -797,16 +820,17 @@ fp_status best_split(fp_plan *p, fp_candidate *h_best) {
   DeviceGuard g(p->device);
   const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
   const size_t M = p->models.size();
-  std::vector<fp_candidate> recs((size_t)ranks * M);
-  unsigned long long total = 0;
+  const size_t nrec = (size_t)ranks * M;
+  // records and the per-bin counts in one stream-ordered round trip (pinned)
+  CUDA_TRY(p, cudaMemcpyAsync(p->h_best, p->d_best, nrec * sizeof(fp_candidate), cudaMemcpyDeviceToHost,
+                              p->last_stream), "D2H best");
+  CUDA_TRY(p, cudaMemcpyAsync(p->h_small, p->d_hist, p->nbins * 8, cudaMemcpyDeviceToHost, p->last_stream),
+           "D2H hist");
   CUDA_TRY(p, cudaStreamSynchronize(p->last_stream), "sync");
-  CUDA_TRY(p, cudaMemcpy(recs.data(), p->d_best, recs.size() * sizeof(fp_candidate), cudaMemcpyDeviceToHost),
-           "D2H best");
-  std::vector<unsigned long long> cnt(p->nbins);
-  CUDA_TRY(p, cudaMemcpy(cnt.data(), p->d_hist, p->nbins * 8, cudaMemcpyDeviceToHost), "D2H hist");
-  for (auto c : cnt) total += c;
+  unsigned long long total = 0;
+  for (uint32_t j = 0; j < p->nbins; ++j) total += p->h_small[j];
   if (total == 0) return fail(p, FP_ERR_EMPTY_TRACE, "global trace is empty");
-  fp_merge_best(recs.data(), ranks, (uint32_t)M, h_best);
+  fp_merge_best(p->h_best, ranks, (uint32_t)M, h_best);
   return FP_OK;
 }
 
