@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfleetplan.so")
+LIB_PATH = os.environ.get("FLEETPLAN_LIB") or os.path.join(_HERE, "lib", "libfleetplan.so")
 
 FP_ABI_VERSION = 1
 FP_FLAG_NO_MASS = 0x1

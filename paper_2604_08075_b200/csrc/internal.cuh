@@ -40,6 +40,7 @@ struct RouteArgs {
   unsigned long long *g_counts;  // [5]
 };
 cudaError_t launch_route(const RouteArgs &a, int grid, int block, cudaStream_t s);
+cudaError_t route_occupancy(int block, int *per_sm);
 
 // ---- K3: candidate evaluation + argmin ---------------------------------------
 struct BlockBest { double cost; uint32_t index; uint32_t valid; };

@@ -104,7 +104,7 @@ __device__ __forceinline__ void store4(uint8_t *dec, uint32_t w) {
 // DEC: write decisions; SMALL: C_L < 2^28 (u32 tile masses); DVEC: the
 // decision address of every uint4 of the body is 4-byte aligned.
 template <bool DEC, bool SMALL, bool DVEC>
-__global__ void __launch_bounds__(512) k4_route(RouteArgs a) {
+__global__ void __launch_bounds__(512, 4) k4_route(RouteArgs a) {
   const uint32_t B = a.b, CS = a.cs, CL = a.cl;
   Acc acc;
   const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.len) & 15u) >> 2);
@@ -178,6 +178,27 @@ __global__ void __launch_bounds__(512) k4_route(RouteArgs a) {
 }
 
 }  // namespace
+
+// Resident blocks per SM guaranteed for every K4 variant: the grid is
+// persistent (tiles are strided over it), so it must not exceed what is
+// resident at once -- a second partial wave costs ~20% on C5.
+cudaError_t route_occupancy(int block, int *per_sm) {
+  void *ks[] = {reinterpret_cast<void *>(&k4_route<true, true, true>),
+                reinterpret_cast<void *>(&k4_route<true, true, false>),
+                reinterpret_cast<void *>(&k4_route<true, false, true>),
+                reinterpret_cast<void *>(&k4_route<true, false, false>),
+                reinterpret_cast<void *>(&k4_route<false, true, false>),
+                reinterpret_cast<void *>(&k4_route<false, false, false>)};
+  int best = 1 << 30;
+  for (void *k : ks) {
+    int n = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, block, 0);
+    if (e != cudaSuccess) return e;
+    best = std::min(best, n);
+  }
+  *per_sm = std::max(1, best);
+  return cudaSuccess;
+}
 
 cudaError_t launch_route(const RouteArgs &a0, int grid, int block, cudaStream_t s) {
   if (a0.n == 0) return cudaSuccess;

@@ -447,8 +447,11 @@ fp_status configure_launch(fp_plan *p) {
   p->k4_block = env_int("FP_K4_BLOCK", 512);
   if (p->k4_block < 64 || p->k4_block > 512 || (p->k4_block & 31))
     return fail(p, FP_ERR_CONFIG, "FP_K4_BLOCK must be a multiple of 32 in [64, 512]");
-  // default: 2,048 threads per SM, 64 B in flight per thread
-  p->k4_grid = p->sm_count * env_int("FP_K4_BLOCKS_PER_SM", 2048 / p->k4_block);
+  // persistent grid = every block resident (4 x 512 threads per SM with
+  // __launch_bounds__(512, 4); profiles/r01_tune_k4.txt)
+  int k4_res = 1;
+  CUDA_TRY(p, route_occupancy(p->k4_block, &k4_res), "k4 occupancy");
+  p->k4_grid = p->sm_count * std::min(k4_res, env_int("FP_K4_BLOCKS_PER_SM", k4_res));
   CUDA_TRY(p, eval_prepare(), "k3 attributes");
   // pinned host mirrors for the small synchronous results
   CUDA_TRY(p, cudaMallocHost(&p->h_best, (size_t)p->world * p->models.size() * sizeof(fp_candidate)),
