@@ -117,9 +117,25 @@ typedef struct fp_plan_desc {
   double hours_per_year;          /* cost horizon (R7), > 0                          */
   int32_t device;                 /* CUDA device ordinal for this rank               */
   int32_t rank, world;            /* 0 <= rank < world                               */
-  const void *nccl_unique_id;     /* 128-byte ncclUniqueId, same on all ranks;
-                                     NULL iff world == 1                             */
+  const void *nccl_unique_id;     /* 128-byte ncclUniqueId, same on all ranks; used
+                                     iff world > 1 and collectives == NULL           */
+  const struct fp_collectives *collectives; /* optional host-side collectives that
+                                     replace NCCL when world > 1 (NULL = NCCL)        */
 } fp_plan_desc;
+
+/* Host-side collective hooks (e.g. MPI or a CPU process group). When given,
+ * the library synchronizes the stream, copies the operand to pinned host
+ * memory, calls the hook, and copies the result back; NCCL is not used.
+ * Every rank must call the hooks in the same order (collective semantics).
+ * Each returns 0 on success; anything else fails the call with FP_ERR_NCCL.
+ * The struct is copied at fleet_plan_create; `user` must outlive the plan. */
+typedef struct fp_collectives {
+  /* in place: hbuf[i] = sum over ranks of hbuf[i], i < count */
+  int (*allreduce_sum_u64)(uint64_t *hbuf, uint64_t count, void *user);
+  /* hrecv[r * bytes .. (r + 1) * bytes) = rank r's hsend[0 .. bytes) */
+  int (*allgather_bytes)(const void *hsend, void *hrecv, uint64_t bytes, void *user);
+  void *user;
+} fp_collectives;
 
 /* ---- outputs -------------------------------------------------------------- */
 

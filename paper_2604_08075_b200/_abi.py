@@ -50,6 +50,14 @@ class fp_grid(ctypes.Structure):
                 ("c_long", ctypes.POINTER(c_u32)), ("n_cl", c_u32)]
 
 
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(c_u64), c_u64, c_vp)
+ALLGATHER_FN = ctypes.CFUNCTYPE(ctypes.c_int, c_vp, c_vp, c_u64, c_vp)
+
+
+class fp_collectives(ctypes.Structure):
+    _fields_ = [("allreduce_sum_u64", ALLREDUCE_FN), ("allgather_bytes", ALLGATHER_FN), ("user", c_vp)]
+
+
 class fp_plan_desc(ctypes.Structure):
     _fields_ = [("abi_version", c_u32), ("flags", c_u32),
                 ("models", ctypes.POINTER(fp_model)), ("n_models", c_u32),
@@ -60,7 +68,8 @@ class fp_plan_desc(ctypes.Structure):
                 ("mu_table", ctypes.POINTER(c_dbl)),
                 ("hours_per_year", c_dbl),
                 ("device", c_i32), ("rank", c_i32), ("world", c_i32),
-                ("nccl_unique_id", c_vp)]
+                ("nccl_unique_id", c_vp),
+                ("collectives", ctypes.POINTER(fp_collectives))]
 
 
 class fp_route_counts(ctypes.Structure):
@@ -144,10 +153,11 @@ def _u32(a):
 class FleetPlan:
     """Owner of an fp_plan* (destroyed with fleet_plan_destroy)."""
 
-    def __init__(self, handle, n_models, device):
+    def __init__(self, handle, n_models, device, keepalive=None):
         self.handle = handle
         self.n_models = n_models
         self.device = device
+        self._keepalive = keepalive     # ctypes callbacks of host collectives
 
     def __del__(self):
         try:
@@ -169,7 +179,10 @@ def desc_from_config(cfg):
 
 
 def fleet_plan_create(*, models, gpus, deploy, b_short, c_short, c_long, windows, mu_table,
-                      hours_per_year=8760.0, device=0, rank=0, world=1, nccl_unique_id=None, flags=0):
+                      hours_per_year=8760.0, device=0, rank=0, world=1, nccl_unique_id=None, flags=0,
+                      collectives=None):
+    """collectives: optional object with allreduce_sum_u64(np.ndarray[uint64]) (in place) and
+    allgather_bytes(bytes) -> bytes (rank order); replaces NCCL when world > 1."""
     nm, ng = len(models), len(gpus)
     M = (fp_model * nm)(*[fp_model(n.encode()[:31], *a) for (n, *a) in models])
     G = (fp_gpu * ng)(*[fp_gpu(n.encode()[:31], *a) for (n, *a) in gpus])
@@ -193,9 +206,30 @@ def fleet_plan_create(*, models, gpus, deploy, b_short, c_short, c_long, windows
     if nccl_unique_id is not None:
         uid = ctypes.create_string_buffer(bytes(nccl_unique_id), 128)
         desc.nccl_unique_id = ctypes.cast(uid, c_vp)
+    keep = None
+    if collectives is not None:
+        def _ar(buf, count, user):
+            try:
+                a = np.ctypeslib.as_array(buf, shape=(count,))
+                collectives.allreduce_sum_u64(a)
+                return 0
+            except Exception:
+                return 1
+
+        def _ag(hsend, hrecv, nbytes, user):
+            try:
+                data = ctypes.string_at(hsend, nbytes)
+                out = collectives.allgather_bytes(data)
+                ctypes.memmove(hrecv, out, len(out))
+                return 0
+            except Exception:
+                return 1
+        coll = fp_collectives(ALLREDUCE_FN(_ar), ALLGATHER_FN(_ag), None)
+        desc.collectives = ctypes.pointer(coll)
+        keep = (coll, _ar, _ag)
     h = c_vp()
     _check(lib.fleet_plan_create(ctypes.byref(desc), ctypes.byref(h)))
-    return FleetPlan(h, nm, device)
+    return FleetPlan(h, nm, device, keepalive=keep)
 
 
 def _trace_ptr(lengths):

@@ -113,6 +113,8 @@ struct fp_plan {
   unsigned long long *h_small = nullptr;   // [2 * nbins + 8]: hist, route counts
   // NCCL
   NcclComm comm = nullptr;
+  fp_collectives coll{};                   // host hooks replacing NCCL (optional)
+  bool has_coll = false;
   // per-kernel event timing (FP_FLAG_KERNEL_TIMING)
   struct Timer {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
@@ -180,8 +182,14 @@ fp_status validate_and_copy(fp_plan *p, const fp_plan_desc *d) {
     return fail(p, FP_ERR_CONFIG, "empty models/gpus/grid/windows");
   if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
     return fail(p, FP_ERR_CONFIG, "rank %d world %d", d->rank, d->world);
-  if ((d->world > 1) != (d->nccl_unique_id != nullptr))
-    return fail(p, FP_ERR_CONFIG, "nccl_unique_id must be set iff world > 1");
+  if (d->world > 1 && !d->nccl_unique_id && !d->collectives)
+    return fail(p, FP_ERR_CONFIG, "world > 1 needs nccl_unique_id or collectives");
+  if (d->collectives && (!d->collectives->allreduce_sum_u64 || !d->collectives->allgather_bytes))
+    return fail(p, FP_ERR_CONFIG, "collectives hooks must both be set");
+  if (d->collectives) {
+    p->coll = *d->collectives;
+    p->has_coll = true;
+  }
   if (!(d->hours_per_year > 0.0) || !std::isfinite(d->hours_per_year))
     return fail(p, FP_ERR_CONFIG, "hours_per_year must be finite and > 0");
   p->models.assign(d->models, d->models + d->n_models);
@@ -523,6 +531,34 @@ fp_status over_trace(fp_plan *p, const uint32_t *len, uint64_t n, cudaStream_t s
   return FP_OK;
 }
 
+// ---- the two cross-rank operations of the path (NCCL or host hooks) ----------
+fp_status all_reduce_u64(fp_plan *p, unsigned long long *dbuf, size_t count, cudaStream_t s, const char *what) {
+  if (!p->has_coll)
+    return nccl_check(p, g_nccl.AllReduce(dbuf, dbuf, count, kNcclUint64, kNcclSum, p->comm, s), what);
+  std::vector<uint64_t> h(count);
+  CUDA_TRY(p, cudaMemcpyAsync(h.data(), dbuf, count * 8, cudaMemcpyDeviceToHost, s), what);
+  CUDA_TRY(p, cudaStreamSynchronize(s), what);
+  if (p->coll.allreduce_sum_u64(h.data(), count, p->coll.user) != 0)
+    return fail(p, FP_ERR_NCCL, "%s: collectives hook failed", what);
+  CUDA_TRY(p, cudaMemcpyAsync(dbuf, h.data(), count * 8, cudaMemcpyHostToDevice, s), what);
+  CUDA_TRY(p, cudaStreamSynchronize(s), what);
+  return FP_OK;
+}
+
+fp_status all_gather_bytes(fp_plan *p, const void *dsend, void *drecv, size_t bytes, cudaStream_t s,
+                           const char *what) {
+  if (!p->has_coll)
+    return nccl_check(p, g_nccl.AllGather(dsend, drecv, bytes, kNcclUint8, p->comm, s), what);
+  std::vector<unsigned char> hs(bytes), hr(bytes * (size_t)p->world);
+  CUDA_TRY(p, cudaMemcpyAsync(hs.data(), dsend, bytes, cudaMemcpyDeviceToHost, s), what);
+  CUDA_TRY(p, cudaStreamSynchronize(s), what);
+  if (p->coll.allgather_bytes(hs.data(), hr.data(), bytes, p->coll.user) != 0)
+    return fail(p, FP_ERR_NCCL, "%s: collectives hook failed", what);
+  CUDA_TRY(p, cudaMemcpyAsync(drecv, hr.data(), hr.size(), cudaMemcpyHostToDevice, s), what);
+  CUDA_TRY(p, cudaStreamSynchronize(s), what);
+  return FP_OK;
+}
+
 }  // namespace
 
 // ============================== ABI ==========================================
@@ -617,7 +653,7 @@ fp_status fleet_plan_create(const fp_plan_desc *desc, fp_plan **out) {
     DeviceGuard g(p->device);
     st = upload(p);
     if (st == FP_OK) st = configure_launch(p);
-    if (st == FP_OK && p->world > 1) {
+    if (st == FP_OK && p->world > 1 && !p->has_coll) {
       std::string err;
       if (!load_nccl(g_nccl, err)) {
         st = fail(p, FP_ERR_NCCL, "%s", err.c_str());
@@ -738,8 +774,7 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
   });
   if (st != FP_OK) return st;
   if (p->world > 1) {
-    st = nccl_check(p, g_nccl.AllReduce(p->d_rcounts, p->d_rcounts, 5, kNcclUint64, kNcclSum, p->comm, s),
-                    "ncclAllReduce(route counts)");
+    st = all_reduce_u64(p, p->d_rcounts, 5, s, "all-reduce(route counts)");
     if (st != FP_OK) return st;
   }
   p->last_stream = s;
@@ -780,9 +815,7 @@ fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, 
   if (st != FP_OK) return st;
   // C1: sum the per-rank histograms
   if (p->world > 1) {
-    st = nccl_check(p, g_nccl.AllReduce(p->d_hist, p->d_hist, 2ull * p->nbins, kNcclUint64, kNcclSum,
-                                        p->comm, s),
-                    "ncclAllReduce(histogram)");
+    st = all_reduce_u64(p, p->d_hist, 2ull * p->nbins, s, "all-reduce(histogram)");
     if (st != FP_OK) return st;
   }
   // K2 + K3: scan, evaluate this rank's candidates, per-model argmin
@@ -801,9 +834,8 @@ fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, 
   // C2: gather every rank's per-model best
   if (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) {
     const size_t bytes = p->models.size() * sizeof(fp_candidate);
-    st = nccl_check(p, g_nccl.AllGather(p->d_best + (size_t)p->rank * p->models.size(), p->d_best, bytes,
-                                        kNcclUint8, p->comm, s),
-                    "ncclAllGather(best)");
+    st = all_gather_bytes(p, p->d_best + (size_t)p->rank * p->models.size(), p->d_best, bytes, s,
+                          "all-gather(best)");
     if (st != FP_OK) return st;
   }
   p->have_sweep = true;

@@ -1,0 +1,119 @@
+"""Multi-rank parity on ONE GPU: two processes, each a rank of a world-2 plan
+on cuda:0, with the library's host-collective hooks carried by a gloo process
+group (127.0.0.1) instead of NCCL (which refuses two ranks on one device).
+This runs the whole world > 1 path of libfleetplan.so -- shard-local K1,
+cross-rank histogram sum, candidate slicing, per-rank argmin, all-gather of
+best records, rank-order merge, route count sum -- and compares with the CPU
+oracle on the whole trace. Only the NCCL calls themselves are not covered.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class GlooCollectives:
+    def __init__(self, world):
+        self.world = world
+
+    def allreduce_sum_u64(self, a):
+        import torch.distributed as dist
+        t = torch.from_numpy(a.view(np.int64))
+        dist.all_reduce(t)
+
+    def allgather_bytes(self, data):
+        import torch.distributed as dist
+        arr = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.empty_like(arr) for _ in range(self.world)]
+        dist.all_gather(out, arr)
+        return b"".join(o.numpy().tobytes() for o in out)
+
+
+def _rank(rank, world, port, name, n, flags, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2604_08075_b200 as fp
+        from synth import configs
+        from synth.gen import generate_device
+        cfg = configs.CONFIGS[name]().with_n(n)
+        first, count = fp.fp_shard_range(n, rank, world)
+        d = generate_device(cfg.shape, cfg.seed, first, count) if count else \
+            torch.zeros(0, dtype=torch.int32, device="cuda")
+        plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=0, rank=rank, world=world,
+                                    flags=flags, collectives=GlooCollectives(world))
+        res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+        best = fp.best_split(plan)
+        edges, cnt, mass = fp.sweep_histogram(plan)
+        counts = fp.route_batch(plan, d, 8192, 16384, 65536)
+        info = fp.fleet_plan_info(plan)
+        q.put((rank, res.tobytes(), best.tobytes(), cnt.tobytes(), mass.tobytes(), counts,
+               info["cand_first"], info["cand_count"], None))
+        fp.fleet_plan_destroy(plan)
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put((rank, None, None, None, None, None, 0, 0, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("name,n,replicated", [("C5", 2_000_003, False), ("C3", 300_001, False),
+                                               ("C4", 500_000, True), ("C1", 1000, False)])
+def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
+    import oracle
+    import paper_2604_08075_b200 as fp
+    from synth import configs
+    from synth.gen import generate_host
+    flags = fp.FP_FLAG_REPLICATED_GRID if replicated else 0
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank, args=(r, 2, port, name, n, flags, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for o in out:
+        assert o[-1] is None, o[-1]
+    cfg = configs.CONFIGS[name]().with_n(n)
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    allc, obest = oracle.sweep(cfg, L)
+    # candidate slices concatenate to the oracle's grid (or each is the whole grid)
+    recs = [np.frombuffer(o[1], dtype=fp.FP_CANDIDATE) for o in out]
+    if replicated:
+        for r in recs:
+            assert r.tobytes() == allc.tobytes()
+    else:
+        assert out[0][6] == 0 and out[0][7] + out[1][7] == cfg.n_candidates()
+        assert np.concatenate(recs).tobytes() == allc.tobytes()
+    for o in out:
+        assert o[2] == obest.tobytes()                      # same best split on every rank
+        cnt = np.frombuffer(o[3], dtype=np.uint64)
+        mass = np.frombuffer(o[4], dtype=np.uint64)
+        edges = np.array(sorted(set(cfg.b_short) | set(cfg.c_long)), dtype=np.uint32)
+        ocnt, omass = oracle.count_le(L, edges)
+        assert np.array_equal(np.cumsum(cnt)[:-1], ocnt) and int(cnt.sum()) == n
+        assert np.array_equal(np.cumsum(mass)[:-1], omass)
+        _, oc = oracle.route_batch(L, 8192, 16384, 65536, want_decisions=False)
+        assert [o[5][k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
+            [int(x) for x in oc]
