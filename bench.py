@@ -176,6 +176,28 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ GPU path ----
+def k3_large_grid(fp, generate_device, reps=5):
+    """K3 alone on a 2^24-candidate grid (SURVEY §8(d) ALU regime)."""
+    import torch
+    from synth import configs
+    cfg = configs.k3_large()
+    d = generate_device(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=fp.FP_FLAG_KERNEL_TIMING)
+    fp.sweep_thresholds(plan, d, cfg.rate_rps)
+    torch.cuda.synchronize()
+    fp.fp_kernel_time_reset(plan)
+    for _ in range(reps):
+        fp.sweep_thresholds(plan, d, cfg.rate_rps)
+    ms, k = fp.fp_kernel_time(plan, fp.FP_KERNEL_EVAL)
+    best = fp.best_split(plan)
+    fp.fleet_plan_destroy(plan)
+    per = ms / k
+    return {"candidates": cfg.n_candidates(), "k3_ms": per,
+            "candidates_per_s": cfg.n_candidates() / (per / 1e3),
+            "note": "K3 only (scan + capacity table + fp64 sizing + argmin), results not copied out",
+            "best_index_model0": int(best[0]["index"])}
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -311,6 +333,8 @@ def run_ours(args, cfg):
                                   for k in ("index", "b_short", "c_short", "c_long", "gpus_dual", "gpus_homo",
                                             "cost_dual", "savings", "predicted_savings")},
             "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
+    if world == 1 and args.k3_grid:
+        line["k3_large_grid"] = k3_large_grid(fp, generate_device)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
@@ -328,6 +352,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-k3-grid", dest="k3_grid", action="store_false",
+                    help="skip the 2^24-candidate K3 measurement")
     ap.add_argument("--ref-sample", type=int, default=10_000_000,
                     help="requests per reference (oracle) step")
     args = ap.parse_args()

@@ -243,4 +243,15 @@ def c5(n: int = 1_000_000_000) -> Config:
         description=f"{n:.0e} MIX, 4 models x 2 GPUs x 64 B x 8 C_L")
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5}
+def k3_large(n: int = 1_000_000) -> Config:
+    """ALU-regime candidate grid: 4 models x 2 GPUs x 512 B x
+    64 C_S x 64 C_L = 16,777,216 candidates, all valid (B < C_S < C_L), on a
+    short MIX trace. Used to measure K3 candidates/s, not a paper workload."""
+    b = [16 * k for k in range(1, 513)]                      # 16 .. 8,192
+    cs = [8192 + 384 * k for k in range(1, 65)]              # 8,576 .. 32,768
+    cl = [32768 + 3584 * k for k in range(1, 65)]            # 36,352 .. 262,144
+    return make_config("K3L", "MIX", SEED0 + 6, n, 10000.0, C5_MODELS, C5_GPUS, b, cs, cl,
+                       description="2^24-candidate ALU-regime grid on a 1e6 MIX trace")
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "K3L": k3_large}
