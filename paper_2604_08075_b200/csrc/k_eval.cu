@@ -59,11 +59,13 @@ __device__ __forceinline__ bool pool_instances(double lam, double mu, uint64_t n
 __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
                          fp_candidate &c) {
   // decompose idx = (((m * G + g) * n_cl + l) * n_cs' + s) * n_b + k
-  uint64_t r = idx;
-  uint32_t k = (uint32_t)(r % a.n_b); r /= a.n_b;
-  uint32_t s = (uint32_t)(r % a.n_cs_eff); r /= a.n_cs_eff;
-  uint32_t l = (uint32_t)(r % a.n_cl); r /= a.n_cl;
-  uint32_t g = (uint32_t)(r % a.n_gpus);
+  // 32-bit index math: the plan guarantees < 2^32 candidates (u64 division
+  // is an emulated ~100-instruction sequence on the GPU)
+  uint32_t r = (uint32_t)idx;
+  const uint32_t k = r % a.n_b; r /= a.n_b;
+  const uint32_t s = r % a.n_cs_eff; r /= a.n_cs_eff;
+  const uint32_t l = r % a.n_cl; r /= a.n_cl;
+  const uint32_t g = r % a.n_gpus;
   uint32_t B = a.b[k], CL = a.cl[l];
   uint32_t CS = a.n_cs ? a.cs[s] : B;
   c.index = (uint32_t)idx; c.model = m; c.gpu = g;
@@ -208,14 +210,19 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   // ---- this block's candidates: model m's part of the rank slice ----
   const uint64_t m_lo = (uint64_t)m * a.per_model, m_hi = m_lo + a.per_model;
   const uint64_t lo = max(m_lo, a.cand_first), hi = min(m_hi, a.cand_first + a.cand_count);
-  const uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // grid-stride over the model's candidates: the per-block prologue (scan,
+  // capacity table) and epilogue (argmin, arrival fence) are amortised over
+  // many candidates per thread on large grids (ncu r01_k3L: one candidate per
+  // thread spent most of its time in the prologue and the arrival fence)
   double bc = 0.0;
   uint32_t bi = 0xffffffffu, bv = 0;
-  if (idx < hi) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
     fp_candidate c;
     evaluate(a, sh, m, idx, c);
     if (a.results) a.results[idx - a.cand_first] = c;
-    if (c.flags & FP_CAND_FEASIBLE) { bc = c.cost_dual; bi = c.index; bv = 1; }
+    // indices increase along the loop, so strict '<' keeps the lowest index on ties
+    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || c.cost_dual < bc)) { bc = c.cost_dual; bi = c.index; bv = 1; }
   }
   warp_argmin(bc, bi, bv);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;

@@ -418,7 +418,11 @@ fp_status upload(fp_plan *p) {
     uint64_t hi = std::min<uint64_t>((uint64_t)(m + 1) * p->per_model, p->cand_first + p->cand_count);
     if (hi > lo) widest = std::max(widest, hi - lo);
   }
-  p->k3_grid_x = (int)std::max<uint64_t>(1, (widest + 255) / 256);
+  // one thread per candidate up to ~8 blocks per SM in total, then grid-stride
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  const uint64_t cap = std::max<uint64_t>(1, (uint64_t)sms * 8 / M);
+  p->k3_grid_x = (int)std::min<uint64_t>(cap, std::max<uint64_t>(1, (widest + 255) / 256));
   if (p->k3_grid_x > 65535 * 64) return fail(p, FP_ERR_CONFIG, "candidate grid too large for one launch");
   CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * p->k3_grid_x * sizeof(BlockBest)), "cudaMalloc block_best");
   CUDA_TRY(p, cudaMalloc(&p->d_done, M * sizeof(unsigned int)), "cudaMalloc done");
