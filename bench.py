@@ -6,6 +6,7 @@ One step = the whole hot path of SURVEY.md §8(a) over one batch (the trace):
   best_split        (per-model best split -> host)
   route_batch       (K4: Alg. 1 for model 0's best split, decision byte per
                      request + global counts -> host)
+issued as the single ABI call sweep_and_route.
 Default workload: C5 (1e9-request MIX trace per GPU, 4,096 candidates) --
 the configuration BASELINE.json's "at 1/2/4/8 B200" metric is quoted on and
 the largest single-GPU one. Multi-GPU (torchrun): weak scaling, 1e9 requests
@@ -232,14 +233,8 @@ def run_ours(args, cfg):
     stream = torch.cuda.current_stream(dev)
 
     def step(lengths):
-        fp.sweep_thresholds(plan, lengths, cfg.rate_rps, stream=stream)
-        best = fp.best_split(plan)
-        b = best[0]
-        if b["index"] == 0xFFFFFFFF:
-            raise RuntimeError("model 0 has no feasible split")
-        counts = fp.route_batch(plan, lengths, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]),
-                                decision=d_dec, stream=stream)
-        return best, counts
+        # sweep_thresholds -> best_split -> route_batch(model 0's best split), one ABI call
+        return fp.sweep_and_route(plan, lengths, cfg.rate_rps, route_model=0, decision=d_dec, stream=stream)
 
     def barrier():
         if world > 1:
@@ -286,10 +281,11 @@ def run_ours(args, cfg):
         if world > 1:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": total_requests * args.e2e_steps / float(dt.item()), "unit": UNIT,
-               "h2d_bytes_per_step": 2 * 4 * n,   # sweep + route each stream the pinned trace
+               "h2d_bytes_per_step": 4 * n,   # the pinned trace crosses PCIe once per step
                "d2h_bytes_per_step": best.nbytes + 5 * 8,
-               "note": "pinned host trace streamed H2D inside sweep_thresholds and route_batch "
-                       "(128 MB chunks, copy/compute overlapped); best records + route counts to host"}
+               "note": "sweep_and_route on a pinned host trace: 128 MB chunks DMA'd into a device copy "
+                       "while K1 consumes them, K4 reads the device copy; best records + route counts "
+                       "to host"}
         del h_len
 
     if rank != 0:

@@ -223,6 +223,18 @@ fp_status sweep_thresholds(fp_plan *plan, const uint32_t *d_len, uint64_t n_loca
  * Errors: FP_ERR_STATE (no sweep yet), FP_ERR_EMPTY_TRACE (global N == 0). */
 fp_status best_split(fp_plan *plan, fp_candidate *h_best);
 
+/* The paper's whole workflow over one trace in one call: sweep_thresholds,
+ * best_split (into h_best[n_models] if non-NULL), then route_batch with the
+ * best split of model `route_model` (decisions into d_decision if non-NULL,
+ * global counts into h_counts if non-NULL). A HOST trace crosses PCIe once:
+ * it is copied into a plan-owned device buffer chunk by chunk while the trace
+ * pass consumes each chunk, and the routing pass reads the device copy.
+ * Synchronizes. Errors: as the three calls; FP_ERR_STATE if route_model has
+ * no feasible split (h_best is still written). */
+fp_status sweep_and_route(fp_plan *plan, const uint32_t *len, uint64_t n_local, double rate_rps,
+                          uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
+                          fp_route_counts *h_counts, void *stream);
+
 /* Global per-bin histogram of the last sweep (K1 output after the cross-rank
  * sum; synchronizes). With E = sortuniq(B u C_L) ascending (|E| = n_edges of
  * fleet_plan_info): h_edges[j] = e_j for j < |E|; bin j < |E| holds the

@@ -25,7 +25,7 @@ STATUS = ["FP_OK", "FP_ERR_INVALID_ARG", "FP_ERR_CONFIG", "FP_ERR_EMPTY_TRACE", 
 EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split", "sweep_histogram",
             "fleet_plan_info", "fp_kernel_launches", "fleet_plan_destroy", "fp_status_string",
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
-            "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset"]
+            "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -123,6 +123,7 @@ def _load():
         "fp_nccl_get_unique_id": (c_i32, [c_vp]),
         "fp_kernel_time": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_dbl), ctypes.POINTER(c_u64)]),
         "fp_kernel_time_reset": (c_i32, [c_vp]),
+        "sweep_and_route": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -359,3 +360,19 @@ def fp_kernel_time(plan, kind):
 
 def fp_kernel_time_reset(plan):
     _check(lib.fp_kernel_time_reset(plan.handle), plan)
+
+
+def sweep_and_route(plan, lengths, rate_rps, route_model=0, decision=None, stream=None):
+    """Whole workflow in one call; returns (best records [n_models], route counts dict)."""
+    ptr, n, _, keep = _trace_ptr(lengths)
+    dptr = None
+    if decision is not None:
+        if decision.numel() < n or not decision.is_cuda:
+            raise ValueError("decision must be a CUDA uint8 tensor with >= n elements")
+        dptr = decision.data_ptr()
+    best = np.zeros(plan.n_models, dtype=FP_CANDIDATE)
+    counts = fp_route_counts()
+    _check(lib.sweep_and_route(plan.handle, ptr, n, float(rate_rps), route_model, dptr, best.ctypes.data,
+                               ctypes.byref(counts), _stream_handle(stream, plan.device)), plan)
+    del keep
+    return best, {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}

@@ -111,6 +111,9 @@ struct fp_plan {
   // pinned host mirrors
   fp_candidate *h_best = nullptr;          // [world][n_models]
   unsigned long long *h_small = nullptr;   // [2 * nbins + 8]: hist, route counts
+  // device copy of a host trace for sweep_and_route
+  uint32_t *d_resident = nullptr;
+  uint64_t resident_cap = 0;
   // NCCL
   NcclComm comm = nullptr;
   fp_collectives coll{};                   // host hooks replacing NCCL (optional)
@@ -508,8 +511,11 @@ fp_status ensure_staging(fp_plan *p) {
 // Run `body(dev_ptr, n, offset)` over a trace that may live on the host: device
 // traces go straight through, host traces are DMA'd chunk by chunk into two
 // staging buffers on the copy stream (double-buffered, event-ordered).
+// With `resident` (device, >= n elements) a host trace is copied there in
+// full (each chunk processed as soon as it lands) instead of through the ring.
 template <class F>
-fp_status over_trace(fp_plan *p, const uint32_t *len, uint64_t n, cudaStream_t s, F body) {
+fp_status over_trace(fp_plan *p, const uint32_t *len, uint64_t n, cudaStream_t s, F body,
+                     uint32_t *resident = nullptr) {
   if (n == 0) return FP_OK;
   if (!is_host_pointer(len)) return body(len, n, 0ull);
   fp_status st = ensure_staging(p);
@@ -523,12 +529,12 @@ fp_status over_trace(fp_plan *p, const uint32_t *len, uint64_t n, cudaStream_t s
   for (uint64_t off = 0, i = 0; off < n; off += kChunkElems, ++i) {
     const int k = (int)(i & 1);
     const uint64_t cnt = std::min<uint64_t>(kChunkElems, n - off);
-    if (i >= 2) CUDA_TRY(p, cudaStreamWaitEvent(p->copy_stream, p->ev_used[k], 0), "wait used");
-    CUDA_TRY(p, cudaMemcpyAsync(p->d_stage[k], len + off, cnt * 4, cudaMemcpyHostToDevice, p->copy_stream),
-             "H2D chunk");
+    uint32_t *dst = resident ? resident + off : p->d_stage[k];
+    if (i >= 2 && !resident) CUDA_TRY(p, cudaStreamWaitEvent(p->copy_stream, p->ev_used[k], 0), "wait used");
+    CUDA_TRY(p, cudaMemcpyAsync(dst, len + off, cnt * 4, cudaMemcpyHostToDevice, p->copy_stream), "H2D chunk");
     CUDA_TRY(p, cudaEventRecord(p->ev_copied[k], p->copy_stream), "record copied");
     CUDA_TRY(p, cudaStreamWaitEvent(s, p->ev_copied[k], 0), "wait copied");
-    st = body(p->d_stage[k], cnt, off);
+    st = body(dst, cnt, off);
     if (st != FP_OK) return st;
     CUDA_TRY(p, cudaEventRecord(p->ev_used[k], s), "record used");
   }
@@ -690,6 +696,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_results);
     cudaFree(p->d_block_best);
     cudaFree(p->d_done);
+    cudaFree(p->d_resident);
     for (int i = 0; i < 2; ++i) {
       cudaFree(p->d_stage[i]);
       if (p->ev_copied[i]) cudaEventDestroy(p->ev_copied[i]);
@@ -795,8 +802,50 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
   return FP_OK;
 }
 
+namespace {
+fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
+                     fp_candidate *h_results, void *stream, uint32_t *resident);
+}
+
 fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                            fp_candidate *h_results, void *stream) {
+  return sweep_impl(p, d_len, n_local, rate_rps, h_results, stream, nullptr);
+}
+
+fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, double rate_rps,
+                          uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
+                          fp_route_counts *h_counts, void *stream) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (route_model >= p->models.size()) return fail(p, FP_ERR_INVALID_ARG, "route_model out of range");
+  DeviceGuard g(p->device);
+  const uint32_t *src = len;
+  uint32_t *resident = nullptr;
+  if (n_local && len && is_host_pointer(len)) {
+    if (p->resident_cap < n_local) {
+      cudaFree(p->d_resident);
+      p->d_resident = nullptr;
+      p->resident_cap = 0;
+      CUDA_TRY(p, cudaMalloc(&p->d_resident, n_local * 4), "cudaMalloc resident trace");
+      p->resident_cap = n_local;
+    }
+    resident = p->d_resident;
+    src = resident;
+  }
+  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident);
+  if (st != FP_OK) return st;
+  std::vector<fp_candidate> best(p->models.size());
+  st = best_split(p, best.data());
+  if (st != FP_OK) return st;
+  if (h_best) memcpy(h_best, best.data(), best.size() * sizeof(fp_candidate));
+  const fp_candidate &b = best[route_model];
+  if (!(b.flags & FP_CAND_FEASIBLE))
+    return fail(p, FP_ERR_STATE, "model %u has no feasible split to route with", route_model);
+  return route_batch(p, src, n_local, b.b_short, b.c_short, b.c_long, d_decision, h_counts, stream);
+}
+
+namespace {
+fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
+                     fp_candidate *h_results, void *stream, uint32_t *resident) {
   if (!p) return FP_ERR_INVALID_ARG;
   if (n_local && !d_len) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
@@ -815,7 +864,7 @@ fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, 
     if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");
     ++p->launches;
     return FP_OK;
-  });
+  }, resident);
   if (st != FP_OK) return st;
   // C1: sum the per-rank histograms
   if (p->world > 1) {
@@ -852,6 +901,8 @@ fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, 
   }
   return FP_OK;
 }
+
+}  // namespace
 
 fp_status best_split(fp_plan *p, fp_candidate *h_best) {
   if (!p || !h_best) return FP_ERR_INVALID_ARG;

@@ -222,3 +222,20 @@ def test_full_size_c5_sampled():
         res = fp.sweep_thresholds(plan, d[first:first + (1 << 24)], cfg.rate_rps, want_results=True)
         allc, _ = oracle.sweep(cfg.with_n(1 << 24), L)
         _compare_records(res, allc.view(fp.FP_CANDIDATE), f"C5 window @{first}")
+
+
+@pytest.mark.parametrize("where", ["device", "pinned", "pageable"])
+def test_sweep_and_route_equals_separate_calls(where):
+    cfg = configs.c5().with_n(2_500_009)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    src = {"device": lambda: _dev(L), "pinned": lambda: torch.from_numpy(L.view(np.int32)).pin_memory(),
+           "pageable": lambda: L}[where]()
+    dec = torch.zeros(L.size, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, src, cfg.rate_rps, route_model=1, decision=dec)
+    _, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[1]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec.cpu().numpy(), odec)
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
