@@ -301,3 +301,68 @@ int or_num_threads(void) {
   return 1;
 #endif
 }
+
+/* ==========================================================================
+ * Token-budget estimation (NEXT-1; TEST INFRASTRUCTURE like the rest).
+ * ========================================================================== */
+
+/* Eq. (5) `eq:conservative` P:453-457 / Alg. 1 line P:494:
+ *   c* = c_hat_k - gamma * sigma_hat_k,
+ * bounded below by c_floor > 0 (the paper does not bound it; DESIGN R22). */
+double or_route_ratio(double c_hat, double sigma, double gamma, double c_floor) {
+  double t = gamma * sigma;
+  double c = c_hat - t;
+  if (!(c >= c_floor)) c = c_floor;
+  return c;
+}
+
+/* Eq. (3) `eq:budget` P:425-429 / Alg. 1 line P:496:
+ *   L_total = ceil(|r| / c*) + max_output_tokens, saturating at 2^32 - 1. */
+uint32_t or_estimate_one(uint32_t bytes, uint32_t max_out, double cstar) {
+  double lin = ceil((double)bytes / cstar);
+  if (!(lin < 4294967296.0)) return 0xFFFFFFFFu;
+  uint64_t t = (uint64_t)lin + (uint64_t)max_out;
+  return t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+/* Per request: category k (k >= n_cats -> the last category, the "mixed /
+ * other" bucket, R23), c* from the frozen snapshot, then L_total. */
+void or_estimate(const uint32_t *bytes, const uint32_t *max_out, const uint8_t *cat, uint64_t n,
+                 const double *c_hat, const double *sigma, uint32_t n_cats, double gamma,
+                 double c_floor, uint32_t *out) {
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t k = cat[i] < n_cats ? cat[i] : n_cats - 1;
+    double cs = or_route_ratio(c_hat[k], sigma[k], gamma, c_floor);
+    out[i] = or_estimate_one(bytes[i], max_out[i], cs);
+  }
+}
+
+/* Alg. 1 on the estimates plus Table 5's mis-route count (P:925-927:
+ * "sending a request to a pool that cannot serve it"): a request routed to
+ * pool p whose TRUE total (true_prompt_tokens + max_output_tokens) exceeds
+ * C_max(p). misroute[0] = short pool, misroute[1] = long pool. */
+void or_route_batch_est(const uint32_t *bytes, const uint32_t *max_out, const uint8_t *cat,
+                        const uint32_t *true_prompt, uint64_t n, const double *c_hat,
+                        const double *sigma, uint32_t n_cats, double gamma, double c_floor,
+                        uint32_t B, uint32_t c_short, uint32_t c_long, uint8_t *decision,
+                        uint32_t *l_total, uint64_t counts[5], uint64_t misroute[2]) {
+  for (int k = 0; k < 5; ++k) counts[k] = 0;
+  misroute[0] = misroute[1] = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint32_t k = cat[i] < n_cats ? cat[i] : n_cats - 1;
+    double cs = or_route_ratio(c_hat[k], sigma[k], gamma, c_floor);
+    uint32_t L = or_estimate_one(bytes[i], max_out[i], cs);
+    int st = 0;
+    int p = or_route(L, B, c_short, c_long, &st);
+    if (decision) decision[i] = (uint8_t)(p | (st << 2));
+    if (l_total) l_total[i] = L;
+    counts[p] += 1;
+    if (p == 0) counts[3] += L;
+    if (p == 1) counts[4] += L;
+    if (true_prompt) {
+      uint64_t t = (uint64_t)true_prompt[i] + max_out[i];
+      if (p == 0 && t > c_short) misroute[0] += 1;
+      if (p == 1 && t > c_long) misroute[1] += 1;
+    }
+  }
+}

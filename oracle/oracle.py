@@ -56,6 +56,10 @@ def lib():
         "or_sweep": (ctypes.c_int, [VP, U64, U32, VP, U32, VP, VP, VP, VP, U32, VP, U32, VP, U32,
                                     VP, U32, VP, F64, F64, VP, VP]),
         "or_num_threads": (ctypes.c_int, []),
+        "or_route_ratio": (F64, [F64, F64, F64, F64]),
+        "or_estimate_one": (U32, [U32, U32, F64]),
+        "or_estimate": (None, [VP, VP, VP, U64, VP, VP, U32, F64, F64, VP]),
+        "or_route_batch_est": (None, [VP, VP, VP, VP, U64, VP, VP, U32, F64, F64, U32, U32, U32, VP, VP, VP, VP]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -169,3 +173,45 @@ def sweep(cfg, L, rate=None, want_all=True):
     if rc != 0:
         raise ValueError(f"or_sweep rc={rc}")
     return out, best
+
+
+# ---- token-budget estimation (NEXT-1) ------------------------------------------
+def route_ratio(c_hat, sigma, gamma, c_floor):
+    return float(lib().or_route_ratio(c_hat, sigma, gamma, c_floor))
+
+
+def estimate_one(nbytes, max_out, cstar):
+    return int(lib().or_estimate_one(nbytes, max_out, cstar))
+
+
+def _est_args(cats):
+    c_hat = np.ascontiguousarray([c[0] for c in cats], dtype=np.float64)
+    sig = np.ascontiguousarray([c[1] for c in cats], dtype=np.float64)
+    return c_hat, sig
+
+
+def estimate(body, max_out, cat, cats, gamma, c_floor):
+    """L_total estimates; cats = [(c_hat, sigma_hat), ...] indexed by category."""
+    body, max_out = _u32(body), _u32(max_out)
+    cat = np.ascontiguousarray(cat, dtype=np.uint8)
+    c_hat, sig = _est_args(cats)
+    out = np.zeros(body.size, dtype=np.uint32)
+    lib().or_estimate(body.ctypes.data, max_out.ctypes.data, cat.ctypes.data, body.size, c_hat.ctypes.data,
+                      sig.ctypes.data, len(cats), gamma, c_floor, out.ctypes.data)
+    return out
+
+
+def route_batch_est(body, max_out, cat, true_prompt, cats, gamma, c_floor, B, c_short, c_long):
+    body, max_out = _u32(body), _u32(max_out)
+    cat = np.ascontiguousarray(cat, dtype=np.uint8)
+    tp = _u32(true_prompt) if true_prompt is not None else None
+    c_hat, sig = _est_args(cats)
+    dec = np.zeros(body.size, dtype=np.uint8)
+    lt = np.zeros(body.size, dtype=np.uint32)
+    counts = np.zeros(5, dtype=np.uint64)
+    mis = np.zeros(2, dtype=np.uint64)
+    lib().or_route_batch_est(body.ctypes.data, max_out.ctypes.data, cat.ctypes.data,
+                             tp.ctypes.data if tp is not None else None, body.size, c_hat.ctypes.data,
+                             sig.ctypes.data, len(cats), gamma, c_floor, B, c_short, c_long, dec.ctypes.data,
+                             lt.ctypes.data, counts.ctypes.data, mis.ctypes.data)
+    return dec, lt, counts, mis

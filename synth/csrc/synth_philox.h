@@ -46,4 +46,26 @@ SYN_HD uint32_t syn_request(const uint32_t *luts, const uint8_t *interp,
   const uint32_t *qo = qi + SYN_LUT_SIZE;
   return syn_sample(qi, interp[2 * comp], c[0]) + syn_sample(qo, interp[2 * comp + 1], c[1]);
 }
+/* Raw request columns (NEXT-1): see synth/shapes.py "Raw request columns".
+ * ratio: [n_cat][65536] 16.16 fixed point; cat_cuts: [n_cat-1] on 16 bits. */
+SYN_HD void syn_request_raw(const uint32_t *luts, const uint8_t *interp, const uint32_t *cuts,
+                            uint32_t n_comp, const uint32_t *ratio, const uint32_t *cat_cuts,
+                            uint32_t n_cat, uint64_t seed, uint64_t i, uint32_t *bytes,
+                            uint32_t *max_out, uint8_t *cat, uint32_t *true_prompt) {
+  uint32_t c[4] = {(uint32_t)i, (uint32_t)(i >> 32), 0u, 0u};
+  syn_philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint32_t comp = 0;
+  for (uint32_t k = 0; k + 1 < n_comp; ++k) comp += (c[2] >= cuts[k]) ? 1u : 0u;
+  const uint32_t *qi = luts + (uint64_t)comp * 2u * SYN_LUT_SIZE;
+  const uint32_t *qo = qi + SYN_LUT_SIZE;
+  uint32_t lin = syn_sample(qi, interp[2 * comp], c[0]);
+  uint32_t lout = syn_sample(qo, interp[2 * comp + 1], c[1]);
+  uint32_t k = 0, lo = c[3] & 0xFFFFu;
+  for (uint32_t j = 0; j + 1 < n_cat; ++j) k += (lo >= cat_cuts[j]) ? 1u : 0u;
+  uint64_t r = ratio[(uint64_t)k * 65536u + (c[3] >> 16)];
+  *bytes = (uint32_t)(((uint64_t)lin * r + 0x8000u) >> 16);
+  *max_out = lout;
+  *cat = (uint8_t)k;
+  *true_prompt = lin;
+}
 #endif

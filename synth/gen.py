@@ -149,3 +149,77 @@ def generate_device(mix: Mixture | str, seed: int, first: int, count: int, out=N
         raise RuntimeError(f"synth_generate_device failed rc={rc}")
     s.synchronize()   # keep the temporary tables alive until the kernel is done
     return out
+
+
+# ------------------------------------------------------- raw request columns ----
+def _raw_tables():
+    from .shapes import category_cuts16, ratio_tables
+    ratio = np.ascontiguousarray(ratio_tables().ravel())
+    cuts = np.array(category_cuts16(), dtype=np.uint32)
+    return ratio, cuts, len(category_cuts16()) + 1
+
+
+def generate_raw_np(mix: Mixture | str, seed: int, first: int, count: int):
+    """Numpy reference: (body_bytes u32, max_output u32, category u8, true_prompt u32)."""
+    from .shapes import category_cuts16, ratio_tables
+    if isinstance(mix, str):
+        mix = mixture(mix)
+    w0, w1, w2, w3 = philox_words(seed, first, count)
+    comp = np.zeros(count, dtype=np.int64)
+    for c in mix.cut:
+        comp += (w2 >= np.uint32(c)).astype(np.int64)
+    lin = np.zeros(count, dtype=np.uint64)
+    lout = np.zeros(count, dtype=np.uint64)
+    for k, sh in enumerate(mix.shapes):
+        m = comp == k
+        if m.any():
+            lin[m] = _sample(sh.t_in, w0[m])
+            lout[m] = _sample(sh.t_out, w1[m])
+    lo = (w3 & np.uint32(0xFFFF)).astype(np.int64)
+    cat = np.zeros(count, dtype=np.int64)
+    for c in category_cuts16():
+        cat += (lo >= c).astype(np.int64)
+    r = ratio_tables()[cat, (w3 >> np.uint32(16)).astype(np.int64)].astype(np.uint64)
+    body = (lin * r + np.uint64(0x8000)) >> np.uint64(16)
+    return (body.astype(np.uint32), lout.astype(np.uint32), cat.astype(np.uint8), lin.astype(np.uint32))
+
+
+def generate_raw_host(mix: Mixture | str, seed: int, first: int, count: int):
+    p = pack(mix)
+    ratio, cuts, ncat = _raw_tables()
+    lib = _load_host()
+    f = lib.synth_generate_raw_host
+    f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+                                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 4
+    f.restype = ctypes.c_int
+    out = (np.empty(count, np.uint32), np.empty(count, np.uint32), np.empty(count, np.uint8),
+           np.empty(count, np.uint32))
+    rc = f(p.luts.ctypes.data, p.interp.ctypes.data, p.cuts.ctypes.data, p.n_comp, ratio.ctypes.data,
+           cuts.ctypes.data, ncat, seed, first, count, *[a.ctypes.data for a in out])
+    if rc != 0:
+        raise RuntimeError(f"synth_generate_raw_host rc={rc}")
+    return out
+
+
+def generate_raw_device(mix: Mixture | str, seed: int, first: int, count: int):
+    """CUDA generator: torch tensors (bytes int32, max_out int32, cat uint8, true_prompt int32)."""
+    import torch
+    p = pack(mix)
+    ratio, cuts, ncat = _raw_tables()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    t = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else a).to(dev)  # noqa: E731
+    luts, interp, ccuts, rat, catc = t(p.luts), t(p.interp), t(p.cuts), t(ratio), t(cuts)
+    out = (torch.empty(count, dtype=torch.int32, device=dev), torch.empty(count, dtype=torch.int32, device=dev),
+           torch.empty(count, dtype=torch.uint8, device=dev), torch.empty(count, dtype=torch.int32, device=dev))
+    lib = _load_dev()
+    f = lib.synth_generate_raw_device
+    f.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_uint32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32,
+                                          ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64] + [ctypes.c_void_p] * 5
+    f.restype = ctypes.c_int
+    s = torch.cuda.current_stream(dev)
+    rc = f(luts.data_ptr(), interp.data_ptr(), ccuts.data_ptr(), p.n_comp, rat.data_ptr(), catc.data_ptr(), ncat,
+           seed, first, count, *[o.data_ptr() for o in out], ctypes.c_void_p(s.cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"synth_generate_raw_device rc={rc}")
+    s.synchronize()
+    return out

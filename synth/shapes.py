@@ -189,3 +189,37 @@ def mixture(name: str) -> Mixture:
     if name == "MIX":
         return Mixture("MIX", (shape_az(), shape_lm(), shape_sg()), _cuts(MIX_WEIGHTS))
     return Mixture(name, (SHAPES[name](),), ())
+
+
+# --------------------------------------------------------------------------
+# Raw request columns for token-budget estimation (NEXT-1; PAPER Eq. `budget`
+# P:425-429 and Table 5). A request carries its body length |r| in
+# bytes, its category k and max_output_tokens; the true prompt token count is
+# L_in (the same L_in as the L_total trace, so L_total_true = L_in + L_out).
+#   bytes = round(L_in * ratio),  ratio = c_k * noise,  fixed point 16.16:
+#   bytes = (L_in * R[k][w3 >> 16] + 2^15) >> 16   (u64 product)
+#   k     = #{j : (w3 & 0xFFFF) >= CAT_CUT[j]}
+# c_k: Table 5 "True c_k"; category weights and the 10% CV
+# log-normal noise are stated assumptions.
+# --------------------------------------------------------------------------
+CATEGORIES = ("prose", "code", "cjk", "mixed")
+CAT_TRUE_RATIO = (4.48, 3.52, 2.01, 3.81)
+CAT_WEIGHTS = (0.55, 0.20, 0.10, 0.15)           # stated
+RATIO_CV = 0.10                                   # stated
+
+
+def category_cuts16():
+    c = np.cumsum(np.asarray(CAT_WEIGHTS, dtype=np.float64))[:-1]
+    return tuple(int(round(x * 65536)) for x in c)
+
+
+@lru_cache(maxsize=None)
+def ratio_tables():
+    """uint32 [n_cat][65536] per-request bytes-per-token ratio in 16.16 fixed point."""
+    sig = np.sqrt(np.log(1.0 + RATIO_CV ** 2))
+    z = stats.norm.ppf((np.arange(65536, dtype=np.float64) + 0.5) / 65536.0)
+    noise = np.exp(sig * z - 0.5 * sig * sig)
+    out = np.zeros((len(CAT_TRUE_RATIO), 65536), dtype=np.uint32)
+    for k, c in enumerate(CAT_TRUE_RATIO):
+        out[k] = np.round(c * noise * 65536.0).astype(np.uint32)
+    return out

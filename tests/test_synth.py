@@ -65,3 +65,36 @@ def test_cuda_generator_matches_host(shape):
     d = generate_device(shape, 11, 5, n).cpu().numpy().view(np.uint32)
     h = generate_host(shape, 11, 5, n)
     assert np.array_equal(d, h)
+
+
+@pytest.mark.parametrize("shape", ["AZ", "MIX"])
+def test_raw_columns_host_matches_numpy_and_trace(shape):
+    from synth.gen import generate_raw_host, generate_raw_np
+    a = generate_raw_np(shape, 5, 1000, 20000)
+    b = generate_raw_host(shape, 5, 1000, 20000)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    # the true total of the raw columns is the L_total trace
+    L = generate_host(shape, 5, 1000, 20000)
+    assert np.array_equal(a[3].astype(np.uint64) + a[1], L)
+
+
+def test_raw_columns_category_ratios():
+    # Table 5 "True c_k": per-category mean bytes/token within 1%
+    from synth.gen import generate_raw_host
+    from synth.shapes import CAT_TRUE_RATIO, CAT_WEIGHTS
+    body, _, cat, lin = generate_raw_host("AZ", 9, 0, 1_000_000)
+    for k, c in enumerate(CAT_TRUE_RATIO):
+        m = (cat == k) & (lin >= 64)
+        assert abs(body[m].sum() / lin[m].sum() - c) / c < 0.01
+        assert abs(np.mean(cat == k) - CAT_WEIGHTS[k]) < 0.005
+
+
+@pytest.mark.gpu
+def test_raw_columns_cuda_matches_host():
+    from synth.gen import generate_raw_device, generate_raw_host
+    d = generate_raw_device("MIX", 3, 7, 500_001)
+    h = generate_raw_host("MIX", 3, 7, 500_001)
+    for x, y in zip(d, h):
+        xv = x.cpu().numpy()
+        assert np.array_equal(xv.view(y.dtype) if xv.dtype != y.dtype else xv, y)
