@@ -124,7 +124,7 @@ typedef struct fp_plan_desc {
 } fp_plan_desc;
 
 /* Host-side collective hooks (e.g. MPI or a CPU process group). When given,
- * the library synchronizes the stream, copies the operand to pinned host
+ * the library synchronizes the stream, copies the operand to host
  * memory, calls the hook, and copies the result back; NCCL is not used.
  * Every rank must call the hooks in the same order (collective semantics).
  * Each returns 0 on success; anything else fails the call with FP_ERR_NCCL.
@@ -234,6 +234,53 @@ fp_status best_split(fp_plan *plan, fp_candidate *h_best);
 fp_status sweep_and_route(fp_plan *plan, const uint32_t *len, uint64_t n_local, double rate_rps,
                           uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
                           fp_route_counts *h_counts, void *stream);
+
+/* ---- token-budget estimation (NEXT-1) ----------------------------------------
+ * Routing key from raw request columns (Eq. `budget`, with the
+ * conservative ratio of Eq. `conservative`, Alg. 1):
+ *   c*_k    = max(c_hat_k - gamma * sigma_hat_k, c_floor)     (R22)
+ *   L_total = min(ceil(|r| / c*_k) + max_output_tokens, 2^32 - 1)
+ * in IEEE binary64 (one division and a ceil per request), category
+ * k >= n_cats counted as the last category ("mixed/other", R23). */
+typedef struct fp_category_calibration {
+  double c_hat;      /* calibrated bytes per token of the category (Eq. `ema`)   */
+  double sigma_hat;  /* its EMA deviation, >= 0                                   */
+} fp_category_calibration;
+
+typedef struct fp_estimator {
+  const fp_category_calibration *cats; /* frozen snapshot, indexed by category  */
+  uint32_t n_cats;                     /* 1..256                                 */
+  double gamma;                        /* conservatism weight, >= 0 (1.0) */
+  double c_floor;                      /* lower bound of c*, > 0                 */
+} fp_estimator;
+
+/* Raw request columns (all device memory, n_local entries each). */
+typedef struct fp_raw_trace {
+  const uint32_t *body_bytes;          /* |r|                                     */
+  const uint32_t *max_output_tokens;   /* r.max_output_tokens (L_out)             */
+  const uint8_t *category;             /* k                                       */
+  const uint32_t *true_prompt_tokens;  /* usage.prompt_tokens, nullable (only
+                                          route_batch_raw reads it)               */
+} fp_raw_trace;
+
+/* sweep_thresholds on L_total estimated in the trace pass itself (9 B per
+ * request read; no L_total column is materialised). Same outputs, errors
+ * and collective semantics as sweep_thresholds; columns must be device
+ * memory (else FP_ERR_INVALID_ARG). */
+fp_status sweep_thresholds_raw(fp_plan *plan, const fp_raw_trace *trace, uint64_t n_local,
+                               const fp_estimator *est, double rate_rps, fp_candidate *h_results,
+                               void *stream);
+
+/* route_batch on the estimated L_total. Optionally writes the estimates
+ * (d_l_total, device) and, when true_prompt_tokens is given, Table 5's
+ * mis-route counts into h_misroute[2]: requests routed to the
+ * short (long) pool whose TRUE total true_prompt_tokens + max_output_tokens
+ * exceeds C_S (C_L). Global over ranks; synchronizes if h_counts or
+ * h_misroute is non-NULL. */
+fp_status route_batch_raw(fp_plan *plan, const fp_raw_trace *trace, uint64_t n_local,
+                          const fp_estimator *est, uint32_t b_short, uint32_t c_short, uint32_t c_long,
+                          uint8_t *d_decision, uint32_t *d_l_total, fp_route_counts *h_counts,
+                          uint64_t *h_misroute, void *stream);
 
 /* Global per-bin histogram of the last sweep (K1 output after the cross-rank
  * sum; synchronizes). With E = sortuniq(B u C_L) ascending (|E| = n_edges of

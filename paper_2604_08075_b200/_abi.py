@@ -25,7 +25,8 @@ STATUS = ["FP_OK", "FP_ERR_INVALID_ARG", "FP_ERR_CONFIG", "FP_ERR_EMPTY_TRACE", 
 EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split", "sweep_histogram",
             "fleet_plan_info", "fp_kernel_launches", "fleet_plan_destroy", "fp_status_string",
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
-            "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route"]
+            "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
+            "sweep_thresholds_raw", "route_batch_raw"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -70,6 +71,20 @@ class fp_plan_desc(ctypes.Structure):
                 ("device", c_i32), ("rank", c_i32), ("world", c_i32),
                 ("nccl_unique_id", c_vp),
                 ("collectives", ctypes.POINTER(fp_collectives))]
+
+
+class fp_category_calibration(ctypes.Structure):
+    _fields_ = [("c_hat", c_dbl), ("sigma_hat", c_dbl)]
+
+
+class fp_estimator(ctypes.Structure):
+    _fields_ = [("cats", ctypes.POINTER(fp_category_calibration)), ("n_cats", c_u32), ("gamma", c_dbl),
+                ("c_floor", c_dbl)]
+
+
+class fp_raw_trace(ctypes.Structure):
+    _fields_ = [("body_bytes", c_vp), ("max_output_tokens", c_vp), ("category", c_vp),
+                ("true_prompt_tokens", c_vp)]
 
 
 class fp_route_counts(ctypes.Structure):
@@ -123,6 +138,10 @@ def _load():
         "fp_nccl_get_unique_id": (c_i32, [c_vp]),
         "fp_kernel_time": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_dbl), ctypes.POINTER(c_u64)]),
         "fp_kernel_time_reset": (c_i32, [c_vp]),
+        "sweep_thresholds_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_dbl,
+                                         c_vp, c_vp]),
+        "route_batch_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_u32, c_u32,
+                                    c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), ctypes.POINTER(c_u64), c_vp]),
         "sweep_and_route": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
     }
     for name, (res, args) in sig.items():
@@ -376,3 +395,49 @@ def sweep_and_route(plan, lengths, rate_rps, route_model=0, decision=None, strea
                                ctypes.byref(counts), _stream_handle(stream, plan.device)), plan)
     del keep
     return best, {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}
+
+
+# ---- token-budget estimation (NEXT-1) ------------------------------------------------
+def _estimator(cats, gamma, c_floor):
+    arr = (fp_category_calibration * len(cats))(*[fp_category_calibration(float(c), float(s)) for c, s in cats])
+    return fp_estimator(arr, len(cats), float(gamma), float(c_floor)), arr
+
+
+def _raw(body, max_out, cat, true_prompt=None):
+    for t in (body, max_out, cat) + ((true_prompt,) if true_prompt is not None else ()):
+        if not (hasattr(t, "is_cuda") and t.is_cuda and t.is_contiguous()):
+            raise ValueError("raw columns must be contiguous CUDA tensors")
+    if body.numel() != max_out.numel() or body.numel() != cat.numel():
+        raise ValueError("raw columns must have the same length")
+    return fp_raw_trace(body.data_ptr(), max_out.data_ptr(), cat.data_ptr(),
+                        true_prompt.data_ptr() if true_prompt is not None else None), body.numel()
+
+
+def sweep_thresholds_raw(plan, body, max_out, cat, cats, rate_rps, gamma=1.0, c_floor=0.5, want_results=False,
+                         stream=None):
+    """Sweep on L_total estimated from (body bytes, max_output, category) in the trace pass.
+    cats = [(c_hat, sigma_hat), ...] indexed by category."""
+    tr, n = _raw(body, max_out, cat)
+    est, keep = _estimator(cats, gamma, c_floor)
+    out = np.zeros(fleet_plan_info(plan)["cand_count"], dtype=FP_CANDIDATE) if want_results else None
+    _check(lib.sweep_thresholds_raw(plan.handle, ctypes.byref(tr), n, ctypes.byref(est), float(rate_rps),
+                                    out.ctypes.data if out is not None else None,
+                                    _stream_handle(stream, plan.device)), plan)
+    del keep
+    return out
+
+
+def route_batch_raw(plan, body, max_out, cat, cats, b_short, c_short, c_long, true_prompt=None, gamma=1.0,
+                    c_floor=0.5, decision=None, l_total=None, stream=None):
+    """Route on estimated L_total; returns (counts dict, misroute [short, long] or None)."""
+    tr, n = _raw(body, max_out, cat, true_prompt)
+    est, keep = _estimator(cats, gamma, c_floor)
+    counts = fp_route_counts()
+    mis = (c_u64 * 2)()
+    _check(lib.route_batch_raw(plan.handle, ctypes.byref(tr), n, ctypes.byref(est), b_short, c_short, c_long,
+                               decision.data_ptr() if decision is not None else None,
+                               l_total.data_ptr() if l_total is not None else None, ctypes.byref(counts),
+                               mis, _stream_handle(stream, plan.device)), plan)
+    del keep
+    c = {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}
+    return c, ([int(mis[0]), int(mis[1])] if true_prompt is not None else None)

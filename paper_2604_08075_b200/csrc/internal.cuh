@@ -26,6 +26,14 @@ struct TraceArgs {
   uint32_t want_mass;
   unsigned long long *g_cnt;   // [n_edges + 1] global accumulators (bins)
   unsigned long long *g_mass;  // [n_edges + 1]
+  // raw columns (NEXT-1; body != nullptr selects them instead of len)
+  const uint32_t *body = nullptr;   // |r| bytes
+  const uint32_t *maxout = nullptr; // max_output_tokens
+  const uint8_t *cat = nullptr;     // category
+  const double *calib = nullptr;    // device [n_cats][2] (c_hat, sigma_hat)
+  uint32_t n_cats = 0;
+  uint32_t raw_vec = 0;             // set by launch_trace
+  double gamma = 1.0, c_floor = 0.5;
 };
 cudaError_t launch_trace(const TraceArgs &a, int grid, int block, size_t smem, cudaStream_t s);
 size_t trace_smem_bytes(const TraceArgs &a, int block);
@@ -40,6 +48,23 @@ struct RouteArgs {
   unsigned long long *g_counts;  // [5]
 };
 cudaError_t launch_route(const RouteArgs &a, int grid, int block, cudaStream_t s);
+
+// K4r: route_batch_raw (NEXT-1): Alg. 1 on estimated L_total + mis-route counts
+struct RouteRawArgs {
+  const uint32_t *body, *maxout;
+  const uint8_t *cat;
+  const uint32_t *true_prompt;      // nullable
+  const double *calib;              // device [n_cats][2]
+  uint32_t n_cats;
+  double gamma, c_floor;
+  uint8_t *decision;                // nullable
+  uint32_t *l_total;                // nullable: estimated L_total out
+  uint64_t n;
+  uint32_t b, cs, cl;
+  unsigned long long *g_counts;     // [5]
+  unsigned long long *g_mis;        // [2] short, long
+};
+cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStream_t s);
 cudaError_t route_occupancy(int block, int *per_sm);
 
 // ---- K3: candidate evaluation + argmin ---------------------------------------

@@ -231,3 +231,80 @@ cudaError_t launch_route(const RouteArgs &a0, int grid, int block, cudaStream_t 
 }
 
 }  // namespace fp
+
+// ============================ K4r: route_batch_raw ====================================
+// NEXT-1: route_batch from the raw columns. Per request the conservative
+// ratio c* (Eq. `conservative`; shared-memory table per block)
+// gives L_total = ceil(|r| / c*) + max_output (Eq. `budget`),
+// which is routed as in K4. With the true prompt tokens the kernel also
+// counts Table 5's mis-routes: requests sent to a pool whose
+// C_max their TRUE total exceeds. Grid-stride over elements (coalesced 4-B
+// loads of every column; 13-21 B/request).
+namespace fp {
+namespace {
+
+__device__ __forceinline__ uint32_t est_raw(uint32_t bytes, uint32_t mo, uint32_t k, const double *cstar,
+                                            uint32_t ncat) {
+  k = k < ncat ? k : ncat - 1;                               // R23
+  const double lin = ceil(__ddiv_rn(__uint2double_rn(bytes), cstar[k]));
+  if (!(lin < 4294967296.0)) return 0xFFFFFFFFu;
+  const unsigned long long t = (unsigned long long)lin + mo;
+  return t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+__global__ void __launch_bounds__(512) k4_route_raw(RouteRawArgs a) {
+  __shared__ double cstar[256];
+  __shared__ unsigned long long red[7][16];
+  for (uint32_t k = threadIdx.x; k < a.n_cats; k += blockDim.x) {
+    double cs = __dsub_rn(a.calib[2 * k], __dmul_rn(a.gamma, a.calib[2 * k + 1]));
+    if (!(cs >= a.c_floor)) cs = a.c_floor;
+    cstar[k] = cs;
+  }
+  __syncthreads();
+  unsigned long long ns = 0, nl = 0, nr = 0, ms = 0, ml = 0, mis_s = 0, mis_l = 0;
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += S) {
+    const uint32_t mo = a.maxout[i];
+    const uint32_t L = est_raw(a.body[i], mo, a.cat[i], cstar, a.n_cats);
+    const bool pa = L > a.b, pb = L > a.cs, pc = L > a.cl;
+    const uint32_t d = (pa ? 1u : 0u) + (pb ? 4u : 0u) + (pc ? 9u : 0u);
+    if (pc) { ++nr; } else if (pa) { ++nl; ml += L; } else { ++ns; ms += L; }
+    if (a.true_prompt) {
+      const unsigned long long t = (unsigned long long)a.true_prompt[i] + mo;
+      mis_s += (!pa && t > a.cs) ? 1ull : 0ull;
+      mis_l += (pa && !pc && t > a.cl) ? 1ull : 0ull;
+    }
+    if (a.decision) a.decision[i] = (uint8_t)d;
+    if (a.l_total) a.l_total[i] = L;
+  }
+  unsigned long long v[7] = {ns, nl, nr, ms, ml, mis_s, mis_l};
+#pragma unroll
+  for (int k = 0; k < 7; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) red[k][w] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    unsigned long long t = 0;
+    for (int j = 0; j < (int)(blockDim.x >> 5); ++j) t += red[threadIdx.x][j];
+    if (t) atomicAdd(threadIdx.x < 5 ? a.g_counts + threadIdx.x : a.g_mis + (threadIdx.x - 5), t);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStream_t s) {
+  if (a.n == 0) return cudaSuccess;
+  if (block > 512 || (block & 31) || a.n_cats == 0 || a.n_cats > 256) return cudaErrorInvalidValue;
+  const uint64_t need = (a.n + block - 1) / block;
+  const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
+  k4_route_raw<<<g, block, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

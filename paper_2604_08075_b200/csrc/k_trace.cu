@@ -145,7 +145,48 @@ __device__ __forceinline__ void flush_mass(const K1Ctx &c, uint32_t nbins) {
   }
 }
 
-template <int LUTW, int R, bool SPLIT, bool MASS>
+// ---- element sources -------------------------------------------------------------
+// Plain: the caller's L_total column. Raw (NEXT-1): body bytes, max_output and
+// category columns; L_total is estimated in the kernel with Eq. `budget`
+// from the per-category conservative ratio c* of Eq.
+// `conservative`, computed once per block into shared memory.
+struct SrcPlain {
+  const uint32_t *len;
+  __device__ __forceinline__ uint4 load4(const uint4 *p4, uint64_t i) const { return ldg_stream(p4 + i); }
+  __device__ __forceinline__ uint32_t load1(uint64_t i) const { return len[i]; }
+};
+
+__device__ __forceinline__ uint32_t estimate_l_total(uint32_t bytes, uint32_t mo, uint32_t k, const double *cstar,
+                                                     uint32_t ncat) {
+  k = k < ncat ? k : ncat - 1;                             // R23: unknown -> last ("mixed")
+  const double lin = ceil(__ddiv_rn(__uint2double_rn(bytes), cstar[k]));
+  if (!(lin < 4294967296.0)) return 0xFFFFFFFFu;
+  const unsigned long long t = (unsigned long long)lin + mo;
+  return t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+}
+
+struct SrcRaw {
+  const uint32_t *body, *mo;
+  const uint8_t *cat;
+  const double *cstar;   // shared memory [ncat]
+  uint32_t ncat;
+  uint64_t base;         // element offset of uint4 index 0 (the aligned head)
+  __device__ __forceinline__ uint4 load4(const uint4 *, uint64_t i) const {
+    const uint64_t e = base + 4 * i;
+    const uint4 b = ldg_stream(reinterpret_cast<const uint4 *>(body + e));
+    const uint4 m = ldg_stream(reinterpret_cast<const uint4 *>(mo + e));
+    const uint32_t k = __ldg(reinterpret_cast<const unsigned int *>(cat + e));
+    return make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, cstar, ncat),
+                      estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, cstar, ncat),
+                      estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, cstar, ncat),
+                      estimate_l_total(b.w, m.w, k >> 24, cstar, ncat));
+  }
+  __device__ __forceinline__ uint32_t load1(uint64_t i) const {
+    return estimate_l_total(body[i], mo[i], cat[i], cstar, ncat);
+  }
+};
+
+template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW>
 __global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
@@ -154,64 +195,93 @@ __global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
   K1Ctx c;
   c.lut = smem;
   c.acc = reinterpret_cast<unsigned long long *>(smem + lut_bytes);
-  c.hist = reinterpret_cast<unsigned char *>(c.acc + nbins);
+  double *cstar = reinterpret_cast<double *>(c.acc + nbins);          // RAW: [ncat]
+  c.hist = reinterpret_cast<unsigned char *>(cstar + (RAW ? a.n_cats : 0));
   c.clampv = a.max_edge + 1u;
   c.round = (1u << a.shift) - 1u;
   c.shift = a.shift;
   c.n_edges = a.n_edges;
   c.lane4 = (R == 32) ? (threadIdx.x & 31u) * 4u : 0u;
 
-  // stage the LUT (or the edge list) and clear the histogram
+  // stage the LUT (or the edge list), the routing ratios, and clear the histogram
   {
     const uint32_t *src = (LUTW == 0) ? a.edges : reinterpret_cast<const uint32_t *>(a.lut);
     uint32_t *dst = reinterpret_cast<uint32_t *>(smem);
     // the device tables are padded to 16 B inside the plan's table blob
     for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) dst[i] = src[i];
     for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) c.acc[i] = 0ull;
+    if (RAW) {
+      // c* = c_hat - gamma * sigma_hat, bounded below by c_floor (R22)
+      for (uint32_t k = threadIdx.x; k < a.n_cats; k += blockDim.x) {
+        double cs = __dsub_rn(a.calib[2 * k], __dmul_rn(a.gamma, a.calib[2 * k + 1]));
+        if (!(cs >= a.c_floor)) cs = a.c_floor;
+        cstar[k] = cs;
+      }
+    }
     const uint32_t words = nbins * R * (MASS ? (SPLIT ? 3u : 2u) : 1u);
     uint32_t *h = reinterpret_cast<uint32_t *>(c.hist);
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) h[i] = 0u;
   }
   __syncthreads();
 
-  // misaligned head (< 4 elements) and the aligned uint4 body
-  const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.len) & 15u) >> 2);
-  const uint64_t head = mis ? umin64(a.n, 4u - mis) : 0u;
-  const uint64_t n4 = (a.n - head) >> 2;                       // uint4 count of the body
-  const uint64_t tail_first = head + (n4 << 2);
-  if (blockIdx.x == 0 && threadIdx.x < head) add_one<LUTW, R, SPLIT, MASS>(c, a.len[threadIdx.x]);
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first)
-    add_one<LUTW, R, SPLIT, MASS>(c, a.len[tail_first + threadIdx.x]);
-
-  const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
-  // grid-stride stripes: at every step the whole grid reads kUnroll contiguous
-  // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
-  // 6.6 TB/s for per-block contiguous tiles; profiles/r01_microbench_*).
-  // The step count is uniform over the grid so the flush barrier is safe.
-  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;         // uint4 per stripe
-  const uint64_t step4 = S * kUnroll;
-  const uint64_t full_steps = n4 / step4;
-  const uint64_t nsteps = (n4 + step4 - 1) / step4;
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t me = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   uint32_t since_flush = 0;
-  for (uint64_t k = 0; k < nsteps; ++k) {
-    const uint64_t base = k * step4 + me;
-    if (k < full_steps) {
-      uint4 v[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ldg_stream(body + base + u * S);
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
-    } else {
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u)
-        if (base + u * S < n4) add_four<LUTW, R, SPLIT, MASS>(c, ldg_stream(body + base + u * S));
-    }
-    if (MASS && ++since_flush == a.flush_iters) {
+  auto maybe_flush = [&](uint32_t period) {
+    if (MASS && ++since_flush == period) {
       since_flush = 0;
       __syncthreads();
       flush_mass<R, SPLIT>(c, nbins);
       __syncthreads();
+    }
+  };
+
+  // element source; RAW without a common 16-B phase of the columns -> scalar rounds
+  SrcPlain sp{a.len};
+  SrcRaw sr{a.body, a.maxout, a.cat, cstar, a.n_cats, 0};
+  const uintptr_t anchor = RAW ? reinterpret_cast<uintptr_t>(a.body) : reinterpret_cast<uintptr_t>(a.len);
+  const uint32_t mis = (uint32_t)((anchor & 15u) >> 2);
+  const uint64_t head = (RAW && !a.raw_vec) ? a.n : (mis ? umin64(a.n, 4u - mis) : 0u);
+  const uint64_t n4 = (a.n - head) >> 2;                       // uint4 count of the body
+  const uint64_t tail_first = head + (n4 << 2);
+  sr.base = head;
+  auto load1 = [&](uint64_t i) -> uint32_t { return RAW ? sr.load1(i) : sp.load1(i); };
+
+  if (RAW && !a.raw_vec) {
+    // scalar rounds over the whole trace (uniform trip count: flush-safe)
+    const uint64_t rounds = (a.n + S - 1) / S;
+    for (uint64_t r = 0; r < rounds; ++r) {
+      const uint64_t i = r * S + me;
+      if (i < a.n) add_one<LUTW, R, SPLIT, MASS>(c, load1(i));
+      maybe_flush(a.flush_iters * 4u * kUnroll);
+    }
+  } else {
+    if (blockIdx.x == 0 && threadIdx.x < head) add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first)
+      add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
+    const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
+    // grid-stride stripes: at every step the whole grid reads kUnroll contiguous
+    // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
+    // 6.6 TB/s for per-block contiguous tiles; profiles/r01_microbench_*).
+    // The step count is uniform over the grid so the flush barrier is safe.
+    const uint64_t step4 = S * kUnroll;
+    const uint64_t full_steps = n4 / step4;
+    const uint64_t nsteps = (n4 + step4 - 1) / step4;
+    for (uint64_t k = 0; k < nsteps; ++k) {
+      const uint64_t base = k * step4 + me;
+      if (k < full_steps) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) v[u] = RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S);
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+          if (base + u * S < n4)
+            add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S));
+      }
+      maybe_flush(a.flush_iters);
     }
   }
   __syncthreads();
@@ -244,6 +314,7 @@ __global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
 
 // ---- variant selection ----------------------------------------------------------
 struct Variant {
+  bool raw;      // estimate L_total from raw columns (NEXT-1)
   int lutw;      // 1, 2 (LUT bytes per cell) or 0 (binary search)
   int R;         // 32 lane-private replicas or 1
   bool split;    // 16-bit mass halves
@@ -257,11 +328,12 @@ size_t smem_for(const TraceArgs &a, const Variant &v) {
   size_t lut = v.lutw == 0 ? (size_t)a.n_edges * 4 : (size_t)a.lut_cells * v.lutw;
   lut = (lut + 15) & ~size_t(15);
   const uint32_t words = v.mass ? (v.split ? 3u : 2u) : 1u;
-  return lut + (size_t)nbins * 8 + (size_t)nbins * v.R * words * 4;
+  return lut + (size_t)nbins * 8 + (v.raw ? (size_t)a.n_cats * 8 : 0) + (size_t)nbins * v.R * words * 4;
 }
 
 Variant choose(const TraceArgs &a, int block) {
   Variant v;
+  v.raw = a.body != nullptr;
   v.lutw = a.lut_cells ? (a.lut_u8 ? 1 : 2) : 0;
   v.mass = a.want_mass != 0;
   v.R = 32;
@@ -288,15 +360,16 @@ uint32_t flush_iters_for(const TraceArgs &a, const Variant &v, int block) {
   return (uint32_t)it;
 }
 
-template <int LUTW, int R, bool SPLIT, bool MASS>
-void *kernel_ptr() { return reinterpret_cast<void *>(&k1_trace<LUTW, R, SPLIT, MASS>); }
+template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW>
+void *kernel_ptr() { return reinterpret_cast<void *>(&k1_trace<LUTW, R, SPLIT, MASS, RAW>); }
 
-void *pick_kernel(const Variant &v) {
+template <bool RAW>
+void *pick_kernel_src(const Variant &v) {
 #define FP_K(L)                                                                  \
   if (v.lutw == L) {                                                             \
-    if (!v.mass) return v.R == 32 ? kernel_ptr<L, 32, false, false>() : kernel_ptr<L, 1, false, false>(); \
-    if (v.R == 32) return v.split ? kernel_ptr<L, 32, true, true>() : kernel_ptr<L, 32, false, true>();   \
-    return v.split ? kernel_ptr<L, 1, true, true>() : kernel_ptr<L, 1, false, true>();                    \
+    if (!v.mass) return v.R == 32 ? kernel_ptr<L, 32, false, false, RAW>() : kernel_ptr<L, 1, false, false, RAW>(); \
+    if (v.R == 32) return v.split ? kernel_ptr<L, 32, true, true, RAW>() : kernel_ptr<L, 32, false, true, RAW>();   \
+    return v.split ? kernel_ptr<L, 1, true, true, RAW>() : kernel_ptr<L, 1, false, true, RAW>();                    \
   }
   FP_K(0)
   FP_K(1)
@@ -304,6 +377,8 @@ void *pick_kernel(const Variant &v) {
 #undef FP_K
   return nullptr;
 }
+
+void *pick_kernel(const Variant &v) { return v.raw ? pick_kernel_src<true>(v) : pick_kernel_src<false>(v); }
 
 }  // namespace
 
@@ -323,8 +398,24 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
   // u32 per-block counters: keep every block below 2^31 requests per launch
   const uint64_t cap = (uint64_t)grid * (1ull << 31);
   void *k = pick_kernel(v);
+  if (v.raw) {
+    // the raw variants carry the c* table: size and opt in per launch
+    smem = smem_for(a, v);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
   for (uint64_t off = 0; off < a0.n; off += cap) {
-    a.len = a0.len + off;
+    if (a0.len) a.len = a0.len + off;
+    if (a0.body) {
+      a.body = a0.body + off;
+      a.maxout = a0.maxout + off;
+      a.cat = a0.cat + off;
+      const uintptr_t b = reinterpret_cast<uintptr_t>(a.body), m = reinterpret_cast<uintptr_t>(a.maxout),
+                      k = reinterpret_cast<uintptr_t>(a.cat);
+      const uint64_t mis = (b & 15u) >> 2, head = mis ? 4 - mis : 0;
+      // vector loads need the three columns in the same 16-B phase
+      a.raw_vec = ((b & 3u) == 0) && ((m & 15u) == (b & 15u)) && (((k + head) & 3u) == 0);
+    }
     a.n = std::min<uint64_t>(cap, a0.n - off);
     void *args[] = {&a};
     cudaError_t e = cudaLaunchKernel(k, dim3(grid), dim3(block), args, smem, s);

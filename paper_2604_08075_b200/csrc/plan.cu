@@ -98,7 +98,8 @@ struct fp_plan {
   TraceArgs ta{};
   EvalArgs ea{};
   unsigned long long *d_hist = nullptr;    // [2][nbins]
-  unsigned long long *d_rcounts = nullptr; // [5]
+  unsigned long long *d_rcounts = nullptr; // [8]: route counts [5], mis-routes [2]
+  double *d_calib = nullptr;               // [256][2] estimator snapshot
   fp_candidate *d_best = nullptr;          // [world][n_models]
   fp_candidate *d_results = nullptr;       // [cand_count] (lazy)
   BlockBest *d_block_best = nullptr;
@@ -366,7 +367,7 @@ fp_status upload(fp_plan *p) {
   CUDA_TRY(p, cudaMemcpy(p->d_blob, blob.data(), p->blob_bytes, cudaMemcpyHostToDevice), "upload tables");
   CUDA_TRY(p, cudaMalloc(&p->d_hist, 2ull * p->nbins * 8), "cudaMalloc hist");
   CUDA_TRY(p, cudaMemset(p->d_hist, 0, 2ull * p->nbins * 8), "memset hist");
-  CUDA_TRY(p, cudaMalloc(&p->d_rcounts, 5 * 8), "cudaMalloc counts");
+  CUDA_TRY(p, cudaMalloc(&p->d_rcounts, 8 * 8), "cudaMalloc counts");
   CUDA_TRY(p, cudaMalloc(&p->d_best, (size_t)p->world * M * sizeof(fp_candidate)), "cudaMalloc best");
   CUDA_TRY(p, cudaMemset(p->d_best, 0, (size_t)p->world * M * sizeof(fp_candidate)), "memset best");
 
@@ -697,6 +698,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_block_best);
     cudaFree(p->d_done);
     cudaFree(p->d_resident);
+    cudaFree(p->d_calib);
     for (int i = 0; i < 2; ++i) {
       cudaFree(p->d_stage[i]);
       if (p->ev_copied[i]) cudaEventDestroy(p->ev_copied[i]);
@@ -804,7 +806,8 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
 
 namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
-                     fp_candidate *h_results, void *stream, uint32_t *resident);
+                     fp_candidate *h_results, void *stream, uint32_t *resident,
+                     const TraceArgs *raw = nullptr);
 }
 
 fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
@@ -823,6 +826,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   if (n_local && len && is_host_pointer(len)) {
     if (p->resident_cap < n_local) {
       cudaFree(p->d_resident);
+    cudaFree(p->d_calib);
       p->d_resident = nullptr;
       p->resident_cap = 0;
       CUDA_TRY(p, cudaMalloc(&p->d_resident, n_local * 4), "cudaMalloc resident trace");
@@ -844,10 +848,126 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
 }
 
 namespace {
-fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
-                     fp_candidate *h_results, void *stream, uint32_t *resident) {
+// Validate an estimator and upload its snapshot (c_hat, sigma) to d_calib.
+fp_status upload_estimator(fp_plan *p, const fp_estimator *est, cudaStream_t s) {
+  if (!est || !est->cats || est->n_cats == 0 || est->n_cats > 256)
+    return fail(p, FP_ERR_INVALID_ARG, "estimator needs 1..256 categories");
+  if (!std::isfinite(est->gamma) || est->gamma < 0.0 || !std::isfinite(est->c_floor) || !(est->c_floor > 0.0))
+    return fail(p, FP_ERR_INVALID_ARG, "estimator needs gamma >= 0 and c_floor > 0 (finite)");
+  std::vector<double> v(2 * est->n_cats);
+  for (uint32_t k = 0; k < est->n_cats; ++k) {
+    if (!std::isfinite(est->cats[k].c_hat) || !std::isfinite(est->cats[k].sigma_hat) || est->cats[k].sigma_hat < 0)
+      return fail(p, FP_ERR_INVALID_ARG, "category %u: c_hat finite, sigma_hat finite and >= 0", k);
+    v[2 * k] = est->cats[k].c_hat;
+    v[2 * k + 1] = est->cats[k].sigma_hat;
+  }
+  if (!p->d_calib) CUDA_TRY(p, cudaMalloc(&p->d_calib, 512 * sizeof(double)), "cudaMalloc calib");
+  // pageable source: staged by the driver before the call returns
+  CUDA_TRY(p, cudaMemcpyAsync(p->d_calib, v.data(), v.size() * 8, cudaMemcpyHostToDevice, s), "H2D calib");
+  return FP_OK;
+}
+
+fp_status check_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n, bool need_true) {
+  if (!t) return fail(p, FP_ERR_INVALID_ARG, "raw trace is NULL");
+  if (!n) return FP_OK;
+  if (!t->body_bytes || !t->max_output_tokens || !t->category)
+    return fail(p, FP_ERR_INVALID_ARG, "raw trace columns must be set");
+  if (is_host_pointer(t->body_bytes) || is_host_pointer(t->max_output_tokens) || is_host_pointer(t->category) ||
+      (need_true && t->true_prompt_tokens && is_host_pointer(t->true_prompt_tokens)))
+    return fail(p, FP_ERR_INVALID_ARG, "raw trace columns must be device memory");
+  return FP_OK;
+}
+}  // namespace
+
+fp_status sweep_thresholds_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, const fp_estimator *est,
+                               double rate_rps, fp_candidate *h_results, void *stream) {
   if (!p) return FP_ERR_INVALID_ARG;
-  if (n_local && !d_len) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
+  fp_status st = check_raw(p, t, n_local, false);
+  if (st != FP_OK) return st;
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = upload_estimator(p, est, s);
+  if (st != FP_OK) return st;
+  TraceArgs a = p->ta;
+  a.len = nullptr;
+  a.n = n_local;
+  a.body = t->body_bytes;
+  a.maxout = t->max_output_tokens;
+  a.cat = t->category;
+  a.calib = p->d_calib;
+  a.n_cats = est->n_cats;
+  a.gamma = est->gamma;
+  a.c_floor = est->c_floor;
+  return sweep_impl(p, nullptr, n_local, rate_rps, h_results, stream, nullptr, &a);
+}
+
+fp_status route_batch_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, const fp_estimator *est,
+                          uint32_t b_short, uint32_t c_short, uint32_t c_long, uint8_t *d_decision,
+                          uint32_t *d_l_total, fp_route_counts *h_counts, uint64_t *h_misroute, void *stream) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (!(b_short >= 1 && b_short <= c_short && c_short <= c_long))
+    return fail(p, FP_ERR_INVALID_ARG, "need 1 <= B_short <= C_S <= C_L (S:316-321)");
+  fp_status st = check_raw(p, t, n_local, true);
+  if (st != FP_OK) return st;
+  if (n_local && ((d_decision && is_host_pointer(d_decision)) || (d_l_total && is_host_pointer(d_l_total))))
+    return fail(p, FP_ERR_INVALID_ARG, "outputs must be device memory");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = upload_estimator(p, est, s);
+  if (st != FP_OK) return st;
+  CUDA_TRY(p, cudaMemsetAsync(p->d_rcounts, 0, 7 * 8, s), "memset counts");
+  if (n_local) {
+    RouteRawArgs a{};
+    a.body = t->body_bytes;
+    a.maxout = t->max_output_tokens;
+    a.cat = t->category;
+    a.true_prompt = t->true_prompt_tokens;
+    a.calib = p->d_calib;
+    a.n_cats = est->n_cats;
+    a.gamma = est->gamma;
+    a.c_floor = est->c_floor;
+    a.decision = d_decision;
+    a.l_total = d_l_total;
+    a.n = n_local;
+    a.b = b_short;
+    a.cs = c_short;
+    a.cl = c_long;
+    a.g_counts = p->d_rcounts;
+    a.g_mis = p->d_rcounts + 5;
+    LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
+    cudaError_t e = launch_route_raw(a, p->k4_grid, p->k4_block, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "route_batch_raw launch");
+    ++p->launches;
+  }
+  if (p->world > 1) {
+    st = all_reduce_u64(p, p->d_rcounts, 7, s, "all-reduce(route counts)");
+    if (st != FP_OK) return st;
+  }
+  p->last_stream = s;
+  if (h_counts || h_misroute) {
+    unsigned long long *c = p->h_small + 2ull * p->nbins;
+    CUDA_TRY(p, cudaMemcpyAsync(c, p->d_rcounts, 7 * 8, cudaMemcpyDeviceToHost, s), "D2H counts");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    if (h_counts) {
+      h_counts->n_short = c[0];
+      h_counts->n_long = c[1];
+      h_counts->n_reject = c[2];
+      h_counts->mass_short = c[3];
+      h_counts->mass_long = c[4];
+    }
+    if (h_misroute) {
+      h_misroute[0] = c[5];
+      h_misroute[1] = c[6];
+    }
+  }
+  return FP_OK;
+}
+
+namespace {
+fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
+                     fp_candidate *h_results, void *stream, uint32_t *resident, const TraceArgs *raw) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (n_local && !d_len && !raw) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
     return fail(p, FP_ERR_INVALID_ARG, "rate_rps must be finite and > 0");
   if (p->world == 1 && n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace (S:170)");
@@ -855,7 +975,15 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   cudaStream_t s = (cudaStream_t)stream;
   // K1: trace pass into the global bin histogram
   CUDA_TRY(p, cudaMemsetAsync(p->d_hist, 0, 2ull * p->nbins * 8, s), "memset hist");
-  fp_status st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t) {
+  fp_status st = FP_OK;
+  if (raw) {
+    if (n_local) {
+      LaunchTimer lt(p, FP_KERNEL_TRACE, s);
+      cudaError_t e = launch_trace(*raw, p->k1_grid, p->k1_block, p->k1_smem, s);
+      if (e != cudaSuccess) return cuda_fail(p, e, "trace pass (raw) launch");
+      ++p->launches;
+    }
+  } else st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t) {
     TraceArgs t = p->ta;
     t.len = ptr;
     t.n = n;
