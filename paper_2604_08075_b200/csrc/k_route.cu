@@ -235,49 +235,80 @@ cudaError_t launch_route(const RouteArgs &a0, int grid, int block, cudaStream_t 
 // ============================ K4r: route_batch_raw ====================================
 // NEXT-1: route_batch from the raw columns. Per request the conservative
 // ratio c* (Eq. `conservative`; shared-memory table per block)
-// gives L_total = ceil(|r| / c*) + max_output (Eq. `budget`),
-// which is routed as in K4. With the true prompt tokens the kernel also
-// counts Table 5's mis-routes: requests sent to a pool whose
-// C_max their TRUE total exceeds. Grid-stride over elements (coalesced 4-B
-// loads of every column; 13-21 B/request).
+// gives L_total = ceil(|r| / c*) + max_output (Eq. `budget`, P:425-429;
+// estimate.cuh), which is routed as in K4. With the true prompt tokens the
+// kernel also counts Table 5's mis-routes: requests sent to a
+// pool whose C_max their TRUE total exceeds. Per-block tiles of 4 requests
+// per thread (128-bit loads of each u32 column, 32-bit load of 4 category
+// bytes, 32-bit store of 4 decisions) when the columns share a 16-B phase;
+// scalar grid-stride otherwise.
+#include "estimate.cuh"
+
 namespace fp {
 namespace {
 
-__device__ __forceinline__ uint32_t est_raw(uint32_t bytes, uint32_t mo, uint32_t k, const double *cstar,
-                                            uint32_t ncat) {
-  k = k < ncat ? k : ncat - 1;                               // R23
-  const double lin = ceil(__ddiv_rn(__uint2double_rn(bytes), cstar[k]));
-  if (!(lin < 4294967296.0)) return 0xFFFFFFFFu;
-  const unsigned long long t = (unsigned long long)lin + mo;
-  return t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+struct RawAcc {
+  unsigned long long ns = 0, nl = 0, nr = 0, ms = 0, ml = 0, mis_s = 0, mis_l = 0;
+};
+
+__device__ __forceinline__ uint32_t route_raw_one(const RouteRawArgs &a, uint32_t L, uint32_t mo, uint32_t tp,
+                                                  RawAcc &c) {
+  const bool pa = L > a.b, pb = L > a.cs, pc = L > a.cl;
+  if (pc) { ++c.nr; } else if (pa) { ++c.nl; c.ml += L; } else { ++c.ns; c.ms += L; }
+  if (a.true_prompt) {
+    const unsigned long long t = (unsigned long long)tp + mo;
+    c.mis_s += (!pa && t > a.cs) ? 1ull : 0ull;
+    c.mis_l += (pa && !pc && t > a.cl) ? 1ull : 0ull;
+  }
+  return (pa ? 1u : 0u) + (pb ? 4u : 0u) + (pc ? 9u : 0u);
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(512) k4_route_raw(RouteRawArgs a) {
-  __shared__ double cstar[256];
+  __shared__ __align__(16) double cst[1024];
   __shared__ unsigned long long red[7][16];
-  for (uint32_t k = threadIdx.x; k < a.n_cats; k += blockDim.x) {
-    double cs = __dsub_rn(a.calib[2 * k], __dmul_rn(a.gamma, a.calib[2 * k + 1]));
-    if (!(cs >= a.c_floor)) cs = a.c_floor;
-    cstar[k] = cs;
-  }
+  setup_cstar(a.calib, a.n_cats, a.gamma, a.c_floor, cst);
   __syncthreads();
-  unsigned long long ns = 0, nl = 0, nr = 0, ms = 0, ml = 0, mis_s = 0, mis_l = 0;
+  RawAcc acc;
   const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += S) {
+  const uint64_t me = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  auto one = [&](uint64_t i) {
     const uint32_t mo = a.maxout[i];
-    const uint32_t L = est_raw(a.body[i], mo, a.cat[i], cstar, a.n_cats);
-    const bool pa = L > a.b, pb = L > a.cs, pc = L > a.cl;
-    const uint32_t d = (pa ? 1u : 0u) + (pb ? 4u : 0u) + (pc ? 9u : 0u);
-    if (pc) { ++nr; } else if (pa) { ++nl; ml += L; } else { ++ns; ms += L; }
-    if (a.true_prompt) {
-      const unsigned long long t = (unsigned long long)a.true_prompt[i] + mo;
-      mis_s += (!pa && t > a.cs) ? 1ull : 0ull;
-      mis_l += (pa && !pc && t > a.cl) ? 1ull : 0ull;
-    }
+    const uint32_t L = estimate_l_total(a.body[i], mo, a.cat[i], cst, a.n_cats);
+    const uint32_t d = route_raw_one(a, L, mo, a.true_prompt ? a.true_prompt[i] : 0u, acc);
     if (a.decision) a.decision[i] = (uint8_t)d;
     if (a.l_total) a.l_total[i] = L;
+  };
+  if constexpr (!VEC) {
+    for (uint64_t i = me; i < a.n; i += S) one(i);
+  } else {
+    const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.body) & 15u) >> 2);
+    const uint64_t head = mis ? (a.n < 4u - mis ? a.n : 4u - mis) : 0u;
+    const uint64_t n4 = (a.n - head) >> 2;
+    const uint64_t tail_first = head + (n4 << 2);
+    if (blockIdx.x == 0 && threadIdx.x < head) one(threadIdx.x);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) one(tail_first + threadIdx.x);
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(a.body + head);
+    const uint4 *m4 = reinterpret_cast<const uint4 *>(a.maxout + head);
+    const uint4 *t4 = a.true_prompt ? reinterpret_cast<const uint4 *>(a.true_prompt + head) : nullptr;
+    const uint32_t *c4 = reinterpret_cast<const uint32_t *>(a.cat + head);
+    uint32_t *d4 = a.decision ? reinterpret_cast<uint32_t *>(a.decision + head) : nullptr;
+    uint4 *l4 = a.l_total ? reinterpret_cast<uint4 *>(a.l_total + head) : nullptr;
+    for (uint64_t i = me; i < n4; i += S) {
+      const uint4 b = ldg_stream(b4 + i), m = ldg_stream(m4 + i);
+      const uint4 t = t4 ? ldg_stream(t4 + i) : make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t k = __ldg(c4 + i);
+      const uint4 L = make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, cst, a.n_cats),
+                                 estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, cst, a.n_cats),
+                                 estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, cst, a.n_cats),
+                                 estimate_l_total(b.w, m.w, k >> 24, cst, a.n_cats));
+      const uint32_t w = route_raw_one(a, L.x, m.x, t.x, acc) | (route_raw_one(a, L.y, m.y, t.y, acc) << 8) |
+                         (route_raw_one(a, L.z, m.z, t.z, acc) << 16) | (route_raw_one(a, L.w, m.w, t.w, acc) << 24);
+      if (d4) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(d4 + i), "r"(w) : "memory");
+      if (l4) l4[i] = L;
+    }
   }
-  unsigned long long v[7] = {ns, nl, nr, ms, ml, mis_s, mis_l};
+  unsigned long long v[7] = {acc.ns, acc.nl, acc.nr, acc.ms, acc.ml, acc.mis_s, acc.mis_l};
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
 #pragma unroll
@@ -303,7 +334,15 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
   if (block > 512 || (block & 31) || a.n_cats == 0 || a.n_cats > 256) return cudaErrorInvalidValue;
   const uint64_t need = (a.n + block - 1) / block;
   const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
-  k4_route_raw<<<g, block, 0, s>>>(a);
+  // vector path: every column in the same 16-B phase (cat / decision in the same 4-B phase)
+  const uintptr_t b = reinterpret_cast<uintptr_t>(a.body);
+  const uint64_t mis = (b & 15u) >> 2, head = mis ? 4 - mis : 0;
+  auto same16 = [&](const void *p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15u) == (b & 15u); };
+  auto al4 = [&](const void *p) { return p == nullptr || ((reinterpret_cast<uintptr_t>(p) + head) & 3u) == 0; };
+  const bool vec = (b & 3u) == 0 && same16(a.maxout) && same16(a.true_prompt) && same16(a.l_total) && al4(a.cat) &&
+                   al4(a.decision);
+  if (vec) k4_route_raw<true><<<g, block, 0, s>>>(a);
+  else k4_route_raw<false><<<g, block, 0, s>>>(a);
   return cudaGetLastError();
 }
 

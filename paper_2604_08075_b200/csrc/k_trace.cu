@@ -27,6 +27,7 @@
 // hot loop is: VIMNMX, IADD, SHF (cell), LDS.U8 (bin), LEA (slot), ATOMS x2.
 #include <algorithm>
 #include <cstdio>
+#include "estimate.cuh"
 #include "internal.cuh"
 
 namespace fp {
@@ -156,15 +157,6 @@ struct SrcPlain {
   __device__ __forceinline__ uint32_t load1(uint64_t i) const { return len[i]; }
 };
 
-__device__ __forceinline__ uint32_t estimate_l_total(uint32_t bytes, uint32_t mo, uint32_t k, const double *cstar,
-                                                     uint32_t ncat) {
-  k = k < ncat ? k : ncat - 1;                             // R23: unknown -> last ("mixed")
-  const double lin = ceil(__ddiv_rn(__uint2double_rn(bytes), cstar[k]));
-  if (!(lin < 4294967296.0)) return 0xFFFFFFFFu;
-  const unsigned long long t = (unsigned long long)lin + mo;
-  return t > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
-}
-
 struct SrcRaw {
   const uint32_t *body, *mo;
   const uint8_t *cat;
@@ -187,7 +179,7 @@ struct SrcRaw {
 };
 
 template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW>
-__global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
+__global__ void __launch_bounds__(512, RAW ? 3 : 1) k1_trace(TraceArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
   uint32_t lut_bytes = (LUTW == 0) ? a.n_edges * 4 : a.lut_cells * LUTW;
@@ -195,8 +187,10 @@ __global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
   K1Ctx c;
   c.lut = smem;
   c.acc = reinterpret_cast<unsigned long long *>(smem + lut_bytes);
-  double *cstar = reinterpret_cast<double *>(c.acc + nbins);          // RAW: [ncat]
-  c.hist = reinterpret_cast<unsigned char *>(cstar + (RAW ? a.n_cats : 0));
+  // RAW: [ncat][c*, 1/c*, lo, hi], 16-B aligned for the LDS.128 pairs
+  double *cstar = RAW ? reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(c.acc + nbins) + 15) & ~uintptr_t(15))
+                      : reinterpret_cast<double *>(c.acc + nbins);
+  c.hist = reinterpret_cast<unsigned char *>(cstar + (RAW ? 4 * a.n_cats : 0));
   c.clampv = a.max_edge + 1u;
   c.round = (1u << a.shift) - 1u;
   c.shift = a.shift;
@@ -210,14 +204,7 @@ __global__ void __launch_bounds__(512) k1_trace(TraceArgs a) {
     // the device tables are padded to 16 B inside the plan's table blob
     for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) dst[i] = src[i];
     for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) c.acc[i] = 0ull;
-    if (RAW) {
-      // c* = c_hat - gamma * sigma_hat, bounded below by c_floor (R22)
-      for (uint32_t k = threadIdx.x; k < a.n_cats; k += blockDim.x) {
-        double cs = __dsub_rn(a.calib[2 * k], __dmul_rn(a.gamma, a.calib[2 * k + 1]));
-        if (!(cs >= a.c_floor)) cs = a.c_floor;
-        cstar[k] = cs;
-      }
-    }
+    if (RAW) setup_cstar(a.calib, a.n_cats, a.gamma, a.c_floor, cstar);
     const uint32_t words = nbins * R * (MASS ? (SPLIT ? 3u : 2u) : 1u);
     uint32_t *h = reinterpret_cast<uint32_t *>(c.hist);
     for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) h[i] = 0u;
@@ -328,7 +315,7 @@ size_t smem_for(const TraceArgs &a, const Variant &v) {
   size_t lut = v.lutw == 0 ? (size_t)a.n_edges * 4 : (size_t)a.lut_cells * v.lutw;
   lut = (lut + 15) & ~size_t(15);
   const uint32_t words = v.mass ? (v.split ? 3u : 2u) : 1u;
-  return lut + (size_t)nbins * 8 + (v.raw ? (size_t)a.n_cats * 8 : 0) + (size_t)nbins * v.R * words * 4;
+  return lut + (size_t)nbins * 8 + (v.raw ? (size_t)a.n_cats * 32 + 8 : 0) + (size_t)nbins * v.R * words * 4;
 }
 
 Variant choose(const TraceArgs &a, int block) {
@@ -403,6 +390,14 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
     smem = smem_for(a, v);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
+    // the grid is persistent: never more blocks than are resident at once
+    // (the raw variant uses more registers than the plain one)
+    int per_sm = 0, dev = 0, sms = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, smem);
+    if (e != cudaSuccess) return e;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = std::min(grid, std::max(1, per_sm) * sms);
   }
   for (uint64_t off = 0; off < a0.n; off += cap) {
     if (a0.len) a.len = a0.len + off;

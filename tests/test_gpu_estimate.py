@@ -84,3 +84,28 @@ def test_raw_errors():
         fp.sweep_thresholds_raw(plan, b, b, c, STATIC, 1000.0, c_floor=0.0)    # floor must be > 0
     with pytest.raises(fp.FleetPlanError):
         fp.route_batch_raw(plan, b, b, c, STATIC, 9000, 8192, 65536)            # B > C_S
+
+
+@pytest.mark.parametrize("cstar", [4.0, 3.5, 4.48 * 0.98 - 0.1 * 4.48, 2.01 * 0.98 - 0.201, 0.5, 0.3, 1.0 / 3.0 + 1.0])
+def test_near_integer_quotients_are_exact(cstar):
+    """Adversarial bytes |r| = round(k c*) + {-2..2} put |r| / c* within a hair
+    of an integer, the case where ceil(fl(|r|/c*)) and ceil(|r|/c*) can differ;
+    the fast reciprocal path must defer to the IEEE division there."""
+    rng = np.random.default_rng(1)
+    k = rng.integers(1, 2**31 // max(1, int(cstar * 2)), 200_000).astype(np.float64)
+    base = np.round(k * cstar)
+    body = np.clip(base[:, None] + np.arange(-2, 3)[None, :], 0, 2**32 - 1).astype(np.uint32).ravel()
+    body = np.concatenate([body, rng.integers(0, 2**32 - 1, 100_000, dtype=np.uint64).astype(np.uint32),
+                           np.arange(0, 100_000, dtype=np.uint32)])
+    n = body.size
+    mo = np.zeros(n, np.uint32)
+    cat = np.zeros(n, np.uint8)
+    cats = [(cstar, 0.0)]
+    plan = fp.fleet_plan_create(**fp.desc_from_config(configs.c1()))
+    lt = torch.zeros(n, dtype=torch.int32, device="cuda")
+    fp.route_batch_raw(plan, _dev(body), _dev(mo), _dev(cat), cats, 8192, 8192, 65536, gamma=1.0, c_floor=0.25,
+                       l_total=lt)
+    ref = oracle.estimate(body, mo, cat, cats, 1.0, 0.25)
+    got = lt.cpu().numpy().view(np.uint32)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, (cstar, body[bad[:5]], got[bad[:5]], ref[bad[:5]])
