@@ -177,6 +177,39 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ GPU path ----
+def next1_fused_estimation(fp, cfg, n, reps=5):
+    """NEXT-1: sweep_thresholds_raw / route_batch_raw on raw request columns
+    (body bytes, max_output, category, true prompt tokens) of the same trace."""
+    import torch
+    from synth.gen import generate_raw_device
+    from synth.shapes import CAT_TRUE_RATIO
+    body, mo, cat, tp = generate_raw_device(cfg.shape, cfg.seed, 0, n)
+    cats = [(c * 0.98, 0.1 * c) for c in CAT_TRUE_RATIO]     # a calibrated snapshot (stated)
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=fp.FP_FLAG_KERNEL_TIMING)
+    dec = torch.empty(n, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        fp.sweep_thresholds_raw(plan, body, mo, cat, cats, cfg.rate_rps)
+        fp.route_batch_raw(plan, body, mo, cat, cats, 8192, 8192, 65536, true_prompt=tp, decision=dec)
+    torch.cuda.synchronize()
+    fp.fp_kernel_time_reset(plan)
+    for _ in range(reps):
+        fp.sweep_thresholds_raw(plan, body, mo, cat, cats, cfg.rate_rps)
+        counts, mis = fp.route_batch_raw(plan, body, mo, cat, cats, 8192, 8192, 65536, true_prompt=tp,
+                                         decision=dec)
+    k1 = fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
+    k4 = fp.fp_kernel_time(plan, fp.FP_KERNEL_ROUTE)
+    fp.fleet_plan_destroy(plan)
+    del body, mo, cat, tp, dec
+    torch.cuda.empty_cache()
+    k1ms, k4ms = k1[0] / k1[1], k4[0] / k4[1]
+    return {"n_requests": n, "k1_raw_ms": k1ms, "k1_raw_GBps": 9.0 * n / (k1ms / 1e3) / 1e9,
+            "k1_raw_requests_per_s": n / (k1ms / 1e3),
+            "k4_raw_ms": k4ms, "k4_raw_GBps": 14.0 * n / (k4ms / 1e3) / 1e9,
+            "misroute_short_long_at_8K": mis,
+            "note": "algorithmic bytes: sweep 9 B/request (bytes u32, max_output u32, category u8); "
+                    "route 13 B in + 1 B decision"}
+
+
 def k3_large_grid(fp, generate_device, reps=5):
     """K3 alone on a 2^24-candidate grid (SURVEY §8(d) ALU regime)."""
     import torch
@@ -331,6 +364,10 @@ def run_ours(args, cfg):
             "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
     if world == 1 and args.k3_grid:
         line["k3_large_grid"] = k3_large_grid(fp, generate_device)
+    if world == 1 and args.next1:
+        del d_len, d_dec
+        torch.cuda.empty_cache()
+        line["next1_fused_estimation"] = next1_fused_estimation(fp, cfg, n)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
@@ -348,6 +385,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next1", dest="next1", action="store_false",
+                    help="skip the fused token-budget estimation measurement (NEXT-1)")
     ap.add_argument("--no-k3-grid", dest="k3_grid", action="store_false",
                     help="skip the 2^24-candidate K3 measurement")
     ap.add_argument("--ref-sample", type=int, default=10_000_000,
