@@ -34,6 +34,8 @@ struct TraceArgs {
   uint32_t n_cats = 0;
   uint32_t raw_vec = 0;             // set by launch_trace
   double gamma = 1.0, c_floor = 0.5;
+  // per-request bin output (sweep_and_route's bin pass), nullable
+  uint8_t *bins_out = nullptr;
 };
 cudaError_t launch_trace(const TraceArgs &a, int grid, int block, size_t smem, cudaStream_t s);
 size_t trace_smem_bytes(const TraceArgs &a, int block);
@@ -65,6 +67,11 @@ struct RouteRawArgs {
   unsigned long long *g_mis;        // [2] short, long
 };
 cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStream_t s);
+
+// K4b: decisions from per-request bins (sweep_and_route): with iB, iCS, iCL
+// the indices in E of B, C_S, C_L, L <= e_j <=> bin <= j.
+cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, uint32_t iB, uint32_t iCS,
+                              uint32_t iCL, uint32_t n_bins_max, int grid, int block, cudaStream_t s);
 cudaError_t route_occupancy(int block, int *per_sm);
 
 // ---- K3: candidate evaluation + argmin ---------------------------------------

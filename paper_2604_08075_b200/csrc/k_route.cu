@@ -347,3 +347,93 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
 }
 
 }  // namespace fp
+
+// ============================ K4b: route from bins =====================================
+// sweep_and_route's second pass: the trace pass already wrote each request's
+// bin b = #{e in E : e < L} (1 B), and E contains B, C_S and C_L, so every
+// comparison of Alg. 1 is a bin comparison: L > e_j <=> b > j. Reads 1 B and
+// writes 1 B per request (16 per thread with 128-bit loads/stores when the two
+// buffers share a 16-B phase). The pool counts and masses of the split are
+// the best candidate's record (the same histogram), so no reduction here.
+namespace fp {
+namespace {
+
+__device__ __forceinline__ uint32_t dec_byte(uint32_t b, uint32_t iB, uint32_t iCS, uint32_t iCL) {
+  return (b > iB ? 1u : 0u) + (b > iCS ? 4u : 0u) + (b > iCL ? 9u : 0u);
+}
+
+// Four packed bins -> four decision bytes. SWAR when every bin < 128: adding
+// 0x7F - j to a byte sets its top bit iff the byte is > j (no carry out of
+// any byte), so a word compare costs one add and one and.
+__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t iB, uint32_t iCS, uint32_t iCL) {
+  return dec_byte(w & 0xFFu, iB, iCS, iCL) | (dec_byte((w >> 8) & 0xFFu, iB, iCS, iCL) << 8) |
+         (dec_byte((w >> 16) & 0xFFu, iB, iCS, iCL) << 16) | (dec_byte(w >> 24, iB, iCS, iCL) << 24);
+}
+
+struct SwarK {
+  uint32_t kB, kCS, kCL;   // (0x7F - j) replicated in every byte
+};
+
+__device__ __forceinline__ uint32_t dec_word_swar(uint32_t w, const SwarK &k) {
+  const uint32_t gB = (w + k.kB) & 0x80808080u;
+  const uint32_t gS = (w + k.kCS) & 0x80808080u;
+  const uint32_t gL = (w + k.kCL) & 0x80808080u;
+  return (gB >> 7) + (gS >> 5) + (gL >> 7) * 9u;     // a + 4 b + 9 c per byte
+}
+
+template <bool VEC, bool SWAR>
+__global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__ bins, uint8_t *__restrict__ dec,
+                                                      uint64_t n, uint32_t iB, uint32_t iCS, uint32_t iCL) {
+  const SwarK sk{(0x7Fu - (iB < 0x7Fu ? iB : 0x7Fu)) * 0x01010101u, (0x7Fu - (iCS < 0x7Fu ? iCS : 0x7Fu)) * 0x01010101u,
+                 (0x7Fu - (iCL < 0x7Fu ? iCL : 0x7Fu)) * 0x01010101u};
+  auto word = [&](uint32_t w) { return SWAR ? dec_word_swar(w, sk) : dec_word(w, iB, iCS, iCL); };
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t me = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (!VEC) {
+    for (uint64_t i = me; i < n; i += S) dec[i] = (uint8_t)dec_byte(bins[i], iB, iCS, iCL);
+  } else {
+    const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(bins) & 15u);
+    const uint64_t head = mis ? (n < 16u - mis ? n : 16u - mis) : 0u;
+    const uint64_t n16 = (n - head) >> 4;
+    const uint64_t tail_first = head + (n16 << 4);
+    if (blockIdx.x == 0 && threadIdx.x < head) dec[threadIdx.x] = (uint8_t)dec_byte(bins[threadIdx.x], iB, iCS, iCL);
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail_first) {
+      const uint64_t i = tail_first + threadIdx.x;
+      dec[i] = (uint8_t)dec_byte(bins[i], iB, iCS, iCL);
+    }
+    const uint4 *b16 = reinterpret_cast<const uint4 *>(bins + head);
+    uint4 *d16 = reinterpret_cast<uint4 *>(dec + head);
+    for (uint64_t i = me; i < n16; i += 2 * S) {
+      const bool two = i + S < n16;
+      const uint4 v = ldg_stream(b16 + i);
+      const uint4 v2 = two ? ldg_stream(b16 + i + S) : make_uint4(0u, 0u, 0u, 0u);
+      const uint4 o = make_uint4(word(v.x), word(v.y), word(v.z), word(v.w));
+      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w)
+                   : "memory");
+      if (two) {
+        const uint4 o2 = make_uint4(word(v2.x), word(v2.y), word(v2.z), word(v2.w));
+        asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i + S), "r"(o2.x), "r"(o2.y), "r"(o2.z),
+                     "r"(o2.w)
+                     : "memory");
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, uint32_t iB, uint32_t iCS,
+                              uint32_t iCL, uint32_t n_bins_max, int grid, int block, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  const bool vec = ((reinterpret_cast<uintptr_t>(bins) ^ reinterpret_cast<uintptr_t>(decision)) & 15u) == 0;
+  const uint64_t need = (n / (vec ? 16 : 1) + block - 1) / block;
+  const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
+  // SWAR needs every bin < 128: bins go up to |E|, and j = iB, iCS, iCL < |E|
+  const bool swar = n_bins_max < 128;
+  if (vec && swar) k4_route_bins<true, true><<<g, block, 0, s>>>(bins, decision, n, iB, iCS, iCL);
+  else if (vec) k4_route_bins<true, false><<<g, block, 0, s>>>(bins, decision, n, iB, iCS, iCL);
+  else k4_route_bins<false, false><<<g, block, 0, s>>>(bins, decision, n, iB, iCS, iCL);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

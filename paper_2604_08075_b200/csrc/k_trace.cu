@@ -91,7 +91,7 @@ __device__ __forceinline__ uint32_t bin_of(const K1Ctx &c, uint32_t L) {
 }
 
 template <int LUTW, int R, bool SPLIT, bool MASS>
-__device__ __forceinline__ void add_one(const K1Ctx &c, uint32_t L) {
+__device__ __forceinline__ uint32_t add_one(const K1Ctx &c, uint32_t L) {
   using Ly = Layout<R, SPLIT, MASS>;
   const uint32_t b = bin_of<LUTW>(c, L);
   unsigned char *slot = c.hist + Ly::bin_off(b) + c.lane4;
@@ -104,14 +104,17 @@ __device__ __forceinline__ void add_one(const K1Ctx &c, uint32_t L) {
       atomicAdd(reinterpret_cast<uint32_t *>(slot + Ly::kStride), L);
     }
   }
+  return b;
 }
 
+// returns the four bins packed in bytes (meaningful when |E| < 256)
 template <int LUTW, int R, bool SPLIT, bool MASS>
-__device__ __forceinline__ void add_four(const K1Ctx &c, const uint4 &v) {
-  add_one<LUTW, R, SPLIT, MASS>(c, v.x);
-  add_one<LUTW, R, SPLIT, MASS>(c, v.y);
-  add_one<LUTW, R, SPLIT, MASS>(c, v.z);
-  add_one<LUTW, R, SPLIT, MASS>(c, v.w);
+__device__ __forceinline__ uint32_t add_four(const K1Ctx &c, const uint4 &v) {
+  const uint32_t b0 = add_one<LUTW, R, SPLIT, MASS>(c, v.x);
+  const uint32_t b1 = add_one<LUTW, R, SPLIT, MASS>(c, v.y);
+  const uint32_t b2 = add_one<LUTW, R, SPLIT, MASS>(c, v.z);
+  const uint32_t b3 = add_one<LUTW, R, SPLIT, MASS>(c, v.w);
+  return b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
 }
 
 template <int R, bool SPLIT>
@@ -178,7 +181,9 @@ struct SrcRaw {
   }
 };
 
-template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW>
+// BINS: also write each request's bin (u8; |E| < 256) to a.bins_out, where
+// (a.bins_out + element index) is 4-B aligned for every uint4 of the body.
+template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS>
 __global__ void __launch_bounds__(512, RAW ? 3 : 1) k1_trace(TraceArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
@@ -243,9 +248,15 @@ __global__ void __launch_bounds__(512, RAW ? 3 : 1) k1_trace(TraceArgs a) {
       maybe_flush(a.flush_iters * 4u * kUnroll);
     }
   } else {
-    if (blockIdx.x == 0 && threadIdx.x < head) add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first)
-      add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
+    if (blockIdx.x == 0 && threadIdx.x < head) {
+      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
+      if (BINS) a.bins_out[threadIdx.x] = (uint8_t)b;
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
+      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
+      if (BINS) a.bins_out[tail_first + threadIdx.x] = (uint8_t)b;
+    }
+    uint32_t *bins4 = BINS ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
     const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
     // grid-stride stripes: at every step the whole grid reads kUnroll contiguous
     // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
@@ -261,12 +272,18 @@ __global__ void __launch_bounds__(512, RAW ? 3 : 1) k1_trace(TraceArgs a) {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) v[u] = RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S);
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
+          if (BINS) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(w) : "memory");
+        }
       } else {
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u)
-          if (base + u * S < n4)
-            add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S));
+          if (base + u * S < n4) {
+            const uint32_t w =
+                add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S));
+            if (BINS) bins4[base + u * S] = w;
+          }
       }
       maybe_flush(a.flush_iters);
     }
@@ -302,6 +319,7 @@ __global__ void __launch_bounds__(512, RAW ? 3 : 1) k1_trace(TraceArgs a) {
 // ---- variant selection ----------------------------------------------------------
 struct Variant {
   bool raw;      // estimate L_total from raw columns (NEXT-1)
+  bool bins;     // also write per-request bins (u8)
   int lutw;      // 1, 2 (LUT bytes per cell) or 0 (binary search)
   int R;         // 32 lane-private replicas or 1
   bool split;    // 16-bit mass halves
@@ -321,6 +339,7 @@ size_t smem_for(const TraceArgs &a, const Variant &v) {
 Variant choose(const TraceArgs &a, int block) {
   Variant v;
   v.raw = a.body != nullptr;
+  v.bins = a.bins_out != nullptr;
   v.lutw = a.lut_cells ? (a.lut_u8 ? 1 : 2) : 0;
   v.mass = a.want_mass != 0;
   v.R = 32;
@@ -347,8 +366,8 @@ uint32_t flush_iters_for(const TraceArgs &a, const Variant &v, int block) {
   return (uint32_t)it;
 }
 
-template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW>
-void *kernel_ptr() { return reinterpret_cast<void *>(&k1_trace<LUTW, R, SPLIT, MASS, RAW>); }
+template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS = false>
+void *kernel_ptr() { return reinterpret_cast<void *>(&k1_trace<LUTW, R, SPLIT, MASS, RAW, BINS>); }
 
 template <bool RAW>
 void *pick_kernel_src(const Variant &v) {
@@ -365,7 +384,18 @@ void *pick_kernel_src(const Variant &v) {
   return nullptr;
 }
 
-void *pick_kernel(const Variant &v) { return v.raw ? pick_kernel_src<true>(v) : pick_kernel_src<false>(v); }
+// the bin-writing variants exist for the plain u8-LUT path only (|E| < 256)
+void *pick_kernel_bins(const Variant &v) {
+  if (v.raw || v.lutw != 1) return nullptr;
+  if (!v.mass) return v.R == 32 ? kernel_ptr<1, 32, false, false, false, true>() : kernel_ptr<1, 1, false, false, false, true>();
+  if (v.R == 32) return v.split ? kernel_ptr<1, 32, true, true, false, true>() : kernel_ptr<1, 32, false, true, false, true>();
+  return v.split ? kernel_ptr<1, 1, true, true, false, true>() : kernel_ptr<1, 1, false, true, false, true>();
+}
+
+void *pick_kernel(const Variant &v) {
+  if (v.bins) return pick_kernel_bins(v);
+  return v.raw ? pick_kernel_src<true>(v) : pick_kernel_src<false>(v);
+}
 
 }  // namespace
 
@@ -385,7 +415,8 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
   // u32 per-block counters: keep every block below 2^31 requests per launch
   const uint64_t cap = (uint64_t)grid * (1ull << 31);
   void *k = pick_kernel(v);
-  if (v.raw) {
+  if (!k) return cudaErrorInvalidValue;
+  if (v.raw || v.bins) {
     // the raw variants carry the c* table: size and opt in per launch
     smem = smem_for(a, v);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -401,6 +432,7 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
   }
   for (uint64_t off = 0; off < a0.n; off += cap) {
     if (a0.len) a.len = a0.len + off;
+    if (a0.bins_out) a.bins_out = a0.bins_out + off;
     if (a0.body) {
       a.body = a0.body + off;
       a.maxout = a0.maxout + off;

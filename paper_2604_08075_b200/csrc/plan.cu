@@ -112,9 +112,11 @@ struct fp_plan {
   // pinned host mirrors
   fp_candidate *h_best = nullptr;          // [world][n_models]
   unsigned long long *h_small = nullptr;   // [2 * nbins + 8]: hist, route counts
-  // device copy of a host trace for sweep_and_route
+  // device copy of a host trace / per-request bins for sweep_and_route
   uint32_t *d_resident = nullptr;
   uint64_t resident_cap = 0;
+  uint8_t *d_bins = nullptr;
+  uint64_t bins_cap = 0;
   // NCCL
   NcclComm comm = nullptr;
   fp_collectives coll{};                   // host hooks replacing NCCL (optional)
@@ -248,8 +250,12 @@ fp_status validate_and_copy(fp_plan *p, const fp_plan_desc *d) {
 
 fp_status build_tables(fp_plan *p) {
   // edge set E = sortuniq(B u C_L): C_S never adds an edge since B <= C_S (R16)
+  // E = sortuniq(B u C_S u C_L): B and C_L give every candidate's counts;
+  // C_S (never needed for the counts since B <= C_S) is included so that every
+  // comparison of Alg. 1 is a bin comparison (sweep_and_route's bin pass)
   p->edges = p->b;
   p->edges.insert(p->edges.end(), p->cl.begin(), p->cl.end());
+  p->edges.insert(p->edges.end(), p->cs.begin(), p->cs.end());
   std::sort(p->edges.begin(), p->edges.end());
   p->edges.erase(std::unique(p->edges.begin(), p->edges.end()), p->edges.end());
   if (p->edges.size() > (size_t)kMaxEdges)
@@ -698,6 +704,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_block_best);
     cudaFree(p->d_done);
     cudaFree(p->d_resident);
+    cudaFree(p->d_bins);
     cudaFree(p->d_calib);
     for (int i = 0; i < 2; ++i) {
       cudaFree(p->d_stage[i]);
@@ -807,7 +814,7 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
 namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident,
-                     const TraceArgs *raw = nullptr);
+                     const TraceArgs *raw = nullptr, uint8_t *bins = nullptr);
 }
 
 fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
@@ -820,13 +827,40 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
                           fp_route_counts *h_counts, void *stream) {
   if (!p) return FP_ERR_INVALID_ARG;
   if (route_model >= p->models.size()) return fail(p, FP_ERR_INVALID_ARG, "route_model out of range");
+  if (d_decision && n_local && is_host_pointer(d_decision))
+    return fail(p, FP_ERR_INVALID_ARG, "d_decision must be device memory");
   DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // Bin pass (|E| < 256, u8 LUT): the trace pass also writes every request's
+  // bin (1 B); the routing pass maps bins to decisions (1 B in, 1 B out) and
+  // the route counts are the best record's counts (same histogram). A host
+  // trace then never needs a device copy. Otherwise: K4 re-reads L_total
+  // (from a device copy for host traces).
+  const bool bin_pass = p->lut_cells && p->lut_u8;
   const uint32_t *src = len;
   uint32_t *resident = nullptr;
-  if (n_local && len && is_host_pointer(len)) {
+  uint8_t *bins = nullptr;
+  if (bin_pass) {
+    if (d_decision && n_local) {
+      // the bin buffer is placed so that bins + i and len + i share the 4-B
+      // phase the trace pass needs for its 32-bit stores of 4 bins
+      // (host traces are processed from 256-B aligned staging chunks: phase 0)
+      const uintptr_t lp = is_host_pointer(len) ? 0 : reinterpret_cast<uintptr_t>(len);
+      const uint64_t head_phase = (4 - ((lp & 15u) >> 2)) & 3u;
+      const uint64_t need = n_local + 16;
+      if (p->bins_cap < need) {
+        cudaFree(p->d_bins);
+        p->d_bins = nullptr;
+        p->bins_cap = 0;
+        CUDA_TRY(p, cudaMalloc(&p->d_bins, need), "cudaMalloc bins");
+        p->bins_cap = need;
+      }
+      bins = p->d_bins + ((4 - head_phase) & 3u);
+    }
+  } else if (n_local && len && is_host_pointer(len)) {
     if (p->resident_cap < n_local) {
       cudaFree(p->d_resident);
-    cudaFree(p->d_calib);
+    cudaFree(p->d_bins);
       p->d_resident = nullptr;
       p->resident_cap = 0;
       CUDA_TRY(p, cudaMalloc(&p->d_resident, n_local * 4), "cudaMalloc resident trace");
@@ -835,7 +869,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     resident = p->d_resident;
     src = resident;
   }
-  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident);
+  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident, nullptr, bins);
   if (st != FP_OK) return st;
   std::vector<fp_candidate> best(p->models.size());
   st = best_split(p, best.data());
@@ -844,7 +878,26 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   const fp_candidate &b = best[route_model];
   if (!(b.flags & FP_CAND_FEASIBLE))
     return fail(p, FP_ERR_STATE, "model %u has no feasible split to route with", route_model);
-  return route_batch(p, src, n_local, b.b_short, b.c_short, b.c_long, d_decision, h_counts, stream);
+  if (!bin_pass) return route_batch(p, src, n_local, b.b_short, b.c_short, b.c_long, d_decision, h_counts, stream);
+  if (d_decision && n_local) {
+    const uint32_t iB = index_of(p->edges, b.b_short), iCS = index_of(p->edges, b.c_short);
+    const uint32_t iCL = index_of(p->edges, b.c_long);
+    LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
+    cudaError_t e =
+        launch_route_bins(bins, d_decision, n_local, iB, iCS, iCL, p->nbins - 1, p->k4_grid, p->k4_block, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
+    ++p->launches;
+  }
+  if (h_counts) {
+    h_counts->n_short = b.n_short;
+    h_counts->n_long = b.n_long;
+    h_counts->n_reject = b.n_reject;
+    h_counts->mass_short = b.mass_short;
+    h_counts->mass_long = b.mass_long;
+  }
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  p->last_stream = s;
+  return FP_OK;
 }
 
 namespace {
@@ -965,7 +1018,8 @@ fp_status route_batch_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, c
 
 namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
-                     fp_candidate *h_results, void *stream, uint32_t *resident, const TraceArgs *raw) {
+                     fp_candidate *h_results, void *stream, uint32_t *resident, const TraceArgs *raw,
+                     uint8_t *bins) {
   if (!p) return FP_ERR_INVALID_ARG;
   if (n_local && !d_len && !raw) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
@@ -983,10 +1037,11 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
       if (e != cudaSuccess) return cuda_fail(p, e, "trace pass (raw) launch");
       ++p->launches;
     }
-  } else st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t) {
+  } else st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t off) {
     TraceArgs t = p->ta;
     t.len = ptr;
     t.n = n;
+    t.bins_out = bins ? bins + off : nullptr;
     LaunchTimer lt(p, FP_KERNEL_TRACE, s);
     cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");

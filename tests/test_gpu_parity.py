@@ -239,3 +239,41 @@ def test_sweep_and_route_equals_separate_calls(where):
     odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
     assert np.array_equal(dec.cpu().numpy(), odec)
     assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
+
+
+@pytest.mark.parametrize("off,doff", [(0, 0), (1, 0), (2, 5), (3, 3), (0, 7)])
+@pytest.mark.parametrize("name", ["C5", "C4", "C2"])
+def test_sweep_and_route_bin_pass_misaligned(name, off, doff):
+    # the bin pass (|E| < 256) at every pointer phase; C4 exercises C_S edges
+    cfg = configs.CONFIGS[name]().with_n(1_000_003)
+    full = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests + off)
+    L = full[off:]
+    plan = _plan(cfg)
+    dec = torch.zeros(L.size + 16, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(full)[off:], cfg.rate_rps, route_model=0, decision=dec[doff:])
+    _, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[0]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec[doff:doff + L.size].cpu().numpy(), odec)
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
+    # the misaligned host path too
+    best2, counts2 = fp.sweep_and_route(plan, full[off:], cfg.rate_rps, route_model=0, decision=dec[doff:])
+    assert best2.tobytes() == obest.tobytes() and counts2 == counts
+    assert np.array_equal(dec[doff:doff + L.size].cpu().numpy(), odec)
+
+
+def test_sweep_and_route_bin_pass_wide_edges():
+    # 200 edges: u8 bins >= 128 -> the byte-wise (non-SWAR) decision path
+    cfg = make_config("wide", "SG", 4, 700_001, 10000.0, ["qwen3-235b-a22b"], ["b200-180g"],
+                      [256 * k for k in range(1, 200)], [], [65536, 262144])
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    assert fp.fleet_plan_info(plan)["n_edges"] >= 128
+    dec = torch.zeros(L.size, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(L), cfg.rate_rps, route_model=0, decision=dec)
+    _, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[0]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec.cpu().numpy(), odec)
