@@ -184,7 +184,7 @@ struct SrcRaw {
 // BINS: also write each request's bin (u8; |E| < 256) to a.bins_out, where
 // (a.bins_out + element index) is 4-B aligned for every uint4 of the body.
 template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS>
-__global__ void __launch_bounds__(512, RAW ? 3 : 1) k1_trace(TraceArgs a) {
+__global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
   uint32_t lut_bytes = (LUTW == 0) ? a.n_edges * 4 : a.lut_cells * LUTW;
