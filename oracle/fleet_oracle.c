@@ -366,3 +366,114 @@ void or_route_batch_est(const uint32_t *bytes, const uint32_t *max_out, const ui
     }
   }
 }
+
+/* ==========================================================================
+ * NEXT-2: three pools ("additional pools (e.g. 4K/16K/64K) yield
+ * only marginal incremental savings (~2%)"). TEST INFRASTRUCTURE.
+ * Pools 1, 2, 3 with windows C1 = B1 < C2 = B2 <= C3 = C_L (the Fig. 6
+ * convention C_S = B for the inner pools, R16). Alg. 1 generalised: a request
+ * goes to the first pool whose threshold it meets (L <= B1, else L <= B2,
+ * else L <= C_L), otherwise it is rejected (R3). Each pool is sized as in
+ * Sec. 3: I_i = ceil(lambda_i / mu(C_i)), lambda_i = (n_i / N) lambda.
+ * ========================================================================== */
+typedef struct {
+  uint32_t index, model, gpu, b1, b2, c_long, flags, _pad;
+  uint64_t n1, n2, n3, n_reject;
+  uint64_t nseq1, nseq2, nseq3;
+  uint64_t inst1, inst2, inst3, inst_homo, gpus, gpus_homo;
+  double cost, cost_homo, savings;
+} or_pool3;
+
+uint32_t or_pool3_size(void) { return (uint32_t)sizeof(or_pool3); }
+
+/* Candidate order (m, g, C_L, pair), pairs (i, j) of B-grid indices with
+ * i < j in lexicographic order; valid iff b[i] < b[j] <= C_L. */
+int or_sweep3(const uint32_t *L, uint64_t n, uint32_t n_models, const uint32_t *arch, uint32_t n_gpus,
+              const uint64_t *gpu_u64, const double *gpu_price, const uint64_t *deploy, const uint32_t *b,
+              uint32_t n_b, const uint32_t *cl, uint32_t n_cl, const uint32_t *windows, uint32_t n_w,
+              const double *mu, double rate, double hours, or_pool3 *out, or_pool3 *best) {
+  if (n == 0) return 1;
+  uint32_t nx = n_b + n_cl;
+  uint32_t *x = (uint32_t *)malloc(sizeof(uint32_t) * nx);
+  uint64_t *cnt = (uint64_t *)malloc(sizeof(uint64_t) * nx);
+  uint64_t *mass = (uint64_t *)malloc(sizeof(uint64_t) * nx);
+  for (uint32_t k = 0; k < n_b; ++k) x[k] = b[k];
+  for (uint32_t k = 0; k < n_cl; ++k) x[n_b + k] = cl[k];
+  or_count_le(L, n, x, nx, cnt, mass);
+  uint64_t n_pairs = (uint64_t)n_b * (n_b - 1) / 2;
+  int rc = 0;
+  for (uint32_t m = 0; m < n_models && !rc; ++m) {
+    or_pool3 bm;
+    memset(&bm, 0, sizeof bm);
+    bm.index = UINT32_MAX;
+    bm.model = m;
+    bm.cost = bm.cost_homo = INFINITY;
+    int have = 0;
+    for (uint32_t g = 0; g < n_gpus && !rc; ++g)
+      for (uint32_t l = 0; l < n_cl && !rc; ++l) {
+        uint64_t p = 0;
+        for (uint32_t i = 0; i < n_b; ++i)
+          for (uint32_t j = i + 1; j < n_b; ++j, ++p) {
+            uint64_t idx = (((uint64_t)m * n_gpus + g) * n_cl + l) * n_pairs + p;
+            or_pool3 c;
+            memset(&c, 0, sizeof c);
+            c.index = (uint32_t)idx;
+            c.model = m;
+            c.gpu = g;
+            c.b1 = b[i];
+            c.b2 = b[j];
+            c.c_long = cl[l];
+            c.cost = c.cost_homo = INFINITY;
+            if (c.b1 < c.b2 && c.b2 <= c.c_long) {
+              const uint64_t *dp = deploy + ((uint64_t)m * n_gpus + g) * 3;
+              uint32_t tp = (uint32_t)dp[0];
+              uint64_t wpg = dp[1], gpi = dp[2];
+              const uint64_t *gu = gpu_u64 + (uint64_t)g * 4;
+              const uint32_t *ar = arch + (uint64_t)m * 4;
+              uint32_t w1 = find_u32(windows, n_w, c.b1), w2 = find_u32(windows, n_w, c.b2);
+              uint32_t w3 = find_u32(windows, n_w, c.c_long);
+              if (w1 == UINT32_MAX || w2 == UINT32_MAX || w3 == UINT32_MAX) { rc = 2; break; }
+              const double *mg = mu + ((uint64_t)m * n_gpus + g) * n_w;
+              /* first-fit routing counts from the CDF */
+              uint64_t c1 = cnt[i], c2 = cnt[j], c3 = cnt[n_b + l];
+              c.n1 = c1;
+              c.n2 = c2 - c1;
+              c.n3 = c3 - c2;
+              c.n_reject = n - c3;
+              uint64_t budget = or_kv_budget(gu[0], (uint32_t)gu[1], (uint32_t)gu[2], wpg, gu[3]);
+              c.nseq1 = or_max_seqs(budget, or_kv_bytes_per_seq(ar[0], ar[1], ar[2], ar[3], c.b1), tp);
+              c.nseq2 = or_max_seqs(budget, or_kv_bytes_per_seq(ar[0], ar[1], ar[2], ar[3], c.b2), tp);
+              c.nseq3 = or_max_seqs(budget, or_kv_bytes_per_seq(ar[0], ar[1], ar[2], ar[3], c.c_long), tp);
+              double lam1 = ((double)c.n1 / (double)n) * rate;
+              double lam2 = ((double)c.n2 / (double)n) * rate;
+              double lam3 = ((double)c.n3 / (double)n) * rate;
+              double lamh = ((double)c3 / (double)n) * rate;
+              int ok1 = or_pool_instances(lam1, mg[w1], c.nseq1, &c.inst1);
+              int ok2 = or_pool_instances(lam2, mg[w2], c.nseq2, &c.inst2);
+              int ok3 = or_pool_instances(lam3, mg[w3], c.nseq3, &c.inst3);
+              int okh = or_pool_instances(lamh, mg[w3], c.nseq3, &c.inst_homo);
+              int ok = ok1 && ok2 && ok3;
+              if (!ok) { c.inst1 = c.inst2 = c.inst3 = 0; }
+              c.gpus = gpi * (c.inst1 + c.inst2 + c.inst3);
+              c.gpus_homo = gpi * c.inst_homo;
+              c.cost = ok ? or_cost(c.gpus, gpu_price[g], hours) : INFINITY;
+              c.cost_homo = okh ? or_cost(c.gpus_homo, gpu_price[g], hours) : INFINITY;
+              c.savings = (ok && okh && c.gpus_homo > 0)
+                              ? ((double)c.gpus_homo - (double)c.gpus) / (double)c.gpus_homo
+                              : 0.0;
+              c.flags = OR_VALID | (ok ? OR_FEASIBLE : 0) | (okh ? OR_HOMO_FEASIBLE : 0);
+            }
+            if (out) out[idx] = c;
+            if ((c.flags & OR_FEASIBLE) && (!have || c.cost < bm.cost)) {
+              bm = c;
+              have = 1;
+            }
+          }
+      }
+    best[m] = bm;
+  }
+  free(x);
+  free(cnt);
+  free(mass);
+  return rc;
+}

@@ -18,6 +18,15 @@ VP = ctypes.c_void_p
 
 OR_VALID, OR_FEASIBLE, OR_HOMO_FEASIBLE = 1, 2, 4
 
+POOL3_DTYPE = np.dtype([
+    ("index", "<u4"), ("model", "<u4"), ("gpu", "<u4"), ("b1", "<u4"), ("b2", "<u4"), ("c_long", "<u4"),
+    ("flags", "<u4"), ("_pad", "<u4"),
+    ("n1", "<u8"), ("n2", "<u8"), ("n3", "<u8"), ("n_reject", "<u8"),
+    ("nseq1", "<u8"), ("nseq2", "<u8"), ("nseq3", "<u8"),
+    ("inst1", "<u8"), ("inst2", "<u8"), ("inst3", "<u8"), ("inst_homo", "<u8"), ("gpus", "<u8"),
+    ("gpus_homo", "<u8"), ("cost", "<f8"), ("cost_homo", "<f8"), ("savings", "<f8"),
+])
+
 CANDIDATE_DTYPE = np.dtype([
     ("index", "<u4"), ("model", "<u4"), ("gpu", "<u4"), ("b_short", "<u4"),
     ("c_short", "<u4"), ("c_long", "<u4"), ("flags", "<u4"), ("_pad", "<u4"),
@@ -57,6 +66,9 @@ def lib():
                                     VP, U32, VP, F64, F64, VP, VP]),
         "or_num_threads": (ctypes.c_int, []),
         "or_route_ratio": (F64, [F64, F64, F64, F64]),
+        "or_pool3_size": (U32, []),
+        "or_sweep3": (ctypes.c_int, [VP, U64, U32, VP, U32, VP, VP, VP, VP, U32, VP, U32, VP, U32, VP, F64, F64,
+                                     VP, VP]),
         "or_estimate_one": (U32, [U32, U32, F64]),
         "or_estimate": (None, [VP, VP, VP, U64, VP, VP, U32, F64, F64, VP]),
         "or_route_batch_est": (None, [VP, VP, VP, VP, U64, VP, VP, U32, F64, F64, U32, U32, U32, VP, VP, VP, VP]),
@@ -66,6 +78,7 @@ def lib():
         f.restype = res
         f.argtypes = args
     assert L.or_candidate_size() == CANDIDATE_DTYPE.itemsize, "oracle record layout drift"
+    assert L.or_pool3_size() == POOL3_DTYPE.itemsize, "oracle pool3 layout drift"
     _lib = L
     return L
 
@@ -215,3 +228,25 @@ def route_batch_est(body, max_out, cat, true_prompt, cats, gamma, c_floor, B, c_
                              sig.ctypes.data, len(cats), gamma, c_floor, B, c_short, c_long, dec.ctypes.data,
                              lt.ctypes.data, counts.ctypes.data, mis.ctypes.data)
     return dec, lt, counts, mis
+
+
+# ---- NEXT-2: three pools -------------------------------------------------------------
+def sweep3(cfg, L, rate=None, want_all=True):
+    """Three-pool sweep (B1 < B2 from the B grid, C_L grid); returns (all or None, best)."""
+    L = _u32(L)
+    a = config_arrays(cfg)
+    nb = len(cfg.b_short)
+    n_cand = len(cfg.models) * len(cfg.gpus) * len(cfg.c_long) * (nb * (nb - 1) // 2)
+    out = np.zeros(n_cand, dtype=POOL3_DTYPE) if want_all else None
+    best = np.zeros(len(cfg.models), dtype=POOL3_DTYPE)
+    rc = lib().or_sweep3(
+        L.ctypes.data, L.size, len(cfg.models), a["arch"].ctypes.data, len(cfg.gpus), a["gpu_u64"].ctypes.data,
+        a["price"].ctypes.data, a["deploy"].ctypes.data, a["b"].ctypes.data, a["b"].size, a["cl"].ctypes.data,
+        a["cl"].size, a["windows"].ctypes.data, a["windows"].size, a["mu"].ctypes.data,
+        float(cfg.rate_rps if rate is None else rate), float(cfg.hours_per_year),
+        out.ctypes.data if out is not None else None, best.ctypes.data)
+    if rc == 1:
+        raise ValueError("empty trace")
+    if rc != 0:
+        raise ValueError(f"or_sweep3 rc={rc}")
+    return out, best

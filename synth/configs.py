@@ -119,7 +119,7 @@ class Config:
     b_short: tuple              # B grid
     c_short: tuple              # C_S grid; empty => C_S = B (Fig. 6 convention)
     c_long: tuple               # C_L grid (= C_H of the homogeneous baseline)
-    mu_mode: str = "pow23"      # "pow23" | "table"
+    mu_mode: str = "pow23"      # "pow23" | "pow23cap8" | "table"
     mu_values: dict = field(default_factory=dict)   # table mode: {(m, g, C): mu}
     hours_per_year: float = 8760.0
     description: str = ""
@@ -139,6 +139,10 @@ class Config:
                 for k, c in enumerate(win):
                     if self.mu_mode == "table":
                         mu[i, j, k] = self.mu_values.get((m.name, g.name, int(c)), 0.0)
+                    elif self.mu_mode == "pow23cap8":
+                        # throughput gain capped at 8x mu_ref ("rho in [4, 8]")
+                        r = min((C_REF / float(c)) ** (2.0 / 3.0), 8.0)
+                        mu[i, j, k] = MU_REF[(m.name, g.name)] * r
                     else:
                         mu[i, j, k] = MU_REF[(m.name, g.name)] * (C_REF / float(c)) ** (2.0 / 3.0)
         return mu
