@@ -300,6 +300,22 @@ def run_ours(args, cfg):
     total_requests = n * world
     value = total_requests / (ms_step / 1e3)
 
+    # ---- NEXT-2: three pools over the same histogram (rank-local, no collective) ----
+    next2 = None
+    if args.next2:
+        fp.fp_kernel_time_reset(plan)
+        for _ in range(3):
+            _, best3 = fp.sweep_three_pools(plan, cfg.rate_rps)
+        ms3, k3n = fp.fp_kernel_time(plan, fp.FP_KERNEL_EVAL)
+        nb = len(cfg.b_short)
+        n3 = len(cfg.models) * len(cfg.gpus) * len(cfg.c_long) * nb * (nb - 1) // 2
+        next2 = {"candidates": n3, "k3_three_pool_ms": ms3 / k3n,
+                 "candidates_per_s": n3 / (ms3 / k3n / 1e3),
+                 "best_savings_two_pools": [float(x) for x in best["savings"]],
+                 "best_savings_three_pools": [float(x) for x in best3["savings"]],
+                 "note": "P:1099-1100 claims ~2% marginal savings for a third pool; under the stated "
+                         "uncapped pow23 mu the gain is larger (it depends on mu saturation, not stated)"}
+
     # ---- e2e: the same step through the C ABI with HOST (pinned) buffers ----
     e2e = None
     if args.e2e_steps > 0:
@@ -368,6 +384,7 @@ def run_ours(args, cfg):
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktime.items()},
             "roofline": roof,
             "gpu_launches": launches,
+            "next2_three_pools": next2,
             "clocks": clk.summary(),
             "e2e": e2e,
             "best_split_model0": {k: (int(best[0][k]) if k not in ("cost_dual", "savings", "predicted_savings")
@@ -398,6 +415,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-next2", dest="next2", action="store_false",
+                    help="skip the three-pool (NEXT-2) measurement")
     ap.add_argument("--no-next1", dest="next1", action="store_false",
                     help="skip the fused token-budget estimation measurement (NEXT-1)")
     ap.add_argument("--no-k3-grid", dest="k3_grid", action="store_false",

@@ -282,6 +282,32 @@ fp_status route_batch_raw(fp_plan *plan, const fp_raw_trace *trace, uint64_t n_l
                           uint8_t *d_decision, uint32_t *d_l_total, fp_route_counts *h_counts,
                           uint64_t *h_misroute, void *stream);
 
+/* ---- NEXT-2: three pools ---------------------------------------
+ * Pools 1, 2, 3 with windows C1 = B1 < C2 = B2 <= C3 = C_L from the B and C_L
+ * grids (pairs i < j of B-grid indices). A request goes to the first pool
+ * whose threshold it meets (L <= B1, else L <= B2, else L <= C_L), otherwise
+ * it is rejected (R3); each pool is sized with the Sec. 3 formulas. Flat
+ * index ((m * n_gpus + g) * n_cl + l) * n_pairs + p, pairs in lexicographic
+ * (i, j) order, n_pairs = n_b (n_b - 1) / 2. 160 bytes. */
+typedef struct fp_pool3_candidate {
+  uint32_t index, model, gpu, b1, b2, c_long, flags, _pad;
+  uint64_t n1, n2, n3, n_reject;           /* routed requests per pool (global)    */
+  uint64_t nseq1, nseq2, nseq3;            /* Eq. (2) N_seq at C1, C2, C3           */
+  uint64_t inst1, inst2, inst3, inst_homo; /* ceil(lambda_i / mu(C_i))              */
+  uint64_t gpus, gpus_homo;
+  double cost, cost_homo, savings;         /* savings vs homogeneous C_H = C_L      */
+} fp_pool3_candidate;
+
+/* Evaluate every three-pool candidate over the histogram of the LAST
+ * sweep_thresholds / sweep_and_route call (global over ranks; every rank
+ * evaluates the whole three-pool grid, no further collective). h_results
+ * (nullable) receives all candidates; h_best[n_models] the per-model cheapest
+ * feasible one (index UINT32_MAX if none). Synchronizes. Every B must be in
+ * desc->windows and 2 <= n_b <= 4096 (else FP_ERR_CONFIG); FP_ERR_STATE
+ * before a sweep. */
+fp_status sweep_three_pools(fp_plan *plan, double rate_rps, fp_pool3_candidate *h_results,
+                            fp_pool3_candidate *h_best, void *stream);
+
 /* Global per-bin histogram of the last sweep (K1 output after the cross-rank
  * sum; synchronizes). With E = sortuniq(B u C_L) ascending (|E| = n_edges of
  * fleet_plan_info): h_edges[j] = e_j for j < |E|; bin j < |E| holds the

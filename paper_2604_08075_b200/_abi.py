@@ -26,7 +26,7 @@ EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split"
             "fleet_plan_info", "fp_kernel_launches", "fleet_plan_destroy", "fp_status_string",
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
             "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
-            "sweep_thresholds_raw", "route_batch_raw"]
+            "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -115,6 +115,18 @@ FP_CANDIDATE = np.dtype([
 ])
 assert FP_CANDIDATE.itemsize == 192
 
+# fp_pool3_candidate (160 bytes), field order of fleet_plan.h
+FP_POOL3 = np.dtype([
+    ("index", "<u4"), ("model", "<u4"), ("gpu", "<u4"), ("b1", "<u4"), ("b2", "<u4"), ("c_long", "<u4"),
+    ("flags", "<u4"), ("_pad", "<u4"),
+    ("n1", "<u8"), ("n2", "<u8"), ("n3", "<u8"), ("n_reject", "<u8"),
+    ("nseq1", "<u8"), ("nseq2", "<u8"), ("nseq3", "<u8"),
+    ("inst1", "<u8"), ("inst2", "<u8"), ("inst3", "<u8"), ("inst_homo", "<u8"),
+    ("gpus", "<u8"), ("gpus_homo", "<u8"),
+    ("cost", "<f8"), ("cost_homo", "<f8"), ("savings", "<f8"),
+])
+assert FP_POOL3.itemsize == 160
+
 
 def _load():
     if not os.path.exists(LIB_PATH):
@@ -142,6 +154,7 @@ def _load():
                                          c_vp, c_vp]),
         "route_batch_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_u32, c_u32,
                                     c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), ctypes.POINTER(c_u64), c_vp]),
+        "sweep_three_pools": (c_i32, [c_vp, c_dbl, c_vp, c_vp, c_vp]),
         "sweep_and_route": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
     }
     for name, (res, args) in sig.items():
@@ -441,3 +454,13 @@ def route_batch_raw(plan, body, max_out, cat, cats, b_short, c_short, c_long, tr
     del keep
     c = {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}
     return c, ([int(mis[0]), int(mis[1])] if true_prompt is not None else None)
+
+
+# ---- NEXT-2: three pools ----------------------------------------------------------------
+def sweep_three_pools(plan, rate_rps, want_results=False, n_results=None, stream=None):
+    """Three-pool grid over the last sweep's histogram; returns (all or None, best)."""
+    out = np.zeros(n_results, dtype=FP_POOL3) if want_results else None
+    best = np.zeros(plan.n_models, dtype=FP_POOL3)
+    _check(lib.sweep_three_pools(plan.handle, float(rate_rps), out.ctypes.data if out is not None else None,
+                                 best.ctypes.data, _stream_handle(stream, plan.device)), plan)
+    return out, best

@@ -99,8 +99,18 @@ struct EvalArgs {
   fp_candidate *best_out;               // [n_models] (this rank's)
   BlockBest *block_best;                // [n_models][grid_x]
   unsigned int *done;                   // [n_models] last-block-done counters (self-resetting)
+  // NEXT-2 three pools (replicated grid): pairs (i | j << 16) of B-grid indices
+  const uint32_t *pairs = nullptr;
+  uint32_t n_pairs = 0;
+  const uint16_t *b_win3 = nullptr;     // window index of each B
+  uint64_t per_model3 = 0;
+  fp_pool3_candidate *results3 = nullptr;
+  fp_pool3_candidate *best3 = nullptr;  // [n_models]
+  BlockBest *block_best3 = nullptr;
+  unsigned int *done3 = nullptr;
 };
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
+cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
 size_t eval_smem_bytes(const EvalArgs &a, int block);
 cudaError_t eval_prepare();
 

@@ -124,6 +124,72 @@ __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64
   c.flags = FP_CAND_VALID | (ok_d ? FP_CAND_FEASIBLE : 0u) | (ok_h ? FP_CAND_HOMO_FEASIBLE : 0u);
 }
 
+// NEXT-2: three pools. idx = ((m * G + g) * n_cl + l) * n_pairs + p,
+// pair p = (i, j), i < j over the B grid; windows C1 = B1, C2 = B2, C3 = C_L;
+// first-fit routing (L <= B1, else L <= B2, else L <= C_L, else rejected) and
+// the Sec. 3 sizing per pool, in the oracle's operation order (or_sweep3).
+__device__ void evaluate3(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx, fp_pool3_candidate &c) {
+  uint32_t r = (uint32_t)idx;
+  const uint32_t p = r % a.n_pairs; r /= a.n_pairs;
+  const uint32_t l = r % a.n_cl; r /= a.n_cl;
+  const uint32_t g = r % a.n_gpus;
+  const uint32_t pr = a.pairs[p], i = pr & 0xFFFFu, j = pr >> 16;
+  const uint32_t B1 = a.b[i], B2 = a.b[j], CL = a.cl[l];
+  c.index = (uint32_t)idx; c.model = m; c.gpu = g; c.b1 = B1; c.b2 = B2; c.c_long = CL;
+  c.flags = 0; c._pad = 0;
+  c.n1 = c.n2 = c.n3 = c.n_reject = 0;
+  c.nseq1 = c.nseq2 = c.nseq3 = 0;
+  c.inst1 = c.inst2 = c.inst3 = c.inst_homo = c.gpus = c.gpus_homo = 0;
+  c.cost = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
+  c.savings = 0.0;
+  if (!(B1 < B2 && B2 <= CL)) return;
+  const unsigned long long N = sh.cnt_le[a.nbins - 1];
+  const unsigned long long c1 = sh.cnt_le[a.b_edge[i]], c2 = sh.cnt_le[a.b_edge[j]], c3 = sh.cnt_le[a.cl_edge[l]];
+  c.n1 = c1;
+  c.n2 = c2 - c1;
+  c.n3 = c3 - c2;
+  c.n_reject = N - c3;
+  const uint32_t gw = g * a.n_windows;
+  const uint32_t w1 = gw + a.b_win3[i], w2 = gw + a.b_win3[j], w3 = gw + a.cl_win[l];
+  c.nseq1 = sh.nseq[w1];
+  c.nseq2 = sh.nseq[w2];
+  c.nseq3 = sh.nseq[w3];
+  const double dN = u2d(N);
+  const double lam1 = __dmul_rn(__ddiv_rn(u2d(c.n1), dN), a.rate);
+  const double lam2 = __dmul_rn(__ddiv_rn(u2d(c.n2), dN), a.rate);
+  const double lam3 = __dmul_rn(__ddiv_rn(u2d(c.n3), dN), a.rate);
+  const double lamh = __dmul_rn(__ddiv_rn(u2d(c3), dN), a.rate);
+  const bool ok1 = pool_instances(lam1, sh.mu[w1], c.nseq1, &c.inst1);
+  const bool ok2 = pool_instances(lam2, sh.mu[w2], c.nseq2, &c.inst2);
+  const bool ok3 = pool_instances(lam3, sh.mu[w3], c.nseq3, &c.inst3);
+  const bool okh = pool_instances(lamh, sh.mu[w3], c.nseq3, &c.inst_homo);
+  const bool ok = ok1 && ok2 && ok3;
+  if (!ok) { c.inst1 = c.inst2 = c.inst3 = 0; }
+  const unsigned long long gpi = a.deploy[((uint64_t)m * a.n_gpus + g) * 3 + 1];
+  c.gpus = gpi * (c.inst1 + c.inst2 + c.inst3);
+  c.gpus_homo = gpi * c.inst_homo;
+  const double price = a.price[g];
+  if (ok) c.cost = __dmul_rn(__dmul_rn(u2d(c.gpus), price), a.hours);
+  if (okh) c.cost_homo = __dmul_rn(__dmul_rn(u2d(c.gpus_homo), price), a.hours);
+  if (ok && okh && c.gpus_homo > 0)
+    c.savings = __ddiv_rn(__dsub_rn(u2d(c.gpus_homo), u2d(c.gpus)), u2d(c.gpus_homo));
+  c.flags = FP_CAND_VALID | (ok ? FP_CAND_FEASIBLE : 0u) | (okh ? FP_CAND_HOMO_FEASIBLE : 0u);
+}
+
+template <bool POOL3> struct RecOf { using T = fp_candidate; };
+template <> struct RecOf<true> { using T = fp_pool3_candidate; };
+
+__device__ __forceinline__ void eval_any(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
+                                         fp_candidate &c, double &cost) {
+  evaluate(a, sh, m, idx, c);
+  cost = c.cost_dual;
+}
+__device__ __forceinline__ void eval_any(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
+                                         fp_pool3_candidate &c, double &cost) {
+  evaluate3(a, sh, m, idx, c);
+  cost = c.cost;
+}
+
 // (cost, index) lexicographic min; non-candidates carry valid = 0.
 __device__ __forceinline__ void better(double &c0, uint32_t &i0, uint32_t &v0, double c1, uint32_t i1,
                                        uint32_t v1) {
@@ -176,7 +242,9 @@ __device__ void block_scan_inclusive(unsigned long long *data, uint32_t n,
   __syncthreads();
 }
 
+template <bool POOL3>
 __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
+  using Rec = typename RecOf<POOL3>::T;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long warp_tot[32];
   __shared__ double red_c[32];
@@ -208,8 +276,11 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   block_scan_inclusive(sh.mass_le, a.nbins, warp_tot);
 
   // ---- this block's candidates: model m's part of the rank slice ----
-  const uint64_t m_lo = (uint64_t)m * a.per_model, m_hi = m_lo + a.per_model;
-  const uint64_t lo = max(m_lo, a.cand_first), hi = min(m_hi, a.cand_first + a.cand_count);
+  const uint64_t per = POOL3 ? a.per_model3 : a.per_model;
+  const uint64_t m_lo = (uint64_t)m * per, m_hi = m_lo + per;
+  // the three-pool grid is evaluated whole on every rank (replicated)
+  const uint64_t lo = POOL3 ? m_lo : max(m_lo, a.cand_first);
+  const uint64_t hi = POOL3 ? m_hi : min(m_hi, a.cand_first + a.cand_count);
   // grid-stride over the model's candidates: the per-block prologue (scan,
   // capacity table) and epilogue (argmin, arrival fence) are amortised over
   // many candidates per thread on large grids (ncu r01_k3L: one candidate per
@@ -218,11 +289,16 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   uint32_t bi = 0xffffffffu, bv = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
-    fp_candidate c;
-    evaluate(a, sh, m, idx, c);
-    if (a.results) a.results[idx - a.cand_first] = c;
+    Rec c;
+    double cost;
+    eval_any(a, sh, m, idx, c, cost);
+    if (POOL3) {
+      if (a.results3) reinterpret_cast<Rec *>(a.results3)[idx] = c;
+    } else if (a.results) {
+      reinterpret_cast<Rec *>(a.results)[idx - a.cand_first] = c;
+    }
     // indices increase along the loop, so strict '<' keeps the lowest index on ties
-    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || c.cost_dual < bc)) { bc = c.cost_dual; bi = c.index; bv = 1; }
+    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || cost < bc)) { bc = cost; bi = c.index; bv = 1; }
   }
   warp_argmin(bc, bi, bv);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
@@ -234,10 +310,10 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
     bv = lane < nw ? red_v[lane] : 0u;
     warp_argmin(bc, bi, bv);
     if (lane == 0) {
-      BlockBest *bb = a.block_best + (size_t)m * gridDim.x + blockIdx.x;
+      BlockBest *bb = (POOL3 ? a.block_best3 : a.block_best) + (size_t)m * gridDim.x + blockIdx.x;
       bb->cost = bc; bb->index = bi; bb->valid = bv;
       __threadfence();
-      unsigned int prev = atomicAdd(a.done + m, 1u);
+      unsigned int prev = atomicAdd((POOL3 ? a.done3 : a.done) + m, 1u);
       is_last = (prev == gridDim.x - 1);
     }
   }
@@ -248,7 +324,7 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   __threadfence();
   bc = 0.0; bi = 0xffffffffu; bv = 0;
   for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
-    const volatile BlockBest *bb = a.block_best + (size_t)m * gridDim.x + j;
+    const volatile BlockBest *bb = (POOL3 ? a.block_best3 : a.block_best) + (size_t)m * gridDim.x + j;
     better(bc, bi, bv, bb->cost, bb->index, bb->valid);
   }
   warp_argmin(bc, bi, bv);
@@ -256,17 +332,24 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int j = 1; j < nw; ++j) better(bc, bi, bv, red_c[j], red_i[j], red_v[j]);
-    fp_candidate c;
+    Rec c;
+    double cost;
     if (bv) {
-      evaluate(a, sh, m, bi, c);
+      eval_any(a, sh, m, bi, c, cost);
     } else {
       memset(&c, 0, sizeof c);
       c.index = 0xffffffffu;
       c.model = m;
-      c.cost_dual = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
+      if constexpr (POOL3) c.cost = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
+      else c.cost_dual = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
     }
-    a.best_out[m] = c;
-    a.done[m] = 0;  // self-reset for the next launch / graph replay
+    if constexpr (POOL3) {
+      a.best3[m] = c;
+      a.done3[m] = 0;
+    } else {
+      a.best_out[m] = c;
+      a.done[m] = 0;  // self-reset for the next launch / graph replay
+    }
   }
 }
 
@@ -277,12 +360,20 @@ size_t eval_smem_bytes(const EvalArgs &a, int) {
 }
 
 cudaError_t eval_prepare() {
-  return cudaFuncSetAttribute(k3_eval, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaError_t e = cudaFuncSetAttribute(k3_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k3_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {
   dim3 grid(grid_x, a.n_models);
-  k3_eval<<<grid, block, smem, s>>>(a);
+  k3_eval<false><<<grid, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {
+  dim3 grid(grid_x, a.n_models);
+  k3_eval<true><<<grid, block, smem, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -117,6 +117,12 @@ struct fp_plan {
   uint64_t resident_cap = 0;
   uint8_t *d_bins = nullptr;
   uint64_t bins_cap = 0;
+  // NEXT-2 three-pool state (lazy)
+  unsigned char *d_p3 = nullptr;           // pairs, b_win3, best3, block_best3, done3
+  fp_pool3_candidate *d_results3 = nullptr;
+  EvalArgs ea3{};
+  int k3p_grid_x = 1;
+  uint64_t n_cand3 = 0;
   // NCCL
   NcclComm comm = nullptr;
   fp_collectives coll{};                   // host hooks replacing NCCL (optional)
@@ -705,6 +711,8 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_done);
     cudaFree(p->d_resident);
     cudaFree(p->d_bins);
+    cudaFree(p->d_p3);
+    cudaFree(p->d_results3);
     cudaFree(p->d_calib);
     for (int i = 0; i < 2; ++i) {
       cudaFree(p->d_stage[i]);
@@ -850,6 +858,8 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
       const uint64_t need = n_local + 16;
       if (p->bins_cap < need) {
         cudaFree(p->d_bins);
+    cudaFree(p->d_p3);
+    cudaFree(p->d_results3);
         p->d_bins = nullptr;
         p->bins_cap = 0;
         CUDA_TRY(p, cudaMalloc(&p->d_bins, need), "cudaMalloc bins");
@@ -861,6 +871,8 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     if (p->resident_cap < n_local) {
       cudaFree(p->d_resident);
     cudaFree(p->d_bins);
+    cudaFree(p->d_p3);
+    cudaFree(p->d_results3);
       p->d_resident = nullptr;
       p->resident_cap = 0;
       CUDA_TRY(p, cudaMalloc(&p->d_resident, n_local * 4), "cudaMalloc resident trace");
@@ -1086,6 +1098,70 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
 }
 
 }  // namespace
+
+fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_results,
+                            fp_pool3_candidate *h_best, void *stream) {
+  if (!p || !h_best) return FP_ERR_INVALID_ARG;
+  if (!p->have_sweep) return fail(p, FP_ERR_STATE, "sweep_three_pools before a sweep");
+  if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
+    return fail(p, FP_ERR_INVALID_ARG, "rate_rps must be finite and > 0");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t nb = (uint32_t)p->b.size(), M = (uint32_t)p->models.size();
+  if (!p->d_p3) {
+    if (nb < 2 || nb > 4096) return fail(p, FP_ERR_CONFIG, "three pools need 2 <= n_b <= 4096");
+    std::vector<uint16_t> bw(nb);
+    for (uint32_t k = 0; k < nb; ++k) {
+      uint32_t w = index_of(p->windows, p->b[k]);
+      if (w == UINT32_MAX) return fail(p, FP_ERR_CONFIG, "B %u missing from windows (three pools)", p->b[k]);
+      bw[k] = (uint16_t)w;
+    }
+    std::vector<uint32_t> pairs;
+    pairs.reserve((size_t)nb * (nb - 1) / 2);
+    for (uint32_t i = 0; i < nb; ++i)
+      for (uint32_t j = i + 1; j < nb; ++j) pairs.push_back(i | (j << 16));
+    const uint64_t per = (uint64_t)p->gpus.size() * p->cl.size() * pairs.size();
+    if (per * M >= 0xffffffffull) return fail(p, FP_ERR_CONFIG, "three-pool grid has >= 2^32 candidates");
+    p->k3p_grid_x = (int)std::min<uint64_t>(std::max<uint64_t>(1, (uint64_t)p->sm_count * 8 / M),
+                                            std::max<uint64_t>(1, (per + 255) / 256));
+    const size_t off_bw = pairs.size() * 4;
+    const size_t off_best = (off_bw + nb * 2 + 15) & ~size_t(15);
+    const size_t off_bb = off_best + M * sizeof(fp_pool3_candidate);
+    const size_t off_done = off_bb + (size_t)M * p->k3p_grid_x * sizeof(BlockBest);
+    const size_t bytes = off_done + M * sizeof(unsigned int);
+    CUDA_TRY(p, cudaMalloc(&p->d_p3, bytes), "cudaMalloc three-pool state");
+    CUDA_TRY(p, cudaMemcpy(p->d_p3, pairs.data(), pairs.size() * 4, cudaMemcpyHostToDevice), "H2D pairs");
+    CUDA_TRY(p, cudaMemcpy(p->d_p3 + off_bw, bw.data(), nb * 2, cudaMemcpyHostToDevice), "H2D b_win3");
+    CUDA_TRY(p, cudaMemset(p->d_p3 + off_done, 0, M * sizeof(unsigned int)), "memset done3");
+    p->ea3 = p->ea;
+    p->ea3.pairs = reinterpret_cast<const uint32_t *>(p->d_p3);
+    p->ea3.n_pairs = (uint32_t)pairs.size();
+    p->ea3.b_win3 = reinterpret_cast<const uint16_t *>(p->d_p3 + off_bw);
+    p->ea3.per_model3 = per;
+    p->ea3.best3 = reinterpret_cast<fp_pool3_candidate *>(p->d_p3 + off_best);
+    p->ea3.block_best3 = reinterpret_cast<BlockBest *>(p->d_p3 + off_bb);
+    p->ea3.done3 = reinterpret_cast<unsigned int *>(p->d_p3 + off_done);
+    p->n_cand3 = per * M;
+  }
+  if (h_results && !p->d_results3)
+    CUDA_TRY(p, cudaMalloc(&p->d_results3, p->n_cand3 * sizeof(fp_pool3_candidate)), "cudaMalloc results3");
+  EvalArgs ea = p->ea3;
+  ea.rate = rate_rps;
+  ea.results3 = h_results ? p->d_results3 : nullptr;
+  {
+    LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+    cudaError_t e = launch_eval3(ea, p->k3p_grid_x, 256, p->k3_smem, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "three-pool evaluation launch");
+  }
+  ++p->launches;
+  CUDA_TRY(p, cudaMemcpyAsync(h_best, ea.best3, M * sizeof(fp_pool3_candidate), cudaMemcpyDeviceToHost, s),
+           "D2H best3");
+  if (h_results)
+    CUDA_TRY(p, cudaMemcpyAsync(h_results, p->d_results3, p->n_cand3 * sizeof(fp_pool3_candidate),
+                                cudaMemcpyDeviceToHost, s), "D2H results3");
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  return FP_OK;
+}
 
 fp_status best_split(fp_plan *p, fp_candidate *h_best) {
   if (!p || !h_best) return FP_ERR_INVALID_ARG;
