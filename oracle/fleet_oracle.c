@@ -477,3 +477,44 @@ int or_sweep3(const uint32_t *L, uint64_t n, uint32_t n_models, const uint32_t *
   free(mass);
   return rc;
 }
+
+/* ==========================================================================
+ * NEXT-3: calibration replay -- Alg. 1 OnResponse with Eq. (4)
+ * `eq:ema` applied to a feedback stream in arrival order.
+ * TEST INFRASTRUCTURE.
+ *   c_obs = |r| / usage.prompt_tokens
+ *   c_hat_k <- beta c_hat_k + (1 - beta) c_obs                    (Eq. ema)
+ *   sigma_k <- beta sigma_k + (1 - beta) |c_obs - c_hat_k(before)| (R26)
+ * Feedback with prompt_tokens == 0 is discarded; categories >= n_cats
+ * use the last category (R23). The state after the snap_at-th observation of
+ * each category is recorded (Table 5 reports n = 50).
+ * ========================================================================== */
+void or_calibrate(const uint32_t *bytes, const uint32_t *tokens, const uint8_t *cat, uint64_t n,
+                  uint32_t n_cats, double beta, const double *c0, const double *s0, double *c_hat,
+                  double *sigma, uint64_t *n_obs, uint64_t snap_at, double *snap_c, double *snap_s) {
+  for (uint32_t k = 0; k < n_cats; ++k) {
+    c_hat[k] = c0[k];
+    sigma[k] = s0[k];
+    n_obs[k] = 0;
+    if (snap_c) snap_c[k] = NAN;
+    if (snap_s) snap_s[k] = NAN;
+  }
+  const double w = 1.0 - beta;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (tokens[i] == 0) continue;
+    uint32_t k = cat[i] < n_cats ? cat[i] : n_cats - 1;
+    double obs = (double)bytes[i] / (double)tokens[i];
+    double prev = c_hat[k];
+    double t1 = beta * prev;
+    double t2 = w * obs;
+    c_hat[k] = t1 + t2;
+    double u1 = beta * sigma[k];
+    double u2 = w * fabs(obs - prev);
+    sigma[k] = u1 + u2;
+    n_obs[k] += 1;
+    if (n_obs[k] == snap_at) {
+      if (snap_c) snap_c[k] = c_hat[k];
+      if (snap_s) snap_s[k] = sigma[k];
+    }
+  }
+}

@@ -67,6 +67,7 @@ def lib():
         "or_num_threads": (ctypes.c_int, []),
         "or_route_ratio": (F64, [F64, F64, F64, F64]),
         "or_pool3_size": (U32, []),
+        "or_calibrate": (None, [VP, VP, VP, U64, U32, F64, VP, VP, VP, VP, VP, U64, VP, VP]),
         "or_sweep3": (ctypes.c_int, [VP, U64, U32, VP, U32, VP, VP, VP, VP, U32, VP, U32, VP, U32, VP, F64, F64,
                                      VP, VP]),
         "or_estimate_one": (U32, [U32, U32, F64]),
@@ -250,3 +251,21 @@ def sweep3(cfg, L, rate=None, want_all=True):
     if rc != 0:
         raise ValueError(f"or_sweep3 rc={rc}")
     return out, best
+
+
+# ---- NEXT-3: calibration replay ------------------------------------------------------------
+def calibrate(body, tokens, cat, n_cats, beta=0.95, c0=4.0, s0=0.5, snap_at=50):
+    """Sequential EMA replay (Alg. 1 OnResponse). Returns dict of per-category arrays."""
+    body, tokens = _u32(body), _u32(tokens)
+    cat = np.ascontiguousarray(cat, dtype=np.uint8)
+    c0a = np.ascontiguousarray(np.broadcast_to(np.asarray(c0, dtype=np.float64), (n_cats,)))
+    s0a = np.ascontiguousarray(np.broadcast_to(np.asarray(s0, dtype=np.float64), (n_cats,)))
+    c_hat = np.zeros(n_cats)
+    sig = np.zeros(n_cats)
+    nobs = np.zeros(n_cats, dtype=np.uint64)
+    sc = np.zeros(n_cats)
+    ss = np.zeros(n_cats)
+    lib().or_calibrate(body.ctypes.data, tokens.ctypes.data, cat.ctypes.data, body.size, n_cats, beta,
+                       c0a.ctypes.data, s0a.ctypes.data, c_hat.ctypes.data, sig.ctypes.data, nobs.ctypes.data,
+                       snap_at, sc.ctypes.data, ss.ctypes.data)
+    return {"c_hat": c_hat, "sigma": sig, "n_obs": nobs, "snap_c": sc, "snap_sigma": ss}
