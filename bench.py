@@ -198,6 +198,16 @@ def next1_fused_estimation(fp, cfg, n, reps=5):
                                          decision=dec)
     k1 = fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
     k4 = fp.fp_kernel_time(plan, fp.FP_KERNEL_ROUTE)
+    # NEXT-3: calibration replay of the same stream as feedback (|r|, usage.prompt_tokens, category)
+    cal = fp.calibrate_replay(plan, body, tp, cat, [(4.0, 0.5)] * 4)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        cal = fp.calibrate_replay(plan, body, tp, cat, [(4.0, 0.5)] * 4)
+    e1.record()
+    torch.cuda.synchronize()
+    cal_ms = e0.elapsed_time(e1) / reps
     fp.fleet_plan_destroy(plan)
     del body, mo, cat, tp, dec
     torch.cuda.empty_cache()
@@ -206,6 +216,9 @@ def next1_fused_estimation(fp, cfg, n, reps=5):
             "k1_raw_requests_per_s": n / (k1ms / 1e3),
             "k4_raw_ms": k4ms, "k4_raw_GBps": 14.0 * n / (k4ms / 1e3) / 1e9,
             "misroute_short_long_at_8K": mis,
+            "next3_calibration_replay": {"records": n, "ms": cal_ms, "records_per_s": n / (cal_ms / 1e3),
+                                         "c_hat": [float(x) for x in cal["c_hat"]],
+                                         "note": "two passes over 9 B/record (parallel affine-map scan)"},
             "note": "algorithmic bytes: sweep 9 B/request (bytes u32, max_output u32, category u8); "
                     "route 13 B in + 1 B decision"}
 

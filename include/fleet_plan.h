@@ -308,6 +308,26 @@ typedef struct fp_pool3_candidate {
 fp_status sweep_three_pools(fp_plan *plan, double rate_rps, fp_pool3_candidate *h_results,
                             fp_pool3_candidate *h_best, void *stream);
 
+/* ---- NEXT-3: calibration replay (Alg. 1 OnResponse) ---------------
+ * Replays a feedback stream in arrival order (device columns: body bytes
+ * |r|, usage.prompt_tokens, category) through the per-category EMA of Eq.
+ * `ema`: c_obs = |r| / prompt_tokens; c_hat <- beta c_hat +
+ * (1 - beta) c_obs; sigma_hat <- beta sigma_hat + (1 - beta) |c_obs -
+ * c_hat(before)| (R26). prompt_tokens == 0 is discarded; category >=
+ * n_cats counts as the last (R23). Starting from init[k], writes the final
+ * state h_final[k], the number of observations h_n_obs[k], and (nullable)
+ * the state right after the snap_at-th observation of each category into
+ * h_snap[k] (NaN if the category has fewer). Computed as a parallel scan of
+ * affine maps: equal to the sequential replay up to fp64 reassociation.
+ * Rank-local (the stream is this rank's). 1 <= n_cats <= 16, 0 < beta < 1.
+ * Synchronizes. The result is the fp_category_calibration snapshot that
+ * sweep_thresholds_raw / route_batch_raw consume. */
+fp_status calibrate_replay(fp_plan *plan, const uint32_t *d_body_bytes, const uint32_t *d_prompt_tokens,
+                           const uint8_t *d_category, uint64_t n, uint32_t n_cats, double beta,
+                           const fp_category_calibration *init, uint64_t snap_at,
+                           fp_category_calibration *h_final, uint64_t *h_n_obs,
+                           fp_category_calibration *h_snap, void *stream);
+
 /* Global per-bin histogram of the last sweep (K1 output after the cross-rank
  * sum; synchronizes). With E = sortuniq(B u C_L) ascending (|E| = n_edges of
  * fleet_plan_info): h_edges[j] = e_j for j < |E|; bin j < |E| holds the

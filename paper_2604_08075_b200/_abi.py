@@ -26,7 +26,7 @@ EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split"
             "fleet_plan_info", "fp_kernel_launches", "fleet_plan_destroy", "fp_status_string",
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
             "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
-            "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools"]
+            "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools", "calibrate_replay"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -155,6 +155,8 @@ def _load():
         "route_batch_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_u32, c_u32,
                                     c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), ctypes.POINTER(c_u64), c_vp]),
         "sweep_three_pools": (c_i32, [c_vp, c_dbl, c_vp, c_vp, c_vp]),
+        "calibrate_replay": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_u64, c_u32, c_dbl, c_vp, c_u64, c_vp, c_vp, c_vp,
+                                     c_vp]),
         "sweep_and_route": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
     }
     for name, (res, args) in sig.items():
@@ -464,3 +466,24 @@ def sweep_three_pools(plan, rate_rps, want_results=False, n_results=None, stream
     _check(lib.sweep_three_pools(plan.handle, float(rate_rps), out.ctypes.data if out is not None else None,
                                  best.ctypes.data, _stream_handle(stream, plan.device)), plan)
     return out, best
+
+
+# ---- NEXT-3: calibration replay ---------------------------------------------------------------
+def calibrate_replay(plan, body, prompt_tokens, cat, init, beta=0.95, snap_at=50, stream=None):
+    """EMA replay of a device feedback stream; init = [(c_hat, sigma_hat), ...] per category.
+    Returns dict(c_hat, sigma, n_obs, snap_c, snap_sigma) of numpy arrays."""
+    for t in (body, prompt_tokens, cat):
+        if not (hasattr(t, "is_cuda") and t.is_cuda and t.is_contiguous()):
+            raise ValueError("feedback columns must be contiguous CUDA tensors")
+    n = body.numel()
+    k = len(init)
+    ini = (fp_category_calibration * k)(*[fp_category_calibration(float(c), float(s)) for c, s in init])
+    fin = (fp_category_calibration * k)()
+    snap = (fp_category_calibration * k)()
+    nobs = np.zeros(k, dtype=np.uint64)
+    _check(lib.calibrate_replay(plan.handle, body.data_ptr(), prompt_tokens.data_ptr(), cat.data_ptr(), n, k,
+                                float(beta), ini, snap_at, fin, nobs.ctypes.data, snap,
+                                _stream_handle(stream, plan.device)), plan)
+    return {"c_hat": np.array([f.c_hat for f in fin]), "sigma": np.array([f.sigma_hat for f in fin]),
+            "n_obs": nobs, "snap_c": np.array([f.c_hat for f in snap]),
+            "snap_sigma": np.array([f.sigma_hat for f in snap])}

@@ -114,4 +114,25 @@ cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, 
 size_t eval_smem_bytes(const EvalArgs &a, int block);
 cudaError_t eval_prepare();
 
+// NEXT-3: calibration replay (k_calib.cu)
+struct CalibArgs {
+  const uint32_t *bytes, *tokens;
+  const uint8_t *cat;
+  uint64_t n;
+  uint32_t n_cats;                  // <= 16
+  double beta;
+  const double *c0, *s0;            // device [n_cats] initial state
+  uint64_t threads, seg;            // segments: thread t owns [t*seg, (t+1)*seg)
+  double *mapA, *mapB, *sigA, *sigB;  // [n_cats][threads]
+  uint32_t *mapN;                   // [n_cats][threads]
+  unsigned long long *preN;         // [n_cats][threads]
+  double *totA, *totB, *totSA, *totSB;  // [n_cats] (totA / totSA: final c_hat / sigma)
+  unsigned long long *totN;         // [n_cats]
+  uint64_t snap_at;
+  double *snap_c, *snap_s;          // [n_cats]
+  unsigned long long *snap_thread;  // [n_cats]
+};
+size_t calib_scratch_bytes(uint64_t threads, uint32_t n_cats);
+cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s);
+
 }  // namespace fp

@@ -123,6 +123,9 @@ struct fp_plan {
   EvalArgs ea3{};
   int k3p_grid_x = 1;
   uint64_t n_cand3 = 0;
+  // NEXT-3 calibration scratch (lazy)
+  unsigned char *d_calib_scratch = nullptr;
+  size_t calib_cap = 0;
   // NCCL
   NcclComm comm = nullptr;
   fp_collectives coll{};                   // host hooks replacing NCCL (optional)
@@ -712,6 +715,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_resident);
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
+    cudaFree(p->d_calib_scratch);
     cudaFree(p->d_results3);
     cudaFree(p->d_calib);
     for (int i = 0; i < 2; ++i) {
@@ -859,6 +863,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
       if (p->bins_cap < need) {
         cudaFree(p->d_bins);
     cudaFree(p->d_p3);
+    cudaFree(p->d_calib_scratch);
     cudaFree(p->d_results3);
         p->d_bins = nullptr;
         p->bins_cap = 0;
@@ -872,6 +877,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
       cudaFree(p->d_resident);
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
+    cudaFree(p->d_calib_scratch);
     cudaFree(p->d_results3);
       p->d_resident = nullptr;
       p->resident_cap = 0;
@@ -1160,6 +1166,96 @@ fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_r
     CUDA_TRY(p, cudaMemcpyAsync(h_results, p->d_results3, p->n_cand3 * sizeof(fp_pool3_candidate),
                                 cudaMemcpyDeviceToHost, s), "D2H results3");
   CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  return FP_OK;
+}
+
+fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint32_t *d_prompt_tokens,
+                           const uint8_t *d_category, uint64_t n, uint32_t n_cats, double beta,
+                           const fp_category_calibration *init, uint64_t snap_at,
+                           fp_category_calibration *h_final, uint64_t *h_n_obs,
+                           fp_category_calibration *h_snap, void *stream) {
+  if (!p || !init || !h_final || !h_n_obs) return FP_ERR_INVALID_ARG;
+  if (n_cats < 1 || n_cats > 16) return fail(p, FP_ERR_INVALID_ARG, "calibrate_replay needs 1 <= n_cats <= 16");
+  if (!(beta > 0.0 && beta < 1.0)) return fail(p, FP_ERR_INVALID_ARG, "beta must be in (0, 1)");
+  for (uint32_t k = 0; k < n_cats; ++k)
+    if (!std::isfinite(init[k].c_hat) || !std::isfinite(init[k].sigma_hat))
+      return fail(p, FP_ERR_INVALID_ARG, "initial state must be finite");
+  if (n && (!d_body_bytes || !d_prompt_tokens || !d_category || is_host_pointer(d_body_bytes) ||
+            is_host_pointer(d_prompt_tokens) || is_host_pointer(d_category)))
+    return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // one segment per thread, ~64 feedback records each, capped at 8 blocks / SM
+  const uint64_t max_threads = (uint64_t)p->sm_count * 8 * 256;
+  uint64_t threads = std::max<uint64_t>(256, std::min<uint64_t>(max_threads, (n + 63) / 64));
+  threads = (threads + 255) / 256 * 256;
+  const uint64_t seg = std::max<uint64_t>(1, (n + threads - 1) / threads);
+  const size_t scratch = calib_scratch_bytes(threads, n_cats);
+  const size_t small = 16 * 8 * 10;
+  if (p->calib_cap < scratch + small) {
+    cudaFree(p->d_calib_scratch);
+    p->d_calib_scratch = nullptr;
+    p->calib_cap = 0;
+    CUDA_TRY(p, cudaMalloc(&p->d_calib_scratch, scratch + small), "cudaMalloc calibration scratch");
+    p->calib_cap = scratch + small;
+  }
+  unsigned char *base = p->d_calib_scratch;
+  const uint64_t KT = (uint64_t)n_cats * threads;
+  CalibArgs a{};
+  a.bytes = d_body_bytes;
+  a.tokens = d_prompt_tokens;
+  a.cat = d_category;
+  a.n = n;
+  a.n_cats = n_cats;
+  a.beta = beta;
+  a.threads = threads;
+  a.seg = seg;
+  a.mapA = reinterpret_cast<double *>(base);
+  a.mapB = a.mapA + KT;
+  a.sigA = a.mapB + KT;
+  a.sigB = a.sigA + KT;
+  a.preN = reinterpret_cast<unsigned long long *>(a.sigB + KT);
+  a.mapN = reinterpret_cast<uint32_t *>(a.preN + KT);
+  double *sm = reinterpret_cast<double *>(base + scratch);     // 16-slot vectors
+  a.totA = sm;
+  a.totB = sm + 16;
+  a.totSA = sm + 32;
+  a.totSB = sm + 48;
+  a.totN = reinterpret_cast<unsigned long long *>(sm + 64);
+  a.snap_c = sm + 80;
+  a.snap_s = sm + 96;
+  a.snap_thread = reinterpret_cast<unsigned long long *>(sm + 112);
+  double *c0 = sm + 128, *s0 = sm + 144;
+  a.c0 = c0;
+  a.s0 = s0;
+  a.snap_at = snap_at;
+  std::vector<double> init_c(16, 0.0), init_s(16, 0.0);
+  for (uint32_t k = 0; k < n_cats; ++k) { init_c[k] = init[k].c_hat; init_s[k] = init[k].sigma_hat; }
+  CUDA_TRY(p, cudaMemcpyAsync(c0, init_c.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
+  CUDA_TRY(p, cudaMemcpyAsync(s0, init_s.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
+  // snapshots start as NaN (all-ones bytes), no snapshot thread (~0)
+  CUDA_TRY(p, cudaMemsetAsync(a.snap_c, 0xFF, 48 * 8, s), "memset snapshots");
+  {
+    LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+    cudaError_t e = launch_calibrate(a, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "calibration replay launch");
+  }
+  p->launches += 5;
+  std::vector<double> h(160);
+  CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 128 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  for (uint32_t k = 0; k < n_cats; ++k) {
+    // the scan kernel leaves the final states in totA / totSA
+    uint64_t nobs;
+    memcpy(&nobs, &h[64 + k], 8);
+    h_final[k].c_hat = h[k];
+    h_final[k].sigma_hat = h[32 + k];
+    h_n_obs[k] = nobs;
+    if (h_snap) {
+      h_snap[k].c_hat = h[80 + k];
+      h_snap[k].sigma_hat = h[96 + k];
+    }
+  }
   return FP_OK;
 }
 
