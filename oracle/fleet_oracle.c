@@ -518,3 +518,110 @@ void or_calibrate(const uint32_t *bytes, const uint32_t *tokens, const uint8_t *
     }
   }
 }
+
+/* ==========================================================================
+ * NEXT-4: peak-window provisioning ("transient overload ... during
+ * traffic bursts"). TEST INFRASTRUCTURE.
+ * Arrival times split the trace into windows w = floor(arrival_ns / W). For
+ * each candidate, every pool is sized for its busiest window instead of the
+ * mean rate: lambda_p = max_w n_p(w) * (1e9 / W), I_p = ceil(lambda_p / mu_p)
+ * (Sec. 3 sizing; R27). Same candidate grid and flat order as or_sweep.
+ * ========================================================================== */
+typedef struct {
+  uint32_t index, model, gpu, b_short, c_short, c_long, flags, _pad;
+  uint64_t peak_short, peak_long, peak_homo;
+  uint64_t inst_short, inst_long, inst_homo, gpus_dual, gpus_homo;
+  double lambda_short, lambda_long, lambda_homo, cost_dual, cost_homo, savings;
+} or_peak;
+
+uint32_t or_peak_size(void) { return (uint32_t)sizeof(or_peak); }
+
+int or_sweep_peak(const uint32_t *L, const uint64_t *arrival_ns, uint64_t n, uint64_t window_ns,
+                  uint32_t n_models, const uint32_t *arch, uint32_t n_gpus, const uint64_t *gpu_u64,
+                  const double *gpu_price, const uint64_t *deploy, const uint32_t *b, uint32_t n_b,
+                  const uint32_t *cs, uint32_t n_cs, const uint32_t *cl, uint32_t n_cl, const uint32_t *windows,
+                  uint32_t n_w, const double *mu, double hours, or_peak *out, or_peak *best) {
+  if (n == 0 || window_ns == 0) return 1;
+  uint64_t nwin = 0;
+  for (uint64_t i = 0; i < n; ++i)
+    if (arrival_ns[i] / window_ns + 1 > nwin) nwin = arrival_ns[i] / window_ns + 1;
+  /* per window, per threshold value (B and C_L): #{L <= x} by definition */
+  uint32_t nx = n_b + n_cl;
+  uint64_t *cnt = (uint64_t *)calloc((size_t)nwin * nx, sizeof(uint64_t));
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t w = arrival_ns[i] / window_ns;
+    for (uint32_t j = 0; j < nx; ++j) {
+      uint32_t x = j < n_b ? b[j] : cl[j - n_b];
+      cnt[w * nx + j] += (L[i] <= x) ? 1u : 0u;
+    }
+  }
+  const double inv_w = 1e9 / (double)window_ns;   /* windows per second */
+  uint32_t n_cs_eff = n_cs ? n_cs : 1;
+  int rc = 0;
+  for (uint32_t m = 0; m < n_models && !rc; ++m) {
+    or_peak bm;
+    memset(&bm, 0, sizeof bm);
+    bm.index = UINT32_MAX;
+    bm.model = m;
+    bm.cost_dual = bm.cost_homo = INFINITY;
+    int have = 0;
+    for (uint32_t g = 0; g < n_gpus && !rc; ++g)
+      for (uint32_t l = 0; l < n_cl && !rc; ++l)
+        for (uint32_t s = 0; s < n_cs_eff && !rc; ++s)
+          for (uint32_t k = 0; k < n_b; ++k) {
+            uint64_t idx = ((((uint64_t)m * n_gpus + g) * n_cl + l) * n_cs_eff + s) * n_b + k;
+            or_peak c;
+            memset(&c, 0, sizeof c);
+            c.index = (uint32_t)idx;
+            c.model = m;
+            c.gpu = g;
+            c.b_short = b[k];
+            c.c_short = n_cs ? cs[s] : b[k];
+            c.c_long = cl[l];
+            c.cost_dual = c.cost_homo = INFINITY;
+            if (c.b_short <= c.c_short && c.c_short <= c.c_long) {
+              const uint64_t *dp = deploy + ((uint64_t)m * n_gpus + g) * 3;
+              uint32_t tp = (uint32_t)dp[0];
+              uint64_t wpg = dp[1], gpi = dp[2];
+              const uint64_t *gu = gpu_u64 + (uint64_t)g * 4;
+              const uint32_t *ar = arch + (uint64_t)m * 4;
+              uint32_t ws = find_u32(windows, n_w, c.c_short), wl = find_u32(windows, n_w, c.c_long);
+              if (ws == UINT32_MAX || wl == UINT32_MAX) { rc = 2; break; }
+              const double *mg = mu + ((uint64_t)m * n_gpus + g) * n_w;
+              for (uint64_t w = 0; w < nwin; ++w) {
+                uint64_t s_ = cnt[w * nx + k], sl = cnt[w * nx + n_b + l];
+                if (s_ > c.peak_short) c.peak_short = s_;
+                if (sl - s_ > c.peak_long) c.peak_long = sl - s_;
+                if (sl > c.peak_homo) c.peak_homo = sl;
+              }
+              uint64_t budget = or_kv_budget(gu[0], (uint32_t)gu[1], (uint32_t)gu[2], wpg, gu[3]);
+              uint64_t nseq_s = or_max_seqs(budget, or_kv_bytes_per_seq(ar[0], ar[1], ar[2], ar[3], c.c_short), tp);
+              uint64_t nseq_l = or_max_seqs(budget, or_kv_bytes_per_seq(ar[0], ar[1], ar[2], ar[3], c.c_long), tp);
+              c.lambda_short = (double)c.peak_short * inv_w;
+              c.lambda_long = (double)c.peak_long * inv_w;
+              c.lambda_homo = (double)c.peak_homo * inv_w;
+              int ok_s = or_pool_instances(c.lambda_short, mg[ws], nseq_s, &c.inst_short);
+              int ok_l = or_pool_instances(c.lambda_long, mg[wl], nseq_l, &c.inst_long);
+              int ok_h = or_pool_instances(c.lambda_homo, mg[wl], nseq_l, &c.inst_homo);
+              int ok_d = ok_s && ok_l;
+              if (!ok_d) { c.inst_short = 0; c.inst_long = 0; }
+              c.gpus_dual = gpi * (c.inst_short + c.inst_long);
+              c.gpus_homo = gpi * c.inst_homo;
+              c.cost_dual = ok_d ? or_cost(c.gpus_dual, gpu_price[g], hours) : INFINITY;
+              c.cost_homo = ok_h ? or_cost(c.gpus_homo, gpu_price[g], hours) : INFINITY;
+              c.savings = (ok_d && ok_h && c.gpus_homo > 0)
+                              ? ((double)c.gpus_homo - (double)c.gpus_dual) / (double)c.gpus_homo
+                              : 0.0;
+              c.flags = OR_VALID | (ok_d ? OR_FEASIBLE : 0) | (ok_h ? OR_HOMO_FEASIBLE : 0);
+            }
+            if (out) out[idx] = c;
+            if ((c.flags & OR_FEASIBLE) && (!have || c.cost_dual < bm.cost_dual)) {
+              bm = c;
+              have = 1;
+            }
+          }
+    best[m] = bm;
+  }
+  free(cnt);
+  return rc;
+}

@@ -27,6 +27,16 @@ POOL3_DTYPE = np.dtype([
     ("gpus_homo", "<u8"), ("cost", "<f8"), ("cost_homo", "<f8"), ("savings", "<f8"),
 ])
 
+PEAK_DTYPE = np.dtype([
+    ("index", "<u4"), ("model", "<u4"), ("gpu", "<u4"), ("b_short", "<u4"), ("c_short", "<u4"),
+    ("c_long", "<u4"), ("flags", "<u4"), ("_pad", "<u4"),
+    ("peak_short", "<u8"), ("peak_long", "<u8"), ("peak_homo", "<u8"),
+    ("inst_short", "<u8"), ("inst_long", "<u8"), ("inst_homo", "<u8"), ("gpus_dual", "<u8"),
+    ("gpus_homo", "<u8"),
+    ("lambda_short", "<f8"), ("lambda_long", "<f8"), ("lambda_homo", "<f8"), ("cost_dual", "<f8"),
+    ("cost_homo", "<f8"), ("savings", "<f8"),
+])
+
 CANDIDATE_DTYPE = np.dtype([
     ("index", "<u4"), ("model", "<u4"), ("gpu", "<u4"), ("b_short", "<u4"),
     ("c_short", "<u4"), ("c_long", "<u4"), ("flags", "<u4"), ("_pad", "<u4"),
@@ -67,6 +77,9 @@ def lib():
         "or_num_threads": (ctypes.c_int, []),
         "or_route_ratio": (F64, [F64, F64, F64, F64]),
         "or_pool3_size": (U32, []),
+        "or_peak_size": (U32, []),
+        "or_sweep_peak": (ctypes.c_int, [VP, VP, U64, U64, U32, VP, U32, VP, VP, VP, VP, U32, VP, U32, VP, U32, VP,
+                                         U32, VP, F64, VP, VP]),
         "or_calibrate": (None, [VP, VP, VP, U64, U32, F64, VP, VP, VP, VP, VP, U64, VP, VP]),
         "or_sweep3": (ctypes.c_int, [VP, U64, U32, VP, U32, VP, VP, VP, VP, U32, VP, U32, VP, U32, VP, F64, F64,
                                      VP, VP]),
@@ -80,6 +93,7 @@ def lib():
         f.argtypes = args
     assert L.or_candidate_size() == CANDIDATE_DTYPE.itemsize, "oracle record layout drift"
     assert L.or_pool3_size() == POOL3_DTYPE.itemsize, "oracle pool3 layout drift"
+    assert L.or_peak_size() == PEAK_DTYPE.itemsize, "oracle peak layout drift"
     _lib = L
     return L
 
@@ -269,3 +283,21 @@ def calibrate(body, tokens, cat, n_cats, beta=0.95, c0=4.0, s0=0.5, snap_at=50):
                        c0a.ctypes.data, s0a.ctypes.data, c_hat.ctypes.data, sig.ctypes.data, nobs.ctypes.data,
                        snap_at, sc.ctypes.data, ss.ctypes.data)
     return {"c_hat": c_hat, "sigma": sig, "n_obs": nobs, "snap_c": sc, "snap_sigma": ss}
+
+
+# ---- NEXT-4: peak-window provisioning --------------------------------------------------------
+def sweep_peak(cfg, L, arrival_ns, window_ns, want_all=True):
+    L = _u32(L)
+    arr = np.ascontiguousarray(arrival_ns, dtype=np.uint64)
+    a = config_arrays(cfg)
+    out = np.zeros(cfg.n_candidates(), dtype=PEAK_DTYPE) if want_all else None
+    best = np.zeros(len(cfg.models), dtype=PEAK_DTYPE)
+    rc = lib().or_sweep_peak(
+        L.ctypes.data, arr.ctypes.data, L.size, int(window_ns), len(cfg.models), a["arch"].ctypes.data,
+        len(cfg.gpus), a["gpu_u64"].ctypes.data, a["price"].ctypes.data, a["deploy"].ctypes.data,
+        a["b"].ctypes.data, a["b"].size, a["cs"].ctypes.data if a["cs"].size else None, a["cs"].size,
+        a["cl"].ctypes.data, a["cl"].size, a["windows"].ctypes.data, a["windows"].size, a["mu"].ctypes.data,
+        float(cfg.hours_per_year), out.ctypes.data if out is not None else None, best.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"or_sweep_peak rc={rc}")
+    return out, best

@@ -57,3 +57,22 @@ extern "C" int synth_generate_raw_device(const uint32_t *d_luts, const uint8_t *
                                                              max_out, cat, true_prompt);
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }
+
+__global__ void synth_gaps_kernel(const uint32_t *__restrict__ gap_table, const uint32_t *__restrict__ burst8,
+                                  uint64_t seed, uint64_t first, uint64_t count, uint32_t *out) {
+  uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < count; j += stride)
+    out[j] = syn_gap(gap_table, burst8, seed, first + j);
+}
+
+extern "C" int synth_gaps_device(const uint32_t *d_gap_table, const uint32_t *d_burst8, uint64_t seed,
+                                 uint64_t first, uint64_t count, uint32_t *d_out, cudaStream_t stream) {
+  if (count == 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  uint64_t blocks = (count + 255) / 256, cap = (uint64_t)sms * 16;
+  if (blocks > cap) blocks = cap;
+  synth_gaps_kernel<<<(unsigned)blocks, 256, 0, stream>>>(d_gap_table, d_burst8, seed, first, count, d_out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}

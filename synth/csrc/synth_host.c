@@ -26,3 +26,11 @@ int synth_generate_raw_host(const uint32_t *luts, const uint8_t *interp, const u
                     bytes + j, max_out + j, cat + j, true_prompt + j);
   return 0;
 }
+
+int synth_gaps_host(const uint32_t *gap_table, const uint32_t *burst8, uint64_t seed, uint64_t first,
+                    uint64_t count, uint32_t *out) {
+  int64_t n = (int64_t)count;
+#pragma omp parallel for schedule(static)
+  for (int64_t j = 0; j < n; ++j) out[j] = syn_gap(gap_table, burst8, seed, first + (uint64_t)j);
+  return 0;
+}

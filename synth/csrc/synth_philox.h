@@ -68,4 +68,11 @@ SYN_HD void syn_request_raw(const uint32_t *luts, const uint8_t *interp, const u
   *cat = (uint8_t)k;
   *true_prompt = lin;
 }
+/* Arrival gaps (NEXT-4): see synth/shapes.py "Arrival times". */
+SYN_HD uint32_t syn_gap(const uint32_t *gap_table, const uint32_t *burst8, uint64_t seed, uint64_t i) {
+  uint32_t c[4] = {(uint32_t)i, (uint32_t)(i >> 32), 1u, 0u};
+  syn_philox4x32_10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+  uint64_t g = gap_table[c[0] >> 16];
+  return (uint32_t)((g * burst8[(i >> 20) & 7u]) >> 3);
+}
 #endif

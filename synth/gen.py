@@ -223,3 +223,51 @@ def generate_raw_device(mix: Mixture | str, seed: int, first: int, count: int):
         raise RuntimeError(f"synth_generate_raw_device rc={rc}")
     s.synchronize()
     return out
+
+
+# ------------------------------------------------------------------- arrivals ----
+def gaps_np(seed: int, first: int, count: int, rate_rps: float) -> np.ndarray:
+    from .philox import philox4x32_10
+    from .shapes import BURST_FACTORS, gap_table
+    idx = np.arange(first, first + count, dtype=np.uint64)
+    w0, _, _, _ = philox4x32_10(idx & np.uint64(0xFFFFFFFF), idx >> np.uint64(32), 1, 0,
+                                seed & 0xFFFFFFFF, (seed >> 32) & 0xFFFFFFFF)
+    g = gap_table(rate_rps).astype(np.uint64)[(w0 >> np.uint32(16)).astype(np.int64)]
+    f = np.asarray(BURST_FACTORS, dtype=np.uint64)[((idx >> np.uint64(20)) & np.uint64(7)).astype(np.int64)]
+    return ((g * f) >> np.uint64(3)).astype(np.uint32)
+
+
+def arrivals_host(seed: int, count: int, rate_rps: float) -> np.ndarray:
+    """uint64 arrival times (ns) of requests [0, count): inclusive sum of the gaps."""
+    from .shapes import BURST_FACTORS, gap_table
+    gt = np.ascontiguousarray(gap_table(rate_rps))
+    b8 = np.asarray(BURST_FACTORS, dtype=np.uint32)
+    g = np.empty(count, dtype=np.uint32)
+    lib = _load_host()
+    f = lib.synth_gaps_host
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                  ctypes.c_void_p]
+    f.restype = ctypes.c_int
+    f(gt.ctypes.data, b8.ctypes.data, seed, 0, count, g.ctypes.data)
+    return np.cumsum(g, dtype=np.uint64)
+
+
+def arrivals_device(seed: int, count: int, rate_rps: float):
+    """CUDA gaps + an integer prefix sum (torch.cumsum on int64: exact)."""
+    import torch
+    from .shapes import BURST_FACTORS, gap_table
+    dev = torch.device("cuda", torch.cuda.current_device())
+    gt = torch.from_numpy(np.ascontiguousarray(gap_table(rate_rps)).view(np.int32)).to(dev)
+    b8 = torch.tensor(BURST_FACTORS, dtype=torch.int32, device=dev)
+    g = torch.empty(count, dtype=torch.int32, device=dev)
+    lib = _load_dev()
+    f = lib.synth_gaps_device
+    f.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
+                  ctypes.c_void_p, ctypes.c_void_p]
+    f.restype = ctypes.c_int
+    s = torch.cuda.current_stream(dev)
+    if f(gt.data_ptr(), b8.data_ptr(), seed, 0, count, g.data_ptr(), ctypes.c_void_p(s.cuda_stream)) != 0:
+        raise RuntimeError("synth_gaps_device failed")
+    out = torch.cumsum(g.to(torch.int64) & 0xFFFFFFFF, dim=0)
+    s.synchronize()
+    return out

@@ -223,3 +223,19 @@ def ratio_tables():
     for k, c in enumerate(CAT_TRUE_RATIO):
         out[k] = np.round(c * noise * 65536.0).astype(np.uint32)
     return out
+
+
+# --------------------------------------------------------------------------
+# Arrival times (NEXT-4): Poisson arrivals ("Poisson arrivals") with
+# stated burst phases. gap_i = G[w >> 16] * F[(i >> 20) & 7] >> 3 ns, where G
+# is the exponential inverse CDF (mean 1e9 / rate ns, 16.16-free integer ns)
+# and F = {8, 8, 8, 4, 8, 8, 2, 8} halves / quarters the gaps in two of
+# every eight 2^20-request phases (2x / 4x bursts, stated); w is the first
+# Philox word of counter (lo32 i, hi32 i, 1, 0). arrival_i = sum_{j <= i} gap_j.
+# --------------------------------------------------------------------------
+BURST_FACTORS = (8, 8, 8, 4, 8, 8, 2, 8)
+
+
+def gap_table(rate_rps: float):
+    u = (np.arange(65536, dtype=np.float64) + 0.5) / 65536.0
+    return np.round(-np.log1p(-u) * (1e9 / rate_rps)).astype(np.uint32)
