@@ -223,6 +223,44 @@ def next1_fused_estimation(fp, cfg, n, reps=5):
                     "route 13 B in + 1 B decision"}
 
 
+def next4_peak_windows(fp, cfg, n, d_len, reps=3):
+    """NEXT-4: peak-window provisioning over the same trace with arrival times
+    (windowed 2-D histogram K1w + scan K2w, K3 peak mode)."""
+    import torch
+    from synth.gen import arrivals_device
+    arr = arrivals_device(cfg.seed, n, cfg.rate_rps)
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=fp.FP_FLAG_KERNEL_TIMING)
+    out = {"n_requests": n, "span_s": float(arr[-1].item()) / 1e9}
+    for wsec in (60, 1):
+        w = wsec * 10**9
+        fp.sweep_peak_windows(plan, d_len, arr, w)
+        torch.cuda.synchronize()
+        fp.fp_kernel_time_reset(plan)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            _, best = fp.sweep_peak_windows(plan, d_len, arr, w)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        kh, nh = fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
+        ke, ne = fp.fp_kernel_time(plan, fp.FP_KERNEL_EVAL)
+        hist_ms = kh / nh
+        out[f"window_{wsec}s"] = {
+            "windows": int(out["span_s"] // wsec) + 1, "ms": ms, "requests_per_s": n / (ms / 1e3),
+            "hist_ms": hist_ms, "hist_GBps": 4.0 * n / (hist_ms / 1e3) / 1e9,
+            "hist_frac": 4.0 * n / (hist_ms / 1e3) / 1e9 / _peaks()[0], "eval_ms": ke / ne,
+            "best_savings_peak": [float(x) for x in best["savings"]],
+            "best_gpus_dual_peak": [int(x) for x in best["gpus_dual"]]}
+    out["note"] = ("hist = K0w window bounds + K1w 2-D histogram + K2w scan/maxima; algorithmic bytes "
+                   "4 B/request (L_total; arrivals are read only at window boundaries, the trace being in "
+                   "arrival order); K3 peak reads the per-(B, C_L) window maxima")
+    fp.fleet_plan_destroy(plan)
+    del arr
+    torch.cuda.empty_cache()
+    return out
+
+
 def k3_large_grid(fp, generate_device, reps=5):
     """K3 alone on a 2^24-candidate grid (SURVEY §8(d) ALU regime)."""
     import torch
@@ -407,6 +445,8 @@ def run_ours(args, cfg):
             "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
     if world == 1 and args.k3_grid:
         line["k3_large_grid"] = k3_large_grid(fp, generate_device)
+    if world == 1 and args.next4:
+        line["next4_peak_windows"] = next4_peak_windows(fp, cfg, n, d_len)
     if world == 1 and args.next1:
         del d_len, d_dec
         torch.cuda.empty_cache()
@@ -432,6 +472,8 @@ def main():
                     help="skip the three-pool (NEXT-2) measurement")
     ap.add_argument("--no-next1", dest="next1", action="store_false",
                     help="skip the fused token-budget estimation measurement (NEXT-1)")
+    ap.add_argument("--no-next4", dest="next4", action="store_false",
+                    help="skip the peak-window provisioning measurement (NEXT-4)")
     ap.add_argument("--no-k3-grid", dest="k3_grid", action="store_false",
                     help="skip the 2^24-candidate K3 measurement")
     ap.add_argument("--ref-sample", type=int, default=10_000_000,

@@ -100,6 +100,7 @@ typedef struct fp_grid {
 #define FP_FLAG_NO_MASS 0x1u         /* skip token-mass sums (occupancy = 0)          */
 #define FP_FLAG_REPLICATED_GRID 0x2u /* world > 1: every rank evaluates all candidates */
 #define FP_FLAG_KERNEL_TIMING 0x4u   /* record CUDA events around every kernel launch   */
+#define FP_FLAG_CHECK_ORDER 0x8u     /* sweep_peak_windows: verify arrival order (8 B/req) */
 
 typedef struct fp_plan_desc {
   uint32_t abi_version;           /* FP_ABI_VERSION                                 */
@@ -327,6 +328,36 @@ fp_status calibrate_replay(fp_plan *plan, const uint32_t *d_body_bytes, const ui
                            const fp_category_calibration *init, uint64_t snap_at,
                            fp_category_calibration *h_final, uint64_t *h_n_obs,
                            fp_category_calibration *h_snap, void *stream);
+
+/* ---- NEXT-4: peak-window provisioning -----------------
+ * Requests carry arrival times (ns, non-decreasing, device u64[n]). The trace
+ * is cut into windows w = floor(arrival / window_ns); for every candidate of
+ * the plan's grid each pool is sized for its busiest window instead of the
+ * mean rate: lambda_p = max_w n_p(w) * (1e9 / window_ns) requests/s, then
+ * I_p = ceil(lambda_p / mu_p) as in Sec. 3 (R27). Same flat index as
+ * fp_candidate. 144 bytes. */
+typedef struct fp_peak_candidate {
+  uint32_t index, model, gpu, b_short, c_short, c_long, flags, _pad;
+  uint64_t peak_short, peak_long, peak_homo;         /* requests in the busiest window */
+  uint64_t inst_short, inst_long, inst_homo, gpus_dual, gpus_homo;
+  double lambda_short, lambda_long, lambda_homo;     /* peak rates, requests/s          */
+  double cost_dual, cost_homo, savings;
+} fp_peak_candidate;
+
+/* Peak-window sweep over d_len / d_arrival_ns (device, n_local each, n_local
+ * < 2^32; rank-local). Precondition: arrivals non-decreasing (a trace is in
+ * arrival order) -- the requests of a window are then one contiguous
+ * index range, which the kernels exploit; the first/last arrivals are always
+ * checked, the whole column only with FP_FLAG_CHECK_ORDER (otherwise an
+ * unsorted column gives unspecified, but memory-safe, results). h_results
+ * (nullable) receives every candidate, h_best[n_models] the per-model
+ * cheapest feasible one. Synchronizes. Errors: FP_ERR_EMPTY_TRACE
+ * (n_local == 0), FP_ERR_INVALID_ARG (window_ns == 0, host or misaligned
+ * pointers, n_local >= 2^32, more than 2^26 windows, arrivals found out of
+ * order), FP_ERR_CONFIG (grid too large for shared memory), FP_ERR_OOM. */
+fp_status sweep_peak_windows(fp_plan *plan, const uint32_t *d_len, const uint64_t *d_arrival_ns,
+                             uint64_t n_local, uint64_t window_ns, fp_peak_candidate *h_results,
+                             fp_peak_candidate *h_best, void *stream);
 
 /* Global per-bin histogram of the last sweep (K1 output after the cross-rank
  * sum; synchronizes). With E = sortuniq(B u C_L) ascending (|E| = n_edges of

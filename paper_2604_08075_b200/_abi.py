@@ -18,6 +18,7 @@ FP_ABI_VERSION = 1
 FP_FLAG_NO_MASS = 0x1
 FP_FLAG_REPLICATED_GRID = 0x2
 FP_FLAG_KERNEL_TIMING = 0x4
+FP_FLAG_CHECK_ORDER = 0x8
 FP_KERNEL_TRACE, FP_KERNEL_EVAL, FP_KERNEL_ROUTE = 0, 1, 2
 FP_CAND_VALID, FP_CAND_FEASIBLE, FP_CAND_HOMO_FEASIBLE = 1, 2, 4
 STATUS = ["FP_OK", "FP_ERR_INVALID_ARG", "FP_ERR_CONFIG", "FP_ERR_EMPTY_TRACE", "FP_ERR_ALIGNMENT",
@@ -26,7 +27,8 @@ EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split"
             "fleet_plan_info", "fp_kernel_launches", "fleet_plan_destroy", "fp_status_string",
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
             "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
-            "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools", "calibrate_replay"]
+            "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools", "calibrate_replay",
+            "sweep_peak_windows"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -127,6 +129,18 @@ FP_POOL3 = np.dtype([
 ])
 assert FP_POOL3.itemsize == 160
 
+# fp_peak_candidate (144 bytes)
+FP_PEAK = np.dtype([
+    ("index", "<u4"), ("model", "<u4"), ("gpu", "<u4"), ("b_short", "<u4"), ("c_short", "<u4"),
+    ("c_long", "<u4"), ("flags", "<u4"), ("_pad", "<u4"),
+    ("peak_short", "<u8"), ("peak_long", "<u8"), ("peak_homo", "<u8"),
+    ("inst_short", "<u8"), ("inst_long", "<u8"), ("inst_homo", "<u8"), ("gpus_dual", "<u8"),
+    ("gpus_homo", "<u8"),
+    ("lambda_short", "<f8"), ("lambda_long", "<f8"), ("lambda_homo", "<f8"),
+    ("cost_dual", "<f8"), ("cost_homo", "<f8"), ("savings", "<f8"),
+])
+assert FP_PEAK.itemsize == 144
+
 
 def _load():
     if not os.path.exists(LIB_PATH):
@@ -155,6 +169,7 @@ def _load():
         "route_batch_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_u32, c_u32,
                                     c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), ctypes.POINTER(c_u64), c_vp]),
         "sweep_three_pools": (c_i32, [c_vp, c_dbl, c_vp, c_vp, c_vp]),
+        "sweep_peak_windows": (c_i32, [c_vp, c_vp, c_vp, c_u64, c_u64, c_vp, c_vp, c_vp]),
         "calibrate_replay": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_u64, c_u32, c_dbl, c_vp, c_u64, c_vp, c_vp, c_vp,
                                      c_vp]),
         "sweep_and_route": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
@@ -487,3 +502,16 @@ def calibrate_replay(plan, body, prompt_tokens, cat, init, beta=0.95, snap_at=50
     return {"c_hat": np.array([f.c_hat for f in fin]), "sigma": np.array([f.sigma_hat for f in fin]),
             "n_obs": nobs, "snap_c": np.array([f.c_hat for f in snap]),
             "snap_sigma": np.array([f.sigma_hat for f in snap])}
+
+
+# ---- NEXT-4: peak-window provisioning -------------------------------------------------------
+def sweep_peak_windows(plan, lengths, arrival_ns, window_ns, want_results=False, stream=None):
+    """lengths: int32/uint32 CUDA tensor; arrival_ns: int64 CUDA tensor (non-decreasing)."""
+    if not (lengths.is_cuda and arrival_ns.is_cuda and lengths.numel() == arrival_ns.numel()):
+        raise ValueError("lengths and arrival_ns must be CUDA tensors of equal length")
+    out = np.zeros(fleet_plan_info(plan)["n_candidates"], dtype=FP_PEAK) if want_results else None
+    best = np.zeros(plan.n_models, dtype=FP_PEAK)
+    _check(lib.sweep_peak_windows(plan.handle, lengths.data_ptr(), arrival_ns.data_ptr(), lengths.numel(),
+                                  int(window_ns), out.ctypes.data if out is not None else None, best.ctypes.data,
+                                  _stream_handle(stream, plan.device)), plan)
+    return out, best

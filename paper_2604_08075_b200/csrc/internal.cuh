@@ -108,11 +108,44 @@ struct EvalArgs {
   fp_pool3_candidate *best3 = nullptr;  // [n_models]
   BlockBest *block_best3 = nullptr;
   unsigned int *done3 = nullptr;
+  // NEXT-4 peak windows: cumulative per-window counts [n_windows][nbins]
+  const uint32_t *colmax_pk = nullptr;  // NEXT-4 per-bin / per-(B, C_L) window maxima
+  const uint32_t *pairmax_pk = nullptr;
+  double inv_w_s = 0.0;                 // windows per second = 1e9 / window_ns
+  fp_peak_candidate *results_pk = nullptr;
+  fp_peak_candidate *best_pk = nullptr;
+  BlockBest *block_best_pk = nullptr;
+  unsigned int *done_pk = nullptr;
 };
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
+cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
 size_t eval_smem_bytes(const EvalArgs &a, int block);
 cudaError_t eval_prepare();
+
+// NEXT-4: peak-window provisioning (k_peak.cu + the k3 peak kernel)
+struct PeakArgs {
+  const uint32_t *len;
+  const uint64_t *arrival;          // ns, non-decreasing
+  uint64_t n;                       // < 2^32
+  uint64_t window_ns;
+  uint64_t n_windows;               // floor(arrival[n-1] / window_ns) + 1
+  uint64_t *start;                  // [n_windows + 1]: first request of each window
+  const void *lut;                  // as TraceArgs
+  const uint32_t *edges;
+  uint32_t lut_cells, lutw, clampv, round, shift, nbins;
+  uint32_t *hist2d;                 // [n_windows][nbins] requests per (window, bin)
+  const uint16_t *b_edge, *cl_edge; // index in E of each B / C_L
+  uint32_t n_b, n_cl;
+  uint32_t rows;                    // windows per K2w shared-memory chunk
+  uint32_t *colmax;                 // [nbins]      max_w cnt_le[w][j]
+  uint32_t *pairmax;                // [n_b * n_cl] max_w cnt_le[w][cl_edge[l]] - cnt_le[w][b_edge[k]]
+  unsigned int *error;
+  bool check_order;
+};
+size_t peak_smem_bytes(const PeakArgs &a);
+size_t peak_scan_smem_bytes(const PeakArgs &a);
+cudaError_t launch_peak_hist(const PeakArgs &a, int grid, cudaStream_t s);
 
 // NEXT-3: calibration replay (k_calib.cu)
 struct CalibArgs {

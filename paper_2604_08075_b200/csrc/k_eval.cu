@@ -353,7 +353,133 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   }
 }
 
+// NEXT-4: peak-window sizing. Same grid and index decomposition
+// as evaluate(); the routing counts of a pool become its busiest window's
+// counts (max over windows of the cumulative per-window histogram), the rates
+// peak * (1e9 / window_ns), and each pool is sized with the Sec. 3 formula in
+// the oracle's operation order (or_sweep_peak).
+__device__ void evaluate_peak(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx, fp_peak_candidate &c) {
+  uint32_t r = (uint32_t)idx;
+  const uint32_t k = r % a.n_b; r /= a.n_b;
+  const uint32_t s = r % a.n_cs_eff; r /= a.n_cs_eff;
+  const uint32_t l = r % a.n_cl; r /= a.n_cl;
+  const uint32_t g = r % a.n_gpus;
+  const uint32_t B = a.b[k], CL = a.cl[l], CS = a.n_cs ? a.cs[s] : B;
+  c.index = (uint32_t)idx; c.model = m; c.gpu = g; c.b_short = B; c.c_short = CS; c.c_long = CL;
+  c.flags = 0; c._pad = 0;
+  c.peak_short = c.peak_long = c.peak_homo = 0;
+  c.inst_short = c.inst_long = c.inst_homo = c.gpus_dual = c.gpus_homo = 0;
+  c.lambda_short = c.lambda_long = c.lambda_homo = 0.0;
+  c.cost_dual = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
+  c.savings = 0.0;
+  if (!(B <= CS && CS <= CL)) return;
+  const uint32_t eb = a.b_edge[k], el = a.cl_edge[l];
+  // busiest-window counts, reduced over windows by K2w (k_peak.cu)
+  const unsigned long long ps = a.colmax_pk[eb], ph = a.colmax_pk[el], pl = a.pairmax_pk[k * a.n_cl + l];
+  c.peak_short = ps; c.peak_long = pl; c.peak_homo = ph;
+  const uint32_t ws = a.n_cs ? a.cs_win[s] : a.b_win[k], wl = a.cl_win[l];
+  const uint32_t gw = g * a.n_windows;
+  const unsigned long long nseq_s = sh.nseq[gw + ws], nseq_l = sh.nseq[gw + wl];
+  c.lambda_short = __dmul_rn(u2d(ps), a.inv_w_s);
+  c.lambda_long = __dmul_rn(u2d(pl), a.inv_w_s);
+  c.lambda_homo = __dmul_rn(u2d(ph), a.inv_w_s);
+  const bool ok_s = pool_instances(c.lambda_short, sh.mu[gw + ws], nseq_s, &c.inst_short);
+  const bool ok_l = pool_instances(c.lambda_long, sh.mu[gw + wl], nseq_l, &c.inst_long);
+  const bool ok_h = pool_instances(c.lambda_homo, sh.mu[gw + wl], nseq_l, &c.inst_homo);
+  const bool ok_d = ok_s && ok_l;
+  if (!ok_d) { c.inst_short = 0; c.inst_long = 0; }
+  const unsigned long long gpi = a.deploy[((uint64_t)m * a.n_gpus + g) * 3 + 1];
+  c.gpus_dual = gpi * (c.inst_short + c.inst_long);
+  c.gpus_homo = gpi * c.inst_homo;
+  const double price = a.price[g];
+  if (ok_d) c.cost_dual = __dmul_rn(__dmul_rn(u2d(c.gpus_dual), price), a.hours);
+  if (ok_h) c.cost_homo = __dmul_rn(__dmul_rn(u2d(c.gpus_homo), price), a.hours);
+  if (ok_d && ok_h && c.gpus_homo > 0)
+    c.savings = __ddiv_rn(__dsub_rn(u2d(c.gpus_homo), u2d(c.gpus_dual)), u2d(c.gpus_homo));
+  c.flags = FP_CAND_VALID | (ok_d ? FP_CAND_FEASIBLE : 0u) | (ok_h ? FP_CAND_HOMO_FEASIBLE : 0u);
+}
+
+__global__ void __launch_bounds__(256) k3_peak(EvalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ double red_c[32];
+  __shared__ uint32_t red_i[32], red_v[32];
+  __shared__ bool is_last;
+  const uint32_t m = blockIdx.y;
+  Shared sh;
+  sh.cnt_le = nullptr;
+  sh.mass_le = nullptr;
+  sh.nseq = reinterpret_cast<unsigned long long *>(smem);
+  sh.mu = reinterpret_cast<double *>(sh.nseq + (size_t)a.n_gpus * a.n_windows);
+  const uint32_t *arch = a.model_arch + 4 * m;
+  for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
+    const uint32_t g = j / a.n_windows, w = j % a.n_windows;
+    const unsigned long long *dp = a.deploy + ((uint64_t)m * a.n_gpus + g) * 3;
+    sh.nseq[j] = max_seqs(kv_budget(a.gpu_u64 + 4 * g, dp[2]), (uint32_t)dp[0], arch, a.windows[w]);
+    sh.mu[j] = a.mu[((uint64_t)m * a.n_gpus + g) * a.n_windows + w];
+  }
+  __syncthreads();
+  const uint64_t lo = (uint64_t)m * a.per_model, hi = lo + a.per_model;
+  double bc = 0.0;
+  uint32_t bi = 0xffffffffu, bv = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
+    fp_peak_candidate c;
+    evaluate_peak(a, sh, m, idx, c);
+    if (a.results_pk) a.results_pk[idx] = c;
+    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || c.cost_dual < bc)) { bc = c.cost_dual; bi = c.index; bv = 1; }
+  }
+  warp_argmin(bc, bi, bv);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) { red_c[w] = bc; red_i[w] = bi; red_v[w] = bv; }
+  __syncthreads();
+  if (w == 0) {
+    bc = lane < nw ? red_c[lane] : 0.0;
+    bi = lane < nw ? red_i[lane] : 0xffffffffu;
+    bv = lane < nw ? red_v[lane] : 0u;
+    warp_argmin(bc, bi, bv);
+    if (lane == 0) {
+      BlockBest *bb = a.block_best_pk + (size_t)m * gridDim.x + blockIdx.x;
+      bb->cost = bc; bb->index = bi; bb->valid = bv;
+      __threadfence();
+      is_last = atomicAdd(a.done_pk + m, 1u) == gridDim.x - 1;
+    }
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+  bc = 0.0; bi = 0xffffffffu; bv = 0;
+  for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
+    const volatile BlockBest *bb = a.block_best_pk + (size_t)m * gridDim.x + j;
+    better(bc, bi, bv, bb->cost, bb->index, bb->valid);
+  }
+  warp_argmin(bc, bi, bv);
+  if (lane == 0) { red_c[w] = bc; red_i[w] = bi; red_v[w] = bv; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < nw; ++j) better(bc, bi, bv, red_c[j], red_i[j], red_v[j]);
+    fp_peak_candidate c;
+    if (bv) {
+      evaluate_peak(a, sh, m, bi, c);
+    } else {
+      memset(&c, 0, sizeof c);
+      c.index = 0xffffffffu;
+      c.model = m;
+      c.cost_dual = c.cost_homo = __longlong_as_double(0x7ff0000000000000ll);
+    }
+    a.best_pk[m] = c;
+    a.done_pk[m] = 0;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k3_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  dim3 grid(grid_x, a.n_models);
+  k3_peak<<<grid, block, smem, s>>>(a);
+  return cudaGetLastError();
+}
 
 size_t eval_smem_bytes(const EvalArgs &a, int) {
   return (size_t)a.nbins * 16 + (size_t)a.n_gpus * a.n_windows * 16;

@@ -1,0 +1,235 @@
+// NEXT-4: peak-window provisioning.
+//
+// A trace is in arrival order, so the requests of window
+// w = floor(arrival / W) are one contiguous index range [start[w], start[w+1]).
+// That turns the two-dimensional histogram cnt[w][b] into K1's problem on
+// sub-ranges and removes the arrival column from the streaming pass:
+//   K0w  start[w] = lower_bound(arrival, w * W): n_windows + 1 binary searches
+//        (O(windows * log n) scattered 8-B reads, not 8 B per request)
+//   K1w  each block streams a contiguous slice of L_total (4 B / request,
+//        16-B vector loads), bins through the same fine-cell LUT as K1 into a
+//        lane-private shared histogram [bin][lane] and flushes one row of
+//        nbins global counters per window it touched; windows too short to
+//        amortise a flush go straight to global atomics
+//   K2w  per chunk of windows: inclusive scan of every row (cnt_le[w][j] =
+//        #{requests of w with L <= e_j}) and the maxima over windows that K3
+//        needs: colmax[j] = max_w cnt_le[w][j] and, for every (B, C_L) pair,
+//        pairmax = max_w (cnt_le[w][C_L] - cnt_le[w][B]). The cumulative rows
+//        are never written back.
+// The arrival order is the caller's contract; FP_FLAG_CHECK_ORDER adds Kc, a
+// full pass that verifies it (8 B / request).
+#include <algorithm>
+#include <cmath>
+#include "internal.cuh"
+
+namespace fp {
+namespace {
+
+constexpr int kHistBlock = 512;
+constexpr uint64_t kSmallSegment = 2048;   // below this a window goes to global atomics
+
+__global__ void k0w_bounds(PeakArgs a) {
+  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w > a.n_windows) return;
+  const uint64_t t = w * a.window_ns;          // no overflow: checked on the host
+  uint64_t lo = 0, n = a.n;
+  while (n > 0) {
+    const uint64_t half = n >> 1;
+    if (a.arrival[lo + half] < t) { lo += half + 1; n -= half + 1; } else { n = half; }
+  }
+  a.start[w] = w == a.n_windows ? a.n : lo;
+}
+
+__global__ void kc_check_order(PeakArgs a) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i + 1 < a.n; i += stride)
+    bad |= __ldcs(a.arrival + i) > __ldg(a.arrival + i + 1);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.error, 1u);
+}
+
+template <int LUTW>
+__device__ __forceinline__ uint32_t bin_of(uint32_t L, const unsigned char *lut, uint32_t clampv, uint32_t round,
+                                           uint32_t shift, uint32_t ne) {
+  if (LUTW == 1) return lut[(min(L, clampv) + round) >> shift];
+  if (LUTW == 2) return reinterpret_cast<const uint16_t *>(lut)[(min(L, clampv) + round) >> shift];
+  const uint32_t *edges = reinterpret_cast<const uint32_t *>(lut);
+  uint32_t lo = 0, n = ne;
+  while (n > 0) {
+    const uint32_t half = n >> 1;
+    if (edges[lo + half] < L) { lo += half + 1; n -= half + 1; } else { n = half; }
+  }
+  return lo;
+}
+
+template <int LUTW>
+__global__ void __launch_bounds__(kHistBlock) k1w_hist(PeakArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t nbins = a.nbins;
+  uint32_t lut_bytes = LUTW ? a.lut_cells * LUTW : (nbins - 1) * 4;
+  lut_bytes = (lut_bytes + 15u) & ~15u;
+  unsigned char *lut = smem;
+  uint32_t *acc = reinterpret_cast<uint32_t *>(smem + lut_bytes);      // [nbins][32]
+  {
+    const uint32_t *src = LUTW ? reinterpret_cast<const uint32_t *>(a.lut) : a.edges;
+    for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(lut)[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < nbins * 32; i += blockDim.x) acc[i] = 0u;
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t clampv = a.clampv, round = a.round, shift = a.shift, ne = nbins - 1;
+  const uint32_t *len = a.len;
+  // contiguous slice per block, a multiple of 4 requests
+  const uint64_t per = ((a.n + gridDim.x - 1) / gridDim.x + 3) & ~3ull;
+  const uint64_t lo = min((uint64_t)blockIdx.x * per, a.n), hi = min(lo + per, a.n);
+  if (lo >= hi) return;
+  // window holding request lo: the last w with start[w] <= lo
+  uint64_t w = 0;
+  {
+    uint64_t l = 0, n = a.n_windows + 1;
+    while (n > 0) {
+      const uint64_t half = n >> 1;
+      if (a.start[l + half] <= lo) { l += half + 1; n -= half + 1; } else { n = half; }
+    }
+    w = l - 1;
+  }
+  // first index whose address is 16-B aligned (len is 4-B aligned)
+  const uint64_t off = ((16u - ((uintptr_t)len & 15u)) & 15u) >> 2;
+  auto add = [&](uint32_t L) { atomicAdd(&acc[bin_of<LUTW>(L, lut, clampv, round, shift, ne) * 32 + lane], 1u); };
+  for (uint64_t s = lo; s < hi; ++w) {
+    const uint64_t e = min(hi, a.start[w + 1]);
+    if (e - s >= kSmallSegment) {
+      const uint64_t s4 = min(e, s + ((off - s) & 3));          // first aligned index >= s
+      const uint64_t q0 = (s4 - off) >> 2, q1 = (e - off) >> 2;  // aligned quads [q0, q1)
+      const uint64_t e4 = off + 4 * q1;
+      for (uint64_t i = s + threadIdx.x; i < s4; i += blockDim.x) add(__ldcs(len + i));
+      const uint4 *v = reinterpret_cast<const uint4 *>(len + off);
+      uint64_t q = q0 + threadIdx.x;
+      for (; q + blockDim.x < q1; q += 2 * blockDim.x) {
+        const uint4 x = __ldcs(v + q), y = __ldcs(v + q + blockDim.x);
+        add(x.x); add(x.y); add(x.z); add(x.w);
+        add(y.x); add(y.y); add(y.z); add(y.w);
+      }
+      if (q < q1) {
+        const uint4 x = __ldcs(v + q);
+        add(x.x); add(x.y); add(x.z); add(x.w);
+      }
+      for (uint64_t i = max(e4, s4) + threadIdx.x; i < e; i += blockDim.x) add(__ldcs(len + i));
+      __syncthreads();
+      uint32_t *row = a.hist2d + w * nbins;
+      for (uint32_t j = warp; j < nbins; j += nwarps) {
+        uint32_t c = acc[j * 32 + lane];
+        acc[j * 32 + lane] = 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0 && c) atomicAdd(row + j, c);
+      }
+      __syncthreads();
+    } else {
+      uint32_t *row = a.hist2d + w * nbins;
+      for (uint64_t i = s + threadIdx.x; i < e; i += blockDim.x)
+        atomicAdd(row + bin_of<LUTW>(__ldcs(len + i), lut, clampv, round, shift, ne), 1u);
+    }
+    s = e;
+  }
+}
+
+// K2w: inclusive scan of each window's row in shared memory, then the window
+// maxima per bin and per (B, C_L) pair; one atomicMax per entry per block
+__global__ void __launch_bounds__(256) k2w_peaks(PeakArgs a) {
+  extern __shared__ __align__(16) uint32_t sm2[];
+  const uint32_t nbins = a.nbins, R = a.rows, n_pairs = a.n_b * a.n_cl;
+  uint32_t *rows = sm2;                       // [R][nbins]
+  uint32_t *pmax = rows + R * nbins;          // [n_pairs]
+  uint32_t *cmax = pmax + n_pairs;            // [nbins]
+  for (uint32_t i = threadIdx.x; i < n_pairs; i += blockDim.x) pmax[i] = 0u;
+  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) cmax[i] = 0u;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (uint64_t w0 = (uint64_t)blockIdx.x * R; w0 < a.n_windows; w0 += (uint64_t)gridDim.x * R) {
+    const uint32_t rn = (uint32_t)min((uint64_t)R, a.n_windows - w0);
+    __syncthreads();
+    const uint32_t *src = a.hist2d + w0 * nbins;
+    for (uint32_t i = threadIdx.x; i < rn * nbins; i += blockDim.x) rows[i] = src[i];
+    __syncthreads();
+    for (uint32_t r = warp; r < rn; r += nwarps) {
+      uint32_t *row = rows + r * nbins, carry = 0;
+      for (uint32_t base = 0; base < nbins; base += 32) {
+        const uint32_t j = base + lane;
+        uint32_t v = j < nbins ? row[j] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += y;
+        }
+        v += carry;
+        if (j < nbins) row[j] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+      }
+    }
+    __syncthreads();
+    for (uint32_t p = threadIdx.x; p < n_pairs; p += blockDim.x) {
+      const uint32_t eb = a.b_edge[p / a.n_cl], el = a.cl_edge[p % a.n_cl];
+      if (eb > el) continue;                  // B > C_L: no valid candidate uses it
+      uint32_t m = pmax[p];
+      for (uint32_t r = 0; r < rn; ++r) m = max(m, rows[r * nbins + el] - rows[r * nbins + eb]);
+      pmax[p] = m;
+    }
+    for (uint32_t j = threadIdx.x; j < nbins; j += blockDim.x) {
+      uint32_t m = cmax[j];
+      for (uint32_t r = 0; r < rn; ++r) m = max(m, rows[r * nbins + j]);
+      cmax[j] = m;
+    }
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n_pairs; i += blockDim.x)
+    if (pmax[i]) atomicMax(a.pairmax + i, pmax[i]);
+  for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x)
+    if (cmax[i]) atomicMax(a.colmax + i, cmax[i]);
+}
+
+template <int LUTW>
+cudaError_t launch_hist(const PeakArgs &a, int sm_count, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k1w_hist<LUTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_hist<LUTW>, kHistBlock, smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t want = (uint64_t)sm_count * (uint64_t)std::max(per_sm, 1);
+  const uint64_t useful = std::max<uint64_t>(1, (a.n + 4095) / 4096);
+  k1w_hist<LUTW><<<(unsigned)std::min(want, useful), kHistBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t peak_smem_bytes(const PeakArgs &a) {
+  const size_t lut = a.lutw ? (size_t)a.lut_cells * a.lutw : (size_t)(a.nbins - 1) * 4;
+  return ((lut + 15) & ~size_t(15)) + (size_t)a.nbins * 32 * 4;
+}
+
+size_t peak_scan_smem_bytes(const PeakArgs &a) {
+  return ((size_t)a.rows * a.nbins + (size_t)a.n_b * a.n_cl + a.nbins) * 4;
+}
+
+cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
+  cudaError_t e;
+  if (a.check_order) {
+    kc_check_order<<<sm_count * 4, 512, 0, s>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  k0w_bounds<<<(unsigned)((a.n_windows + 1 + 255) / 256), 256, 0, s>>>(a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t smem = peak_smem_bytes(a);
+  e = a.lutw == 1 ? launch_hist<1>(a, sm_count, smem, s)
+      : a.lutw == 2 ? launch_hist<2>(a, sm_count, smem, s)
+                    : launch_hist<0>(a, sm_count, smem, s);
+  if (e != cudaSuccess) return e;
+  const size_t smem2 = peak_scan_smem_bytes(a);
+  e = cudaFuncSetAttribute(k2w_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  if (e != cudaSuccess) return e;
+  const uint64_t chunks = (a.n_windows + a.rows - 1) / a.rows;
+  k2w_peaks<<<(unsigned)std::min<uint64_t>(chunks, (uint64_t)sm_count * 4), 256, smem2, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace fp

@@ -123,6 +123,10 @@ struct fp_plan {
   EvalArgs ea3{};
   int k3p_grid_x = 1;
   uint64_t n_cand3 = 0;
+  // NEXT-4 peak-window scratch (lazy)
+  unsigned char *d_peak = nullptr;
+  size_t peak_cap = 0;
+  fp_peak_candidate *d_results_pk = nullptr;
   // NEXT-3 calibration scratch (lazy)
   unsigned char *d_calib_scratch = nullptr;
   size_t calib_cap = 0;
@@ -716,6 +720,8 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
     cudaFree(p->d_calib_scratch);
+    cudaFree(p->d_peak);
+    cudaFree(p->d_results_pk);
     cudaFree(p->d_results3);
     cudaFree(p->d_calib);
     for (int i = 0; i < 2; ++i) {
@@ -864,6 +870,8 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
         cudaFree(p->d_bins);
     cudaFree(p->d_p3);
     cudaFree(p->d_calib_scratch);
+    cudaFree(p->d_peak);
+    cudaFree(p->d_results_pk);
     cudaFree(p->d_results3);
         p->d_bins = nullptr;
         p->bins_cap = 0;
@@ -878,6 +886,8 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
     cudaFree(p->d_calib_scratch);
+    cudaFree(p->d_peak);
+    cudaFree(p->d_results_pk);
     cudaFree(p->d_results3);
       p->d_resident = nullptr;
       p->resident_cap = 0;
@@ -1194,6 +1204,8 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   const size_t small = 16 * 8 * 10;
   if (p->calib_cap < scratch + small) {
     cudaFree(p->d_calib_scratch);
+    cudaFree(p->d_peak);
+    cudaFree(p->d_results_pk);
     p->d_calib_scratch = nullptr;
     p->calib_cap = 0;
     CUDA_TRY(p, cudaMalloc(&p->d_calib_scratch, scratch + small), "cudaMalloc calibration scratch");
@@ -1256,6 +1268,128 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
       h_snap[k].sigma_hat = h[96 + k];
     }
   }
+  return FP_OK;
+}
+
+fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *d_arrival_ns, uint64_t n_local,
+                             uint64_t window_ns, fp_peak_candidate *h_results, fp_peak_candidate *h_best,
+                             void *stream) {
+  if (!p || !h_best) return FP_ERR_INVALID_ARG;
+  if (n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace");
+  if (n_local > 0xffffffffull) return fail(p, FP_ERR_INVALID_ARG, "n_local must be < 2^32 (u32 window counters)");
+  if (window_ns == 0) return fail(p, FP_ERR_INVALID_ARG, "window_ns must be > 0");
+  if (!d_len || !d_arrival_ns || is_host_pointer(d_len) || is_host_pointer(d_arrival_ns))
+    return fail(p, FP_ERR_INVALID_ARG, "length and arrival columns must be device memory");
+  if (((uintptr_t)d_len & 3) || ((uintptr_t)d_arrival_ns & 7))
+    return fail(p, FP_ERR_INVALID_ARG, "misaligned column");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // windows from the first and last request's arrival (the trace is in arrival order)
+  uint64_t *ends = reinterpret_cast<uint64_t *>(p->h_small);
+  CUDA_TRY(p, cudaMemcpyAsync(ends, d_arrival_ns, 8, cudaMemcpyDeviceToHost, s), "D2H first arrival");
+  CUDA_TRY(p, cudaMemcpyAsync(ends + 1, d_arrival_ns + (n_local - 1), 8, cudaMemcpyDeviceToHost, s),
+           "D2H last arrival");
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  const uint64_t first = ends[0], last = ends[1];
+  if (first > last) return fail(p, FP_ERR_INVALID_ARG, "arrivals not in order (first > last)");
+  if (last > ~0ull - window_ns) return fail(p, FP_ERR_INVALID_ARG, "arrival + window_ns overflows");
+  const uint64_t n_twin = last / window_ns + 1;
+  const size_t hbytes = (size_t)n_twin * p->nbins * 4;
+  if (n_twin > (1ull << 26) || hbytes > (4ull << 30))
+    return fail(p, FP_ERR_INVALID_ARG, "%llu windows x %u bins is too many", (unsigned long long)n_twin, p->nbins);
+  const uint32_t M = (uint32_t)p->models.size();
+  const uint32_t n_b = (uint32_t)p->b.size(), n_cl = (uint32_t)p->cl.size();
+  const int grid_x = (int)std::min<uint64_t>(std::max<uint64_t>(1, (uint64_t)p->sm_count * 8 / M),
+                                             std::max<uint64_t>(1, (p->per_model + 255) / 256));
+  // scratch: [hist2d | colmax | pairmax | error] (zeroed together), start, best, block bests, done
+  const size_t zbytes = ((hbytes + ((size_t)p->nbins + (size_t)n_b * n_cl + 1) * 4) + 15) & ~size_t(15);
+  const size_t sbytes = (n_twin + 1) * 8;
+  const size_t need = zbytes + sbytes + M * sizeof(fp_peak_candidate) + (size_t)M * grid_x * sizeof(BlockBest) +
+                      M * sizeof(unsigned int) + 64;
+  if (p->peak_cap < need) {
+    cudaFree(p->d_peak);
+    p->d_peak = nullptr;
+    p->peak_cap = 0;
+    CUDA_TRY(p, cudaMalloc(&p->d_peak, need), "cudaMalloc peak scratch");
+    p->peak_cap = need;
+  }
+  unsigned char *base = p->d_peak;
+  uint32_t *hist2d = reinterpret_cast<uint32_t *>(base);
+  uint32_t *colmax = hist2d + (size_t)n_twin * p->nbins;
+  uint32_t *pairmax = colmax + p->nbins;
+  unsigned int *err = pairmax + (size_t)n_b * n_cl;
+  size_t off = zbytes;
+  uint64_t *start = reinterpret_cast<uint64_t *>(base + off);
+  off += (sbytes + 15) & ~size_t(15);
+  fp_peak_candidate *best = reinterpret_cast<fp_peak_candidate *>(base + off);
+  off += M * sizeof(fp_peak_candidate);
+  BlockBest *bb = reinterpret_cast<BlockBest *>(base + off);
+  off += (size_t)M * grid_x * sizeof(BlockBest);
+  unsigned int *done = reinterpret_cast<unsigned int *>(base + off);
+  CUDA_TRY(p, cudaMemsetAsync(hist2d, 0, zbytes, s), "memset hist2d");
+  CUDA_TRY(p, cudaMemsetAsync(done, 0, M * sizeof(unsigned int), s), "memset done");
+  PeakArgs pa{};
+  pa.len = d_len;
+  pa.arrival = d_arrival_ns;
+  pa.n = n_local;
+  pa.window_ns = window_ns;
+  pa.n_windows = n_twin;
+  pa.start = start;
+  pa.lut = p->ta.lut;
+  pa.edges = p->ta.edges;
+  pa.lut_cells = p->lut_cells;
+  pa.lutw = p->lut_cells ? (p->lut_u8 ? 1 : 2) : 0;
+  pa.clampv = p->max_edge + 1u;
+  pa.round = (1u << p->shift) - 1u;
+  pa.shift = p->shift;
+  pa.nbins = p->nbins;
+  pa.hist2d = hist2d;
+  pa.b_edge = p->ea.b_edge;
+  pa.cl_edge = p->ea.cl_edge;
+  pa.n_b = n_b;
+  pa.n_cl = n_cl;
+  pa.colmax = colmax;
+  pa.pairmax = pairmax;
+  pa.error = err;
+  pa.check_order = (p->flags & FP_FLAG_CHECK_ORDER) != 0;
+  {
+    const size_t fixed = ((size_t)n_b * n_cl + p->nbins) * 4;
+    const size_t budget = 96 * 1024;
+    if (fixed + (size_t)p->nbins * 4 > 200 * 1024) return fail(p, FP_ERR_CONFIG, "too many (B, C_L) pairs");
+    pa.rows = (uint32_t)std::max<size_t>(1, std::min<size_t>(64, (budget > fixed ? budget - fixed : 0) /
+                                                                     ((size_t)p->nbins * 4)));
+  }
+  if (peak_smem_bytes(pa) > 200 * 1024) return fail(p, FP_ERR_CONFIG, "peak LUT too large");
+  {
+    LaunchTimer lt(p, FP_KERNEL_TRACE, s);
+    cudaError_t e = launch_peak_hist(pa, p->sm_count, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "peak histogram launch");
+  }
+  p->launches += pa.check_order ? 4 : 3;
+  EvalArgs ea = p->ea;
+  ea.colmax_pk = colmax;
+  ea.pairmax_pk = pairmax;
+  ea.inv_w_s = 1e9 / (double)window_ns;
+  ea.best_pk = best;
+  ea.block_best_pk = bb;
+  ea.done_pk = done;
+  if (h_results && !p->d_results_pk)
+    CUDA_TRY(p, cudaMalloc(&p->d_results_pk, p->n_cand * sizeof(fp_peak_candidate)), "cudaMalloc peak results");
+  ea.results_pk = h_results ? p->d_results_pk : nullptr;
+  {
+    LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+    cudaError_t e = launch_eval_peak(ea, grid_x, 256, (size_t)ea.n_gpus * ea.n_windows * 16, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "peak evaluation launch");
+  }
+  ++p->launches;
+  unsigned int *herr = reinterpret_cast<unsigned int *>(ends);
+  CUDA_TRY(p, cudaMemcpyAsync(herr, err, 4, cudaMemcpyDeviceToHost, s), "D2H error flag");
+  CUDA_TRY(p, cudaMemcpyAsync(h_best, best, M * sizeof(fp_peak_candidate), cudaMemcpyDeviceToHost, s), "D2H best");
+  if (h_results)
+    CUDA_TRY(p, cudaMemcpyAsync(h_results, p->d_results_pk, p->n_cand * sizeof(fp_peak_candidate),
+                                cudaMemcpyDeviceToHost, s), "D2H peak results");
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  if (*herr) return fail(p, FP_ERR_INVALID_ARG, "arrivals not in order (FP_FLAG_CHECK_ORDER)");
   return FP_OK;
 }
 
