@@ -217,8 +217,10 @@ def next1_fused_estimation(fp, cfg, n, reps=5):
             "k4_raw_ms": k4ms, "k4_raw_GBps": 14.0 * n / (k4ms / 1e3) / 1e9,
             "misroute_short_long_at_8K": mis,
             "next3_calibration_replay": {"records": n, "ms": cal_ms, "records_per_s": n / (cal_ms / 1e3),
+                                         "GBps": 18.0 * n / (cal_ms / 1e3) / 1e9,
                                          "c_hat": [float(x) for x in cal["c_hat"]],
-                                         "note": "two passes over 9 B/record (parallel affine-map scan)"},
+                                         "note": "two passes (C1 maps, C3 replay) over 9 B/record = 18 B/record; "
+                                                 "issue-bound (~60 instructions/record/pass), not HBM-bound"},
             "note": "algorithmic bytes: sweep 9 B/request (bytes u32, max_output u32, category u8); "
                     "route 13 B in + 1 B decision"}
 

@@ -155,17 +155,22 @@ struct CalibArgs {
   uint32_t n_cats;                  // <= 16
   double beta;
   const double *c0, *s0;            // device [n_cats] initial state
-  uint64_t threads, seg;            // segments: thread t owns [t*seg, (t+1)*seg)
-  double *mapA, *mapB, *sigA, *sigB;  // [n_cats][threads]
-  uint32_t *mapN;                   // [n_cats][threads]
-  unsigned long long *preN;         // [n_cats][threads]
-  double *totA, *totB, *totSA, *totSB;  // [n_cats] (totA / totSA: final c_hat / sigma)
-  unsigned long long *totN;         // [n_cats]
+  uint64_t threads, blocks, seg;    // thread t owns [t*seg, (t+1)*seg); seg % 16 == 0; 256 threads / block
+  double *thrA, *thrB;              // [n_cats][threads] within-block exclusive c_hat maps
+  uint32_t *thrN;
+  double *blkA, *blkB;              // [n_cats][blocks] c_hat block totals -> exclusive prefixes
+  unsigned long long *blkN;
+  double *sblkA, *sblkB;            // [n_cats][blocks] sigma block totals -> exclusive prefixes
+  double *totA, *totSA;             // [n_cats] final c_hat / sigma
+  unsigned long long *totN;         // [n_cats] observations
   uint64_t snap_at;
   double *snap_c, *snap_s;          // [n_cats]
-  unsigned long long *snap_thread;  // [n_cats]
+  double *snap_sa, *snap_sb;        // [n_cats] sigma map from the snapshot's block start
+  unsigned long long *snap_block;   // [n_cats] (~0: no snapshot)
+  bool vec_bt, vec_c;               // 16-B aligned columns: vector loads
 };
-size_t calib_scratch_bytes(uint64_t threads, uint32_t n_cats);
+size_t calib_scratch_bytes(uint64_t blocks, uint32_t n_cats);
+int calib_blocks_per_sm(uint32_t n_cats);
 cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s);
 
 }  // namespace fp

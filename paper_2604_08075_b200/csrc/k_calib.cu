@@ -4,14 +4,30 @@
 //   c_k   <- beta c_k + (1 - beta) c_obs
 //   s_k   <- beta s_k + (1 - beta) |c_obs - c_k(before)|          (R26)
 // Both recurrences are affine in their state, x -> a x + b, and affine maps
-// compose associatively: (a2, b2) o (a1, b1) = (a2 a1, a2 b1 + b2). The
-// stream is cut into one contiguous segment per thread:
-//   C1  each thread composes, per category, the maps of its segment (c_hat)
-//   C2  one block per category scans the per-thread maps (exclusive prefix)
-//   C3  each thread replays its segment from its prefix state (exactly the
-//       sequential update), which yields every c_hat(before) and so the
-//       sigma maps; records the n = snap_at snapshot of c_hat
-//   C2  again for the sigma maps, C4 replays the segments holding a snapshot
+// compose associatively: (a2, b2) o (a1, b1) = (a2 a1, a2 b1 + b2); n
+// observations of one category compose to a = beta^n. The stream is cut into
+// one contiguous segment per thread, 256 consecutive segments per block:
+//   C1  each thread composes, per category, the c_hat maps of its segment; a
+//       block scan turns them into within-block exclusive prefixes and one
+//       block total
+//   C2  one block per category scans the block totals (exclusive prefixes;
+//       the grand total applied to c_0 is the final c_hat)
+//   C3  each thread replays its segment from its start state (block prefix,
+//       then within-block prefix, applied to c_0) -- exactly the sequential
+//       update -- which yields every c_hat(before) and so the sigma maps; at
+//       the snap_at-th observation of a category it records c_hat and the
+//       sigma map composed so far; block scan of the sigma maps as in C1
+//   C2  again for the sigma block totals; C4 applies the snapshot's sigma map
+//       (from its block's start) to the sigma state at that block's start
+// Category state lives in registers (select chains) for n_cats <= 4 and in
+// shared memory [k][thread] above that.
+// Segments are contiguous per thread, but the columns are read coalesced: in
+// each round a block stages the next 16 records of all 256 of its segments
+// into shared memory (64-B pieces, 16-B loads, a warp covering 8 segments),
+// swizzled so that each thread then reads its own 16 records with
+// conflict-free 16-B shared loads; the global loads of round r+1 are issued
+// before round r is consumed. Records past a segment's end are staged with
+// prompt_tokens = 0, which the update skips.
 // The composition reassociates the fp64 sums, so results agree with the
 // sequential oracle to rounding (tests: <= 1e-12 relative), not bit for bit.
 #include <cmath>
@@ -22,204 +38,448 @@ namespace fp {
 namespace {
 
 constexpr int kCalBlock = 256;
+constexpr int kRound = 16;                 // records per segment per round
 
 __device__ __forceinline__ uint64_t umin(uint64_t x, uint64_t y) { return x < y ? x : y; }
 
-struct Obs {
-  bool valid;
-  uint32_t k;
-  double c;
+// ---- affine maps and their block scan ------------------------------------------
+struct Aff {
+  double a, b;
+  unsigned long long n;
 };
 
-__device__ __forceinline__ Obs load_obs(const CalibArgs &a, uint64_t i) {
-  Obs o;
-  const uint32_t t = a.tokens[i];
-  o.valid = t != 0;                                   // invalid feedback dropped
-  const uint32_t k = a.cat[i];
-  o.k = k < a.n_cats ? k : a.n_cats - 1;              // R23
-  o.c = o.valid ? __ddiv_rn(__uint2double_rn(a.bytes[i]), __uint2double_rn(t)) : 0.0;
-  return o;
+__device__ __forceinline__ Aff aff_id() { return Aff{1.0, 0.0, 0ull}; }
+
+// e first, then l
+__device__ __forceinline__ Aff compose(const Aff &e, const Aff &l) {
+  return Aff{__dmul_rn(l.a, e.a), __fma_rn(l.a, e.b, l.b), e.n + l.n};
 }
 
-// per-thread map state in shared memory: [k][thread] (conflict-free)
-struct MapSmem {
-  double *A, *B;
-  uint32_t *cnt;
-  __device__ double &a(uint32_t k) { return A[k * kCalBlock + threadIdx.x]; }
-  __device__ double &b(uint32_t k) { return B[k * kCalBlock + threadIdx.x]; }
-  __device__ uint32_t &n(uint32_t k) { return cnt[k * kCalBlock + threadIdx.x]; }
+__device__ __forceinline__ Aff shfl_up(const Aff &x, int o) {
+  return Aff{__shfl_up_sync(0xffffffffu, x.a, o), __shfl_up_sync(0xffffffffu, x.b, o),
+             __shfl_up_sync(0xffffffffu, x.n, o)};
+}
+
+__device__ __forceinline__ Aff warp_inclusive(Aff inc, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const Aff y = shfl_up(inc, o);
+    if (lane >= o) inc = compose(y, inc);
+  }
+  return inc;
+}
+
+// exclusive prefix of x over the block's threads in order, and the block total;
+// sw: shared scratch of 32 maps. Every thread of the block must call it.
+__device__ __forceinline__ void block_scan(const Aff &x, Aff &excl, Aff &total, Aff *sw) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const Aff inc = warp_inclusive(x, lane);
+  if (lane == 31) sw[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    Aff w = lane < nw ? sw[lane] : aff_id();
+    w = warp_inclusive(w, lane);
+    if (lane < nw) sw[lane] = w;
+  }
+  __syncthreads();
+  Aff ex = shfl_up(inc, 1);
+  if (lane == 0) ex = aff_id();
+  excl = warp ? compose(sw[warp - 1], ex) : ex;
+  total = sw[nw - 1];
+  __syncthreads();
+}
+
+__device__ __forceinline__ double apply(const Aff &m, double x) { return __fma_rn(m.a, x, m.b); }
+
+// ---- per-category state: registers (NC <= 4) or shared memory ----------------
+template <int NC, bool REG>
+struct Vec;
+
+template <int NC>
+struct Vec<NC, true> {
+  double v[NC];
+  __device__ __forceinline__ void bind(double *) {}
+  __device__ __forceinline__ double get(uint32_t k) const {
+    double r = v[0];
+#pragma unroll
+    for (int j = 1; j < NC; ++j) r = k == (uint32_t)j ? v[j] : r;
+    return r;
+  }
+  __device__ __forceinline__ void set(uint32_t k, double x) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) v[j] = k == (uint32_t)j ? x : v[j];
+  }
 };
 
-__device__ __forceinline__ MapSmem map_smem(unsigned char *smem, uint32_t n_cats) {
-  MapSmem m;
-  m.A = reinterpret_cast<double *>(smem);
-  m.B = m.A + n_cats * kCalBlock;
-  m.cnt = reinterpret_cast<uint32_t *>(m.B + n_cats * kCalBlock);
-  return m;
-}
+template <int NC>
+struct Vec<NC, false> {
+  double *p;
+  __device__ __forceinline__ void bind(double *q) { p = q; }
+  __device__ __forceinline__ double get(uint32_t k) const { return p[k * kCalBlock + threadIdx.x]; }
+  __device__ __forceinline__ void set(uint32_t k, double x) { p[k * kCalBlock + threadIdx.x] = x; }
+};
 
-__device__ __forceinline__ void segment(const CalibArgs &a, uint64_t t, uint64_t &lo, uint64_t &hi) {
-  lo = umin(a.n, t * a.seg);
-  hi = umin(a.n, lo + a.seg);
-}
+template <int NC, bool REG>
+struct UVec;
 
-// C1: per-thread composed maps of the c_hat recurrence
-__global__ void __launch_bounds__(kCalBlock) c1_maps(CalibArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  MapSmem s = map_smem(smem, a.n_cats);
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (uint32_t k = 0; k < a.n_cats; ++k) { s.a(k) = 1.0; s.b(k) = 0.0; s.n(k) = 0; }
-  uint64_t lo, hi;
-  segment(a, t, lo, hi);
-  const double w = __dsub_rn(1.0, a.beta);
-  for (uint64_t i = lo; i < hi; ++i) {
-    const Obs o = load_obs(a, i);
-    if (!o.valid) continue;
-    s.a(o.k) = __dmul_rn(a.beta, s.a(o.k));
-    s.b(o.k) = __dadd_rn(__dmul_rn(a.beta, s.b(o.k)), __dmul_rn(w, o.c));
-    s.n(o.k) += 1;
+// NC <= 4 counters of < 2^16 (seg <= 65,520) packed in one u64: one shift-add per update
+template <int NC>
+struct UVec<NC, true> {
+  static_assert(NC <= 4, "packed counters hold 4 categories");
+  unsigned long long v;
+  __device__ __forceinline__ void bind(uint32_t *) { v = 0ull; }
+  __device__ __forceinline__ uint32_t get(uint32_t k) const { return (uint32_t)(v >> (16 * k)) & 0xffffu; }
+  __device__ __forceinline__ void inc(uint32_t k) { v += 1ull << (16 * k); }
+  __device__ __forceinline__ void set(uint32_t k, uint32_t x) {
+    v = (v & ~(0xffffull << (16 * k))) | ((unsigned long long)(x & 0xffffu) << (16 * k));
   }
-  if (t < a.threads)
-    for (uint32_t k = 0; k < a.n_cats; ++k) {
-      a.mapA[k * a.threads + t] = s.a(k);
-      a.mapB[k * a.threads + t] = s.b(k);
-      a.mapN[k * a.threads + t] = s.n(k);
+  // field k equal in both
+  __device__ __forceinline__ bool eq(uint32_t k, const UVec &o) const { return !(((v ^ o.v) >> (16 * k)) & 0xffffu); }
+};
+
+template <int NC>
+struct UVec<NC, false> {
+  uint32_t *p;
+  __device__ __forceinline__ void bind(uint32_t *q) { p = q; }
+  __device__ __forceinline__ uint32_t get(uint32_t k) const { return p[k * kCalBlock + threadIdx.x]; }
+  __device__ __forceinline__ void inc(uint32_t k) { p[k * kCalBlock + threadIdx.x] += 1u; }
+  __device__ __forceinline__ void set(uint32_t k, uint32_t x) { p[k * kCalBlock + threadIdx.x] = x; }
+  __device__ __forceinline__ bool eq(uint32_t k, const UVec &o) const { return get(k) == o.get(k); }
+};
+
+// ---- coalesced staging of per-thread segments ---------------------------------
+// bytes / tokens [segment][16] u32 with 16-B groups swizzled by (segment >> 1) & 3,
+// categories [segment][16] u8
+struct StageSmem {
+  uint32_t *b, *t, *c;
+};
+
+constexpr size_t kStageBytes = (size_t)kCalBlock * kRound * 4 * 2 + (size_t)kCalBlock * kRound;
+constexpr size_t kScanBytes = 32 * sizeof(Aff);
+
+__device__ __forceinline__ uint32_t swz(uint32_t seg, uint32_t group) {
+  return seg * kRound + ((group ^ ((seg >> 1) & 3u)) << 2);
+}
+
+struct Pieces {              // the next round, held in registers while the current one runs
+  uint4 b[4], t[4], c;
+};
+
+__device__ __forceinline__ uint4 load4(const uint32_t *p, uint64_t g, uint64_t end, bool vec) {
+  if (vec && g + 4 <= end) return __ldcs(reinterpret_cast<const uint4 *>(p + g));
+  uint4 v;
+  v.x = g + 0 < end ? p[g + 0] : 0u;
+  v.y = g + 1 < end ? p[g + 1] : 0u;
+  v.z = g + 2 < end ? p[g + 2] : 0u;
+  v.w = g + 3 < end ? p[g + 3] : 0u;
+  return v;
+}
+
+__device__ __forceinline__ void fetch(const CalibArgs &a, uint64_t t0, uint64_t r, Pieces &pc) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q >> 2, part = q & 3u;
+    const uint64_t base = (t0 + seg) * a.seg, end = umin(a.n, base + a.seg);
+    const uint64_t g = base + r * kRound + part * 4;
+    pc.b[i] = load4(a.bytes, g, end, a.vec_bt);
+    pc.t[i] = load4(a.tokens, g, end, a.vec_bt);
+  }
+  const uint64_t base = (t0 + threadIdx.x) * a.seg, end = umin(a.n, base + a.seg);
+  const uint64_t g = base + r * kRound;
+  if (a.vec_c && g + kRound <= end) {
+    pc.c = __ldcs(reinterpret_cast<const uint4 *>(a.cat + g));
+  } else {
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    for (int j = 0; j < kRound; ++j)
+      if (g + j < end) w[j >> 2] |= (uint32_t)a.cat[g + j] << (8 * (j & 3));
+    pc.c = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+__device__ __forceinline__ void put(const StageSmem &st, const Pieces &pc) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q >> 2, part = q & 3u;
+    *reinterpret_cast<uint4 *>(st.b + swz(seg, part)) = pc.b[i];
+    *reinterpret_cast<uint4 *>(st.t + swz(seg, part)) = pc.t[i];
+  }
+  *reinterpret_cast<uint4 *>(st.c + threadIdx.x * 4) = pc.c;
+}
+
+__device__ __forceinline__ uint32_t get(const uint4 &v, int e) {
+  return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+}
+
+// exact u32 -> f64 on the FP64 pipe (2^52 + x is exact), instead of the
+// conversion unit that the reciprocal seed also needs
+__device__ __forceinline__ double u2d(uint32_t x) {
+  return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
+}
+
+// c_obs = |r| / tokens without the IEEE division's slow-path branch: the
+// hardware f64 reciprocal estimate refined by two Newton steps (relative
+// error <= 2^-20 -> 2^-40 -> below fp64 rounding), then one multiply: within
+// 2 ulp of the correctly rounded quotient, which the replay's reassociated
+// sums absorb (1e-12).
+__device__ __forceinline__ double ratio(uint32_t num, uint32_t den) {
+  const double d = u2d(den);
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
+  y = __fma_rn(y, __fma_rn(-d, y, 1.0), y);
+  return __dmul_rn(u2d(num), y);
+}
+
+template <typename Body>
+__device__ __forceinline__ void consume(const StageSmem &st, uint32_t last, Body &body) {
+  const uint4 cc = *reinterpret_cast<const uint4 *>(st.c + threadIdx.x * 4);
+#pragma unroll
+  for (int gi = 0; gi < 4; ++gi) {
+    const uint4 vb = *reinterpret_cast<const uint4 *>(st.b + swz(threadIdx.x, gi));
+    const uint4 vt = *reinterpret_cast<const uint4 *>(st.t + swz(threadIdx.x, gi));
+    const uint32_t cw = get(cc, gi);
+    double o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = ratio(get(vb, e), get(vt, e) | (get(vt, e) == 0u));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t cat = (cw >> (8 * e)) & 0xffu;
+      if (get(vt, e) != 0u) body(o[e], cat < last ? cat : last);   // S:240 drop; R23
     }
-}
-
-// C2: exclusive scan of the per-thread maps of one category (block = category)
-__global__ void __launch_bounds__(1024) c2_scan(CalibArgs a, int which) {
-  __shared__ double sA[1024], sB[1024];
-  __shared__ unsigned long long sN[1024];
-  const uint32_t k = blockIdx.x;
-  double *A = (which ? a.sigA : a.mapA) + (uint64_t)k * a.threads;
-  double *B = (which ? a.sigB : a.mapB) + (uint64_t)k * a.threads;
-  uint32_t *N = a.mapN + (uint64_t)k * a.threads;
-  const uint32_t T = blockDim.x, tid = threadIdx.x;
-  const uint64_t per = (a.threads + T - 1) / T;
-  const uint64_t lo = umin(a.threads, tid * per), hi = umin(a.threads, lo + per);
-  // compose my run: later maps on the outside
-  double ra = 1.0, rb = 0.0;
-  unsigned long long rn = 0;
-  for (uint64_t j = lo; j < hi; ++j) {
-    rb = __dadd_rn(__dmul_rn(A[j], rb), B[j]);
-    ra = __dmul_rn(A[j], ra);
-    rn += N[j];
-  }
-  sA[tid] = ra; sB[tid] = rb; sN[tid] = rn;
-  __syncthreads();
-  if (tid == 0) {   // exclusive scan over the 1,024 run maps (cheap, sequential)
-    double pa = 1.0, pb = 0.0;
-    unsigned long long pn = 0;
-    for (uint32_t j = 0; j < T; ++j) {
-      const double ja = sA[j], jb = sB[j];
-      const unsigned long long jn = sN[j];
-      sA[j] = pa; sB[j] = pb; sN[j] = pn;
-      pb = __dadd_rn(__dmul_rn(ja, pb), jb);
-      pa = __dmul_rn(ja, pa);
-      pn += jn;
-    }
-    // final state = the total composed map applied to the initial state
-    if (which == 0) { a.totA[k] = __dadd_rn(__dmul_rn(pa, a.c0[k]), pb); a.totN[k] = pn; }
-    else { a.totSA[k] = __dadd_rn(__dmul_rn(pa, a.s0[k]), pb); }
-  }
-  __syncthreads();
-  double pa = sA[tid], pb = sB[tid];
-  unsigned long long pn = sN[tid];
-  for (uint64_t j = lo; j < hi; ++j) {          // rewrite as exclusive prefixes
-    const double ja = A[j], jb = B[j];
-    const uint32_t jn = N[j];
-    A[j] = pa; B[j] = pb;
-    if (which == 0) a.preN[(uint64_t)k * a.threads + j] = pn;
-    pb = __dadd_rn(__dmul_rn(ja, pb), jb);
-    pa = __dmul_rn(ja, pa);
-    pn += jn;
   }
 }
 
-// C3: replay each segment from its c_hat prefix; sigma maps; c_hat snapshot
-__global__ void __launch_bounds__(kCalBlock) c3_replay(CalibArgs a) {
+// Runs body(c_obs, category) over this thread's segment in order (valid records only).
+template <typename Body>
+__device__ __forceinline__ void for_segment(const CalibArgs &a, const StageSmem &st, Body body) {
+  const uint64_t t0 = (uint64_t)blockIdx.x * kCalBlock;
+  const uint64_t rounds = (a.seg + kRound - 1) / kRound;
+  const uint32_t last = a.n_cats - 1;
+  Pieces pc;
+  fetch(a, t0, 0, pc);
+  for (uint64_t r = 0; r < rounds; ++r) {
+    __syncthreads();                 // previous round consumed
+    put(st, pc);
+    __syncthreads();
+    if (r + 1 < rounds) fetch(a, t0, r + 1, pc);
+    consume(st, last, body);
+  }
+}
+
+// beta^n by squaring (the maps' multiplicative part: one factor per observation)
+__device__ __forceinline__ double pow_n(double beta, uint32_t n) {
+  double r = 1.0, b = beta;
+  while (n) {
+    if (n & 1u) r = __dmul_rn(r, b);
+    b = __dmul_rn(b, b);
+    n >>= 1;
+  }
+  return r;
+}
+
+struct Smem {
+  StageSmem st;
+  Aff *scan;
+  double *d0, *d1;      // [NC][kCalBlock]: d0 shared-memory state only, d1 always (sigma maps)
+  uint32_t *u0, *u1;
+};
+
+__device__ __forceinline__ Smem smem_layout(unsigned char *smem, uint32_t nc, bool reg) {
+  Smem s;
+  s.st.b = reinterpret_cast<uint32_t *>(smem);
+  s.st.t = s.st.b + kCalBlock * kRound;
+  s.st.c = s.st.t + kCalBlock * kRound;
+  s.scan = reinterpret_cast<Aff *>(smem + kStageBytes);
+  s.d0 = reinterpret_cast<double *>(smem + kStageBytes + kScanBytes);
+  s.d1 = s.d0 + (reg ? 0 : nc * kCalBlock);
+  s.u0 = reinterpret_cast<uint32_t *>(s.d1 + nc * kCalBlock);
+  s.u1 = s.u0 + (reg ? 0 : nc * kCalBlock);
+  return s;
+}
+
+// C1: per-thread c_hat maps -> within-block exclusive prefixes + block totals
+template <int NC, bool REG>
+__global__ void __launch_bounds__(kCalBlock, 3) c1_maps(CalibArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  MapSmem s = map_smem(smem, a.n_cats);            // a/b: sigma map, c state in cst
-  double *cst = reinterpret_cast<double *>(s.cnt + a.n_cats * kCalBlock);
-  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool live = t < a.threads;
+  const Smem sm = smem_layout(smem, NC, REG);
+  Vec<NC, REG> b;
+  UVec<NC, REG> n;
+  b.bind(sm.d0);
+  n.bind(sm.u0);
+  for (uint32_t k = 0; k < NC; ++k) { b.set(k, 0.0); n.set(k, 0u); }
+  const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
+  for_segment(a, sm.st, [&](double c, uint32_t k) {
+    b.set(k, __fma_rn(beta, b.get(k), __dmul_rn(w, c)));
+    n.inc(k);
+  });
+  const uint64_t t = (uint64_t)blockIdx.x * kCalBlock + threadIdx.x;
   for (uint32_t k = 0; k < a.n_cats; ++k) {
-    s.a(k) = 1.0; s.b(k) = 0.0;
-    s.n(k) = live ? (uint32_t)0 : 0u;
-    cst[k * kCalBlock + threadIdx.x] =
-        live ? __dadd_rn(__dmul_rn(a.mapA[k * a.threads + t], a.c0[k]), a.mapB[k * a.threads + t]) : 0.0;
-  }
-  uint64_t lo, hi;
-  segment(a, t, lo, hi);
-  const double w = __dsub_rn(1.0, a.beta);
-  for (uint64_t i = lo; i < hi; ++i) {
-    const Obs o = load_obs(a, i);
-    if (!o.valid) continue;
-    double &c = cst[o.k * kCalBlock + threadIdx.x];
-    const double prev = c;
-    c = __dadd_rn(__dmul_rn(a.beta, prev), __dmul_rn(w, o.c));
-    const double d = fabs(__dsub_rn(o.c, prev));
-    s.a(o.k) = __dmul_rn(a.beta, s.a(o.k));
-    s.b(o.k) = __dadd_rn(__dmul_rn(a.beta, s.b(o.k)), __dmul_rn(w, d));
-    const uint32_t seen = ++s.n(o.k);
-    if (a.preN[(uint64_t)o.k * a.threads + t] + seen == a.snap_at) {
-      a.snap_c[o.k] = c;
-      a.snap_thread[o.k] = t;
+    const uint32_t nk = n.get(k);
+    Aff ex, tot;
+    block_scan(Aff{pow_n(beta, nk), b.get(k), nk}, ex, tot, sm.scan);
+    a.thrA[k * a.threads + t] = ex.a;
+    a.thrB[k * a.threads + t] = ex.b;
+    a.thrN[k * a.threads + t] = (uint32_t)ex.n;
+    if (threadIdx.x == 0) {
+      a.blkA[k * a.blocks + blockIdx.x] = tot.a;
+      a.blkB[k * a.blocks + blockIdx.x] = tot.b;
+      a.blkN[k * a.blocks + blockIdx.x] = tot.n;
     }
   }
-  if (live)
-    for (uint32_t k = 0; k < a.n_cats; ++k) {
-      a.sigA[k * a.threads + t] = s.a(k);
-      a.sigB[k * a.threads + t] = s.b(k);
-    }
 }
 
-// C4: sigma snapshot -- replay the segment that holds each category's snapshot
-__global__ void __launch_bounds__(32) c4_snap(CalibArgs a) {
+// C2: exclusive scan of the block totals of one category (block = category);
+// which = 0: c_hat maps (final c_hat, counts), 1: sigma maps (final sigma)
+__global__ void __launch_bounds__(1024) c2_scan(CalibArgs a, int which) {
+  __shared__ Aff sw[32];
   const uint32_t k = blockIdx.x;
-  if (threadIdx.x != 0 || a.snap_thread[k] == ~0ull) return;
-  const uint64_t t = a.snap_thread[k];
-  double c = __dadd_rn(__dmul_rn(a.mapA[k * a.threads + t], a.c0[k]), a.mapB[k * a.threads + t]);
-  double sg = __dadd_rn(__dmul_rn(a.sigA[k * a.threads + t], a.s0[k]), a.sigB[k * a.threads + t]);
-  uint64_t lo, hi;
-  segment(a, t, lo, hi);
-  const double w = __dsub_rn(1.0, a.beta);
-  uint64_t seen = a.preN[(uint64_t)k * a.threads + t];
-  for (uint64_t i = lo; i < hi; ++i) {
-    const Obs o = load_obs(a, i);
-    if (!o.valid || o.k != k) continue;
-    const double prev = c;
-    c = __dadd_rn(__dmul_rn(a.beta, prev), __dmul_rn(w, o.c));
-    sg = __dadd_rn(__dmul_rn(a.beta, sg), __dmul_rn(w, fabs(__dsub_rn(o.c, prev))));
-    if (++seen == a.snap_at) {
-      a.snap_s[k] = sg;
-      return;
+  double *A = (which ? a.sblkA : a.blkA) + (uint64_t)k * a.blocks;
+  double *B = (which ? a.sblkB : a.blkB) + (uint64_t)k * a.blocks;
+  unsigned long long *N = a.blkN + (uint64_t)k * a.blocks;
+  Aff carry = aff_id();
+  for (uint64_t base = 0; base < a.blocks; base += blockDim.x) {
+    const uint64_t j = base + threadIdx.x;
+    const bool in = j < a.blocks;
+    const Aff x = in ? Aff{A[j], B[j], which ? 0ull : N[j]} : aff_id();
+    Aff ex, tot;
+    block_scan(x, ex, tot, sw);
+    const Aff pre = compose(carry, ex);
+    if (in) {
+      A[j] = pre.a;
+      B[j] = pre.b;
+      if (!which) N[j] = pre.n;
+    }
+    carry = compose(carry, tot);
+  }
+  if (threadIdx.x == 0) {
+    if (which == 0) { a.totA[k] = apply(carry, a.c0[k]); a.totN[k] = carry.n; }
+    else { a.totSA[k] = apply(carry, a.s0[k]); }
+  }
+}
+
+// C3: replay each segment from its c_hat start state; sigma maps; snapshots
+template <int NC, bool REG>
+__global__ void __launch_bounds__(kCalBlock, 3) c3_replay(CalibArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const Smem sm = smem_layout(smem, NC, REG);
+  Vec<NC, REG> c;
+  Vec<NC, false> sb;              // shared memory: frees the select chains for c
+  UVec<NC, REG> n, target;
+  c.bind(sm.d0);
+  sb.bind(sm.d1);
+  n.bind(sm.u0);
+  target.bind(sm.u1);
+  const uint64_t t = (uint64_t)blockIdx.x * kCalBlock + threadIdx.x;
+  for (uint32_t k = 0; k < NC; ++k) {
+    double ck = 0.0;
+    uint32_t tk = 0u;
+    if (k < a.n_cats) {
+      const Aff blk{a.blkA[k * a.blocks + blockIdx.x], a.blkB[k * a.blocks + blockIdx.x],
+                    a.blkN[k * a.blocks + blockIdx.x]};
+      const Aff thr{a.thrA[k * a.threads + t], a.thrB[k * a.threads + t], a.thrN[k * a.threads + t]};
+      const Aff pre = compose(blk, thr);
+      ck = apply(pre, a.c0[k]);
+      // observations of category k before this segment; the snapshot fires at seen == target
+      tk = (a.snap_at > pre.n && a.snap_at - pre.n <= a.seg) ? (uint32_t)(a.snap_at - pre.n) : 0u;
+    }
+    c.set(k, ck);
+    sb.set(k, 0.0);
+    n.set(k, 0u);
+    target.set(k, tk);
+  }
+  const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
+  uint32_t snapped = 0u;          // bit k: this thread holds category k's snapshot
+  for_segment(a, sm.st, [&](double o, uint32_t k) {
+    const double prev = c.get(k);
+    const double cn = __fma_rn(beta, prev, __dmul_rn(w, o));
+    c.set(k, cn);
+    const double sn = __fma_rn(beta, sb.get(k), __dmul_rn(w, fabs(__dsub_rn(o, prev))));
+    sb.set(k, sn);
+    n.inc(k);
+    if (n.eq(k, target)) {
+      a.snap_c[k] = cn;
+      a.snap_sa[k] = pow_n(beta, target.get(k));
+      a.snap_sb[k] = sn;
+      snapped |= 1u << k;
+    }
+  });
+  for (uint32_t k = 0; k < a.n_cats; ++k) {
+    const uint32_t nk = n.get(k);
+    Aff ex, tot;
+    block_scan(Aff{pow_n(beta, nk), sb.get(k), nk}, ex, tot, sm.scan);
+    if (threadIdx.x == 0) {
+      a.sblkA[k * a.blocks + blockIdx.x] = tot.a;
+      a.sblkB[k * a.blocks + blockIdx.x] = tot.b;
+    }
+    if (snapped & (1u << k)) {      // snapshot map from the block's start
+      const Aff part{a.snap_sa[k], a.snap_sb[k], 0ull};
+      const Aff m = compose(ex, part);
+      a.snap_sa[k] = m.a;
+      a.snap_sb[k] = m.b;
+      a.snap_block[k] = blockIdx.x;
     }
   }
+}
+
+// C4: sigma snapshot = (map from its block's start) applied to sigma at that start
+__global__ void c4_snap(CalibArgs a) {
+  const uint32_t k = threadIdx.x;
+  if (k >= a.n_cats || a.snap_block[k] == ~0ull) return;
+  const uint64_t j = a.snap_block[k];
+  const double s_start = __fma_rn(a.sblkA[k * a.blocks + j], a.s0[k], a.sblkB[k * a.blocks + j]);
+  a.snap_s[k] = __fma_rn(a.snap_sa[k], s_start, a.snap_sb[k]);
+}
+
+size_t calib_smem(uint32_t nc, bool reg) {
+  return kStageBytes + kScanBytes + (size_t)nc * kCalBlock * 8 + (reg ? 0 : (size_t)nc * kCalBlock * (8 + 4 * 2));
+}
+
+template <int NC, bool REG>
+cudaError_t set_attrs() {
+  const size_t smem = calib_smem(NC, REG);
+  cudaError_t e = cudaFuncSetAttribute(c1_maps<NC, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(c3_replay<NC, REG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+template <int NC, bool REG>
+int blocks_per_sm() {
+  if (set_attrs<NC, REG>() != cudaSuccess) return 0;
+  const size_t smem = calib_smem(NC, REG);
+  int b1 = 0, b3 = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, c1_maps<NC, REG>, kCalBlock, smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, c3_replay<NC, REG>, kCalBlock, smem) != cudaSuccess)
+    return 0;
+  return b1 < b3 ? b1 : b3;
+}
+
+template <int NC, bool REG>
+cudaError_t launch(const CalibArgs &a, cudaStream_t s) {
+  cudaError_t e = set_attrs<NC, REG>();
+  if (e != cudaSuccess) return e;
+  const size_t smem = calib_smem(NC, REG);
+  c1_maps<NC, REG><<<(unsigned)a.blocks, kCalBlock, smem, s>>>(a);
+  c2_scan<<<a.n_cats, 1024, 0, s>>>(a, 0);
+  c3_replay<NC, REG><<<(unsigned)a.blocks, kCalBlock, smem, s>>>(a);
+  c2_scan<<<a.n_cats, 1024, 0, s>>>(a, 1);
+  c4_snap<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t calib_scratch_bytes(uint64_t threads, uint32_t n_cats) {
-  // mapA, mapB, sigA, sigB (double), mapN (u32), preN (u64) per (category, thread)
-  return (size_t)threads * n_cats * (8 * 4 + 4 + 8);
+size_t calib_scratch_bytes(uint64_t blocks, uint32_t n_cats) {
+  // thrA, thrB (double), thrN (u32) per (category, thread); blkA, blkB, sblkA,
+  // sblkB (double), blkN (u64) per (category, block)
+  return (size_t)blocks * n_cats * ((size_t)kCalBlock * (8 * 2 + 4) + 8 * 5);
+}
+
+int calib_blocks_per_sm(uint32_t n_cats) {
+  return n_cats <= 4 ? blocks_per_sm<4, true>() : blocks_per_sm<16, false>();
 }
 
 cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s) {
-  const size_t sm1 = (size_t)a.n_cats * kCalBlock * (8 * 2 + 4);
-  const size_t sm3 = sm1 + (size_t)a.n_cats * kCalBlock * 8;
-  cudaError_t e = cudaFuncSetAttribute(c1_maps, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(c3_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-  if (e != cudaSuccess) return e;
-  const unsigned blocks = (unsigned)((a.threads + kCalBlock - 1) / kCalBlock);
-  c1_maps<<<blocks, kCalBlock, sm1, s>>>(a);
-  c2_scan<<<a.n_cats, 1024, 0, s>>>(a, 0);
-  c3_replay<<<blocks, kCalBlock, sm3, s>>>(a);
-  c2_scan<<<a.n_cats, 1024, 0, s>>>(a, 1);
-  c4_snap<<<a.n_cats, 32, 0, s>>>(a);
-  return cudaGetLastError();
+  return a.n_cats <= 4 ? launch<4, true>(a, s) : launch<16, false>(a, s);
 }
 
 }  // namespace fp

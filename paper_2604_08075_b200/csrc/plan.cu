@@ -868,11 +868,6 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
       const uint64_t need = n_local + 16;
       if (p->bins_cap < need) {
         cudaFree(p->d_bins);
-    cudaFree(p->d_p3);
-    cudaFree(p->d_calib_scratch);
-    cudaFree(p->d_peak);
-    cudaFree(p->d_results_pk);
-    cudaFree(p->d_results3);
         p->d_bins = nullptr;
         p->bins_cap = 0;
         CUDA_TRY(p, cudaMalloc(&p->d_bins, need), "cudaMalloc bins");
@@ -883,12 +878,6 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   } else if (n_local && len && is_host_pointer(len)) {
     if (p->resident_cap < n_local) {
       cudaFree(p->d_resident);
-    cudaFree(p->d_bins);
-    cudaFree(p->d_p3);
-    cudaFree(p->d_calib_scratch);
-    cudaFree(p->d_peak);
-    cudaFree(p->d_results_pk);
-    cudaFree(p->d_results3);
       p->d_resident = nullptr;
       p->resident_cap = 0;
       CUDA_TRY(p, cudaMalloc(&p->d_resident, n_local * 4), "cudaMalloc resident trace");
@@ -1195,24 +1184,26 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
     return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
-  // one segment per thread, ~64 feedback records each, capped at 8 blocks / SM
-  const uint64_t max_threads = (uint64_t)p->sm_count * 8 * 256;
-  uint64_t threads = std::max<uint64_t>(256, std::min<uint64_t>(max_threads, (n + 63) / 64));
-  threads = (threads + 255) / 256 * 256;
-  const uint64_t seg = std::max<uint64_t>(1, (n + threads - 1) / threads);
-  const size_t scratch = calib_scratch_bytes(threads, n_cats);
+  // one contiguous segment per thread (a multiple of 16 records), one resident wave
+  const int bps = calib_blocks_per_sm(n_cats);
+  if (bps < 1) return fail(p, FP_ERR_CUDA, "calibration kernels do not fit an SM");
+  const uint64_t max_blocks = (uint64_t)p->sm_count * bps;
+  // (segments stay below 65,536 records: the n_cats <= 4 kernels pack 16-bit counters)
+  const uint64_t blocks = std::max<uint64_t>({1, std::min<uint64_t>(max_blocks, (n + 256 * 64 - 1) / (256 * 64)),
+                                              (n + 256ull * 65520 - 1) / (256ull * 65520)});
+  const uint64_t threads = blocks * 256;
+  const uint64_t seg = std::max<uint64_t>(16, ((n + threads - 1) / threads + 15) / 16 * 16);
+  const size_t scratch = calib_scratch_bytes(blocks, n_cats);
   const size_t small = 16 * 8 * 10;
   if (p->calib_cap < scratch + small) {
     cudaFree(p->d_calib_scratch);
-    cudaFree(p->d_peak);
-    cudaFree(p->d_results_pk);
     p->d_calib_scratch = nullptr;
     p->calib_cap = 0;
     CUDA_TRY(p, cudaMalloc(&p->d_calib_scratch, scratch + small), "cudaMalloc calibration scratch");
     p->calib_cap = scratch + small;
   }
   unsigned char *base = p->d_calib_scratch;
-  const uint64_t KT = (uint64_t)n_cats * threads;
+  const uint64_t KT = (uint64_t)n_cats * threads, KB = (uint64_t)n_cats * blocks;
   CalibArgs a{};
   a.bytes = d_body_bytes;
   a.tokens = d_prompt_tokens;
@@ -1221,31 +1212,36 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   a.n_cats = n_cats;
   a.beta = beta;
   a.threads = threads;
+  a.blocks = blocks;
   a.seg = seg;
-  a.mapA = reinterpret_cast<double *>(base);
-  a.mapB = a.mapA + KT;
-  a.sigA = a.mapB + KT;
-  a.sigB = a.sigA + KT;
-  a.preN = reinterpret_cast<unsigned long long *>(a.sigB + KT);
-  a.mapN = reinterpret_cast<uint32_t *>(a.preN + KT);
+  a.thrA = reinterpret_cast<double *>(base);
+  a.thrB = a.thrA + KT;
+  a.blkA = a.thrB + KT;
+  a.blkB = a.blkA + KB;
+  a.sblkA = a.blkB + KB;
+  a.sblkB = a.sblkA + KB;
+  a.blkN = reinterpret_cast<unsigned long long *>(a.sblkB + KB);
+  a.thrN = reinterpret_cast<uint32_t *>(a.blkN + KB);
   double *sm = reinterpret_cast<double *>(base + scratch);     // 16-slot vectors
   a.totA = sm;
-  a.totB = sm + 16;
-  a.totSA = sm + 32;
-  a.totSB = sm + 48;
-  a.totN = reinterpret_cast<unsigned long long *>(sm + 64);
-  a.snap_c = sm + 80;
-  a.snap_s = sm + 96;
-  a.snap_thread = reinterpret_cast<unsigned long long *>(sm + 112);
+  a.totSA = sm + 16;
+  a.totN = reinterpret_cast<unsigned long long *>(sm + 32);
+  a.snap_c = sm + 48;
+  a.snap_s = sm + 64;
+  a.snap_block = reinterpret_cast<unsigned long long *>(sm + 80);
+  a.snap_sa = sm + 96;
+  a.snap_sb = sm + 112;
   double *c0 = sm + 128, *s0 = sm + 144;
   a.c0 = c0;
   a.s0 = s0;
   a.snap_at = snap_at;
+  a.vec_bt = !(((uintptr_t)d_body_bytes | (uintptr_t)d_prompt_tokens) & 15);
+  a.vec_c = !((uintptr_t)d_category & 15);
   std::vector<double> init_c(16, 0.0), init_s(16, 0.0);
   for (uint32_t k = 0; k < n_cats; ++k) { init_c[k] = init[k].c_hat; init_s[k] = init[k].sigma_hat; }
   CUDA_TRY(p, cudaMemcpyAsync(c0, init_c.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
   CUDA_TRY(p, cudaMemcpyAsync(s0, init_s.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
-  // snapshots start as NaN (all-ones bytes), no snapshot thread (~0)
+  // snapshots start as NaN (all-ones bytes), no snapshot block (~0)
   CUDA_TRY(p, cudaMemsetAsync(a.snap_c, 0xFF, 48 * 8, s), "memset snapshots");
   {
     LaunchTimer lt(p, FP_KERNEL_EVAL, s);
@@ -1253,19 +1249,18 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
     if (e != cudaSuccess) return cuda_fail(p, e, "calibration replay launch");
   }
   p->launches += 5;
-  std::vector<double> h(160);
-  CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 128 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");
+  std::vector<double> h(128);
+  CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 80 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");
   CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
   for (uint32_t k = 0; k < n_cats; ++k) {
-    // the scan kernel leaves the final states in totA / totSA
     uint64_t nobs;
-    memcpy(&nobs, &h[64 + k], 8);
+    memcpy(&nobs, &h[32 + k], 8);
     h_final[k].c_hat = h[k];
-    h_final[k].sigma_hat = h[32 + k];
+    h_final[k].sigma_hat = h[16 + k];
     h_n_obs[k] = nobs;
     if (h_snap) {
-      h_snap[k].c_hat = h[80 + k];
-      h_snap[k].sigma_hat = h[96 + k];
+      h_snap[k].c_hat = h[48 + k];
+      h_snap[k].sigma_hat = h[64 + k];
     }
   }
   return FP_OK;

@@ -59,3 +59,18 @@ def test_replay_feeds_the_estimator():
     static = fp.route_batch_raw(plan, _dev(body), _dev(mo), _dev(cat), [(4.0, 0.0)] * 4, 8192, 8192, 65536,
                                 true_prompt=_dev(tp))[1]
     assert mis[0] <= static[0]       # calibration reduces short-pool mis-routes (Table 5)
+
+
+@pytest.mark.parametrize("shift", [1, 3])
+def test_replay_misaligned_columns(shift):
+    """Columns that start mid-vector take the scalar staging path for their pieces."""
+    n = 777_777
+    body, mo, cat, tp = generate_raw_host("MIX", 21, 0, n)
+    pad = lambda a: np.concatenate([np.zeros(shift, a.dtype), a])   # noqa: E731
+    plan = fp.fleet_plan_create(**fp.desc_from_config(configs.c1()))
+    g = fp.calibrate_replay(plan, _dev(pad(body))[shift:], _dev(pad(tp))[shift:], _dev(pad(cat))[shift:],
+                            [(4.0, 0.5)] * 4, beta=0.9, snap_at=50)
+    o = oracle.calibrate(body, tp, cat, 4, beta=0.9, c0=4.0, s0=0.5, snap_at=50)
+    assert np.array_equal(g["n_obs"], o["n_obs"])
+    assert _close(g["c_hat"], o["c_hat"]) and _close(g["sigma"], o["sigma"])
+    assert _close(g["snap_c"], o["snap_c"]) and _close(g["snap_sigma"], o["snap_sigma"])

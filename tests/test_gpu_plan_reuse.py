@@ -1,0 +1,48 @@
+"""One plan driven through every entry point in turn, with growing inputs, so
+that each lazily grown scratch buffer is reallocated while the others are
+live (regression: a reallocation once freed unrelated buffers)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2604_08075_b200 as fp  # noqa: E402
+from synth import configs  # noqa: E402
+from synth.gen import arrivals_host, generate_host, generate_raw_host  # noqa: E402
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32) if a.dtype == np.uint32 else a).cuda()
+
+
+def test_all_entry_points_on_one_plan():
+    cfg = configs.c5()
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg))
+    for n in (10_000, 1_500_000, 4_000_000):
+        c = cfg.with_n(n)
+        L = generate_host(c.shape, c.seed, 0, n)
+        # host trace (resident copy grows), then the bin pass (bin buffer grows)
+        best, _ = fp.sweep_and_route(plan, torch.from_numpy(L.view(np.int32)), c.rate_rps, route_model=0)
+        dec = torch.empty(n, dtype=torch.uint8, device="cuda")
+        best_d, _ = fp.sweep_and_route(plan, _dev(L), c.rate_rps, route_model=0, decision=dec)
+        _, obest = oracle.sweep(c, L)
+        assert best.tobytes() == obest.tobytes() and best_d.tobytes() == obest.tobytes()
+        _, best3 = fp.sweep_three_pools(plan, c.rate_rps)
+        _, obest3 = oracle.sweep3(c, L)
+        assert best3.tobytes() == obest3.tobytes()
+        arr = arrivals_host(c.seed, n, c.rate_rps)
+        _, bpk = fp.sweep_peak_windows(plan, _dev(L), torch.from_numpy(arr.view(np.int64)).cuda(), 10**9)
+        _, opk = oracle.sweep_peak(c, L, arr, 10**9)
+        assert bpk.tobytes() == opk.tobytes()
+        body, mo, cat, tp = generate_raw_host("MIX", 5, 0, n)
+        g = fp.calibrate_replay(plan, _dev(body), _dev(tp), _dev(cat), [(4.0, 0.5)] * 4)
+        o = oracle.calibrate(body, tp, cat, 4, beta=0.95, c0=4.0, s0=0.5)
+        assert np.allclose(g["c_hat"], o["c_hat"], rtol=1e-12, atol=0)
+        # the three-pool records must still be readable after the other reallocations
+        _, best3b = fp.sweep_three_pools(plan, c.rate_rps)
+        assert best3b.tobytes() == best3.tobytes()
