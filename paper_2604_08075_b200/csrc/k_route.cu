@@ -247,18 +247,26 @@ cudaError_t launch_route(const RouteArgs &a0, int grid, int block, cudaStream_t 
 namespace fp {
 namespace {
 
+// per-thread tallies: counts in u32 (a thread routes < 2^32 requests; checked
+// at launch), token masses in u64; branch-free (B <= C_S <= C_L: short = !pa)
 struct RawAcc {
-  unsigned long long ns = 0, nl = 0, nr = 0, ms = 0, ml = 0, mis_s = 0, mis_l = 0;
+  uint32_t ns = 0, nl = 0, nr = 0, mis_s = 0, mis_l = 0;
+  unsigned long long ms = 0, ml = 0;
 };
 
 __device__ __forceinline__ uint32_t route_raw_one(const RouteRawArgs &a, uint32_t L, uint32_t mo, uint32_t tp,
                                                   RawAcc &c) {
   const bool pa = L > a.b, pb = L > a.cs, pc = L > a.cl;
-  if (pc) { ++c.nr; } else if (pa) { ++c.nl; c.ml += L; } else { ++c.ns; c.ms += L; }
+  const bool lng = pa && !pc;
+  c.nr += pc;
+  c.nl += lng;
+  c.ns += !pa;
+  c.ml += lng ? L : 0u;
+  c.ms += pa ? 0u : L;
   if (a.true_prompt) {
     const unsigned long long t = (unsigned long long)tp + mo;
-    c.mis_s += (!pa && t > a.cs) ? 1ull : 0ull;
-    c.mis_l += (pa && !pc && t > a.cl) ? 1ull : 0ull;
+    c.mis_s += (!pa && t > a.cs);
+    c.mis_l += (lng && t > a.cl);
   }
   return (pa ? 1u : 0u) + (pb ? 4u : 0u) + (pc ? 9u : 0u);
 }
@@ -308,7 +316,7 @@ __global__ void __launch_bounds__(512) k4_route_raw(RouteRawArgs a) {
       if (l4) l4[i] = L;
     }
   }
-  unsigned long long v[7] = {acc.ns, acc.nl, acc.nr, acc.ms, acc.ml, acc.mis_s, acc.mis_l};
+  unsigned long long v[7] = {acc.ns, acc.nl, acc.nr, acc.ms, acc.ml, acc.mis_s, acc.mis_l};   // widened
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
 #pragma unroll
@@ -334,6 +342,7 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
   if (block > 512 || (block & 31) || a.n_cats == 0 || a.n_cats > 256) return cudaErrorInvalidValue;
   const uint64_t need = (a.n + block - 1) / block;
   const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
+  if (a.n / ((uint64_t)g * block) >= (1ull << 31)) return cudaErrorInvalidValue;   // u32 per-thread tallies
   // vector path: every column in the same 16-B phase (cat / decision in the same 4-B phase)
   const uintptr_t b = reinterpret_cast<uintptr_t>(a.body);
   const uint64_t mis = (b & 15u) >> 2, head = mis ? 4 - mis : 0;

@@ -185,6 +185,7 @@ struct SrcRaw {
 // (a.bins_out + element index) is 4-B aligned for every uint4 of the body.
 template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS>
 __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs a) {
+  constexpr int U = kUnroll;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
   uint32_t lut_bytes = (LUTW == 0) ? a.n_edges * 4 : a.lut_cells * LUTW;
@@ -192,10 +193,12 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
   K1Ctx c;
   c.lut = smem;
   c.acc = reinterpret_cast<unsigned long long *>(smem + lut_bytes);
-  // RAW: [ncat][c*, 1/c*, lo, hi], 16-B aligned for the LDS.128 pairs
-  double *cstar = RAW ? reinterpret_cast<double *>((reinterpret_cast<uintptr_t>(c.acc + nbins) + 15) & ~uintptr_t(15))
-                      : reinterpret_cast<double *>(c.acc + nbins);
-  c.hist = reinterpret_cast<unsigned char *>(cstar + (RAW ? 4 * a.n_cats : 0));
+  // RAW: [ncat][c*, 1/c*, lo, hi], 16-B aligned for the LDS.128 pairs. Offsets
+  // are integer arithmetic on `smem` so the compiler keeps the shared state
+  // space (a pointer rounded through uintptr_t becomes generic: ATOM.E/LD.E)
+  const uint32_t cst_off = RAW ? ((lut_bytes + nbins * 8u + 15u) & ~15u) : lut_bytes + nbins * 8u;
+  double *cstar = reinterpret_cast<double *>(smem + cst_off);
+  c.hist = smem + cst_off + (RAW ? 32u * a.n_cats : 0u);
   c.clampv = a.max_edge + 1u;
   c.round = (1u << a.shift) - 1u;
   c.shift = a.shift;
@@ -262,23 +265,23 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
     // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
     // 6.6 TB/s for per-block contiguous tiles; profiles/r01_microbench_*).
     // The step count is uniform over the grid so the flush barrier is safe.
-    const uint64_t step4 = S * kUnroll;
+    const uint64_t step4 = S * U;
     const uint64_t full_steps = n4 / step4;
     const uint64_t nsteps = (n4 + step4 - 1) / step4;
     for (uint64_t k = 0; k < nsteps; ++k) {
       const uint64_t base = k * step4 + me;
       if (k < full_steps) {
-        uint4 v[kUnroll];
+        uint4 v[U];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) v[u] = RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S);
+        for (int u = 0; u < U; ++u) v[u] = RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S);
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < U; ++u) {
           const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
           if (BINS) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(w) : "memory");
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u)
+        for (int u = 0; u < U; ++u)
           if (base + u * S < n4) {
             const uint32_t w =
                 add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S));
