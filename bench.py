@@ -333,14 +333,18 @@ def run_ours(args, cfg):
     fp.fp_kernel_time_reset(plan)
     l0 = fp.fp_kernel_launches(plan)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
-        for _ in range(args.steps):
+        for k in range(args.steps):
             best, counts = step(d_len)
+            ev[k].record(stream)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
+    per_step = sorted([e0.elapsed_time(ev[0])] + [ev[k - 1].elapsed_time(ev[k]) for k in range(1, args.steps)])
+    pct = lambda q: per_step[min(len(per_step) - 1, int(q * len(per_step)))]   # noqa: E731
     launches = fp.fp_kernel_launches(plan) - l0
     ms_local = e0.elapsed_time(e1)
     ktime = {k: fp.fp_kernel_time(plan, kind) for k, kind in
@@ -416,6 +420,7 @@ def run_ours(args, cfg):
              "route": "K4b k4_route_bins" if bin_pass else "K4 k4_route"}
     roof = {"bound": "hbm", "kernel": kname.get(dom, dom),
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "frac_of_nominal_7700": achieved / 7700.0,
             "traffic": _traffic(cfg.name, dom), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": per_launch_bytes,
             "per_kernel_GBps": k_gbs,
@@ -429,6 +434,7 @@ def run_ours(args, cfg):
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
             "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic (seeded Philox MIX trace, generated on device; not timed)",
             "config": _workload(cfg, n, world),
