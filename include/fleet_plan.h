@@ -320,7 +320,10 @@ fp_status sweep_three_pools(fp_plan *plan, double rate_rps, fp_pool3_candidate *
  * the state right after the snap_at-th observation of each category into
  * h_snap[k] (NaN if the category has fewer). Computed as a parallel scan of
  * affine maps: equal to the sequential replay up to fp64 reassociation.
- * Rank-local (the stream is this rank's). 1 <= n_cats <= 16, 0 < beta < 1.
+ * world > 1: the stream is sharded in order (rank r holds the r-th piece,
+ * n may be 0); ranks all-gather their composed maps (three small exchanges)
+ * and every rank returns the state of the WHOLE stream. 1 <= n_cats <= 16,
+ * 0 < beta < 1.
  * Synchronizes. The result is the fp_category_calibration snapshot that
  * sweep_thresholds_raw / route_batch_raw consume. */
 fp_status calibrate_replay(fp_plan *plan, const uint32_t *d_body_bytes, const uint32_t *d_prompt_tokens,
@@ -344,8 +347,11 @@ typedef struct fp_peak_candidate {
   double cost_dual, cost_homo, savings;
 } fp_peak_candidate;
 
-/* Peak-window sweep over d_len / d_arrival_ns (device, n_local each, n_local
- * < 2^32; rank-local). Precondition: arrivals non-decreasing (a trace is in
+/* Peak-window sweep over d_len / d_arrival_ns (device, n_local each; the
+ * whole trace < 2^32 requests). world > 1: each rank holds a shard (any
+ * split, n_local may be 0); ranks agree on the window range (all-gather) and
+ * sum their window x bin histograms (all-reduce), then every rank evaluates
+ * the whole grid. Precondition: arrivals non-decreasing (a trace is in
  * arrival order) -- the requests of a window are then one contiguous
  * index range, which the kernels exploit; the first/last arrivals are always
  * checked, the whole column only with FP_FLAG_CHECK_ORDER (otherwise an

@@ -145,7 +145,8 @@ struct PeakArgs {
 };
 size_t peak_smem_bytes(const PeakArgs &a);
 size_t peak_scan_smem_bytes(const PeakArgs &a);
-cudaError_t launch_peak_hist(const PeakArgs &a, int grid, cudaStream_t s);
+cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s);   // Kc?, K0w, K1w
+cudaError_t launch_peak_scan(const PeakArgs &a, int sm_count, cudaStream_t s);   // K2w
 
 // NEXT-3: calibration replay (k_calib.cu)
 struct CalibArgs {
@@ -163,6 +164,10 @@ struct CalibArgs {
   double *sblkA, *sblkB;            // [n_cats][blocks] sigma block totals -> exclusive prefixes
   double *totA, *totSA;             // [n_cats] final c_hat / sigma
   unsigned long long *totN;         // [n_cats] observations
+  double *mapA, *mapB;              // [n_cats] this stream's total c_hat map (world > 1 exchange)
+  unsigned long long *mapN;
+  double *smapA, *smapB;            // [n_cats] this stream's total sigma map
+  unsigned long long snap_off[16];  // observations of each category on lower ranks
   uint64_t snap_at;
   double *snap_c, *snap_s;          // [n_cats]
   double *snap_sa, *snap_sb;        // [n_cats] sigma map from the snapshot's block start
@@ -171,6 +176,9 @@ struct CalibArgs {
 };
 size_t calib_scratch_bytes(uint64_t blocks, uint32_t n_cats);
 int calib_blocks_per_sm(uint32_t n_cats);
-cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s);
+cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s);        // C1 C2 C3 C2 C4 (one rank)
+cudaError_t launch_calib_maps(const CalibArgs &a, cudaStream_t s);   // C1 C2
+cudaError_t launch_calib_replay(const CalibArgs &a, cudaStream_t s); // C3 C2
+cudaError_t launch_calib_snap(const CalibArgs &a, cudaStream_t s);   // C4
 
 }  // namespace fp

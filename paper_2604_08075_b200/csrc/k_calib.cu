@@ -352,8 +352,14 @@ __global__ void __launch_bounds__(1024) c2_scan(CalibArgs a, int which) {
     carry = compose(carry, tot);
   }
   if (threadIdx.x == 0) {
-    if (which == 0) { a.totA[k] = apply(carry, a.c0[k]); a.totN[k] = carry.n; }
-    else { a.totSA[k] = apply(carry, a.s0[k]); }
+    if (which == 0) {
+      a.totA[k] = apply(carry, a.c0[k]);
+      a.totN[k] = carry.n;
+      a.mapA[k] = carry.a; a.mapB[k] = carry.b; a.mapN[k] = carry.n;
+    } else {
+      a.totSA[k] = apply(carry, a.s0[k]);
+      a.smapA[k] = carry.a; a.smapB[k] = carry.b;
+    }
   }
 }
 
@@ -380,7 +386,8 @@ __global__ void __launch_bounds__(kCalBlock, 3) c3_replay(CalibArgs a) {
       const Aff pre = compose(blk, thr);
       ck = apply(pre, a.c0[k]);
       // observations of category k before this segment; the snapshot fires at seen == target
-      tk = (a.snap_at > pre.n && a.snap_at - pre.n <= a.seg) ? (uint32_t)(a.snap_at - pre.n) : 0u;
+      const unsigned long long before = pre.n + a.snap_off[k];
+      tk = (a.snap_at > before && a.snap_at - before <= a.seg) ? (uint32_t)(a.snap_at - before) : 0u;
     }
     c.set(k, ck);
     sb.set(k, 0.0);
@@ -454,15 +461,18 @@ int blocks_per_sm() {
 }
 
 template <int NC, bool REG>
-cudaError_t launch(const CalibArgs &a, cudaStream_t s) {
+cudaError_t launch_maps(const CalibArgs &a, cudaStream_t s) {
   cudaError_t e = set_attrs<NC, REG>();
   if (e != cudaSuccess) return e;
-  const size_t smem = calib_smem(NC, REG);
-  c1_maps<NC, REG><<<(unsigned)a.blocks, kCalBlock, smem, s>>>(a);
+  c1_maps<NC, REG><<<(unsigned)a.blocks, kCalBlock, calib_smem(NC, REG), s>>>(a);
   c2_scan<<<a.n_cats, 1024, 0, s>>>(a, 0);
-  c3_replay<NC, REG><<<(unsigned)a.blocks, kCalBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NC, bool REG>
+cudaError_t launch_replay(const CalibArgs &a, cudaStream_t s) {
+  c3_replay<NC, REG><<<(unsigned)a.blocks, kCalBlock, calib_smem(NC, REG), s>>>(a);
   c2_scan<<<a.n_cats, 1024, 0, s>>>(a, 1);
-  c4_snap<<<1, 32, 0, s>>>(a);
   return cudaGetLastError();
 }
 
@@ -478,8 +488,24 @@ int calib_blocks_per_sm(uint32_t n_cats) {
   return n_cats <= 4 ? blocks_per_sm<4, true>() : blocks_per_sm<16, false>();
 }
 
+cudaError_t launch_calib_maps(const CalibArgs &a, cudaStream_t s) {
+  return a.n_cats <= 4 ? launch_maps<4, true>(a, s) : launch_maps<16, false>(a, s);
+}
+
+cudaError_t launch_calib_replay(const CalibArgs &a, cudaStream_t s) {
+  return a.n_cats <= 4 ? launch_replay<4, true>(a, s) : launch_replay<16, false>(a, s);
+}
+
+cudaError_t launch_calib_snap(const CalibArgs &a, cudaStream_t s) {
+  c4_snap<<<1, 32, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s) {
-  return a.n_cats <= 4 ? launch<4, true>(a, s) : launch<16, false>(a, s);
+  cudaError_t e = launch_calib_maps(a, s);
+  if (e == cudaSuccess) e = launch_calib_replay(a, s);
+  if (e == cudaSuccess) e = launch_calib_snap(a, s);
+  return e;
 }
 
 }  // namespace fp

@@ -224,8 +224,12 @@ cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
       : a.lutw == 2 ? launch_hist<2>(a, sm_count, smem, s)
                     : launch_hist<0>(a, sm_count, smem, s);
   if (e != cudaSuccess) return e;
+  return cudaSuccess;
+}
+
+cudaError_t launch_peak_scan(const PeakArgs &a, int sm_count, cudaStream_t s) {
   const size_t smem2 = peak_scan_smem_bytes(a);
-  e = cudaFuncSetAttribute(k2w_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  cudaError_t e = cudaFuncSetAttribute(k2w_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (e != cudaSuccess) return e;
   const uint64_t chunks = (a.n_windows + a.rows - 1) / a.rows;
   k2w_peaks<<<(unsigned)std::min<uint64_t>(chunks, (uint64_t)sm_count * 4), 256, smem2, s>>>(a);

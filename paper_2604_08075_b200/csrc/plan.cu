@@ -26,7 +26,7 @@ using namespace fp;
 namespace {
 typedef struct { char internal[128]; } NcclUniqueId;
 typedef void *NcclComm;
-enum { kNcclUint8 = 1, kNcclUint64 = 5 };
+enum { kNcclUint8 = 1, kNcclUint32 = 3, kNcclUint64 = 5 };
 enum { kNcclSum = 0 };
 struct NcclApi {
   void *h = nullptr;
@@ -124,6 +124,7 @@ struct fp_plan {
   int k3p_grid_x = 1;
   uint64_t n_cand3 = 0;
   // NEXT-4 peak-window scratch (lazy)
+  uint64_t *d_xch = nullptr;               // [world + 1][4] small all-gather exchange
   unsigned char *d_peak = nullptr;
   size_t peak_cap = 0;
   fp_peak_candidate *d_results_pk = nullptr;
@@ -575,6 +576,22 @@ fp_status all_reduce_u64(fp_plan *p, unsigned long long *dbuf, size_t count, cud
   return FP_OK;
 }
 
+fp_status all_reduce_u32(fp_plan *p, uint32_t *dbuf, size_t count, cudaStream_t s, const char *what) {
+  if (!p->has_coll)
+    return nccl_check(p, g_nccl.AllReduce(dbuf, dbuf, count, kNcclUint32, kNcclSum, p->comm, s), what);
+  // host hooks carry u64 sums: widen, reduce, narrow (sums are bounded by the caller)
+  std::vector<uint32_t> h(count);
+  CUDA_TRY(p, cudaMemcpyAsync(h.data(), dbuf, count * 4, cudaMemcpyDeviceToHost, s), what);
+  CUDA_TRY(p, cudaStreamSynchronize(s), what);
+  std::vector<uint64_t> w(h.begin(), h.end());
+  if (p->coll.allreduce_sum_u64(w.data(), count, p->coll.user) != 0)
+    return fail(p, FP_ERR_NCCL, "%s: collectives hook failed", what);
+  for (size_t i = 0; i < count; ++i) h[i] = (uint32_t)w[i];
+  CUDA_TRY(p, cudaMemcpyAsync(dbuf, h.data(), count * 4, cudaMemcpyHostToDevice, s), what);
+  CUDA_TRY(p, cudaStreamSynchronize(s), what);
+  return FP_OK;
+}
+
 fp_status all_gather_bytes(fp_plan *p, const void *dsend, void *drecv, size_t bytes, cudaStream_t s,
                            const char *what) {
   if (!p->has_coll)
@@ -721,6 +738,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_p3);
     cudaFree(p->d_calib_scratch);
     cudaFree(p->d_peak);
+    cudaFree(p->d_xch);
     cudaFree(p->d_results_pk);
     cudaFree(p->d_results3);
     cudaFree(p->d_calib);
@@ -1168,6 +1186,22 @@ fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_r
   return FP_OK;
 }
 
+namespace {
+struct HostAff {
+  double a = 1.0, b = 0.0;
+  uint64_t n = 0;
+};
+// e first, then l (as the device's compose)
+HostAff host_compose(const HostAff &e, const HostAff &l) {
+  return HostAff{l.a * e.a, std::fma(l.a, e.b, l.b), e.n + l.n};
+}
+
+fp_status ensure_xch(fp_plan *p) {
+  if (!p->d_xch) CUDA_TRY(p, cudaMalloc(&p->d_xch, (size_t)(p->world + 1) * 512), "cudaMalloc exchange");
+  return FP_OK;
+}
+}  // namespace
+
 fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint32_t *d_prompt_tokens,
                            const uint8_t *d_category, uint64_t n, uint32_t n_cats, double beta,
                            const fp_category_calibration *init, uint64_t snap_at,
@@ -1179,9 +1213,11 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   for (uint32_t k = 0; k < n_cats; ++k)
     if (!std::isfinite(init[k].c_hat) || !std::isfinite(init[k].sigma_hat))
       return fail(p, FP_ERR_INVALID_ARG, "initial state must be finite");
-  if (n && (!d_body_bytes || !d_prompt_tokens || !d_category || is_host_pointer(d_body_bytes) ||
-            is_host_pointer(d_prompt_tokens) || is_host_pointer(d_category)))
-    return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
+  // a rank-specific failure is exchanged (world > 1) so that all ranks fail together
+  const bool bad = n && (!d_body_bytes || !d_prompt_tokens || !d_category || is_host_pointer(d_body_bytes) ||
+                         is_host_pointer(d_prompt_tokens) || is_host_pointer(d_category));
+  if (bad && p->world == 1) return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
+  if (bad) n = 0;
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   // one contiguous segment per thread (a multiple of 16 records), one resident wave
@@ -1194,7 +1230,7 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   const uint64_t threads = blocks * 256;
   const uint64_t seg = std::max<uint64_t>(16, ((n + threads - 1) / threads + 15) / 16 * 16);
   const size_t scratch = calib_scratch_bytes(blocks, n_cats);
-  const size_t small = 16 * 8 * 10;
+  const size_t small = 16 * 16 * 8;
   if (p->calib_cap < scratch + small) {
     cudaFree(p->d_calib_scratch);
     p->d_calib_scratch = nullptr;
@@ -1222,18 +1258,26 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   a.sblkB = a.sblkA + KB;
   a.blkN = reinterpret_cast<unsigned long long *>(a.sblkB + KB);
   a.thrN = reinterpret_cast<uint32_t *>(a.blkN + KB);
-  double *sm = reinterpret_cast<double *>(base + scratch);     // 16-slot vectors
-  a.totA = sm;
-  a.totSA = sm + 16;
-  a.totN = reinterpret_cast<unsigned long long *>(sm + 32);
-  a.snap_c = sm + 48;
-  a.snap_s = sm + 64;
-  a.snap_block = reinterpret_cast<unsigned long long *>(sm + 80);
-  a.snap_sa = sm + 96;
-  a.snap_sb = sm + 112;
-  double *c0 = sm + 128, *s0 = sm + 144;
+  // 16 slots of 16 doubles; slots 3-5 and 10-13 / 14-15 are the exchange records
+  double *sm = reinterpret_cast<double *>(base + scratch);
+  auto slot = [&](int i) { return sm + 16 * i; };
+  a.totA = slot(0);
+  a.totSA = slot(1);
+  a.totN = reinterpret_cast<unsigned long long *>(slot(2));
+  a.snap_c = slot(3);
+  a.snap_s = slot(4);
+  a.snap_block = reinterpret_cast<unsigned long long *>(slot(5));
+  a.snap_sa = slot(6);
+  a.snap_sb = slot(7);
+  double *c0 = slot(8), *s0 = slot(9);
   a.c0 = c0;
   a.s0 = s0;
+  a.mapA = slot(10);
+  a.mapB = slot(11);
+  a.mapN = reinterpret_cast<unsigned long long *>(slot(12));
+  double *flag = slot(13);
+  a.smapA = slot(14);
+  a.smapB = slot(15);
   a.snap_at = snap_at;
   a.vec_bt = !(((uintptr_t)d_body_bytes | (uintptr_t)d_prompt_tokens) & 15);
   a.vec_c = !((uintptr_t)d_category & 15);
@@ -1243,26 +1287,115 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   CUDA_TRY(p, cudaMemcpyAsync(s0, init_s.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
   // snapshots start as NaN (all-ones bytes), no snapshot block (~0)
   CUDA_TRY(p, cudaMemsetAsync(a.snap_c, 0xFF, 48 * 8, s), "memset snapshots");
+  if (p->world == 1) {
+    {
+      LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+      cudaError_t e = launch_calibrate(a, s);
+      if (e != cudaSuccess) return cuda_fail(p, e, "calibration replay launch");
+    }
+    p->launches += 5;
+    std::vector<double> h(96);
+    CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 96 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    for (uint32_t k = 0; k < n_cats; ++k) {
+      uint64_t nobs;
+      memcpy(&nobs, &h[32 + k], 8);
+      h_final[k].c_hat = h[k];
+      h_final[k].sigma_hat = h[16 + k];
+      h_n_obs[k] = nobs;
+      if (h_snap) {
+        h_snap[k].c_hat = h[48 + k];
+        h_snap[k].sigma_hat = h[64 + k];
+      }
+    }
+    return FP_OK;
+  }
+
+  // world > 1: the stream is sharded in order over the ranks (rank r holds the
+  // r-th contiguous piece). Each rank composes its piece's maps; an all-gather
+  // gives every rank the maps of the ranks before it, hence its start state
+  // and the observations that precede it; the same for the sigma maps.
+  fp_status st = ensure_xch(p);
+  if (st != FP_OK) return st;
+  const int W = p->world, R = p->rank;
+  const double flagv = bad ? 1.0 : 0.0;
+  CUDA_TRY(p, cudaMemcpyAsync(flag, &flagv, 8, cudaMemcpyHostToDevice, s), "H2D flag");
   {
     LaunchTimer lt(p, FP_KERNEL_EVAL, s);
-    cudaError_t e = launch_calibrate(a, s);
+    cudaError_t e = launch_calib_maps(a, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "calibration maps launch");
+  }
+  st = all_gather_bytes(p, slot(10), p->d_xch, 64 * 8, s, "all-gather(calibration maps)");
+  if (st != FP_OK) return st;
+  std::vector<double> g1((size_t)W * 64);
+  CUDA_TRY(p, cudaMemcpyAsync(g1.data(), p->d_xch, g1.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  for (int r = 0; r < W; ++r)
+    if (g1[64 * r + 48] != 0.0) return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
+  auto map_of = [&](const std::vector<double> &g, int r, uint32_t k, bool with_n) {
+    HostAff m;
+    m.a = g[(size_t)r * 64 + k];
+    m.b = g[(size_t)r * 64 + 16 + k];
+    if (with_n) memcpy(&m.n, &g[(size_t)r * 64 + 32 + k], 8);
+    return m;
+  };
+  std::vector<double> c0r(16, 0.0), s0r(16, 0.0);
+  for (uint32_t k = 0; k < n_cats; ++k) {
+    HostAff pre, tot;
+    for (int r = 0; r < W; ++r) {
+      if (r == R) pre = tot;
+      tot = host_compose(tot, map_of(g1, r, k, true));
+    }
+    c0r[k] = std::fma(pre.a, init_c[k], pre.b);
+    a.snap_off[k] = pre.n;
+    h_final[k].c_hat = std::fma(tot.a, init_c[k], tot.b);
+    h_n_obs[k] = tot.n;
+  }
+  CUDA_TRY(p, cudaMemcpyAsync(c0, c0r.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D rank start");
+  {
+    LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+    cudaError_t e = launch_calib_replay(a, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "calibration replay launch");
   }
-  p->launches += 5;
-  std::vector<double> h(128);
-  CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 80 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");
+  st = all_gather_bytes(p, slot(14), p->d_xch, 32 * 8, s, "all-gather(sigma maps)");
+  if (st != FP_OK) return st;
+  std::vector<double> g2((size_t)W * 32);
+  CUDA_TRY(p, cudaMemcpyAsync(g2.data(), p->d_xch, g2.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
   CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
   for (uint32_t k = 0; k < n_cats; ++k) {
-    uint64_t nobs;
-    memcpy(&nobs, &h[32 + k], 8);
-    h_final[k].c_hat = h[k];
-    h_final[k].sigma_hat = h[16 + k];
-    h_n_obs[k] = nobs;
-    if (h_snap) {
-      h_snap[k].c_hat = h[48 + k];
-      h_snap[k].sigma_hat = h[64 + k];
+    HostAff pre, tot;
+    for (int r = 0; r < W; ++r) {
+      if (r == R) pre = tot;
+      tot = host_compose(tot, HostAff{g2[(size_t)r * 32 + k], g2[(size_t)r * 32 + 16 + k], 0});
     }
+    s0r[k] = std::fma(pre.a, init_s[k], pre.b);
+    h_final[k].sigma_hat = std::fma(tot.a, init_s[k], tot.b);
   }
+  CUDA_TRY(p, cudaMemcpyAsync(s0, s0r.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D rank sigma start");
+  {
+    LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+    cudaError_t e = launch_calib_snap(a, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "calibration snapshot launch");
+  }
+  p->launches += 5;
+  st = all_gather_bytes(p, slot(3), p->d_xch, 48 * 8, s, "all-gather(snapshots)");
+  if (st != FP_OK) return st;
+  std::vector<double> g3((size_t)W * 48);
+  CUDA_TRY(p, cudaMemcpyAsync(g3.data(), p->d_xch, g3.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+  if (h_snap)
+    for (uint32_t k = 0; k < n_cats; ++k) {
+      h_snap[k].c_hat = std::nan("");
+      h_snap[k].sigma_hat = std::nan("");
+      for (int r = 0; r < W; ++r) {
+        uint64_t blk;
+        memcpy(&blk, &g3[(size_t)r * 48 + 32 + k], 8);
+        if (blk != ~0ull) {
+          h_snap[k].c_hat = g3[(size_t)r * 48 + k];
+          h_snap[k].sigma_hat = g3[(size_t)r * 48 + 16 + k];
+        }
+      }
+    }
   return FP_OK;
 }
 
@@ -1270,25 +1403,55 @@ fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *
                              uint64_t window_ns, fp_peak_candidate *h_results, fp_peak_candidate *h_best,
                              void *stream) {
   if (!p || !h_best) return FP_ERR_INVALID_ARG;
-  if (n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace");
-  if (n_local > 0xffffffffull) return fail(p, FP_ERR_INVALID_ARG, "n_local must be < 2^32 (u32 window counters)");
+  // checks every rank takes identically come first; rank-specific ones are
+  // exchanged below so that all ranks fail together (no rank left waiting)
   if (window_ns == 0) return fail(p, FP_ERR_INVALID_ARG, "window_ns must be > 0");
-  if (!d_len || !d_arrival_ns || is_host_pointer(d_len) || is_host_pointer(d_arrival_ns))
-    return fail(p, FP_ERR_INVALID_ARG, "length and arrival columns must be device memory");
-  if (((uintptr_t)d_len & 3) || ((uintptr_t)d_arrival_ns & 7))
-    return fail(p, FP_ERR_INVALID_ARG, "misaligned column");
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
-  // windows from the first and last request's arrival (the trace is in arrival order)
   uint64_t *ends = reinterpret_cast<uint64_t *>(p->h_small);
-  CUDA_TRY(p, cudaMemcpyAsync(ends, d_arrival_ns, 8, cudaMemcpyDeviceToHost, s), "D2H first arrival");
-  CUDA_TRY(p, cudaMemcpyAsync(ends + 1, d_arrival_ns + (n_local - 1), 8, cudaMemcpyDeviceToHost, s),
-           "D2H last arrival");
-  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
-  const uint64_t first = ends[0], last = ends[1];
-  if (first > last) return fail(p, FP_ERR_INVALID_ARG, "arrivals not in order (first > last)");
-  if (last > ~0ull - window_ns) return fail(p, FP_ERR_INVALID_ARG, "arrival + window_ns overflows");
-  const uint64_t n_twin = last / window_ns + 1;
+  uint64_t bad = 0;
+  if (n_local && (!d_len || !d_arrival_ns || is_host_pointer(d_len) || is_host_pointer(d_arrival_ns)))
+    bad = 1;
+  else if (n_local && (((uintptr_t)d_len & 3) || ((uintptr_t)d_arrival_ns & 7)))
+    bad = 2;
+  uint64_t first = 0, last = 0;
+  if (!bad && n_local) {
+    CUDA_TRY(p, cudaMemcpyAsync(ends, d_arrival_ns, 8, cudaMemcpyDeviceToHost, s), "D2H first arrival");
+    CUDA_TRY(p, cudaMemcpyAsync(ends + 1, d_arrival_ns + (n_local - 1), 8, cudaMemcpyDeviceToHost, s),
+             "D2H last arrival");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    first = ends[0];
+    last = ends[1];
+    if (first > last) bad = 3;
+  }
+  // global extent: every rank's (bad, n_local, last)
+  uint64_t n_total = n_local, last_all = last, bad_all = bad;
+  if (p->world > 1) {
+    fp_status st = ensure_xch(p);
+    if (st != FP_OK) return st;
+    const uint64_t mine[4] = {bad, n_local, last, 0};
+    CUDA_TRY(p, cudaMemcpyAsync(p->d_xch, mine, 32, cudaMemcpyHostToDevice, s), "H2D exchange");
+    st = all_gather_bytes(p, p->d_xch, p->d_xch + 4, 32, s, "all-gather(peak extents)");
+    if (st != FP_OK) return st;
+    std::vector<uint64_t> all(4 * (size_t)p->world);
+    CUDA_TRY(p, cudaMemcpyAsync(all.data(), p->d_xch + 4, all.size() * 8, cudaMemcpyDeviceToHost, s), "D2H");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    n_total = 0;
+    last_all = 0;
+    bad_all = 0;
+    for (int r = 0; r < p->world; ++r) {
+      bad_all = std::max<uint64_t>(bad_all, all[4 * r]);
+      n_total += all[4 * r + 1];
+      if (all[4 * r + 1]) last_all = std::max<uint64_t>(last_all, all[4 * r + 2]);
+    }
+  }
+  if (bad_all == 1) return fail(p, FP_ERR_INVALID_ARG, "length and arrival columns must be device memory");
+  if (bad_all == 2) return fail(p, FP_ERR_INVALID_ARG, "misaligned column");
+  if (bad_all == 3) return fail(p, FP_ERR_INVALID_ARG, "arrivals not in order (first > last)");
+  if (n_total == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace");
+  if (n_total > 0xffffffffull) return fail(p, FP_ERR_INVALID_ARG, "trace must be < 2^32 requests (u32 window counters)");
+  if (last_all > ~0ull - window_ns) return fail(p, FP_ERR_INVALID_ARG, "arrival + window_ns overflows");
+  const uint64_t n_twin = last_all / window_ns + 1;
   const size_t hbytes = (size_t)n_twin * p->nbins * 4;
   if (n_twin > (1ull << 26) || hbytes > (4ull << 30))
     return fail(p, FP_ERR_INVALID_ARG, "%llu windows x %u bins is too many", (unsigned long long)n_twin, p->nbins);
@@ -1357,10 +1520,21 @@ fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *
   if (peak_smem_bytes(pa) > 200 * 1024) return fail(p, FP_ERR_CONFIG, "peak LUT too large");
   {
     LaunchTimer lt(p, FP_KERNEL_TRACE, s);
-    cudaError_t e = launch_peak_hist(pa, p->sm_count, s);
+    cudaError_t e = n_local ? launch_peak_hist(pa, p->sm_count, s) : cudaSuccess;
     if (e != cudaSuccess) return cuda_fail(p, e, "peak histogram launch");
   }
-  p->launches += pa.check_order ? 4 : 3;
+  if (n_local) p->launches += pa.check_order ? 3 : 2;
+  if (p->world > 1) {
+    // global windows: sum the per-rank 2-D histograms (and order-check flags)
+    fp_status st = all_reduce_u32(p, hist2d, zbytes / 4, s, "all-reduce(window histogram)");
+    if (st != FP_OK) return st;
+  }
+  {
+    LaunchTimer lt(p, FP_KERNEL_TRACE, s);
+    cudaError_t e = launch_peak_scan(pa, p->sm_count, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "peak scan launch");
+  }
+  ++p->launches;
   EvalArgs ea = p->ea;
   ea.colmax_pk = colmax;
   ea.pairmax_pk = pairmax;
