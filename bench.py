@@ -318,9 +318,11 @@ def run_ours(args, cfg):
     d_dec = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step(lengths):
-        # sweep_thresholds -> best_split -> route_batch(model 0's best split), one ABI call
-        return fp.sweep_and_route(plan, lengths, cfg.rate_rps, route_model=0, decision=d_dec, stream=stream)
+    def step(lengths, want_best=False):
+        # sweep_thresholds -> per-model argmin -> route_batch(model 0's best split), one ABI call;
+        # the device-timed steps leave the best records on the device (asynchronous call)
+        return fp.sweep_and_route(plan, lengths, cfg.rate_rps, route_model=0, decision=d_dec, stream=stream,
+                                  want_best=want_best)
 
     def barrier():
         if world > 1:
@@ -343,6 +345,7 @@ def run_ours(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
+    best = fp.best_split(plan)                  # the records of the last timed step
     per_step = sorted([e0.elapsed_time(ev[0])] + [ev[k - 1].elapsed_time(ev[k]) for k in range(1, args.steps)])
     pct = lambda q: per_step[min(len(per_step) - 1, int(q * len(per_step)))]   # noqa: E731
     launches = fp.fp_kernel_launches(plan) - l0
@@ -377,11 +380,11 @@ def run_ours(args, cfg):
     e2e = None
     if args.e2e_steps > 0:
         h_len = d_len.cpu().pin_memory()
-        step(h_len)
+        step(h_len, want_best=True)
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            step(h_len)
+            step(h_len, want_best=True)
         barrier()
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if world > 1:
@@ -437,6 +440,9 @@ def run_ours(args, cfg):
             "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
             "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic (seeded Philox MIX trace, generated on device; not timed)",
+            "step": "sweep_and_route: K1 trace pass (+bins) -> K3 sweep + per-model argmin -> device split pick "
+                    "-> K4b routing pass, stream-ordered with no host round trip; the best records stay on the "
+                    "device and are read once after the timed loop (e2e reads them every step)",
             "config": _workload(cfg, n, world),
             "candidates_per_s": cand_per_s,
             "candidates_per_s_step": cfg.n_candidates() / (ms_step / 1e3),

@@ -230,8 +230,14 @@ fp_status best_split(fp_plan *plan, fp_candidate *h_best);
  * global counts into h_counts if non-NULL). A HOST trace crosses PCIe once:
  * it is copied into a plan-owned device buffer chunk by chunk while the trace
  * pass consumes each chunk, and the routing pass reads the device copy.
- * Synchronizes. Errors: as the three calls; FP_ERR_STATE if route_model has
- * no feasible split (h_best is still written). */
+ * With |E| < 256 (u8 LUT) the trace pass also writes each request's 1-B bin
+ * and the split is picked and applied on the device (no host round trip).
+ * Synchronizes -- except in that bin mode with a device trace when h_best and
+ * h_counts are both NULL: then the call is stream-ordered and asynchronous,
+ * the records stay on the device for a later best_split, and a model without
+ * a feasible split leaves d_decision untouched (best_split shows it).
+ * Errors: as the three calls; FP_ERR_STATE if route_model has no feasible
+ * split (h_best is still written). */
 fp_status sweep_and_route(fp_plan *plan, const uint32_t *len, uint64_t n_local, double rate_rps,
                           uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
                           fp_route_counts *h_counts, void *stream);

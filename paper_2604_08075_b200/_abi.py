@@ -411,14 +411,21 @@ def fp_kernel_time_reset(plan):
     _check(lib.fp_kernel_time_reset(plan.handle), plan)
 
 
-def sweep_and_route(plan, lengths, rate_rps, route_model=0, decision=None, stream=None):
-    """Whole workflow in one call; returns (best records [n_models], route counts dict)."""
+def sweep_and_route(plan, lengths, rate_rps, route_model=0, decision=None, stream=None, want_best=True):
+    """Whole workflow in one call; returns (best records [n_models], route counts dict).
+    want_best=False (device trace, bin mode): asynchronous, returns (None, None);
+    read the records later with best_split()."""
     ptr, n, _, keep = _trace_ptr(lengths)
     dptr = None
     if decision is not None:
         if decision.numel() < n or not decision.is_cuda:
             raise ValueError("decision must be a CUDA uint8 tensor with >= n elements")
         dptr = decision.data_ptr()
+    if not want_best:
+        _check(lib.sweep_and_route(plan.handle, ptr, n, float(rate_rps), route_model, dptr, None, None,
+                                   _stream_handle(stream, plan.device)), plan)
+        del keep
+        return None, None
     best = np.zeros(plan.n_models, dtype=FP_CANDIDATE)
     counts = fp_route_counts()
     _check(lib.sweep_and_route(plan.handle, ptr, n, float(rate_rps), route_model, dptr, best.ctypes.data,

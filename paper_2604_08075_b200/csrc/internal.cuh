@@ -70,8 +70,9 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
 
 // K4b: decisions from per-request bins (sweep_and_route): with iB, iCS, iCL
 // the indices in E of B, C_S, C_L, L <= e_j <=> bin <= j.
-cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, uint32_t iB, uint32_t iCS,
-                              uint32_t iCL, uint32_t n_bins_max, int grid, int block, cudaStream_t s);
+cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
+                              int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,
+                              uint32_t *route, int grid, int block, cudaStream_t s);
 cudaError_t route_occupancy(int block, int *per_sm);
 
 // ---- K3: candidate evaluation + argmin ---------------------------------------

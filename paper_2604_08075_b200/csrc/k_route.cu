@@ -390,9 +390,57 @@ __device__ __forceinline__ uint32_t dec_word_swar(uint32_t w, const SwarK &k) {
   return (gB >> 7) + (gS >> 5) + (gL >> 7) * 9u;     // a + 4 b + 9 c per byte
 }
 
+// The split to route with, picked on the device so that the step needs no
+// host round trip between the sweep and the routing pass: per-model argmin
+// over the ranks' best records (feasible, min cost, ties to the lowest index:
+// fp_merge_best's rule), then the edge indices of its B, C_S, C_L
+// (#{e in E : e < v}, one ballot per 32 edges). out = {iB, iCS, iCL, ok}.
+__global__ void k_pick_route(const fp_candidate *recs, int ranks, uint32_t n_models, uint32_t m,
+                             const uint32_t *edges, uint32_t n_edges, uint32_t *out) {
+  const int lane = threadIdx.x;
+  bool ok = false;
+  double cost = 0.0;
+  uint32_t idx = 0xffffffffu;
+  int who = lane;
+  if (lane < ranks) {
+    const fp_candidate &c = recs[(size_t)lane * n_models + m];
+    ok = (c.flags & FP_CAND_FEASIBLE) != 0;
+    cost = c.cost_dual;
+    idx = c.index;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const bool ok2 = __shfl_down_sync(0xffffffffu, ok, o);
+    const double cost2 = __shfl_down_sync(0xffffffffu, cost, o);
+    const uint32_t idx2 = __shfl_down_sync(0xffffffffu, idx, o);
+    const int who2 = __shfl_down_sync(0xffffffffu, who, o);
+    if (lane + o < 32 && ok2 && (!ok || cost2 < cost || (cost2 == cost && idx2 < idx))) {
+      ok = true; cost = cost2; idx = idx2; who = who2;
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  who = __shfl_sync(0xffffffffu, who, 0);
+  if (!ok) {
+    if (lane == 0) out[3] = 0u;
+    return;
+  }
+  const fp_candidate &c = recs[(size_t)who * n_models + m];
+  const uint32_t vb = c.b_short, vs = c.c_short, vl = c.c_long;
+  uint32_t nb = 0, ns = 0, nl = 0;
+  for (uint32_t base = 0; base < n_edges; base += 32) {
+    const uint32_t e = base + lane < n_edges ? edges[base + lane] : 0xffffffffu;
+    nb += __popc(__ballot_sync(0xffffffffu, e < vb));
+    ns += __popc(__ballot_sync(0xffffffffu, e < vs));
+    nl += __popc(__ballot_sync(0xffffffffu, e < vl));
+  }
+  if (lane == 0) { out[0] = nb; out[1] = ns; out[2] = nl; out[3] = 1u; }
+}
+
 template <bool VEC, bool SWAR>
 __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__ bins, uint8_t *__restrict__ dec,
-                                                      uint64_t n, uint32_t iB, uint32_t iCS, uint32_t iCL) {
+                                                      uint64_t n, const uint32_t *__restrict__ route) {
+  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
+  if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
+  const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
   const SwarK sk{(0x7Fu - (iB < 0x7Fu ? iB : 0x7Fu)) * 0x01010101u, (0x7Fu - (iCS < 0x7Fu ? iCS : 0x7Fu)) * 0x01010101u,
                  (0x7Fu - (iCL < 0x7Fu ? iCL : 0x7Fu)) * 0x01010101u};
   auto word = [&](uint32_t w) { return SWAR ? dec_word_swar(w, sk) : dec_word(w, iB, iCS, iCL); };
@@ -431,17 +479,20 @@ __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__
 
 }  // namespace
 
-cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, uint32_t iB, uint32_t iCS,
-                              uint32_t iCL, uint32_t n_bins_max, int grid, int block, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
+cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
+                              int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,
+                              uint32_t *route, int grid, int block, cudaStream_t s) {
+  k_pick_route<<<1, 32, 0, s>>>(recs, ranks, n_models, model, edges, n_edges, route);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || n == 0) return e;
   const bool vec = ((reinterpret_cast<uintptr_t>(bins) ^ reinterpret_cast<uintptr_t>(decision)) & 15u) == 0;
   const uint64_t need = (n / (vec ? 16 : 1) + block - 1) / block;
   const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
   // SWAR needs every bin < 128: bins go up to |E|, and j = iB, iCS, iCL < |E|
-  const bool swar = n_bins_max < 128;
-  if (vec && swar) k4_route_bins<true, true><<<g, block, 0, s>>>(bins, decision, n, iB, iCS, iCL);
-  else if (vec) k4_route_bins<true, false><<<g, block, 0, s>>>(bins, decision, n, iB, iCS, iCL);
-  else k4_route_bins<false, false><<<g, block, 0, s>>>(bins, decision, n, iB, iCS, iCL);
+  const bool swar = n_edges < 128;
+  if (vec && swar) k4_route_bins<true, true><<<g, block, 0, s>>>(bins, decision, n, route);
+  else if (vec) k4_route_bins<true, false><<<g, block, 0, s>>>(bins, decision, n, route);
+  else k4_route_bins<false, false><<<g, block, 0, s>>>(bins, decision, n, route);
   return cudaGetLastError();
 }
 

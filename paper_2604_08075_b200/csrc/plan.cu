@@ -906,23 +906,28 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   }
   fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident, nullptr, bins);
   if (st != FP_OK) return st;
+  if (bin_pass && d_decision && n_local) {
+    // pick the split and route on the device: no host round trip in the step
+    const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
+    LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
+    cudaError_t e = launch_route_bins(bins, d_decision, n_local, p->d_best, ranks, (uint32_t)p->models.size(),
+                                      route_model, p->ta.edges, (uint32_t)p->edges.size(),
+                                      reinterpret_cast<uint32_t *>(p->d_rcounts), p->k4_grid, p->k4_block, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
+    p->launches += 2;
+  }
+  if (bin_pass && !h_best && !h_counts && !is_host_pointer(len)) {
+    p->last_stream = s;                     // asynchronous: the records stay on the device
+    return FP_OK;
+  }
   std::vector<fp_candidate> best(p->models.size());
-  st = best_split(p, best.data());
+  st = best_split(p, best.data());          // D2H of the records, after the routing pass
   if (st != FP_OK) return st;
   if (h_best) memcpy(h_best, best.data(), best.size() * sizeof(fp_candidate));
   const fp_candidate &b = best[route_model];
   if (!(b.flags & FP_CAND_FEASIBLE))
     return fail(p, FP_ERR_STATE, "model %u has no feasible split to route with", route_model);
   if (!bin_pass) return route_batch(p, src, n_local, b.b_short, b.c_short, b.c_long, d_decision, h_counts, stream);
-  if (d_decision && n_local) {
-    const uint32_t iB = index_of(p->edges, b.b_short), iCS = index_of(p->edges, b.c_short);
-    const uint32_t iCL = index_of(p->edges, b.c_long);
-    LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
-    cudaError_t e =
-        launch_route_bins(bins, d_decision, n_local, iB, iCS, iCL, p->nbins - 1, p->k4_grid, p->k4_block, s);
-    if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
-    ++p->launches;
-  }
   if (h_counts) {
     h_counts->n_short = b.n_short;
     h_counts->n_long = b.n_long;
@@ -930,7 +935,6 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     h_counts->mass_short = b.mass_short;
     h_counts->mass_long = b.mass_long;
   }
-  CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
   p->last_stream = s;
   return FP_OK;
 }

@@ -277,3 +277,23 @@ def test_sweep_and_route_bin_pass_wide_edges():
     b = obest[0]
     odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
     assert np.array_equal(dec.cpu().numpy(), odec)
+
+
+@pytest.mark.parametrize("name,model", [("C5", 3), ("C4", 0), ("C3", 2)])
+def test_sweep_and_route_async_device_pick(name, model):
+    """Asynchronous step (no host outputs): the split is picked and applied on
+    the device; decisions and the later best_split equal the oracle's."""
+    cfg = configs.CONFIGS[name]().with_n(800_001)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    dec = torch.zeros(L.size, dtype=torch.uint8, device="cuda")
+    d = _dev(L)
+    for _ in range(2):                       # back-to-back steps on one stream
+        assert fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=model, decision=dec, want_best=False) == \
+            (None, None)
+    best = fp.best_split(plan)
+    _, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[model]
+    odec, _ = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec.cpu().numpy(), odec)
