@@ -93,6 +93,7 @@ struct EvalArgs {
   const unsigned long long *deploy;     // [m][g][3] tp, gpus_per_instance, weights
   const uint32_t *windows;              // [n_windows]
   const double *mu;                     // [m][g][w]
+  const unsigned long long *cap_nseq = nullptr;  // [m][g][w] N_seq (Eq. 2), computed once per plan
   double rate, hours;
   uint64_t per_model;                   // candidates per model
   uint64_t cand_first, cand_count;      // this rank's slice
@@ -100,6 +101,11 @@ struct EvalArgs {
   fp_candidate *best_out;               // [n_models] (this rank's)
   BlockBest *block_best;                // [n_models][grid_x]
   unsigned int *done;                   // [n_models] last-block-done counters (self-resetting)
+  // sweep_and_route (one rank's grid is the whole grid): the last block of
+  // model route_model also writes {iB, iCS, iCL, ok} of its best split
+  const uint32_t *edges = nullptr;
+  uint32_t n_edges = 0, route_model = 0;
+  uint32_t *route_out = nullptr;
   // NEXT-2 three pools (replicated grid): pairs (i | j << 16) of B-grid indices
   const uint32_t *pairs = nullptr;
   uint32_t n_pairs = 0;
@@ -119,6 +125,7 @@ struct EvalArgs {
   unsigned int *done_pk = nullptr;
 };
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
+cudaError_t launch_capacity(const EvalArgs &a, unsigned long long *cap, cudaStream_t s);  // fills cap_nseq
 cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
 size_t eval_smem_bytes(const EvalArgs &a, int block);

@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   __shared__ unsigned long long warp_tot[32];
   __shared__ double red_c[32];
   __shared__ uint32_t red_i[32], red_v[32];
+  __shared__ uint32_t route_v[4];
   __shared__ bool is_last;
   const uint32_t m = blockIdx.y;
 
@@ -263,13 +264,9 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
     sh.cnt_le[j] = a.hist_cnt[j];
     sh.mass_le[j] = a.hist_mass[j];
   }
-  const uint32_t *arch = a.model_arch + 4 * m;
   for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
-    const uint32_t g = j / a.n_windows, w = j % a.n_windows;
-    const unsigned long long *dp = a.deploy + ((uint64_t)m * a.n_gpus + g) * 3;
-    const unsigned long long budget = kv_budget(a.gpu_u64 + 4 * g, dp[2]);
-    sh.nseq[j] = max_seqs(budget, (uint32_t)dp[0], arch, a.windows[w]);
-    sh.mu[j] = a.mu[((uint64_t)m * a.n_gpus + g) * a.n_windows + w];
+    sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    sh.mu[j] = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
   }
   __syncthreads();
   block_scan_inclusive(sh.cnt_le, a.nbins, warp_tot);
@@ -349,8 +346,38 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
     } else {
       a.best_out[m] = c;
       a.done[m] = 0;  // self-reset for the next launch / graph replay
+      if (a.route_out && m == a.route_model) {
+        route_v[0] = c.b_short; route_v[1] = c.c_short; route_v[2] = c.c_long;
+        route_v[3] = (c.flags & FP_CAND_FEASIBLE) ? 1u : 0u;
+      }
     }
   }
+  if constexpr (!POOL3) {
+    // the split to route with: edge indices #{e in E : e < v} of its B, C_S, C_L
+    if (a.route_out && m == a.route_model) {
+      __syncthreads();
+      if (w == 0) {
+        uint32_t nb = 0, ns = 0, nl = 0;
+        for (uint32_t base = 0; base < a.n_edges; base += 32) {
+          const uint32_t e = base + lane < a.n_edges ? a.edges[base + lane] : 0xffffffffu;
+          nb += __popc(__ballot_sync(0xffffffffu, e < route_v[0]));
+          ns += __popc(__ballot_sync(0xffffffffu, e < route_v[1]));
+          nl += __popc(__ballot_sync(0xffffffffu, e < route_v[2]));
+        }
+        if (lane == 0) *reinterpret_cast<uint4 *>(a.route_out) = make_uint4(nb, ns, nl, route_v[3]);
+      }
+    }
+  }
+}
+
+// N_seq (Eq. 2) for every (model, GPU, window): plan data only, computed once
+__global__ void k_capacity(EvalArgs a, unsigned long long *cap) {
+  const uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= (uint64_t)a.n_models * a.n_gpus * a.n_windows) return;
+  const uint32_t w = (uint32_t)(j % a.n_windows), g = (uint32_t)(j / a.n_windows % a.n_gpus);
+  const uint32_t m = (uint32_t)(j / ((uint64_t)a.n_windows * a.n_gpus));
+  const unsigned long long *dp = a.deploy + ((uint64_t)m * a.n_gpus + g) * 3;
+  cap[j] = max_seqs(kv_budget(a.gpu_u64 + 4 * g, dp[2]), (uint32_t)dp[0], a.model_arch + 4 * m, a.windows[w]);
 }
 
 // NEXT-4: peak-window sizing. Same grid and index decomposition
@@ -410,12 +437,9 @@ __global__ void __launch_bounds__(256) k3_peak(EvalArgs a) {
   sh.mass_le = nullptr;
   sh.nseq = reinterpret_cast<unsigned long long *>(smem);
   sh.mu = reinterpret_cast<double *>(sh.nseq + (size_t)a.n_gpus * a.n_windows);
-  const uint32_t *arch = a.model_arch + 4 * m;
   for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
-    const uint32_t g = j / a.n_windows, w = j % a.n_windows;
-    const unsigned long long *dp = a.deploy + ((uint64_t)m * a.n_gpus + g) * 3;
-    sh.nseq[j] = max_seqs(kv_budget(a.gpu_u64 + 4 * g, dp[2]), (uint32_t)dp[0], arch, a.windows[w]);
-    sh.mu[j] = a.mu[((uint64_t)m * a.n_gpus + g) * a.n_windows + w];
+    sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    sh.mu[j] = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
   }
   __syncthreads();
   const uint64_t lo = (uint64_t)m * a.per_model, hi = lo + a.per_model;
@@ -489,6 +513,12 @@ cudaError_t eval_prepare() {
   cudaError_t e = cudaFuncSetAttribute(k3_eval<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k3_eval<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+cudaError_t launch_capacity(const EvalArgs &a, unsigned long long *cap, cudaStream_t s) {
+  const uint64_t n = (uint64_t)a.n_models * a.n_gpus * a.n_windows;
+  k_capacity<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, cap);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {

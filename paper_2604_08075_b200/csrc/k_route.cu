@@ -482,7 +482,8 @@ __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__
 cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
                               int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,
                               uint32_t *route, int grid, int block, cudaStream_t s) {
-  k_pick_route<<<1, 32, 0, s>>>(recs, ranks, n_models, model, edges, n_edges, route);
+  // recs == NULL: K3 already wrote route (one rank's grid is the whole grid)
+  if (recs) k_pick_route<<<1, 32, 0, s>>>(recs, ranks, n_models, model, edges, n_edges, route);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || n == 0) return e;
   const bool vec = ((reinterpret_cast<uintptr_t>(bins) ^ reinterpret_cast<uintptr_t>(decision)) & 15u) == 0;

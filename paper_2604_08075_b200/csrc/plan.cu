@@ -98,13 +98,14 @@ struct fp_plan {
   TraceArgs ta{};
   EvalArgs ea{};
   unsigned long long *d_hist = nullptr;    // [2][nbins]
-  unsigned long long *d_rcounts = nullptr; // [8]: route counts [5], mis-routes [2]
+  unsigned long long *d_rcounts = nullptr; // [8]: route counts [5], mis-routes [2] (or the picked split)
+  unsigned long long *d_cap = nullptr;     // [M][G][W] N_seq
   double *d_calib = nullptr;               // [256][2] estimator snapshot
   fp_candidate *d_best = nullptr;          // [world][n_models]
   fp_candidate *d_results = nullptr;       // [cand_count] (lazy)
   BlockBest *d_block_best = nullptr;
   unsigned int *d_done = nullptr;
-  int k3_grid_x = 1;
+  int k3_grid_x = 1, k3_block = 256;
   // host streaming
   uint32_t *d_stage[2] = {nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;
@@ -308,6 +309,11 @@ fp_status build_tables(fp_plan *p) {
   return FP_OK;
 }
 
+int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 // Copy every table into one device blob and fill ta / ea pointers.
 fp_status upload(fp_plan *p) {
   const uint32_t G = (uint32_t)p->gpus.size(), M = (uint32_t)p->models.size();
@@ -434,6 +440,16 @@ fp_status upload(fp_plan *p) {
   ea.cand_first = p->cand_first;
   ea.cand_count = p->cand_count;
   ea.best_out = p->d_best + (size_t)((p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->rank : 0) * M;
+  ea.edges = ta.edges;
+  ea.n_edges = ta.n_edges;
+  // capacity table N_seq[m][g][w] (Eq. 2): plan data only, computed once here
+  CUDA_TRY(p, cudaMalloc(&p->d_cap, (size_t)M * G * W * 8), "cudaMalloc capacity table");
+  {
+    cudaError_t e = launch_capacity(ea, p->d_cap, 0);
+    if (e != cudaSuccess) return cuda_fail(p, e, "capacity table launch");
+    CUDA_TRY(p, cudaDeviceSynchronize(), "capacity table");
+  }
+  ea.cap_nseq = p->d_cap;
 
   // K3 grid: enough blocks for the largest per-model part of this rank's slice
   uint64_t widest = 0;
@@ -446,14 +462,19 @@ fp_status upload(fp_plan *p) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
   const uint64_t cap = std::max<uint64_t>(1, (uint64_t)sms * 8 / M);
-  p->k3_grid_x = (int)std::min<uint64_t>(cap, std::max<uint64_t>(1, (widest + 255) / 256));
+  // block size: small grids (the paper's) are latency-bound -> more, smaller blocks
+  p->k3_block = env_int("FP_K3_BLOCK", widest <= (uint64_t)sms * 128 ? 128 : 256);
+  if (p->k3_block < 32 || p->k3_block > 256 || (p->k3_block & 31))
+    return fail(p, FP_ERR_CONFIG, "FP_K3_BLOCK must be a multiple of 32 in [32, 256]");
+  p->k3_grid_x = (int)std::min<uint64_t>(cap * (256 / p->k3_block),
+                                         std::max<uint64_t>(1, (widest + p->k3_block - 1) / p->k3_block));
   if (p->k3_grid_x > 65535 * 64) return fail(p, FP_ERR_CONFIG, "candidate grid too large for one launch");
   CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * p->k3_grid_x * sizeof(BlockBest)), "cudaMalloc block_best");
   CUDA_TRY(p, cudaMalloc(&p->d_done, M * sizeof(unsigned int)), "cudaMalloc done");
   CUDA_TRY(p, cudaMemset(p->d_done, 0, M * sizeof(unsigned int)), "memset done");
   ea.block_best = p->d_block_best;
   ea.done = p->d_done;
-  p->k3_smem = eval_smem_bytes(ea, 256);
+  p->k3_smem = eval_smem_bytes(ea, p->k3_block);
   if (p->k3_smem > 190 * 1024)
     return fail(p, FP_ERR_CONFIG, "histogram + capacity table need %zu B of shared memory", p->k3_smem);
   return FP_OK;
@@ -462,10 +483,6 @@ fp_status upload(fp_plan *p) {
 fp_status configure_launch(fp_plan *p) {
   CUDA_TRY(p, cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, p->device), "attr");
   // tuning knobs (measurement only; defaults are the measured best on B200)
-  auto env_int = [](const char *name, int dflt) {
-    const char *v = getenv(name);
-    return (v && *v) ? atoi(v) : dflt;
-  };
   p->ta.flush_iters = 1;  // set per launch by launch_trace's smem config
   p->k1_block = env_int("FP_K1_BLOCK", 512);
   if (p->k1_block < 64 || p->k1_block > 512 || (p->k1_block & 31))
@@ -729,6 +746,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_blob);
     cudaFree(p->d_hist);
     cudaFree(p->d_rcounts);
+    cudaFree(p->d_cap);
     cudaFree(p->d_best);
     cudaFree(p->d_results);
     cudaFree(p->d_block_best);
@@ -850,7 +868,8 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
 namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident,
-                     const TraceArgs *raw = nullptr, uint8_t *bins = nullptr);
+                     const TraceArgs *raw = nullptr, uint8_t *bins = nullptr, uint32_t *route_out = nullptr,
+                     uint32_t route_model = 0);
 }
 
 fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
@@ -904,17 +923,23 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     resident = p->d_resident;
     src = resident;
   }
-  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident, nullptr, bins);
+  // pick the split and route on the device: no host round trip in the step.
+  // With one rank's grid = the whole grid, K3's last block of route_model
+  // writes the split's edge indices; otherwise a one-warp kernel merges the
+  // ranks' records after the all-gather.
+  const bool routing = bin_pass && d_decision && n_local;
+  const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
+  uint32_t *route = reinterpret_cast<uint32_t *>(p->d_rcounts);
+  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident, nullptr, bins,
+                            routing && ranks == 1 ? route : nullptr, route_model);
   if (st != FP_OK) return st;
-  if (bin_pass && d_decision && n_local) {
-    // pick the split and route on the device: no host round trip in the step
-    const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
+  if (routing) {
     LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
-    cudaError_t e = launch_route_bins(bins, d_decision, n_local, p->d_best, ranks, (uint32_t)p->models.size(),
-                                      route_model, p->ta.edges, (uint32_t)p->edges.size(),
-                                      reinterpret_cast<uint32_t *>(p->d_rcounts), p->k4_grid, p->k4_block, s);
+    cudaError_t e = launch_route_bins(bins, d_decision, n_local, ranks == 1 ? nullptr : p->d_best, ranks,
+                                      (uint32_t)p->models.size(), route_model, p->ta.edges,
+                                      (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
-    p->launches += 2;
+    p->launches += ranks == 1 ? 1 : 2;
   }
   if (bin_pass && !h_best && !h_counts && !is_host_pointer(len)) {
     p->last_stream = s;                     // asynchronous: the records stay on the device
@@ -1058,7 +1083,7 @@ fp_status route_batch_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, c
 namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident, const TraceArgs *raw,
-                     uint8_t *bins) {
+                     uint8_t *bins, uint32_t *route_out, uint32_t route_model) {
   if (!p) return FP_ERR_INVALID_ARG;
   if (n_local && !d_len && !raw) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
@@ -1099,10 +1124,12 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   EvalArgs ea = p->ea;
   ea.rate = rate_rps;
   ea.results = h_results ? p->d_results : nullptr;
+  ea.route_out = route_out;
+  ea.route_model = route_model;
   cudaError_t e;
   {
     LaunchTimer lt(p, FP_KERNEL_EVAL, s);
-    e = launch_eval(ea, p->k3_grid_x, 256, p->k3_smem, s);
+    e = launch_eval(ea, p->k3_grid_x, p->k3_block, p->k3_smem, s);
   }
   if (e != cudaSuccess) return cuda_fail(p, e, "candidate evaluation launch");
   ++p->launches;
