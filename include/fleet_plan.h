@@ -101,6 +101,9 @@ typedef struct fp_grid {
 #define FP_FLAG_REPLICATED_GRID 0x2u /* world > 1: every rank evaluates all candidates */
 #define FP_FLAG_KERNEL_TIMING 0x4u   /* record CUDA events around every kernel launch   */
 #define FP_FLAG_CHECK_ORDER 0x8u     /* sweep_peak_windows: verify arrival order (8 B/req) */
+#define FP_FLAG_COLLECTIVES 0x10u    /* run the cross-rank steps even when world == 1
+                                        (a one-rank NCCL communicator or the hooks): the
+                                        multi-rank code path on a single GPU, for tests  */
 
 typedef struct fp_plan_desc {
   uint32_t abi_version;           /* FP_ABI_VERSION                                 */
@@ -119,7 +122,8 @@ typedef struct fp_plan_desc {
   int32_t device;                 /* CUDA device ordinal for this rank               */
   int32_t rank, world;            /* 0 <= rank < world                               */
   const void *nccl_unique_id;     /* 128-byte ncclUniqueId, same on all ranks; used
-                                     iff world > 1 and collectives == NULL           */
+                                     iff (world > 1 or FP_FLAG_COLLECTIVES) and
+                                     collectives == NULL                             */
   const struct fp_collectives *collectives; /* optional host-side collectives that
                                      replace NCCL when world > 1 (NULL = NCCL)        */
 } fp_plan_desc;

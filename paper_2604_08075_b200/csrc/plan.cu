@@ -85,6 +85,7 @@ struct fp_plan {
   double hours = 8760.0;
   uint32_t flags = 0;
   int device = 0, rank = 0, world = 1;
+  bool dist = false;                       // cross-rank steps run (world > 1 or FP_FLAG_COLLECTIVES)
   // derived
   std::vector<uint32_t> edges;
   uint32_t shift = 0, lut_cells = 0, lut_u8 = 0, max_edge = 0, nbins = 0;
@@ -203,8 +204,8 @@ fp_status validate_and_copy(fp_plan *p, const fp_plan_desc *d) {
     return fail(p, FP_ERR_CONFIG, "empty models/gpus/grid/windows");
   if (d->world < 1 || d->rank < 0 || d->rank >= d->world)
     return fail(p, FP_ERR_CONFIG, "rank %d world %d", d->rank, d->world);
-  if (d->world > 1 && !d->nccl_unique_id && !d->collectives)
-    return fail(p, FP_ERR_CONFIG, "world > 1 needs nccl_unique_id or collectives");
+  if ((d->world > 1 || (d->flags & FP_FLAG_COLLECTIVES)) && !d->nccl_unique_id && !d->collectives)
+    return fail(p, FP_ERR_CONFIG, "world > 1 (or FP_FLAG_COLLECTIVES) needs nccl_unique_id or collectives");
   if (d->collectives && (!d->collectives->allreduce_sum_u64 || !d->collectives->allgather_bytes))
     return fail(p, FP_ERR_CONFIG, "collectives hooks must both be set");
   if (d->collectives) {
@@ -226,6 +227,7 @@ fp_status validate_and_copy(fp_plan *p, const fp_plan_desc *d) {
   p->device = d->device;
   p->rank = d->rank;
   p->world = d->world;
+  p->dist = d->world > 1 || (d->flags & FP_FLAG_COLLECTIVES);
 
   for (auto &m : p->models) {
     if (!m.n_layers || !m.n_kv_heads || !m.head_dim ||
@@ -300,7 +302,7 @@ fp_status build_tables(fp_plan *p) {
   p->per_model = (uint64_t)p->gpus.size() * p->cl.size() * p->n_cs_eff * p->b.size();
   p->n_cand = p->per_model * p->models.size();
   if (p->n_cand >= 0xffffffffull) return fail(p, FP_ERR_CONFIG, "grid has >= 2^32 - 1 candidates");
-  if (p->flags & FP_FLAG_REPLICATED_GRID || p->world == 1) {
+  if (p->flags & FP_FLAG_REPLICATED_GRID || !p->dist) {
     p->cand_first = 0;
     p->cand_count = p->n_cand;
   } else {
@@ -439,7 +441,7 @@ fp_status upload(fp_plan *p) {
   ea.per_model = p->per_model;
   ea.cand_first = p->cand_first;
   ea.cand_count = p->cand_count;
-  ea.best_out = p->d_best + (size_t)((p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->rank : 0) * M;
+  ea.best_out = p->d_best + (size_t)((p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->rank : 0) * M;
   ea.edges = ta.edges;
   ea.n_edges = ta.n_edges;
   // capacity table N_seq[m][g][w] (Eq. 2): plan data only, computed once here
@@ -717,7 +719,7 @@ fp_status fleet_plan_create(const fp_plan_desc *desc, fp_plan **out) {
     DeviceGuard g(p->device);
     st = upload(p);
     if (st == FP_OK) st = configure_launch(p);
-    if (st == FP_OK && p->world > 1 && !p->has_coll) {
+    if (st == FP_OK && p->dist && !p->has_coll) {
       std::string err;
       if (!load_nccl(g_nccl, err)) {
         st = fail(p, FP_ERR_NCCL, "%s", err.c_str());
@@ -847,7 +849,7 @@ fp_status route_batch(fp_plan *p, const uint32_t *d_len, uint64_t n_local, uint3
     return FP_OK;
   });
   if (st != FP_OK) return st;
-  if (p->world > 1) {
+  if (p->dist) {
     st = all_reduce_u64(p, p->d_rcounts, 5, s, "all-reduce(route counts)");
     if (st != FP_OK) return st;
   }
@@ -928,18 +930,18 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   // writes the split's edge indices; otherwise a one-warp kernel merges the
   // ranks' records after the all-gather.
   const bool routing = bin_pass && d_decision && n_local;
-  const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
+  const bool sliced = p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID);   // ranks split the grid
   uint32_t *route = reinterpret_cast<uint32_t *>(p->d_rcounts);
   fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident, nullptr, bins,
-                            routing && ranks == 1 ? route : nullptr, route_model);
+                            routing && !sliced ? route : nullptr, route_model);
   if (st != FP_OK) return st;
   if (routing) {
     LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
-    cudaError_t e = launch_route_bins(bins, d_decision, n_local, ranks == 1 ? nullptr : p->d_best, ranks,
-                                      (uint32_t)p->models.size(), route_model, p->ta.edges,
-                                      (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s);
+    cudaError_t e = launch_route_bins(bins, d_decision, n_local, sliced ? p->d_best : nullptr,
+                                      sliced ? p->world : 1, (uint32_t)p->models.size(), route_model,
+                                      p->ta.edges, (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
-    p->launches += ranks == 1 ? 1 : 2;
+    p->launches += sliced ? 2 : 1;
   }
   if (bin_pass && !h_best && !h_counts && !is_host_pointer(len)) {
     p->last_stream = s;                     // asynchronous: the records stay on the device
@@ -1056,7 +1058,7 @@ fp_status route_batch_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, c
     if (e != cudaSuccess) return cuda_fail(p, e, "route_batch_raw launch");
     ++p->launches;
   }
-  if (p->world > 1) {
+  if (p->dist) {
     st = all_reduce_u64(p, p->d_rcounts, 7, s, "all-reduce(route counts)");
     if (st != FP_OK) return st;
   }
@@ -1088,7 +1090,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   if (n_local && !d_len && !raw) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
     return fail(p, FP_ERR_INVALID_ARG, "rate_rps must be finite and > 0");
-  if (p->world == 1 && n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace (S:170)");
+  if (!p->dist && n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace (S:170)");
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   // K1: trace pass into the global bin histogram
@@ -1114,7 +1116,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   }, resident);
   if (st != FP_OK) return st;
   // C1: sum the per-rank histograms
-  if (p->world > 1) {
+  if (p->dist) {
     st = all_reduce_u64(p, p->d_hist, 2ull * p->nbins, s, "all-reduce(histogram)");
     if (st != FP_OK) return st;
   }
@@ -1134,7 +1136,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   if (e != cudaSuccess) return cuda_fail(p, e, "candidate evaluation launch");
   ++p->launches;
   // C2: gather every rank's per-model best
-  if (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) {
+  if (p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID)) {
     const size_t bytes = p->models.size() * sizeof(fp_candidate);
     st = all_gather_bytes(p, p->d_best + (size_t)p->rank * p->models.size(), p->d_best, bytes, s,
                           "all-gather(best)");
@@ -1247,7 +1249,7 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   // a rank-specific failure is exchanged (world > 1) so that all ranks fail together
   const bool bad = n && (!d_body_bytes || !d_prompt_tokens || !d_category || is_host_pointer(d_body_bytes) ||
                          is_host_pointer(d_prompt_tokens) || is_host_pointer(d_category));
-  if (bad && p->world == 1) return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
+  if (bad && !p->dist) return fail(p, FP_ERR_INVALID_ARG, "feedback columns must be device memory");
   if (bad) n = 0;
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
@@ -1318,7 +1320,7 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   CUDA_TRY(p, cudaMemcpyAsync(s0, init_s.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
   // snapshots start as NaN (all-ones bytes), no snapshot block (~0)
   CUDA_TRY(p, cudaMemsetAsync(a.snap_c, 0xFF, 48 * 8, s), "memset snapshots");
-  if (p->world == 1) {
+  if (!p->dist) {
     {
       LaunchTimer lt(p, FP_KERNEL_EVAL, s);
       cudaError_t e = launch_calibrate(a, s);
@@ -1457,7 +1459,7 @@ fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *
   }
   // global extent: every rank's (bad, n_local, last)
   uint64_t n_total = n_local, last_all = last, bad_all = bad;
-  if (p->world > 1) {
+  if (p->dist) {
     fp_status st = ensure_xch(p);
     if (st != FP_OK) return st;
     const uint64_t mine[4] = {bad, n_local, last, 0};
@@ -1555,7 +1557,7 @@ fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *
     if (e != cudaSuccess) return cuda_fail(p, e, "peak histogram launch");
   }
   if (n_local) p->launches += pa.check_order ? 3 : 2;
-  if (p->world > 1) {
+  if (p->dist) {
     // global windows: sum the per-rank 2-D histograms (and order-check flags)
     fp_status st = all_reduce_u32(p, hist2d, zbytes / 4, s, "all-reduce(window histogram)");
     if (st != FP_OK) return st;
@@ -1597,7 +1599,7 @@ fp_status best_split(fp_plan *p, fp_candidate *h_best) {
   if (!p || !h_best) return FP_ERR_INVALID_ARG;
   if (!p->have_sweep) return fail(p, FP_ERR_STATE, "best_split before sweep_thresholds");
   DeviceGuard g(p->device);
-  const int ranks = (p->world > 1 && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
+  const int ranks = (p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->world : 1;
   const size_t M = p->models.size();
   const size_t nrec = (size_t)ranks * M;
   // records and the per-bin counts in one stream-ordered round trip (pinned)
