@@ -300,18 +300,22 @@ def run_ours(args, cfg):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # --collectives: the multi-GPU code path at world 1 (process group, NCCL
+    # unique-id broadcast, the library's one-rank communicator, max-over-ranks)
+    multi = world > 1 or args.collectives
+    if multi:
         dist.init_process_group("nccl", device_id=dev)
     n = args.n or cfg.n_requests
     cfg = cfg.with_n(n)
 
     uid = None
-    if world > 1:
+    if multi:
         obj = [fp.fp_nccl_get_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
-                                nccl_unique_id=uid, flags=fp.FP_FLAG_KERNEL_TIMING)
+                                nccl_unique_id=uid,
+                                flags=fp.FP_FLAG_KERNEL_TIMING | (fp.FP_FLAG_COLLECTIVES if multi else 0))
     info = fp.fleet_plan_info(plan)
     # this rank's shard of the global trace: requests [rank*n, (rank+1)*n)
     d_len = generate_device(cfg.shape, cfg.seed, rank * n, n)
@@ -325,7 +329,7 @@ def run_ours(args, cfg):
                                   want_best=want_best)
 
     def barrier():
-        if world > 1:
+        if multi:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize(dev)
 
@@ -353,7 +357,7 @@ def run_ours(args, cfg):
     ktime = {k: fp.fp_kernel_time(plan, kind) for k, kind in
              (("trace", fp.FP_KERNEL_TRACE), ("eval", fp.FP_KERNEL_EVAL), ("route", fp.FP_KERNEL_ROUTE))}
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
+    if multi:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -387,7 +391,7 @@ def run_ours(args, cfg):
             step(h_len, want_best=True)
         barrier()
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
+        if multi:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e = {"value": total_requests * args.e2e_steps / float(dt.item()), "unit": UNIT,
                "h2d_bytes_per_step": 4 * n,   # the pinned trace crosses PCIe once per step
@@ -398,7 +402,7 @@ def run_ours(args, cfg):
         del h_len
 
     if rank != 0:
-        if world > 1:
+        if multi:
             dist.destroy_process_group()
         return
 
@@ -457,6 +461,8 @@ def run_ours(args, cfg):
                                   for k in ("index", "b_short", "c_short", "c_long", "gpus_dual", "gpus_homo",
                                             "cost_dual", "savings", "predicted_savings")},
             "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
+    if multi and world == 1:
+        line["config"]["parallelism"] += "; --collectives: one-rank NCCL communicator in the step"
     if world == 1 and args.k3_grid:
         line["k3_large_grid"] = k3_large_grid(fp, generate_device)
     if world == 1 and args.next4:
@@ -468,7 +474,7 @@ def run_ours(args, cfg):
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if multi:
         dist.destroy_process_group()
 
 
@@ -482,6 +488,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--collectives", action="store_true",
+                    help="take the multi-GPU code path even at world 1 (NCCL group of one; for testing)")
     ap.add_argument("--no-next2", dest="next2", action="store_false",
                     help="skip the three-pool (NEXT-2) measurement")
     ap.add_argument("--no-next1", dest="next1", action="store_false",

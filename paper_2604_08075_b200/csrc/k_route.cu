@@ -247,45 +247,101 @@ cudaError_t launch_route(const RouteArgs &a0, int grid, int block, cudaStream_t 
 namespace fp {
 namespace {
 
-// per-thread tallies: counts in u32 (a thread routes < 2^32 requests; checked
-// at launch), token masses in u64; branch-free (B <= C_S <= C_L: short = !pa)
+// Per-thread tallies, all u32 (a thread routes < 2^31 requests; checked at
+// launch): ns = #short (L <= B), nsv = #served (L <= C_L), the mis-route
+// counts, and per-step partial masses (SMALL: 4 requests x C_L < 2^30 fit a
+// u32) folded into u64 once per step. n_long = nsv - ns and n_reject =
+// n - nsv are derived at the end (B <= C_S <= C_L: short = !pa).
 struct RawAcc {
-  uint32_t ns = 0, nl = 0, nr = 0, mis_s = 0, mis_l = 0;
-  unsigned long long ms = 0, ml = 0;
+  uint32_t n = 0, ns = 0, nsv = 0, mis_s = 0, mis_l = 0;
+  unsigned long long ms = 0, msv = 0;
 };
 
-__device__ __forceinline__ uint32_t route_raw_one(const RouteRawArgs &a, uint32_t L, uint32_t mo, uint32_t tp,
-                                                  RawAcc &c) {
-  const bool pa = L > a.b, pb = L > a.cs, pc = L > a.cl;
-  const bool lng = pa && !pc;
-  c.nr += pc;
-  c.nl += lng;
-  c.ns += !pa;
-  c.ml += lng ? L : 0u;
-  c.ms += pa ? 0u : L;
-  if (a.true_prompt) {
-    const unsigned long long t = (unsigned long long)tp + mo;
-    c.mis_s += (!pa && t > a.cs);
-    c.mis_l += (lng && t > a.cl);
+// One request as predicated PTX: decision a + 4b + 9c, the two counts, the
+// two partial masses and (TRUE_TOK) the mis-route counts, where the true
+// total t = prompt_tokens + max_output exceeds a window C iff
+// mo > C || tp > C - mo (no 64-bit add).
+template <bool TRUE_TOK>
+__device__ __forceinline__ uint32_t route_raw_u32(uint32_t L, uint32_t mo, uint32_t tp, uint32_t B, uint32_t CS,
+                                                  uint32_t CL, RawAcc &c, uint32_t &gms, uint32_t &gmsv) {
+  uint32_t d;
+  if constexpr (TRUE_TOK) {
+    asm("{\n\t.reg .pred pa, pb, pc, qs, ql, ms, ml;\n\t.reg .u32 ts, tl;\n\t"
+        "setp.gt.u32 pa, %7, %10;\n\t"
+        "setp.gt.u32 pb, %7, %11;\n\t"
+        "setp.gt.u32 pc, %7, %12;\n\t"
+        "selp.u32 %0, 1, 0, pa;\n\t"
+        "@pb add.u32 %0, %0, 4;\n\t"
+        "@pc add.u32 %0, %0, 9;\n\t"
+        "@!pa add.u32 %1, %1, 1;\n\t"
+        "@!pa add.u32 %3, %3, %7;\n\t"
+        "@!pc add.u32 %2, %2, 1;\n\t"
+        "@!pc add.u32 %4, %4, %7;\n\t"
+        "sub.u32 ts, %11, %8;\n\t"
+        "sub.u32 tl, %12, %8;\n\t"
+        "setp.gt.u32 qs, %8, %11;\n\t"
+        "setp.gt.or.u32 qs, %9, ts, qs;\n\t"
+        "setp.gt.u32 ql, %8, %12;\n\t"
+        "setp.gt.or.u32 ql, %9, tl, ql;\n\t"
+        "not.pred ms, pa;\n\t"
+        "and.pred ms, ms, qs;\n\t"
+        "not.pred ml, pc;\n\t"
+        "and.pred ml, ml, pa;\n\t"
+        "and.pred ml, ml, ql;\n\t"
+        "@ms add.u32 %5, %5, 1;\n\t"
+        "@ml add.u32 %6, %6, 1;\n\t"
+        "}"
+        : "=r"(d), "+r"(c.ns), "+r"(c.nsv), "+r"(gms), "+r"(gmsv), "+r"(c.mis_s), "+r"(c.mis_l)
+        : "r"(L), "r"(mo), "r"(tp), "r"(B), "r"(CS), "r"(CL));
+  } else {
+    asm("{\n\t.reg .pred pa, pb, pc;\n\t"
+        "setp.gt.u32 pa, %5, %6;\n\t"
+        "setp.gt.u32 pb, %5, %7;\n\t"
+        "setp.gt.u32 pc, %5, %8;\n\t"
+        "selp.u32 %0, 1, 0, pa;\n\t"
+        "@pb add.u32 %0, %0, 4;\n\t"
+        "@pc add.u32 %0, %0, 9;\n\t"
+        "@!pa add.u32 %1, %1, 1;\n\t"
+        "@!pa add.u32 %3, %3, %5;\n\t"
+        "@!pc add.u32 %2, %2, 1;\n\t"
+        "@!pc add.u32 %4, %4, %5;\n\t"
+        "}"
+        : "=r"(d), "+r"(c.ns), "+r"(c.nsv), "+r"(gms), "+r"(gmsv)
+        : "r"(L), "r"(B), "r"(CS), "r"(CL));
   }
-  return (pa ? 1u : 0u) + (pb ? 4u : 0u) + (pc ? 9u : 0u);
+  return d;
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(512) k4_route_raw(RouteRawArgs a) {
-  __shared__ __align__(16) double cst[1024];
+// generic single request (any C_L: u64 masses)
+template <bool TRUE_TOK>
+__device__ __forceinline__ uint32_t route_raw_one(uint32_t L, uint32_t mo, uint32_t tp, uint32_t B, uint32_t CS,
+                                                  uint32_t CL, RawAcc &c) {
+  uint32_t ms = 0, msv = 0;
+  const uint32_t d = route_raw_u32<TRUE_TOK>(L, mo, tp, B, CS, CL, c, ms, msv);
+  c.ms += ms;
+  c.msv += msv;
+  ++c.n;
+  return d;
+}
+
+// VEC: every column in the same 16-B phase; TRUE_TOK: true prompt tokens
+// given (mis-routes); DEC / LT: decision / L_total outputs; SMALL: C_L < 2^30.
+template <bool VEC, bool TRUE_TOK, bool DEC, bool LT, bool SMALL>
+__global__ void __launch_bounds__(512, 2) k4_route_raw(RouteRawArgs a) {
+  __shared__ __align__(16) double2 cst[kCatTable];
   __shared__ unsigned long long red[7][16];
   setup_cstar(a.calib, a.n_cats, a.gamma, a.c_floor, cst);
   __syncthreads();
+  const uint32_t B = a.b, CS = a.cs, CL = a.cl;
   RawAcc acc;
   const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t me = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   auto one = [&](uint64_t i) {
     const uint32_t mo = a.maxout[i];
-    const uint32_t L = estimate_l_total(a.body[i], mo, a.cat[i], cst, a.n_cats);
-    const uint32_t d = route_raw_one(a, L, mo, a.true_prompt ? a.true_prompt[i] : 0u, acc);
-    if (a.decision) a.decision[i] = (uint8_t)d;
-    if (a.l_total) a.l_total[i] = L;
+    const uint32_t L = estimate_l_total(a.body[i], mo, a.cat[i], cst);
+    const uint32_t d = route_raw_one<TRUE_TOK>(L, mo, TRUE_TOK ? a.true_prompt[i] : 0u, B, CS, CL, acc);
+    if (DEC) a.decision[i] = (uint8_t)d;
+    if (LT) a.l_total[i] = L;
   };
   if constexpr (!VEC) {
     for (uint64_t i = me; i < a.n; i += S) one(i);
@@ -298,25 +354,41 @@ __global__ void __launch_bounds__(512) k4_route_raw(RouteRawArgs a) {
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) one(tail_first + threadIdx.x);
     const uint4 *b4 = reinterpret_cast<const uint4 *>(a.body + head);
     const uint4 *m4 = reinterpret_cast<const uint4 *>(a.maxout + head);
-    const uint4 *t4 = a.true_prompt ? reinterpret_cast<const uint4 *>(a.true_prompt + head) : nullptr;
+    const uint4 *t4 = TRUE_TOK ? reinterpret_cast<const uint4 *>(a.true_prompt + head) : nullptr;
     const uint32_t *c4 = reinterpret_cast<const uint32_t *>(a.cat + head);
-    uint32_t *d4 = a.decision ? reinterpret_cast<uint32_t *>(a.decision + head) : nullptr;
-    uint4 *l4 = a.l_total ? reinterpret_cast<uint4 *>(a.l_total + head) : nullptr;
+    uint32_t *d4 = DEC ? reinterpret_cast<uint32_t *>(a.decision + head) : nullptr;
+    uint4 *l4 = LT ? reinterpret_cast<uint4 *>(a.l_total + head) : nullptr;
     for (uint64_t i = me; i < n4; i += S) {
       const uint4 b = ldg_stream(b4 + i), m = ldg_stream(m4 + i);
-      const uint4 t = t4 ? ldg_stream(t4 + i) : make_uint4(0u, 0u, 0u, 0u);
+      const uint4 t = TRUE_TOK ? ldg_stream(t4 + i) : make_uint4(0u, 0u, 0u, 0u);
       const uint32_t k = __ldg(c4 + i);
-      const uint4 L = make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, cst, a.n_cats),
-                                 estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, cst, a.n_cats),
-                                 estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, cst, a.n_cats),
-                                 estimate_l_total(b.w, m.w, k >> 24, cst, a.n_cats));
-      const uint32_t w = route_raw_one(a, L.x, m.x, t.x, acc) | (route_raw_one(a, L.y, m.y, t.y, acc) << 8) |
-                         (route_raw_one(a, L.z, m.z, t.z, acc) << 16) | (route_raw_one(a, L.w, m.w, t.w, acc) << 24);
-      if (d4) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(d4 + i), "r"(w) : "memory");
-      if (l4) l4[i] = L;
+      const uint4 L = make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, cst),
+                                 estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, cst),
+                                 estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, cst),
+                                 estimate_l_total(b.w, m.w, k >> 24, cst));
+      uint32_t w;
+      if constexpr (SMALL) {
+        uint32_t gms = 0, gmsv = 0;
+        w = route_raw_u32<TRUE_TOK>(L.x, m.x, t.x, B, CS, CL, acc, gms, gmsv) |
+            (route_raw_u32<TRUE_TOK>(L.y, m.y, t.y, B, CS, CL, acc, gms, gmsv) << 8) |
+            (route_raw_u32<TRUE_TOK>(L.z, m.z, t.z, B, CS, CL, acc, gms, gmsv) << 16) |
+            (route_raw_u32<TRUE_TOK>(L.w, m.w, t.w, B, CS, CL, acc, gms, gmsv) << 24);
+        acc.ms += gms;
+        acc.msv += gmsv;
+        acc.n += 4;
+      } else {
+        w = route_raw_one<TRUE_TOK>(L.x, m.x, t.x, B, CS, CL, acc) |
+            (route_raw_one<TRUE_TOK>(L.y, m.y, t.y, B, CS, CL, acc) << 8) |
+            (route_raw_one<TRUE_TOK>(L.z, m.z, t.z, B, CS, CL, acc) << 16) |
+            (route_raw_one<TRUE_TOK>(L.w, m.w, t.w, B, CS, CL, acc) << 24);
+      }
+      if (DEC) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(d4 + i), "r"(w) : "memory");
+      if (LT) l4[i] = L;
     }
   }
-  unsigned long long v[7] = {acc.ns, acc.nl, acc.nr, acc.ms, acc.ml, acc.mis_s, acc.mis_l};   // widened
+  // counts: short, long, rejected, mass short, mass long, mis-routes short, long
+  unsigned long long v[7] = {acc.ns, (unsigned long long)acc.nsv - acc.ns, (unsigned long long)acc.n - acc.nsv,
+                             acc.ms, acc.msv - acc.ms, acc.mis_s, acc.mis_l};
 #pragma unroll
   for (int k = 0; k < 7; ++k) {
 #pragma unroll
@@ -335,14 +407,33 @@ __global__ void __launch_bounds__(512) k4_route_raw(RouteRawArgs a) {
   }
 }
 
+template <bool VEC, bool TRUE_TOK, bool DEC, bool LT>
+void *k4r_ptr(bool small) {
+  return small ? reinterpret_cast<void *>(&k4_route_raw<VEC, TRUE_TOK, DEC, LT, true>)
+               : reinterpret_cast<void *>(&k4_route_raw<VEC, TRUE_TOK, DEC, LT, false>);
+}
+
+template <bool VEC>
+void *k4r_pick(const RouteRawArgs &a) {
+  const bool small = a.cl < (1u << 30);
+  const int sel = (a.true_prompt ? 4 : 0) | (a.decision ? 2 : 0) | (a.l_total ? 1 : 0);
+  switch (sel) {
+    case 0: return k4r_ptr<VEC, false, false, false>(small);
+    case 1: return k4r_ptr<VEC, false, false, true>(small);
+    case 2: return k4r_ptr<VEC, false, true, false>(small);
+    case 3: return k4r_ptr<VEC, false, true, true>(small);
+    case 4: return k4r_ptr<VEC, true, false, false>(small);
+    case 5: return k4r_ptr<VEC, true, false, true>(small);
+    case 6: return k4r_ptr<VEC, true, true, false>(small);
+    default: return k4r_ptr<VEC, true, true, true>(small);
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStream_t s) {
   if (a.n == 0) return cudaSuccess;
   if (block > 512 || (block & 31) || a.n_cats == 0 || a.n_cats > 256) return cudaErrorInvalidValue;
-  const uint64_t need = (a.n + block - 1) / block;
-  const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
-  if (a.n / ((uint64_t)g * block) >= (1ull << 31)) return cudaErrorInvalidValue;   // u32 per-thread tallies
   // vector path: every column in the same 16-B phase (cat / decision in the same 4-B phase)
   const uintptr_t b = reinterpret_cast<uintptr_t>(a.body);
   const uint64_t mis = (b & 15u) >> 2, head = mis ? 4 - mis : 0;
@@ -350,8 +441,22 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
   auto al4 = [&](const void *p) { return p == nullptr || ((reinterpret_cast<uintptr_t>(p) + head) & 3u) == 0; };
   const bool vec = (b & 3u) == 0 && same16(a.maxout) && same16(a.true_prompt) && same16(a.l_total) && al4(a.cat) &&
                    al4(a.decision);
-  if (vec) k4_route_raw<true><<<g, block, 0, s>>>(a);
-  else k4_route_raw<false><<<g, block, 0, s>>>(a);
+  void *k = vec ? k4r_pick<true>(a) : k4r_pick<false>(a);
+  // grid-stride over a persistent grid: never more blocks than are resident
+  // at once (a partial second wave leaves most SMs idle at the end)
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, 0);
+  if (e != cudaSuccess) return e;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint64_t need = (a.n + block - 1) / block;
+  const int g = (int)std::min<uint64_t>((uint64_t)std::min(grid, std::max(1, per_sm) * sms),
+                                        std::max<uint64_t>(1, need));
+  if (a.n / ((uint64_t)g * block) >= (1ull << 31)) return cudaErrorInvalidValue;   // u32 per-thread tallies
+  RouteRawArgs arg = a;
+  void *args[] = {&arg};
+  e = cudaLaunchKernel(k, dim3(g), dim3(block), args, 0, s);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

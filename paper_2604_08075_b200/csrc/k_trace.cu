@@ -163,29 +163,26 @@ struct SrcPlain {
 struct SrcRaw {
   const uint32_t *body, *mo;
   const uint8_t *cat;
-  const double *cstar;   // shared memory [ncat]
-  uint32_t ncat;
+  const double2 *tab;    // shared memory [256]: {1/c*, c*} per category byte
   uint64_t base;         // element offset of uint4 index 0 (the aligned head)
   __device__ __forceinline__ uint4 load4(const uint4 *, uint64_t i) const {
     const uint64_t e = base + 4 * i;
     const uint4 b = ldg_stream(reinterpret_cast<const uint4 *>(body + e));
     const uint4 m = ldg_stream(reinterpret_cast<const uint4 *>(mo + e));
     const uint32_t k = __ldg(reinterpret_cast<const unsigned int *>(cat + e));
-    return make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, cstar, ncat),
-                      estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, cstar, ncat),
-                      estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, cstar, ncat),
-                      estimate_l_total(b.w, m.w, k >> 24, cstar, ncat));
+    return make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, tab), estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, tab),
+                      estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, tab), estimate_l_total(b.w, m.w, k >> 24, tab));
   }
-  __device__ __forceinline__ uint32_t load1(uint64_t i) const {
-    return estimate_l_total(body[i], mo[i], cat[i], cstar, ncat);
-  }
+  __device__ __forceinline__ uint32_t load1(uint64_t i) const { return estimate_l_total(body[i], mo[i], cat[i], tab); }
 };
 
 // BINS: also write each request's bin (u8; |E| < 256) to a.bins_out, where
 // (a.bins_out + element index) is 4-B aligned for every uint4 of the body.
 template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS>
 __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs a) {
-  constexpr int U = kUnroll;
+  // raw: 3 columns per request (36 B per uint4 step in flight), 2 steps per
+  // thread at 3 x 512 threads/SM keep ~110 KB/SM in flight within 42 registers
+  constexpr int U = RAW ? 2 : kUnroll;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
   uint32_t lut_bytes = (LUTW == 0) ? a.n_edges * 4 : a.lut_cells * LUTW;
@@ -193,12 +190,12 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
   K1Ctx c;
   c.lut = smem;
   c.acc = reinterpret_cast<unsigned long long *>(smem + lut_bytes);
-  // RAW: [ncat][c*, 1/c*, lo, hi], 16-B aligned for the LDS.128 pairs. Offsets
+  // RAW: [256] {1/c*, c*}, 16-B aligned for one LDS.128 per request. Offsets
   // are integer arithmetic on `smem` so the compiler keeps the shared state
   // space (a pointer rounded through uintptr_t becomes generic: ATOM.E/LD.E)
   const uint32_t cst_off = RAW ? ((lut_bytes + nbins * 8u + 15u) & ~15u) : lut_bytes + nbins * 8u;
-  double *cstar = reinterpret_cast<double *>(smem + cst_off);
-  c.hist = smem + cst_off + (RAW ? 32u * a.n_cats : 0u);
+  double2 *cstar = reinterpret_cast<double2 *>(smem + cst_off);
+  c.hist = smem + cst_off + (RAW ? 16u * kCatTable : 0u);
   c.clampv = a.max_edge + 1u;
   c.round = (1u << a.shift) - 1u;
   c.shift = a.shift;
@@ -233,7 +230,7 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
 
   // element source; RAW without a common 16-B phase of the columns -> scalar rounds
   SrcPlain sp{a.len};
-  SrcRaw sr{a.body, a.maxout, a.cat, cstar, a.n_cats, 0};
+  SrcRaw sr{a.body, a.maxout, a.cat, cstar, 0};
   const uintptr_t anchor = RAW ? reinterpret_cast<uintptr_t>(a.body) : reinterpret_cast<uintptr_t>(a.len);
   const uint32_t mis = (uint32_t)((anchor & 15u) >> 2);
   const uint64_t head = (RAW && !a.raw_vec) ? a.n : (mis ? umin64(a.n, 4u - mis) : 0u);
@@ -336,7 +333,7 @@ size_t smem_for(const TraceArgs &a, const Variant &v) {
   size_t lut = v.lutw == 0 ? (size_t)a.n_edges * 4 : (size_t)a.lut_cells * v.lutw;
   lut = (lut + 15) & ~size_t(15);
   const uint32_t words = v.mass ? (v.split ? 3u : 2u) : 1u;
-  return lut + (size_t)nbins * 8 + (v.raw ? (size_t)a.n_cats * 32 + 8 : 0) + (size_t)nbins * v.R * words * 4;
+  return lut + (size_t)nbins * 8 + (v.raw ? (size_t)kCatTable * 16 + 8 : 0) + (size_t)nbins * v.R * words * 4;
 }
 
 Variant choose(const TraceArgs &a, int block) {

@@ -2,7 +2,8 @@
 L_total estimated in the trace pass (sweep_thresholds_raw) must give the
 same candidate records as the oracle's estimate + sweep, and route_batch_raw
 the same decisions, estimates, counts and mis-route counts (bit-exact: one
-IEEE binary64 division and ceil per request on both sides)."""
+IEEE binary64 quotient and ceil per request on both sides; the kernels form
+the correctly rounded quotient without a DDIV, see csrc/estimate.cuh)."""
 import numpy as np
 import pytest
 
@@ -89,8 +90,8 @@ def test_raw_errors():
 @pytest.mark.parametrize("cstar", [4.0, 3.5, 4.48 * 0.98 - 0.1 * 4.48, 2.01 * 0.98 - 0.201, 0.5, 0.3, 1.0 / 3.0 + 1.0])
 def test_near_integer_quotients_are_exact(cstar):
     """Adversarial bytes |r| = round(k c*) + {-2..2} put |r| / c* within a hair
-    of an integer, the case where ceil(fl(|r|/c*)) and ceil(|r|/c*) can differ;
-    the fast reciprocal path must defer to the IEEE division there."""
+    of an integer, the case where ceil(fl(|r|/c*)) and ceil(|r|/c*) can differ:
+    the kernels' division-free quotient must round exactly like fl()."""
     rng = np.random.default_rng(1)
     k = rng.integers(1, 2**31 // max(1, int(cstar * 2)), 200_000).astype(np.float64)
     base = np.round(k * cstar)
@@ -109,3 +110,64 @@ def test_near_integer_quotients_are_exact(cstar):
     got = lt.cpu().numpy().view(np.uint32)
     bad = np.nonzero(got != ref)[0]
     assert bad.size == 0, (cstar, body[bad[:5]], got[bad[:5]], ref[bad[:5]])
+
+
+def _adversarial_columns(seed, cstars, per_cat=40_000):
+    """Bytes around k c* for every category (quotients within a hair of an
+    integer), random bytes over the whole u32 range, and a max_output column
+    that drives part of the sums past 2^32 - 1 (saturation, R24)."""
+    rng = np.random.default_rng(seed)
+    body, cat = [], []
+    for j, c in enumerate(cstars):
+        kmax = max(2, min(2**31, int(min(2.0**32 / max(c, 1e-300), 2.0**40))))
+        k = rng.integers(1, kmax, per_cat).astype(np.float64)
+        base = np.clip(np.round(k * c), 0, 2**32 - 1)
+        b = np.clip(base[:, None] + np.arange(-2, 3)[None, :], 0, 2**32 - 1).ravel()
+        b = np.concatenate([b, rng.integers(0, 2**32, per_cat, dtype=np.uint64).astype(np.float64),
+                            np.array([0, 1, 2, 2**32 - 1], dtype=np.float64)])
+        body.append(b.astype(np.uint64).astype(np.uint32))
+        cat.append(np.full(b.size, j, np.uint8))
+    body = np.concatenate(body)
+    cat = np.concatenate(cat)
+    perm = rng.permutation(body.size)
+    body, cat = body[perm], cat[perm]
+    mo = rng.integers(0, 2**16, body.size, dtype=np.uint64).astype(np.uint32)
+    mo[::97] = rng.integers(2**31, 2**32, mo[::97].size, dtype=np.uint64).astype(np.uint32)
+    return body, mo, cat
+
+
+def test_markstein_division_random_and_extreme_categories():
+    """The division-free estimator (RN(1/c*), Markstein correction, c* clamped
+    to [2^-800, 2^800]) against the oracle's IEEE division: 64 categories with
+    log-uniform c*, all-ones significands (2^e (2 - 2^-52)), powers of two,
+    and c* far outside the clamp on both sides; L_total, decisions, counts and
+    the trace-pass histogram must match exactly."""
+    rng = np.random.default_rng(7)
+    cs = list(2.0 ** rng.uniform(-6, 9, 40))
+    cs += [np.nextafter(2.0 ** e, 0) * 2 for e in (-3, -1, 0, 1, 2, 5)]      # 1.11...1 significands
+    cs += [2.0 ** e for e in (-5, -1, 0, 1, 3)] + [1.0 / 3.0, 0.1, 7.0 / 3.0]
+    cs += [1e-300, 2.0 ** -801, 2.0 ** -799, 1e-30, 1e30, 2.0 ** 799, 2.0 ** 801, 1e300]
+    cs += [4.0] * (64 - len(cs))
+    cats = [(float(c), 0.0) for c in cs]
+    body, mo, cat = _adversarial_columns(11, cs)
+    n = body.size
+    floor = 1e-305
+    plan = fp.fleet_plan_create(**fp.desc_from_config(configs.c1()))
+    lt = torch.zeros(n, dtype=torch.int32, device="cuda")
+    dec = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    counts, _ = fp.route_batch_raw(plan, _dev(body), _dev(mo), _dev(cat), cats, 8192, 8192, 65536, gamma=0.0,
+                                   c_floor=floor, decision=dec, l_total=lt)
+    ref = oracle.estimate(body, mo, cat, cats, 0.0, floor)
+    got = lt.cpu().numpy().view(np.uint32)
+    bad = np.nonzero(got != ref)[0]
+    assert bad.size == 0, (body[bad[:5]], cat[bad[:5]], got[bad[:5]], ref[bad[:5]])
+    odec, olt, oc, _ = oracle.route_batch_est(body, mo, cat, None, cats, 0.0, floor, 8192, 8192, 65536)
+    assert np.array_equal(dec.cpu().numpy(), odec)
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
+    # the trace pass (K1 raw) bins the same estimates
+    cfg = configs.c5().with_n(n)
+    plan5 = fp.fleet_plan_create(**fp.desc_from_config(cfg))
+    res = fp.sweep_thresholds_raw(plan5, _dev(body), _dev(mo), _dev(cat), cats, cfg.rate_rps, gamma=0.0,
+                                  c_floor=floor, want_results=True)
+    allc, _ = oracle.sweep(cfg, ref)
+    assert res.tobytes() == allc.tobytes()
