@@ -414,8 +414,12 @@ def run_ours(args, cfg):
     # the bin pass (|E| < 255, u8 LUT) the trace pass reads 4 B and writes a 1-B
     # bin per request and the routing pass maps 1 B of bins to 1 B of decisions;
     # otherwise the routing pass re-reads the 4-B L_total and writes 1 B.
+    # With |E| + 1 <= 64 bins (C5: 56) and a device trace the bins are 6-bit
+    # packed: 0.75 B per request written and read back.
     bin_pass = info["lut_cells"] > 0 and info["n_edges"] < 255
-    algo_bytes = ({"trace": 5.0 * n, "route": 2.0 * n, "eval": 0.0} if bin_pass
+    packed = bin_pass and info["n_edges"] + 1 <= 64
+    bin_bytes = 0.75 if packed else 1.0
+    algo_bytes = ({"trace": (4.0 + bin_bytes) * n, "route": (bin_bytes + 1.0) * n, "eval": 0.0} if bin_pass
                   else {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0})
     kms, kcount = ktime[dom]
     per_launch_ms = kms / max(kcount, 1)
@@ -423,8 +427,8 @@ def run_ours(args, cfg):
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
     k_gbs = {k: (algo_bytes[k] * args.steps / (ktime[k][0] / 1e3) / 1e9 if ktime[k][0] and algo_bytes[k] else None)
              for k in ktime}
-    kname = {"trace": "K1 k1_trace" + (" (bin pass)" if bin_pass else ""),
-             "route": "K4b k4_route_bins" if bin_pass else "K4 k4_route"}
+    kname = {"trace": "K1 k1_trace" + ((" (6-bit packed bin pass)" if packed else " (bin pass)") if bin_pass else ""),
+             "route": ("K4p k4_route_packed" if packed else "K4b k4_route_bins") if bin_pass else "K4 k4_route"}
     roof = {"bound": "hbm", "kernel": kname.get(dom, dom),
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "frac_of_nominal_7700": achieved / 7700.0,
@@ -444,9 +448,9 @@ def run_ours(args, cfg):
             "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
             "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic (seeded Philox MIX trace, generated on device; not timed)",
-            "step": "sweep_and_route: K1 trace pass (+bins) -> K3 sweep + per-model argmin -> device split pick "
-                    "-> K4b routing pass, stream-ordered with no host round trip; the best records stay on the "
-                    "device and are read once after the timed loop (e2e reads them every step)",
+            "step": "sweep_and_route: K1 trace pass (+6-bit packed bins) -> K3 sweep + per-model argmin -> device "
+                    "split pick -> K4p routing pass, stream-ordered with no host round trip; the best records stay "
+                    "on the device and are read once after the timed loop (e2e reads them every step)",
             "config": _workload(cfg, n, world),
             "candidates_per_s": cand_per_s,
             "candidates_per_s_step": cfg.n_candidates() / (ms_step / 1e3),

@@ -36,8 +36,20 @@ struct TraceArgs {
   double gamma = 1.0, c_floor = 0.5;
   // per-request bin output (sweep_and_route's bin pass), nullable
   uint8_t *bins_out = nullptr;
+  // bins_pack: |E| + 1 <= 64 bins fit 6 bits. Packed per (step k, thread t)
+  // of the trace pass -- its 4 uint4 j = 4 k S + u S + t (u < 4, S = grid x
+  // block threads) = 16 requests -- into chunk c = k S + t: a u64 of low
+  // nibbles in bins_out (bin 4u + e at bits 16u + 4e) and a u32 of high 2-bit
+  // parts in bins_hi (at bits 8u + 2e). One 8-B and one 4-B coalesced store
+  // per 16 requests. The < 4 head / < 4 tail elements' bins go to
+  // bins_side[0..3) / [4..7) as bytes. Device traces of one launch only.
+  uint32_t bins_pack = 0;
+  uint8_t *bins_hi = nullptr;
+  uint8_t *bins_side = nullptr;
 };
 cudaError_t launch_trace(const TraceArgs &a, int grid, int block, size_t smem, cudaStream_t s);
+// the grid launch_trace uses for `a` (the bin/raw variants are clamped to the resident grid)
+int trace_grid(const TraceArgs &a, int grid, int block);
 size_t trace_smem_bytes(const TraceArgs &a, int block);
 cudaError_t trace_occupancy(const TraceArgs &a, int block, size_t smem, int *per_sm);
 
@@ -73,6 +85,13 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
 cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
                               int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,
                               uint32_t *route, int grid, int block, cudaStream_t s);
+// K4p: the same from K1's 6-bit packed bins (TraceArgs::bins_pack), launched
+// with the trace pass's grid x block (k1_grid x k1_block) so thread t reads
+// the chunks it wrote
+cudaError_t launch_route_packed(const uint8_t *lo, const uint8_t *hi, const uint8_t *side, uint32_t head,
+                                uint8_t *decision, uint64_t n, const fp_candidate *recs, int ranks, uint32_t n_models,
+                                uint32_t model, const uint32_t *edges, uint32_t n_edges, uint32_t *route, int k1_grid,
+                                int k1_block, cudaStream_t s);
 cudaError_t route_occupancy(int block, int *per_sm);
 
 // ---- K3: candidate evaluation + argmin ---------------------------------------

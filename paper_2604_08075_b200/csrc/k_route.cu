@@ -582,7 +582,100 @@ __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__
   }
 }
 
+// The 6-bit packed bins of K1 (|E| < 64; TraceArgs::bins_pack): chunk
+// c = k S + t holds the bins of the trace pass's step k, thread t -- uint4
+// j = 4 k S + u S + t, u < 4 -- as a u64 of low nibbles and a u32 of high
+// 2-bit parts, so the step moves 0.75 B of bins per request each way instead
+// of 1 B. Launched with the trace pass's own grid x block: thread t reads its
+// chunks with one 8-B and one 4-B coalesced load per 16 requests and writes
+// 4 decision words (each warp store 128 B contiguous).
+__device__ __forceinline__ uint32_t unplane6(uint32_t lo16, uint32_t hi8) {
+  uint32_t n = (lo16 | (lo16 << 8)) & 0x00FF00FFu;
+  n = (n | (n << 4)) & 0x0F0F0F0Fu;             // nibble e -> byte e
+  uint32_t c = (hi8 | (hi8 << 12)) & 0x000F000Fu;
+  c = (c | (c << 6)) & 0x03030303u;             // crumb e -> byte e
+  return n | (c << 4);
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long *__restrict__ lo,
+                                                       const uint32_t *__restrict__ hi,
+                                                       const uint8_t *__restrict__ side, uint8_t *__restrict__ dec,
+                                                       uint64_t n, uint32_t head, const uint32_t *__restrict__ route) {
+  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
+  if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
+  const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
+  const SwarK sk{(0x7Fu - (iB < 0x7Fu ? iB : 0x7Fu)) * 0x01010101u, (0x7Fu - (iCS < 0x7Fu ? iCS : 0x7Fu)) * 0x01010101u,
+                 (0x7Fu - (iCL < 0x7Fu ? iCL : 0x7Fu)) * 0x01010101u};
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t h = head < n ? head : n;
+  const uint64_t n4 = (n - h) >> 2;
+  const uint64_t tail_first = h + (n4 << 2);
+  if (blockIdx.x == 0 && threadIdx.x < h) dec[threadIdx.x] = (uint8_t)dec_byte(side[threadIdx.x], iB, iCS, iCL);
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail_first)
+    dec[tail_first + threadIdx.x] = (uint8_t)dec_byte(side[4 + threadIdx.x], iB, iCS, iCL);
+  uint8_t *body = dec + h;
+  const uint64_t nsteps = (n4 + 4 * S - 1) / (4 * S);
+  const uint64_t full = n4 / (4 * S);             // steps whose 4 uint4 all exist
+  auto put = [&](uint8_t *q, uint32_t d) {
+    if (VEC) {
+      asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(q), "r"(d) : "memory");
+    } else {
+      q[0] = (uint8_t)d; q[1] = (uint8_t)(d >> 8); q[2] = (uint8_t)(d >> 16); q[3] = (uint8_t)(d >> 24);
+    }
+  };
+  auto word = [&](unsigned long long l, uint32_t c, int u) {
+    return dec_word_swar(unplane6((uint32_t)(l >> (16 * u)) & 0xFFFFu, (c >> (8 * u)) & 0xFFu), sk);
+  };
+  const uint64_t ustride = 4 * S;                 // bytes between a chunk's uint4 u and u + 1
+  // full steps: four steps' chunks in flight per thread (48 B of loads), no bounds checks
+  constexpr int KU = 4;
+  uint64_t k = 0;
+  for (; k + KU <= full; k += KU) {
+    unsigned long long l[KU];
+    uint32_t c[KU];
+#pragma unroll
+    for (int q = 0; q < KU; ++q) {
+      l[q] = __ldcs(lo + (k + q) * S + t);
+      c[q] = __ldcs(hi + (k + q) * S + t);
+    }
+#pragma unroll
+    for (int q = 0; q < KU; ++q) {
+      uint8_t *d = body + 16 * S * (k + q) + 4 * t;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) put(d + u * ustride, word(l[q], c[q], u));
+    }
+  }
+  // the remaining steps (the last one partial)
+  for (; k < nsteps; ++k) {
+    const unsigned long long l = __ldcs(lo + k * S + t);
+    const uint32_t c = __ldcs(hi + k * S + t);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t j = 4 * k * S + u * S + t;
+      if (j < n4) put(body + 4 * j, word(l, c, u));
+    }
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_route_packed(const uint8_t *lo, const uint8_t *hi, const uint8_t *side, uint32_t head,
+                                uint8_t *decision, uint64_t n, const fp_candidate *recs, int ranks, uint32_t n_models,
+                                uint32_t model, const uint32_t *edges, uint32_t n_edges, uint32_t *route, int k1_grid,
+                                int k1_block, cudaStream_t s) {
+  if (recs) k_pick_route<<<1, 32, 0, s>>>(recs, ranks, n_models, model, edges, n_edges, route);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || n == 0) return e;
+  const uint64_t h = head < n ? head : n;
+  const bool vec = (reinterpret_cast<uintptr_t>(decision + h) & 3u) == 0;
+  const auto *l8 = reinterpret_cast<const unsigned long long *>(lo);
+  const auto *h4 = reinterpret_cast<const uint32_t *>(hi);
+  if (vec) k4_route_packed<true><<<k1_grid, k1_block, 0, s>>>(l8, h4, side, decision, n, head, route);
+  else k4_route_packed<false><<<k1_grid, k1_block, 0, s>>>(l8, h4, side, decision, n, head, route);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
                               int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,

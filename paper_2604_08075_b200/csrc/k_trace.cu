@@ -176,9 +176,36 @@ struct SrcRaw {
   __device__ __forceinline__ uint32_t load1(uint64_t i) const { return estimate_l_total(body[i], mo[i], cat[i], tab); }
 };
 
+// Four bins packed in bytes (each < 64) -> the two parts of the 6-bit
+// packing: low nibbles as 16 bits (bin e at bits 4e) and high 2-bit parts as
+// 8 bits (bin e at bits 2e). ALU only (no shuffles: the hot loop's
+// shared-memory atomics already load the MIO pipe).
+__device__ __forceinline__ void split6(uint32_t w, uint32_t &lo16, uint32_t &hi8) {
+  uint32_t t = w & 0x0F0F0F0Fu;
+  t |= t >> 4;                                   // byte 0 = n1 n0, byte 2 = n3 n2
+  lo16 = __byte_perm(t, 0u, 0x4420);             // bytes 0, 2
+  uint32_t h = (w >> 4) & 0x03030303u;
+  h |= h >> 6;                                   // byte 0 = c1 c0 (4 bits), byte 2 = c3 c2
+  hi8 = (h & 0xFu) | ((h >> 12) & 0xF0u);
+}
+
+// accumulate uint4 u of this thread's step into the chunk words
+__device__ __forceinline__ void pack_into(uint32_t w, int u, unsigned long long &lo, uint32_t &hi) {
+  uint32_t l, h;
+  split6(w, l, h);
+  lo |= (unsigned long long)l << (16 * u);
+  hi |= h << (8 * u);
+}
+
+__device__ __forceinline__ void store_chunk(const TraceArgs &a, uint64_t c, unsigned long long lo, uint32_t hi) {
+  asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(a.bins_out + 8 * c), "l"(lo) : "memory");
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(a.bins_hi + 4 * c), "r"(hi) : "memory");
+}
+
 // BINS: also write each request's bin (u8; |E| < 256) to a.bins_out, where
-// (a.bins_out + element index) is 4-B aligned for every uint4 of the body.
-template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS>
+// (a.bins_out + element index) is 4-B aligned for every uint4 of the body;
+// BINS && PACK: the 6-bit chunks of a.bins_out / a.bins_hi (|E| < 64).
+template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS, bool PACK = false>
 __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs a) {
   // raw: 3 columns per request (36 B per uint4 step in flight), 2 steps per
   // thread at 3 x 512 threads/SM keep ~110 KB/SM in flight within 42 registers
@@ -250,13 +277,16 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
   } else {
     if (blockIdx.x == 0 && threadIdx.x < head) {
       const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
-      if (BINS) a.bins_out[threadIdx.x] = (uint8_t)b;
+      if (BINS) (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)b;
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
       const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
-      if (BINS) a.bins_out[tail_first + threadIdx.x] = (uint8_t)b;
+      if (BINS) {
+        if (PACK) a.bins_side[4 + threadIdx.x] = (uint8_t)b;
+        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)b;
+      }
     }
-    uint32_t *bins4 = BINS ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
+    uint32_t *bins4 = (BINS && !PACK) ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
     const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
     // grid-stride stripes: at every step the whole grid reads kUnroll contiguous
     // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
@@ -271,19 +301,28 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
         uint4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S);
+        unsigned long long plo = 0ull;
+        uint32_t phi = 0u;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
-          if (BINS) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(w) : "memory");
+          if (BINS && PACK) pack_into(w, u, plo, phi);
+          else if (BINS) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(w) : "memory");
         }
+        if (BINS && PACK) store_chunk(a, k * S + me, plo, phi);
       } else {
+        unsigned long long plo = 0ull;
+        uint32_t phi = 0u;
 #pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (base + u * S < n4) {
-            const uint32_t w =
-                add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S));
-            if (BINS) bins4[base + u * S] = w;
+        for (int u = 0; u < U; ++u) {
+          const uint64_t j = base + u * S;
+          if (j < n4) {
+            const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, j) : sp.load4(body, j));
+            if (BINS && PACK) pack_into(w, u, plo, phi);
+            else if (BINS) bins4[j] = w;
           }
+        }
+        if (BINS && PACK) store_chunk(a, k * S + me, plo, phi);
       }
       maybe_flush(a.flush_iters);
     }
@@ -320,6 +359,7 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
 struct Variant {
   bool raw;      // estimate L_total from raw columns (NEXT-1)
   bool bins;     // also write per-request bins (u8)
+  bool pack;     // ... 6-bit packed (|E| < 64)
   int lutw;      // 1, 2 (LUT bytes per cell) or 0 (binary search)
   int R;         // 32 lane-private replicas or 1
   bool split;    // 16-bit mass halves
@@ -340,6 +380,7 @@ Variant choose(const TraceArgs &a, int block) {
   Variant v;
   v.raw = a.body != nullptr;
   v.bins = a.bins_out != nullptr;
+  v.pack = v.bins && a.bins_pack;
   v.lutw = a.lut_cells ? (a.lut_u8 ? 1 : 2) : 0;
   v.mass = a.want_mass != 0;
   v.R = 32;
@@ -366,8 +407,8 @@ uint32_t flush_iters_for(const TraceArgs &a, const Variant &v, int block) {
   return (uint32_t)it;
 }
 
-template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS = false>
-void *kernel_ptr() { return reinterpret_cast<void *>(&k1_trace<LUTW, R, SPLIT, MASS, RAW, BINS>); }
+template <int LUTW, int R, bool SPLIT, bool MASS, bool RAW, bool BINS = false, bool PACK = false>
+void *kernel_ptr() { return reinterpret_cast<void *>(&k1_trace<LUTW, R, SPLIT, MASS, RAW, BINS, PACK>); }
 
 template <bool RAW>
 void *pick_kernel_src(const Variant &v) {
@@ -385,21 +426,37 @@ void *pick_kernel_src(const Variant &v) {
 }
 
 // the bin-writing variants exist for the plain u8-LUT path only (|E| < 256)
+template <bool PACK>
 void *pick_kernel_bins(const Variant &v) {
   if (v.raw || v.lutw != 1) return nullptr;
-  if (!v.mass) return v.R == 32 ? kernel_ptr<1, 32, false, false, false, true>() : kernel_ptr<1, 1, false, false, false, true>();
-  if (v.R == 32) return v.split ? kernel_ptr<1, 32, true, true, false, true>() : kernel_ptr<1, 32, false, true, false, true>();
-  return v.split ? kernel_ptr<1, 1, true, true, false, true>() : kernel_ptr<1, 1, false, true, false, true>();
+  if (!v.mass)
+    return v.R == 32 ? kernel_ptr<1, 32, false, false, false, true, PACK>() : kernel_ptr<1, 1, false, false, false, true, PACK>();
+  if (v.R == 32)
+    return v.split ? kernel_ptr<1, 32, true, true, false, true, PACK>() : kernel_ptr<1, 32, false, true, false, true, PACK>();
+  return v.split ? kernel_ptr<1, 1, true, true, false, true, PACK>() : kernel_ptr<1, 1, false, true, false, true, PACK>();
 }
 
 void *pick_kernel(const Variant &v) {
-  if (v.bins) return pick_kernel_bins(v);
+  if (v.bins) return v.pack ? pick_kernel_bins<true>(v) : pick_kernel_bins<false>(v);
   return v.raw ? pick_kernel_src<true>(v) : pick_kernel_src<false>(v);
 }
 
 }  // namespace
 
 size_t trace_smem_bytes(const TraceArgs &a, int block) { return smem_for(a, choose(a, block)); }
+
+int trace_grid(const TraceArgs &a, int grid, int block) {
+  const Variant v = choose(a, block);
+  if (!(v.raw || v.bins)) return grid;
+  void *k = pick_kernel(v);
+  const size_t smem = smem_for(a, v);
+  if (!k || cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return grid;
+  int per_sm = 0, dev = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, block, smem) != cudaSuccess) return grid;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return std::min(grid, std::max(1, per_sm) * sms);
+}
 
 cudaError_t trace_occupancy(const TraceArgs &a, int block, size_t smem, int *per_sm) {
   void *k = pick_kernel(choose(a, block));
@@ -414,6 +471,9 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
   a.flush_iters = flush_iters_for(a, v, block);
   // u32 per-block counters: keep every block below 2^31 requests per launch
   const uint64_t cap = (uint64_t)grid * (1ull << 31);
+  // the packed bin stream assumes one body per trace (a piece boundary would
+  // put a body uint4 into the side bytes); cap is ~1e12 requests anyway
+  if (a0.bins_out && a0.bins_pack && a0.n > cap) return cudaErrorInvalidValue;
   void *k = pick_kernel(v);
   if (!k) return cudaErrorInvalidValue;
   if (v.raw || v.bins) {
@@ -432,7 +492,7 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
   }
   for (uint64_t off = 0; off < a0.n; off += cap) {
     if (a0.len) a.len = a0.len + off;
-    if (a0.bins_out) a.bins_out = a0.bins_out + off;
+    if (a0.bins_out && !a0.bins_pack) a.bins_out = a0.bins_out + off;   // (packed: one piece, checked above)
     if (a0.body) {
       a.body = a0.body + off;
       a.maxout = a0.maxout + off;

@@ -871,7 +871,7 @@ namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident,
                      const TraceArgs *raw = nullptr, uint8_t *bins = nullptr, uint32_t *route_out = nullptr,
-                     uint32_t route_model = 0);
+                     uint32_t route_model = 0, uint8_t *bins_side = nullptr, uint8_t *bins_hi = nullptr);
 }
 
 fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
@@ -894,17 +894,35 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   // trace then never needs a device copy. Otherwise: K4 re-reads L_total
   // (from a device copy for host traces).
   const bool bin_pass = p->lut_cells && p->lut_u8;
+  // |E| + 1 <= 64 bins, device trace: 6-bit packed bins (0.75 B per request each way)
+  const bool pack = bin_pass && p->nbins <= 64 && !(len && is_host_pointer(len));
   const uint32_t *src = len;
   uint32_t *resident = nullptr;
-  uint8_t *bins = nullptr;
+  uint8_t *bins = nullptr, *side = nullptr, *bins_hi = nullptr;
+  uint32_t head = 0;
+  int k1_grid_used = p->k1_grid;
   if (bin_pass) {
     if (d_decision && n_local) {
-      // the bin buffer is placed so that bins + i and len + i share the 4-B
-      // phase the trace pass needs for its 32-bit stores of 4 bins
-      // (host traces are processed from 256-B aligned staging chunks: phase 0)
+      // elements before the trace pass's first 16-B aligned uint4 (host traces
+      // are processed from 256-B aligned staging chunks: none)
       const uintptr_t lp = is_host_pointer(len) ? 0 : reinterpret_cast<uintptr_t>(len);
       const uint64_t head_phase = (4 - ((lp & 15u) >> 2)) & 3u;
-      const uint64_t need = n_local + 16;
+      head = (uint32_t)head_phase;
+      // packed: [16 B side bytes (head / tail bins)][u64 x chunks][u32 x chunks],
+      // one chunk per (step, thread) of the trace pass (TraceArgs::bins_pack);
+      // bytes: one bin per request, placed so that bins + i and len + i share
+      // the 4-B phase the trace pass needs for its 32-bit stores of 4 bins
+      uint64_t chunks = 0;
+      if (pack) {
+        TraceArgs tq = p->ta;
+        tq.bins_out = reinterpret_cast<uint8_t *>(16);   // any non-null: the bin variant's grid
+        tq.bins_pack = 1;
+        k1_grid_used = trace_grid(tq, p->k1_grid, p->k1_block);
+        const uint64_t S = (uint64_t)k1_grid_used * p->k1_block;
+        const uint64_t n4 = (n_local - std::min<uint64_t>(n_local, head_phase)) / 4;
+        chunks = std::max<uint64_t>(1, (n4 + 4 * S - 1) / (4 * S)) * S;
+      }
+      const uint64_t need = pack ? 16 + 12 * chunks + 16 : n_local + 16;
       if (p->bins_cap < need) {
         cudaFree(p->d_bins);
         p->d_bins = nullptr;
@@ -912,7 +930,13 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
         CUDA_TRY(p, cudaMalloc(&p->d_bins, need), "cudaMalloc bins");
         p->bins_cap = need;
       }
-      bins = p->d_bins + ((4 - head_phase) & 3u);
+      if (pack) {
+        side = p->d_bins;
+        bins = p->d_bins + 16;                 // u64 low nibbles [chunks]
+        bins_hi = bins + 8 * chunks;           // u32 high parts [chunks]
+      } else {
+        bins = p->d_bins + ((4 - head_phase) & 3u);
+      }
     }
   } else if (n_local && len && is_host_pointer(len)) {
     if (p->resident_cap < n_local) {
@@ -933,13 +957,18 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   const bool sliced = p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID);   // ranks split the grid
   uint32_t *route = reinterpret_cast<uint32_t *>(p->d_rcounts);
   fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, stream, resident, nullptr, bins,
-                            routing && !sliced ? route : nullptr, route_model);
+                            routing && !sliced ? route : nullptr, route_model, side, bins_hi);
   if (st != FP_OK) return st;
   if (routing) {
     LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
-    cudaError_t e = launch_route_bins(bins, d_decision, n_local, sliced ? p->d_best : nullptr,
-                                      sliced ? p->world : 1, (uint32_t)p->models.size(), route_model,
-                                      p->ta.edges, (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s);
+    const fp_candidate *recs = sliced ? p->d_best : nullptr;
+    const int ranks = sliced ? p->world : 1;
+    cudaError_t e =
+        pack ? launch_route_packed(bins, bins_hi, side, head, d_decision, n_local, recs, ranks,
+                                   (uint32_t)p->models.size(), route_model, p->ta.edges, (uint32_t)p->edges.size(),
+                                   route, k1_grid_used, p->k1_block, s)
+             : launch_route_bins(bins, d_decision, n_local, recs, ranks, (uint32_t)p->models.size(), route_model,
+                                 p->ta.edges, (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
     p->launches += sliced ? 2 : 1;
   }
@@ -1085,7 +1114,8 @@ fp_status route_batch_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, c
 namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident, const TraceArgs *raw,
-                     uint8_t *bins, uint32_t *route_out, uint32_t route_model) {
+                     uint8_t *bins, uint32_t *route_out, uint32_t route_model, uint8_t *bins_side,
+                     uint8_t *bins_hi) {
   if (!p) return FP_ERR_INVALID_ARG;
   if (n_local && !d_len && !raw) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
@@ -1107,7 +1137,12 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
     TraceArgs t = p->ta;
     t.len = ptr;
     t.n = n;
-    t.bins_out = bins ? bins + off : nullptr;
+    // packed bins: this chunk's body starts at global uint4 off / 4 (chunks are
+    // whole multiples of 4 elements except the last, and have no head)
+    t.bins_out = bins ? bins + (bins_side ? 0 : off) : nullptr;   // packed: device traces (one call, off = 0)
+    t.bins_hi = bins_hi;
+    t.bins_pack = bins_side ? 1u : 0u;
+    t.bins_side = bins_side;
     LaunchTimer lt(p, FP_KERNEL_TRACE, s);
     cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");

@@ -297,3 +297,29 @@ def test_sweep_and_route_async_device_pick(name, model):
     b = obest[model]
     odec, _ = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
     assert np.array_equal(dec.cpu().numpy(), odec)
+
+
+@pytest.mark.parametrize("n,off,doff", [(1, 0, 0), (3, 1, 0), (5, 3, 1), (17, 2, 0), (1000, 1, 2),
+                                        (227_328 * 16 + 7, 0, 0), (227_328 * 16 * 3 + 5, 3, 4),
+                                        (2_000_001, 2, 3)])
+def test_sweep_and_route_packed_bins_63_edges(n, off, doff):
+    """6-bit packed bins at the limit (63 edges -> 64 bins, bins 0..63 all
+    used): tiny and ragged traces, every pointer phase of the trace and of the
+    decision buffer, and sizes that end exactly on / just past a whole step of
+    the trace pass's grid (its chunk layout)."""
+    b = [256 * k for k in range(1, 63)]                        # 62 thresholds + C_L = 63 edges
+    cfg = make_config("e63", "SG", 9, n, 10000.0, ["qwen3-235b-a22b"], ["b200-180g"], b, [], [262144])
+    full = generate_host(cfg.shape, cfg.seed, 0, n + off)
+    L = full[off:]
+    plan = _plan(cfg)
+    assert fp.fleet_plan_info(plan)["n_edges"] == 63
+    dec = torch.full((n + 16,), 255, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(full)[off:], cfg.rate_rps, route_model=0, decision=dec[doff:])
+    _, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    bb = obest[0]
+    odec, oc = oracle.route_batch(L, int(bb["b_short"]), int(bb["c_short"]), int(bb["c_long"]))
+    got = dec.cpu().numpy()
+    assert np.array_equal(got[doff:doff + n], odec)
+    assert (got[:doff] == 255).all() and (got[doff + n:] == 255).all()     # nothing written outside
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
