@@ -173,7 +173,7 @@ def run_reference(args, cfg):
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
                              "sample": f"each step: first {n:,} requests of the {cfg.name} trace"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ GPU path ----
@@ -477,12 +477,28 @@ def run_ours(args, cfg):
         line["next1_fused_estimation"] = next1_fused_estimation(fp, cfg, n)
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
-    print(json.dumps(line), flush=True)
+    emit(line)
     if multi:
         dist.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line on stdout. Everything else that writes to fd 1 (NCCL's
+    version banner at communicator init, library diagnostics) is sent to
+    stderr by main(), so stdout carries exactly this line."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)

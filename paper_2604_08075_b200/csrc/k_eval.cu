@@ -309,16 +309,20 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
     if (lane == 0) {
       BlockBest *bb = (POOL3 ? a.block_best3 : a.block_best) + (size_t)m * gridDim.x + blockIdx.x;
       bb->cost = bc; bb->index = bi; bb->valid = bv;
-      __threadfence();
-      unsigned int prev = atomicAdd((POOL3 ? a.done3 : a.done) + m, 1u);
-      is_last = (prev == gridDim.x - 1);
+      if (gridDim.x == 1) {
+        is_last = true;                 // one block per model: no arrival protocol
+      } else {
+        __threadfence();
+        unsigned int prev = atomicAdd((POOL3 ? a.done3 : a.done) + m, 1u);
+        is_last = (prev == gridDim.x - 1);
+      }
     }
   }
   __syncthreads();
   if (!is_last) return;
 
   // ---- last block of model m: reduce the per-block winners, emit the record ----
-  __threadfence();
+  if (gridDim.x > 1) __threadfence();
   bc = 0.0; bi = 0xffffffffu; bv = 0;
   for (uint32_t j = threadIdx.x; j < gridDim.x; j += blockDim.x) {
     const volatile BlockBest *bb = (POOL3 ? a.block_best3 : a.block_best) + (size_t)m * gridDim.x + j;

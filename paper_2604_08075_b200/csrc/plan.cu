@@ -470,6 +470,7 @@ fp_status upload(fp_plan *p) {
     return fail(p, FP_ERR_CONFIG, "FP_K3_BLOCK must be a multiple of 32 in [32, 256]");
   p->k3_grid_x = (int)std::min<uint64_t>(cap * (256 / p->k3_block),
                                          std::max<uint64_t>(1, (widest + p->k3_block - 1) / p->k3_block));
+  p->k3_grid_x = std::max(1, std::min(p->k3_grid_x, env_int("FP_K3_GRID", p->k3_grid_x)));
   if (p->k3_grid_x > 65535 * 64) return fail(p, FP_ERR_CONFIG, "candidate grid too large for one launch");
   CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * p->k3_grid_x * sizeof(BlockBest)), "cudaMalloc block_best");
   CUDA_TRY(p, cudaMalloc(&p->d_done, M * sizeof(unsigned int)), "cudaMalloc done");
