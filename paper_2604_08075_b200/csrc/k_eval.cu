@@ -23,7 +23,30 @@ struct Shared {
   unsigned long long *mass_le;  // [nbins]
   unsigned long long *nseq;     // [n_gpus][n_windows]
   double *mu;                   // [n_gpus][n_windows]
+  double *rmu;                  // [n_gpus][n_windows] RN(1/mu), 0 = use the IEEE division
+  double rN;                    // RN(1/N), 0 = use the IEEE division
 };
+
+// RN(x / d) for x >= 0. With y = RN(1/d) (y != 0: d and x in range) it is
+// Markstein's correction q0 = x y, r = x - d q0 (exact, one FMA), q = q0 + r y,
+// which returns the correctly rounded quotient -- the IEEE division the oracle
+// performs -- in 3 FP64 operations instead of a DDIV sequence (~40
+// instructions with a MUFU and a slow-path branch). Its preconditions are
+// exponent ranges: |x|, |d| in [2^-400, 2^400] keep the quotient, the
+// residual and its correction normal. Otherwise: the IEEE division itself.
+__device__ __forceinline__ double mdiv(double x, double d, double y) {
+  if (y != 0.0 && x <= 0x1p400 && (x >= 0x1p-400 || x == 0.0)) {
+    const double q0 = __dmul_rn(x, y);
+    const double r = __fma_rn(-d, q0, x);
+    return __fma_rn(y, r, q0);
+  }
+  return __ddiv_rn(x, d);
+}
+
+// the reciprocal mdiv may use for divisor d (0 when d is out of its range)
+__device__ __forceinline__ double mrcp(double d) {
+  return (d >= 0x1p-400 && d <= 0x1p400) ? __ddiv_rn(1.0, d) : 0.0;
+}
 
 __device__ __forceinline__ double u2d(unsigned long long x) { return __ull2double_rn(x); }
 
@@ -45,12 +68,13 @@ __device__ __forceinline__ unsigned long long kv_budget(const unsigned long long
 }
 
 // One pool: I = ceil(lambda / mu); lambda == 0 -> 0; no capacity -> infeasible (R13).
-__device__ __forceinline__ bool pool_instances(double lam, double mu, uint64_t nseq,
+// rmu = RN(1/mu) or 0 (mdiv).
+__device__ __forceinline__ bool pool_instances(double lam, double mu, double rmu, uint64_t nseq,
                                                uint64_t *inst) {
   *inst = 0;
   if (lam == 0.0) return true;
   if (nseq == 0 || !(mu > 0.0)) return false;
-  double x = __ddiv_rn(lam, mu);
+  double x = mdiv(lam, mu, rmu);
   if (!(x <= 9007199254740992.0)) return false;
   *inst = (unsigned long long)ceil(x);
   return true;
@@ -93,16 +117,17 @@ __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64
   c.nseq_short = sh.nseq[gw + ws];
   c.nseq_long = sh.nseq[gw + wl];
   const double mu_s = sh.mu[gw + ws], mu_l = sh.mu[gw + wl];
+  const double rmu_s = sh.rmu[gw + ws], rmu_l = sh.rmu[gw + wl];
 
   const double dN = u2d(N);
-  c.alpha = __ddiv_rn(u2d(n_s), dN);
+  c.alpha = mdiv(u2d(n_s), dN, sh.rN);
   const double lam_s = __dmul_rn(c.alpha, a.rate);
-  const double lam_l = __dmul_rn(__ddiv_rn(u2d(c.n_long), dN), a.rate);
-  const double lam_h = __dmul_rn(__ddiv_rn(u2d(n_sl), dN), a.rate);
+  const double lam_l = __dmul_rn(mdiv(u2d(c.n_long), dN, sh.rN), a.rate);
+  const double lam_h = __dmul_rn(mdiv(u2d(n_sl), dN, sh.rN), a.rate);
 
-  const bool ok_s = pool_instances(lam_s, mu_s, c.nseq_short, &c.inst_short);
-  const bool ok_l = pool_instances(lam_l, mu_l, c.nseq_long, &c.inst_long);
-  const bool ok_h = pool_instances(lam_h, mu_l, c.nseq_long, &c.inst_homo);
+  const bool ok_s = pool_instances(lam_s, mu_s, rmu_s, c.nseq_short, &c.inst_short);
+  const bool ok_l = pool_instances(lam_l, mu_l, rmu_l, c.nseq_long, &c.inst_long);
+  const bool ok_h = pool_instances(lam_h, mu_l, rmu_l, c.nseq_long, &c.inst_homo);
   const bool ok_d = ok_s && ok_l;
   if (!ok_d) { c.inst_short = 0; c.inst_long = 0; }
   const unsigned long long gpi = a.deploy[((uint64_t)m * a.n_gpus + g) * 3 + 1];
@@ -114,8 +139,9 @@ __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64
   if (ok_d && ok_h && c.gpus_homo > 0)
     c.savings = __ddiv_rn(__dsub_rn(u2d(c.gpus_homo), u2d(c.gpus_dual)), u2d(c.gpus_homo));
   if (mu_s > 0.0 && mu_l > 0.0) {
-    c.rho = __ddiv_rn(mu_s, mu_l);
-    c.predicted_savings = __dmul_rn(c.alpha, __dsub_rn(1.0, __ddiv_rn(1.0, c.rho)));
+    c.rho = mdiv(mu_s, mu_l, rmu_l);
+    // the oracle's guard: a rho that underflows to 0 leaves predicted at 0
+    if (c.rho > 0.0) c.predicted_savings = __dmul_rn(c.alpha, __dsub_rn(1.0, __ddiv_rn(1.0, c.rho)));
   }
   if (c.n_short)
     c.occupancy_short = __ddiv_rn(u2d(c.mass_short), __dmul_rn(u2d(c.n_short), u2d(CS)));
@@ -155,14 +181,14 @@ __device__ void evaluate3(const EvalArgs &a, const Shared &sh, uint32_t m, uint6
   c.nseq2 = sh.nseq[w2];
   c.nseq3 = sh.nseq[w3];
   const double dN = u2d(N);
-  const double lam1 = __dmul_rn(__ddiv_rn(u2d(c.n1), dN), a.rate);
-  const double lam2 = __dmul_rn(__ddiv_rn(u2d(c.n2), dN), a.rate);
-  const double lam3 = __dmul_rn(__ddiv_rn(u2d(c.n3), dN), a.rate);
-  const double lamh = __dmul_rn(__ddiv_rn(u2d(c3), dN), a.rate);
-  const bool ok1 = pool_instances(lam1, sh.mu[w1], c.nseq1, &c.inst1);
-  const bool ok2 = pool_instances(lam2, sh.mu[w2], c.nseq2, &c.inst2);
-  const bool ok3 = pool_instances(lam3, sh.mu[w3], c.nseq3, &c.inst3);
-  const bool okh = pool_instances(lamh, sh.mu[w3], c.nseq3, &c.inst_homo);
+  const double lam1 = __dmul_rn(mdiv(u2d(c.n1), dN, sh.rN), a.rate);
+  const double lam2 = __dmul_rn(mdiv(u2d(c.n2), dN, sh.rN), a.rate);
+  const double lam3 = __dmul_rn(mdiv(u2d(c.n3), dN, sh.rN), a.rate);
+  const double lamh = __dmul_rn(mdiv(u2d(c3), dN, sh.rN), a.rate);
+  const bool ok1 = pool_instances(lam1, sh.mu[w1], sh.rmu[w1], c.nseq1, &c.inst1);
+  const bool ok2 = pool_instances(lam2, sh.mu[w2], sh.rmu[w2], c.nseq2, &c.inst2);
+  const bool ok3 = pool_instances(lam3, sh.mu[w3], sh.rmu[w3], c.nseq3, &c.inst3);
+  const bool okh = pool_instances(lamh, sh.mu[w3], sh.rmu[w3], c.nseq3, &c.inst_homo);
   const bool ok = ok1 && ok2 && ok3;
   if (!ok) { c.inst1 = c.inst2 = c.inst3 = 0; }
   const unsigned long long gpi = a.deploy[((uint64_t)m * a.n_gpus + g) * 3 + 1];
@@ -258,6 +284,7 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   sh.mass_le = sh.cnt_le + a.nbins;
   sh.nseq = sh.mass_le + a.nbins;
   sh.mu = reinterpret_cast<double *>(sh.nseq + (size_t)a.n_gpus * a.n_windows);
+  sh.rmu = sh.mu + (size_t)a.n_gpus * a.n_windows;
 
   // ---- prologue: K2 scan + capacity table for model m ----
   for (uint32_t j = threadIdx.x; j < a.nbins; j += blockDim.x) {
@@ -266,11 +293,14 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   }
   for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
     sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];
-    sh.mu[j] = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    const double mu = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    sh.mu[j] = mu;
+    sh.rmu[j] = mrcp(mu);
   }
   __syncthreads();
   block_scan_inclusive(sh.cnt_le, a.nbins, warp_tot);
   block_scan_inclusive(sh.mass_le, a.nbins, warp_tot);
+  sh.rN = mrcp(u2d(sh.cnt_le[a.nbins - 1]));
 
   // ---- this block's candidates: model m's part of the rank slice ----
   const uint64_t per = POOL3 ? a.per_model3 : a.per_model;
@@ -414,9 +444,9 @@ __device__ void evaluate_peak(const EvalArgs &a, const Shared &sh, uint32_t m, u
   c.lambda_short = __dmul_rn(u2d(ps), a.inv_w_s);
   c.lambda_long = __dmul_rn(u2d(pl), a.inv_w_s);
   c.lambda_homo = __dmul_rn(u2d(ph), a.inv_w_s);
-  const bool ok_s = pool_instances(c.lambda_short, sh.mu[gw + ws], nseq_s, &c.inst_short);
-  const bool ok_l = pool_instances(c.lambda_long, sh.mu[gw + wl], nseq_l, &c.inst_long);
-  const bool ok_h = pool_instances(c.lambda_homo, sh.mu[gw + wl], nseq_l, &c.inst_homo);
+  const bool ok_s = pool_instances(c.lambda_short, sh.mu[gw + ws], sh.rmu[gw + ws], nseq_s, &c.inst_short);
+  const bool ok_l = pool_instances(c.lambda_long, sh.mu[gw + wl], sh.rmu[gw + wl], nseq_l, &c.inst_long);
+  const bool ok_h = pool_instances(c.lambda_homo, sh.mu[gw + wl], sh.rmu[gw + wl], nseq_l, &c.inst_homo);
   const bool ok_d = ok_s && ok_l;
   if (!ok_d) { c.inst_short = 0; c.inst_long = 0; }
   const unsigned long long gpi = a.deploy[((uint64_t)m * a.n_gpus + g) * 3 + 1];
@@ -441,9 +471,13 @@ __global__ void __launch_bounds__(256) k3_peak(EvalArgs a) {
   sh.mass_le = nullptr;
   sh.nseq = reinterpret_cast<unsigned long long *>(smem);
   sh.mu = reinterpret_cast<double *>(sh.nseq + (size_t)a.n_gpus * a.n_windows);
+  sh.rmu = sh.mu + (size_t)a.n_gpus * a.n_windows;
+  sh.rN = 0.0;
   for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
     sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];
-    sh.mu[j] = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    const double mu = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    sh.mu[j] = mu;
+    sh.rmu[j] = mrcp(mu);
   }
   __syncthreads();
   const uint64_t lo = (uint64_t)m * a.per_model, hi = lo + a.per_model;
@@ -510,7 +544,7 @@ cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t sm
 }
 
 size_t eval_smem_bytes(const EvalArgs &a, int) {
-  return (size_t)a.nbins * 16 + (size_t)a.n_gpus * a.n_windows * 16;
+  return (size_t)a.nbins * 16 + (size_t)a.n_gpus * a.n_windows * 24;
 }
 
 cudaError_t eval_prepare() {

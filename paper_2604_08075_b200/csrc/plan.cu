@@ -1616,7 +1616,7 @@ fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *
   ea.results_pk = h_results ? p->d_results_pk : nullptr;
   {
     LaunchTimer lt(p, FP_KERNEL_EVAL, s);
-    cudaError_t e = launch_eval_peak(ea, grid_x, 256, (size_t)ea.n_gpus * ea.n_windows * 16, s);
+    cudaError_t e = launch_eval_peak(ea, grid_x, 256, (size_t)ea.n_gpus * ea.n_windows * 24, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "peak evaluation launch");
   }
   ++p->launches;
