@@ -245,13 +245,15 @@ def next4_peak_windows(fp, cfg, n, d_len, reps=3):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
+        # per call: the trace timer records two launches per call (K0w+K1w, then K2w)
         kh, nh = fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
         ke, ne = fp.fp_kernel_time(plan, fp.FP_KERNEL_EVAL)
-        hist_ms = kh / nh
+        hist_ms = kh / reps
         out[f"window_{wsec}s"] = {
             "windows": int(out["span_s"] // wsec) + 1, "ms": ms, "requests_per_s": n / (ms / 1e3),
             "hist_ms": hist_ms, "hist_GBps": 4.0 * n / (hist_ms / 1e3) / 1e9,
-            "hist_frac": 4.0 * n / (hist_ms / 1e3) / 1e9 / _peaks()[0], "eval_ms": ke / ne,
+            "hist_frac": 4.0 * n / (hist_ms / 1e3) / 1e9 / _peaks()[0], "eval_ms": ke / reps,
+            "timed_launches_per_call": {"hist": nh / reps, "eval": ne / reps},
             "best_savings_peak": [float(x) for x in best["savings"]],
             "best_gpus_dual_peak": [int(x) for x in best["gpus_dual"]]}
     out["note"] = ("hist = K0w window bounds + K1w 2-D histogram + K2w scan/maxima; algorithmic bytes "

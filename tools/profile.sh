@@ -19,9 +19,9 @@ cap() {
 }
 MAIN="$BENCH --no-next1 --no-next2 --no-next4 --no-k3-grid"
 cap trace k1_trace 3 "$MAIN"
-cap route k4_route_bins 3 "$MAIN"
+cap route k4_route_packed 3 "$MAIN"
 cap eval k3_eval 3 "$MAIN"
-cap pick k_pick_route 3 "$MAIN"
+RANK=0 WORLD_SIZE=1 LOCAL_RANK=0 MASTER_ADDR=127.0.0.1 MASTER_PORT=29561 cap pick_nccl k_pick_route 3 "$MAIN --collectives"
 cap k1_raw k1_trace 2 "python tools/raw_only.py 1000000000"
 cap k4_raw k4_route_raw 2 "python tools/raw_only.py 1000000000"
 cap c1_maps c1_maps 1 "python tools/calib_only.py --reps 1"
