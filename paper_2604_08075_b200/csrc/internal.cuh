@@ -105,6 +105,8 @@ struct EvalArgs {
   const uint16_t *b_edge, *cl_edge;     // index in E of each B / C_L
   const uint16_t *b_win, *cs_win, *cl_win;  // index in windows of each B / C_S / C_L
   uint32_t n_b, n_cs, n_cl, n_cs_eff;
+  // exact 32-bit division by n_b, n_cs_eff, n_cl, n_gpus: q = umul64hi(x, mul) (mul = ceil(2^64 / d), 0 for d = 1)
+  unsigned long long div_b = 0, div_cs = 0, div_cl = 0, div_g = 0;
   uint32_t n_models, n_gpus, n_windows;
   const uint32_t *model_arch;           // [m][4] n_l, n_h, d_h, b
   const unsigned long long *gpu_u64;    // [g][4] hbm, u_num, u_den, act

@@ -80,16 +80,28 @@ __device__ __forceinline__ bool pool_instances(double lam, double mu, double rmu
   return true;
 }
 
+// x / d and x % d for x < 2^32 by a precomputed multiplier mul = ceil(2^64 / d)
+// (0 for d = 1): floor(x mul / 2^64) = floor(x / d + delta), delta < 2^-32 <= 1/d,
+// so the quotient is exact (a 32-bit IDIV sequence costs ~20 instructions)
+__device__ __forceinline__ uint32_t divmod(uint32_t x, uint32_t d, unsigned long long mul, uint32_t &rem) {
+  const uint32_t q = mul ? (uint32_t)__umul64hi((unsigned long long)x, mul) : x;
+  rem = x - q * d;
+  return q;
+}
+
+// FULL: the whole record; otherwise only what the argmin needs (index,
+// flags, cost_dual -- bit-identical to the full record's), skipping the
+// savings / rho / predicted / occupancy divisions (large grids without results)
+template <bool FULL>
 __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
                          fp_candidate &c) {
   // decompose idx = (((m * G + g) * n_cl + l) * n_cs' + s) * n_b + k
-  // 32-bit index math: the plan guarantees < 2^32 candidates (u64 division
-  // is an emulated ~100-instruction sequence on the GPU)
-  uint32_t r = (uint32_t)idx;
-  const uint32_t k = r % a.n_b; r /= a.n_b;
-  const uint32_t s = r % a.n_cs_eff; r /= a.n_cs_eff;
-  const uint32_t l = r % a.n_cl; r /= a.n_cl;
-  const uint32_t g = r % a.n_gpus;
+  // 32-bit index math: the plan guarantees < 2^32 candidates
+  uint32_t r = (uint32_t)idx, k, s, l, g;
+  r = divmod(r, a.n_b, a.div_b, k);
+  r = divmod(r, a.n_cs_eff, a.div_cs, s);
+  r = divmod(r, a.n_cl, a.div_cl, l);
+  divmod(r, a.n_gpus, a.div_g, g);
   uint32_t B = a.b[k], CL = a.cl[l];
   uint32_t CS = a.n_cs ? a.cs[s] : B;
   c.index = (uint32_t)idx; c.model = m; c.gpu = g;
@@ -136,6 +148,8 @@ __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64
   const double price = a.price[g];
   if (ok_d) c.cost_dual = __dmul_rn(__dmul_rn(u2d(c.gpus_dual), price), a.hours);
   if (ok_h) c.cost_homo = __dmul_rn(__dmul_rn(u2d(c.gpus_homo), price), a.hours);
+  c.flags = FP_CAND_VALID | (ok_d ? FP_CAND_FEASIBLE : 0u) | (ok_h ? FP_CAND_HOMO_FEASIBLE : 0u);
+  if constexpr (!FULL) return;
   if (ok_d && ok_h && c.gpus_homo > 0)
     c.savings = __ddiv_rn(__dsub_rn(u2d(c.gpus_homo), u2d(c.gpus_dual)), u2d(c.gpus_homo));
   if (mu_s > 0.0 && mu_l > 0.0) {
@@ -147,7 +161,6 @@ __device__ void evaluate(const EvalArgs &a, const Shared &sh, uint32_t m, uint64
     c.occupancy_short = __ddiv_rn(u2d(c.mass_short), __dmul_rn(u2d(c.n_short), u2d(CS)));
   if (c.n_long)
     c.occupancy_long = __ddiv_rn(u2d(c.mass_long), __dmul_rn(u2d(c.n_long), u2d(CL)));
-  c.flags = FP_CAND_VALID | (ok_d ? FP_CAND_FEASIBLE : 0u) | (ok_h ? FP_CAND_HOMO_FEASIBLE : 0u);
 }
 
 // NEXT-2: three pools. idx = ((m * G + g) * n_cl + l) * n_pairs + p,
@@ -205,11 +218,13 @@ __device__ void evaluate3(const EvalArgs &a, const Shared &sh, uint32_t m, uint6
 template <bool POOL3> struct RecOf { using T = fp_candidate; };
 template <> struct RecOf<true> { using T = fp_pool3_candidate; };
 
+template <bool FULL = true>
 __device__ __forceinline__ void eval_any(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
                                          fp_candidate &c, double &cost) {
-  evaluate(a, sh, m, idx, c);
+  evaluate<FULL>(a, sh, m, idx, c);
   cost = c.cost_dual;
 }
+template <bool FULL = true>
 __device__ __forceinline__ void eval_any(const EvalArgs &a, const Shared &sh, uint32_t m, uint64_t idx,
                                          fp_pool3_candidate &c, double &cost) {
   evaluate3(a, sh, m, idx, c);
@@ -315,17 +330,26 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   double bc = 0.0;
   uint32_t bi = 0xffffffffu, bv = 0;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
-    Rec c;
-    double cost;
-    eval_any(a, sh, m, idx, c, cost);
-    if (POOL3) {
-      if (a.results3) reinterpret_cast<Rec *>(a.results3)[idx] = c;
-    } else if (a.results) {
-      reinterpret_cast<Rec *>(a.results)[idx - a.cand_first] = c;
+  const bool want = POOL3 ? a.results3 != nullptr : a.results != nullptr;
+  if (want) {
+    for (uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
+      Rec c;
+      double cost;
+      eval_any<true>(a, sh, m, idx, c, cost);
+      if (POOL3) reinterpret_cast<Rec *>(a.results3)[idx] = c;
+      else reinterpret_cast<Rec *>(a.results)[idx - a.cand_first] = c;
+      // indices increase along the loop, so strict '<' keeps the lowest index on ties
+      if ((c.flags & FP_CAND_FEASIBLE) && (!bv || cost < bc)) { bc = cost; bi = c.index; bv = 1; }
     }
-    // indices increase along the loop, so strict '<' keeps the lowest index on ties
-    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || cost < bc)) { bc = cost; bi = c.index; bv = 1; }
+  } else {
+    // no records requested: the argmin's fields only (the winner is
+    // re-evaluated in full by the last block)
+    for (uint64_t idx = lo + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
+      Rec c;
+      double cost;
+      eval_any<false>(a, sh, m, idx, c, cost);
+      if ((c.flags & FP_CAND_FEASIBLE) && (!bv || cost < bc)) { bc = cost; bi = c.index; bv = 1; }
+    }
   }
   warp_argmin(bc, bi, bv);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;

@@ -431,6 +431,12 @@ fp_status upload(fp_plan *p) {
   ea.n_models = M;
   ea.n_gpus = G;
   ea.n_windows = W;
+  // K3's index decomposition multipliers: ceil(2^64 / d), 0 for d = 1
+  auto magic = [](uint64_t d) -> unsigned long long { return d <= 1 ? 0ull : (~0ull) / d + 1ull; };
+  ea.div_b = magic(ea.n_b);
+  ea.div_cs = magic(ea.n_cs_eff);
+  ea.div_cl = magic(ea.n_cl);
+  ea.div_g = magic(G);
   ea.model_arch = reinterpret_cast<const uint32_t *>(B0 + off_arch);
   ea.gpu_u64 = reinterpret_cast<const unsigned long long *>(B0 + off_gu);
   ea.price = reinterpret_cast<const double *>(B0 + off_price);
