@@ -114,7 +114,8 @@ def _workload(cfg, n_per_rank, world):
     return {"workload": f"{cfg.name}: {cfg.description}", "name": cfg.name,
             "trace": cfg.shape, "seed": cfg.seed, "n_requests_per_gpu": n_per_rank,
             "n_requests_total": n_per_rank * world, "n_candidates": cfg.n_candidates(),
-            "rate_rps": cfg.rate_rps, "l2": "inputs larger than L2 (4 B x 1e9 = 4 GB per GPU > 126 MB)",
+            "rate_rps": cfg.rate_rps,
+            "l2": f"inputs larger than L2 (4 B x {n_per_rank:.3g} = {4 * n_per_rank / 1e9:.3g} GB per GPU > 126 MB)",
             "parallelism": f"dp{world} (trace sharded by global request index)"}
 
 
@@ -308,6 +309,12 @@ def run_ours(args, cfg):
     if multi:
         dist.init_process_group("nccl", device_id=dev)
     n = args.n or cfg.n_requests
+    if args.strong:
+        # strong scaling: the config's trace split over the ranks (global-index
+        # shards, fp_shard_range's rounding), instead of n requests per rank
+        first, n = fp.fp_shard_range(n, rank, world)
+    else:
+        first = rank * n
     cfg = cfg.with_n(n)
 
     uid = None
@@ -320,7 +327,7 @@ def run_ours(args, cfg):
                                 flags=fp.FP_FLAG_KERNEL_TIMING | (fp.FP_FLAG_COLLECTIVES if multi else 0))
     info = fp.fleet_plan_info(plan)
     # this rank's shard of the global trace: requests [rank*n, (rank+1)*n)
-    d_len = generate_device(cfg.shape, cfg.seed, rank * n, n)
+    d_len = generate_device(cfg.shape, cfg.seed, first, n)
     d_dec = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
@@ -363,7 +370,7 @@ def run_ours(args, cfg):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    total_requests = n * world
+    total_requests = (args.n or cfg.n_requests) if args.strong else n * world
     value = total_requests / (ms_step / 1e3)
 
     # ---- NEXT-2: three pools over the same histogram (rank-local, no collective) ----
@@ -446,14 +453,15 @@ def run_ours(args, cfg):
     cand_per_s = cfg.n_candidates() * args.steps / (ktime["eval"][0] / 1e3) if ktime["eval"][0] else None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if args.strong else "weak",
             "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
             "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic (seeded Philox MIX trace, generated on device; not timed)",
             "step": "sweep_and_route: K1 trace pass (+6-bit packed bins) -> K3 sweep + per-model argmin -> device "
                     "split pick -> K4p routing pass, stream-ordered with no host round trip; the best records stay "
                     "on the device and are read once after the timed loop (e2e reads them every step)",
-            "config": _workload(cfg, n, world),
+            "config": dict(_workload(cfg, n, world), n_requests_total=total_requests),
             "candidates_per_s": cand_per_s,
             "candidates_per_s_step": cfg.n_candidates() / (ms_step / 1e3),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktime.items()},
@@ -510,6 +518,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: split the config's trace over the ranks (default: weak, n per rank)")
     ap.add_argument("--collectives", action="store_true",
                     help="take the multi-GPU code path even at world 1 (NCCL group of one; for testing)")
     ap.add_argument("--no-next2", dest="next2", action="store_false",
