@@ -24,8 +24,9 @@ struct TraceArgs {
   uint32_t max_edge;        // e_max (mass is accumulated only for L <= e_max)
   uint32_t flush_iters;     // lane-slot mass flush period (iterations), >= 1
   uint32_t want_mass;
-  unsigned long long *g_cnt;   // [n_edges + 1] global accumulators (bins)
-  unsigned long long *g_mass;  // [n_edges + 1]
+  unsigned long long *g_cnt;   // copy 0 of the global accumulators: [copies][2][n_edges + 1] (cnt, mass)
+  unsigned long long *g_mass;  // = g_cnt + n_edges + 1
+  uint32_t hist_copies = 1;    // block b adds into copy b % hist_copies (spreads same-address atomics)
   // raw columns (NEXT-1; body != nullptr selects them instead of len)
   const uint32_t *body = nullptr;   // |r| bytes
   const uint32_t *maxout = nullptr; // max_output_tokens
@@ -98,8 +99,10 @@ cudaError_t route_occupancy(int block, int *per_sm);
 struct BlockBest { double cost; uint32_t index; uint32_t valid; };
 
 struct EvalArgs {
-  const unsigned long long *hist_cnt;   // [nbins] per-bin counts (global, all ranks)
-  const unsigned long long *hist_mass;  // [nbins]
+  const unsigned long long *hist_cnt;   // [copies][2][nbins] per-bin counts (global, all ranks), copy 0
+  const unsigned long long *hist_mass;  // = hist_cnt + nbins
+  uint32_t hist_copies = 1;             // K3 sums the copies (K1's spread atomics)
+  unsigned long long *hist_out = nullptr;  // [2][nbins] the summed histogram (written by block (0, 0))
   uint32_t nbins;                       // |E| + 1
   const uint32_t *b, *cs, *cl;          // grid values
   const uint16_t *b_edge, *cl_edge;     // index in E of each B / C_L

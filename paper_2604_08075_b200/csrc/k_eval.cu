@@ -302,9 +302,20 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   sh.rmu = sh.mu + (size_t)a.n_gpus * a.n_windows;
 
   // ---- prologue: K2 scan + capacity table for model m ----
+  // sum K1's accumulator copies; block (0, 0) also publishes the summed
+  // histogram (sweep_histogram, best_split's empty-trace check)
   for (uint32_t j = threadIdx.x; j < a.nbins; j += blockDim.x) {
-    sh.cnt_le[j] = a.hist_cnt[j];
-    sh.mass_le[j] = a.hist_mass[j];
+    unsigned long long cnt = 0, mass = 0;
+    for (uint32_t c = 0; c < a.hist_copies; ++c) {
+      cnt += a.hist_cnt[(size_t)c * 2 * a.nbins + j];
+      mass += a.hist_mass[(size_t)c * 2 * a.nbins + j];
+    }
+    sh.cnt_le[j] = cnt;
+    sh.mass_le[j] = mass;
+    if (a.hist_out && blockIdx.x == 0 && blockIdx.y == 0) {
+      a.hist_out[j] = cnt;
+      a.hist_out[a.nbins + j] = mass;
+    }
   }
   for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
     sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];

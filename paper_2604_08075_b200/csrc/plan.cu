@@ -98,7 +98,9 @@ struct fp_plan {
   size_t blob_bytes = 0;
   TraceArgs ta{};
   EvalArgs ea{};
-  unsigned long long *d_hist = nullptr;    // [2][nbins]
+  unsigned long long *d_hist = nullptr;    // [2][nbins] summed histogram (written by K3)
+  unsigned long long *d_hcopies = nullptr; // [hist_copies][2][nbins] K1's accumulators
+  uint32_t hist_copies = 1;
   unsigned long long *d_rcounts = nullptr; // [8]: route counts [5], mis-routes [2] (or the picked split)
   unsigned long long *d_cap = nullptr;     // [M][G][W] N_seq
   double *d_calib = nullptr;               // [256][2] estimator snapshot
@@ -395,6 +397,11 @@ fp_status upload(fp_plan *p) {
   CUDA_TRY(p, cudaMemcpy(p->d_blob, blob.data(), p->blob_bytes, cudaMemcpyHostToDevice), "upload tables");
   CUDA_TRY(p, cudaMalloc(&p->d_hist, 2ull * p->nbins * 8), "cudaMalloc hist");
   CUDA_TRY(p, cudaMemset(p->d_hist, 0, 2ull * p->nbins * 8), "memset hist");
+  // K1's accumulator copies: 16 for small |E| (a few KB), one for large ones
+  // (K3 sums them per block)
+  p->hist_copies = p->nbins <= 256 ? 16u : 1u;
+  CUDA_TRY(p, cudaMalloc(&p->d_hcopies, (size_t)p->hist_copies * 2 * p->nbins * 8), "cudaMalloc hist copies");
+  CUDA_TRY(p, cudaMemset(p->d_hcopies, 0, (size_t)p->hist_copies * 2 * p->nbins * 8), "memset hist copies");
   CUDA_TRY(p, cudaMalloc(&p->d_rcounts, 8 * 8), "cudaMalloc counts");
   CUDA_TRY(p, cudaMalloc(&p->d_best, (size_t)p->world * M * sizeof(fp_candidate)), "cudaMalloc best");
   CUDA_TRY(p, cudaMemset(p->d_best, 0, (size_t)p->world * M * sizeof(fp_candidate)), "memset best");
@@ -409,12 +416,15 @@ fp_status upload(fp_plan *p) {
   ta.n_edges = (uint32_t)p->edges.size();
   ta.max_edge = p->max_edge;
   ta.want_mass = !(p->flags & FP_FLAG_NO_MASS);
-  ta.g_cnt = p->d_hist;
-  ta.g_mass = p->d_hist + p->nbins;
+  ta.g_cnt = p->d_hcopies;
+  ta.g_mass = p->d_hcopies + p->nbins;
+  ta.hist_copies = p->hist_copies;
 
   EvalArgs &ea = p->ea;
-  ea.hist_cnt = p->d_hist;
-  ea.hist_mass = p->d_hist + p->nbins;
+  ea.hist_cnt = p->d_hcopies;
+  ea.hist_mass = p->d_hcopies + p->nbins;
+  ea.hist_copies = p->hist_copies;
+  ea.hist_out = p->d_hist;
   ea.nbins = p->nbins;
   ea.b = reinterpret_cast<const uint32_t *>(B0 + off_b);
   ea.cs = reinterpret_cast<const uint32_t *>(B0 + off_cs);
@@ -754,6 +764,7 @@ void fleet_plan_destroy(fp_plan *p) {
     if (p->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(p->comm);
     cudaFree(p->d_blob);
     cudaFree(p->d_hist);
+    cudaFree(p->d_hcopies);
     cudaFree(p->d_rcounts);
     cudaFree(p->d_cap);
     cudaFree(p->d_best);
@@ -1131,7 +1142,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
   // K1: trace pass into the global bin histogram
-  CUDA_TRY(p, cudaMemsetAsync(p->d_hist, 0, 2ull * p->nbins * 8, s), "memset hist");
+  CUDA_TRY(p, cudaMemsetAsync(p->d_hcopies, 0, (size_t)p->hist_copies * 2 * p->nbins * 8, s), "memset hist");
   fp_status st = FP_OK;
   if (raw) {
     if (n_local) {
@@ -1159,7 +1170,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   if (st != FP_OK) return st;
   // C1: sum the per-rank histograms
   if (p->dist) {
-    st = all_reduce_u64(p, p->d_hist, 2ull * p->nbins, s, "all-reduce(histogram)");
+    st = all_reduce_u64(p, p->d_hcopies, (size_t)p->hist_copies * 2 * p->nbins, s, "all-reduce(histogram)");
     if (st != FP_OK) return st;
   }
   // K2 + K3: scan, evaluate this rank's candidates, per-model argmin
