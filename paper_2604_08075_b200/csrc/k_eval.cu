@@ -284,7 +284,7 @@ __device__ void block_scan_inclusive(unsigned long long *data, uint32_t n,
 }
 
 template <bool POOL3>
-__global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
+__global__ void __launch_bounds__(256, 3) k3_eval(EvalArgs a) {
   using Rec = typename RecOf<POOL3>::T;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ unsigned long long warp_tot[32];
@@ -306,9 +306,21 @@ __global__ void __launch_bounds__(256) k3_eval(EvalArgs a) {
   // histogram (sweep_histogram, best_split's empty-trace check)
   for (uint32_t j = threadIdx.x; j < a.nbins; j += blockDim.x) {
     unsigned long long cnt = 0, mass = 0;
-    for (uint32_t c = 0; c < a.hist_copies; ++c) {
-      cnt += a.hist_cnt[(size_t)c * 2 * a.nbins + j];
-      mass += a.hist_mass[(size_t)c * 2 * a.nbins + j];
+    if (a.hist_copies == 16) {
+      // all 32 loads in flight at once (one L2 round trip, not sixteen)
+      unsigned long long vc[16], vm[16];
+#pragma unroll
+      for (uint32_t c = 0; c < 16; ++c) {
+        vc[c] = a.hist_cnt[(size_t)c * 2 * a.nbins + j];
+        vm[c] = a.hist_mass[(size_t)c * 2 * a.nbins + j];
+      }
+#pragma unroll
+      for (uint32_t c = 0; c < 16; ++c) { cnt += vc[c]; mass += vm[c]; }
+    } else {
+      for (uint32_t c = 0; c < a.hist_copies; ++c) {
+        cnt += a.hist_cnt[(size_t)c * 2 * a.nbins + j];
+        mass += a.hist_mass[(size_t)c * 2 * a.nbins + j];
+      }
     }
     sh.cnt_le[j] = cnt;
     sh.mass_le[j] = mass;
