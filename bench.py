@@ -288,6 +288,13 @@ def k3_large_grid(fp, generate_device, reps=5):
             "best_index_model0": int(best[0]["index"])}
 
 
+def _bcast_uid(fp, dist, rank):
+    """A fresh ncclUniqueId from rank 0 for the library's communicator."""
+    obj = [fp.fp_nccl_get_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
 def run_ours(args, cfg):
     import numpy as np
     import torch
@@ -317,24 +324,25 @@ def run_ours(args, cfg):
         first = rank * n
     cfg = cfg.with_n(n)
 
-    uid = None
-    if multi:
-        obj = [fp.fp_nccl_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+    uid = _bcast_uid(fp, dist, rank) if multi else None
+    # the timed loop's plan records CUDA events around the trace pass (the
+    # dominant kernel, for the roofline) only: an event pair costs a few us of
+    # stream time, and timing K3 and K4 too would add ~16 us to every step
+    # (1.5% of C5's, a third of C2's); the per-kernel breakdown is a second loop
+    coll = fp.FP_FLAG_COLLECTIVES if multi else 0
     plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
                                 nccl_unique_id=uid,
-                                flags=fp.FP_FLAG_KERNEL_TIMING | (fp.FP_FLAG_COLLECTIVES if multi else 0))
+                                flags=(0 if args.no_kernel_events else fp.FP_FLAG_TIME_TRACE) | coll)
     info = fp.fleet_plan_info(plan)
     # this rank's shard of the global trace: requests [rank*n, (rank+1)*n)
     d_len = generate_device(cfg.shape, cfg.seed, first, n)
     d_dec = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
 
-    def step(lengths, want_best=False):
+    def step(lengths, want_best=False, pl=None):
         # sweep_thresholds -> per-model argmin -> route_batch(model 0's best split), one ABI call;
         # the device-timed steps leave the best records on the device (asynchronous call)
-        return fp.sweep_and_route(plan, lengths, cfg.rate_rps, route_model=0, decision=d_dec, stream=stream,
+        return fp.sweep_and_route(pl or plan, lengths, cfg.rate_rps, route_model=0, decision=d_dec, stream=stream,
                                   want_best=want_best)
 
     def barrier():
@@ -345,25 +353,41 @@ def run_ours(args, cfg):
     for _ in range(args.warmup):
         step(d_len)
     barrier()
-    fp.fp_kernel_time_reset(plan)
+    if not args.no_kernel_events:
+        fp.fp_kernel_time_reset(plan)
     l0 = fp.fp_kernel_launches(plan)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
         for k in range(args.steps):
-            best, counts = step(d_len)
-            ev[k].record(stream)
+            step(d_len)
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
     best = fp.best_split(plan)                  # the records of the last timed step
-    per_step = sorted([e0.elapsed_time(ev[0])] + [ev[k - 1].elapsed_time(ev[k]) for k in range(1, args.steps)])
-    pct = lambda q: per_step[min(len(per_step) - 1, int(q * len(per_step)))]   # noqa: E731
     launches = fp.fp_kernel_launches(plan) - l0
     ms_local = e0.elapsed_time(e1)
-    ktime = {k: fp.fp_kernel_time(plan, kind) for k, kind in
+    k1_time = (0.0, 0) if args.no_kernel_events else fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
+
+    # ---- per-kernel breakdown and per-step spread: a second loop on a plan that
+    # times every kernel (not part of the headline value) ----
+    plan_b = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
+                                  nccl_unique_id=_bcast_uid(fp, dist, rank) if multi else None,
+                                  flags=fp.FP_FLAG_KERNEL_TIMING | coll)
+    for _ in range(2):
+        step(d_len, pl=plan_b)
+    barrier()
+    fp.fp_kernel_time_reset(plan_b)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    for k in range(args.steps):
+        step(d_len, pl=plan_b)
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize(dev)
+    per_step = sorted(ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps))
+    pct = lambda q: per_step[min(len(per_step) - 1, int(q * len(per_step)))]   # noqa: E731
+    ktime = {k: fp.fp_kernel_time(plan_b, kind) for k, kind in
              (("trace", fp.FP_KERNEL_TRACE), ("eval", fp.FP_KERNEL_EVAL), ("route", fp.FP_KERNEL_ROUTE))}
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     if multi:
@@ -376,10 +400,10 @@ def run_ours(args, cfg):
     # ---- NEXT-2: three pools over the same histogram (rank-local, no collective) ----
     next2 = None
     if args.next2:
-        fp.fp_kernel_time_reset(plan)
+        fp.fp_kernel_time_reset(plan_b)        # (its last sweep's histogram)
         for _ in range(3):
-            _, best3 = fp.sweep_three_pools(plan, cfg.rate_rps)
-        ms3, k3n = fp.fp_kernel_time(plan, fp.FP_KERNEL_EVAL)
+            _, best3 = fp.sweep_three_pools(plan_b, cfg.rate_rps)
+        ms3, k3n = fp.fp_kernel_time(plan_b, fp.FP_KERNEL_EVAL)
         nb = len(cfg.b_short)
         n3 = len(cfg.models) * len(cfg.gpus) * len(cfg.c_long) * nb * (nb - 1) // 2
         next2 = {"candidates": n3, "k3_three_pool_ms": ms3 / k3n,
@@ -430,10 +454,12 @@ def run_ours(args, cfg):
     bin_bytes = 0.75 if packed else 1.0
     algo_bytes = ({"trace": (4.0 + bin_bytes) * n, "route": (bin_bytes + 1.0) * n, "eval": 0.0} if bin_pass
                   else {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0})
-    kms, kcount = ktime[dom]
+    # the dominant kernel's launches inside the timed region (k1_time); the
+    # other kernels' numbers come from the breakdown loop
+    kms, kcount = k1_time if dom == "trace" else ktime[dom]
     per_launch_ms = kms / max(kcount, 1)
     per_launch_bytes = algo_bytes[dom] / max(1.0, kcount / args.steps)   # bytes per step / launches per step
-    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9
+    achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else float("nan")
     k_gbs = {k: (algo_bytes[k] * args.steps / (ktime[k][0] / 1e3) / 1e9 if ktime[k][0] and algo_bytes[k] else None)
              for k in ktime}
     kname = {"trace": "K1 k1_trace" + ((" (6-bit packed bin pass)" if packed else " (bin pass)") if bin_pass else ""),
@@ -444,7 +470,7 @@ def run_ours(args, cfg):
             "traffic": _traffic(cfg.name, dom), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": per_launch_bytes,
             "per_kernel_GBps": k_gbs,
-            "step_share": {k: v / ms_total for k, v in shares.items()},
+            "step_share": {k: v / sum(per_step) for k, v in shares.items()},   # breakdown loop
             # the whole step against the SURVEY §8(d) per-request figures of the
             # path it replaces (4 B sweep read + 4 B route read + 1 B decision)
             "step_paper_bytes_per_request": 9.0,
@@ -465,6 +491,10 @@ def run_ours(args, cfg):
             "candidates_per_s": cand_per_s,
             "candidates_per_s_step": cfg.n_candidates() / (ms_step / 1e3),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktime.items()},
+            "kernel_timing": ("timed loop: CUDA events around the trace pass only (value, roofline); "
+                              "kernel_ms_per_step, step_share and the p10/p50/p90 from a second loop of "
+                              "the same steps on a plan that times every kernel (~16 us of event overhead "
+                              "per step)"),
             "roofline": roof,
             "gpu_launches": launches,
             "next2_three_pools": next2,
@@ -518,6 +548,8 @@ def main():
     ap.add_argument("--n", type=int, default=0, help="requests per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernel-events", action="store_true",
+                    help="diagnostic: no per-kernel CUDA events in the timed loop (no roofline)")
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: split the config's trace over the ranks (default: weak, n per rank)")
     ap.add_argument("--collectives", action="store_true",

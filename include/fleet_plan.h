@@ -101,6 +101,9 @@ typedef struct fp_grid {
 #define FP_FLAG_REPLICATED_GRID 0x2u /* world > 1: every rank evaluates all candidates */
 #define FP_FLAG_KERNEL_TIMING 0x4u   /* record CUDA events around every kernel launch   */
 #define FP_FLAG_CHECK_ORDER 0x8u     /* sweep_peak_windows: verify arrival order (8 B/req) */
+#define FP_FLAG_TIME_TRACE 0x20u     /* record CUDA events around the trace-pass kernel
+                                        only (each event pair costs a few us of stream
+                                        time; timing K3/K4 too adds ~16 us per step)    */
 #define FP_FLAG_COLLECTIVES 0x10u    /* run the cross-rank steps even when world == 1
                                         (a one-rank NCCL communicator or the hooks): the
                                         multi-rank code path on a single GPU, for tests  */
@@ -398,10 +401,11 @@ uint64_t fp_kernel_launches(const fp_plan *plan);
 #define FP_KERNEL_EVAL 1  /* K3: scan + candidate evaluation + argmin      */
 #define FP_KERNEL_ROUTE 2 /* K4: route_batch                               */
 
-/* With FP_FLAG_KERNEL_TIMING: total device time (ms, CUDA events recorded on
- * the launch stream around each launch) and launch count of kernel `kind`
- * since the last fp_kernel_time_reset (or creation). Synchronizes those
- * events. FP_ERR_STATE without the flag. */
+/* With FP_FLAG_KERNEL_TIMING (every kind) or FP_FLAG_TIME_TRACE (FP_KERNEL_TRACE
+ * only): total device time (ms, CUDA events recorded on the launch stream
+ * around each launch) and launch count of kernel `kind` since the last
+ * fp_kernel_time_reset (or creation). Synchronizes those events. FP_ERR_STATE
+ * when the kind is not timed by the plan's flags. */
 fp_status fp_kernel_time(fp_plan *plan, int32_t kind, double *total_ms, uint64_t *launches);
 fp_status fp_kernel_time_reset(fp_plan *plan);
 

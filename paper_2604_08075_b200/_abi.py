@@ -20,6 +20,7 @@ FP_FLAG_REPLICATED_GRID = 0x2
 FP_FLAG_KERNEL_TIMING = 0x4
 FP_FLAG_CHECK_ORDER = 0x8
 FP_FLAG_COLLECTIVES = 0x10
+FP_FLAG_TIME_TRACE = 0x20
 FP_KERNEL_TRACE, FP_KERNEL_EVAL, FP_KERNEL_ROUTE = 0, 1, 2
 FP_CAND_VALID, FP_CAND_FEASIBLE, FP_CAND_HOMO_FEASIBLE = 1, 2, 4
 STATUS = ["FP_OK", "FP_ERR_INVALID_ARG", "FP_ERR_CONFIG", "FP_ERR_EMPTY_TRACE", "FP_ERR_ALIGNMENT",

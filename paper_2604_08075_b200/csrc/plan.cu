@@ -538,7 +538,8 @@ struct LaunchTimer {
   cudaStream_t s;
   cudaEvent_t stop = nullptr;
   LaunchTimer(fp_plan *p_, int kind, cudaStream_t s_) : p(p_), s(s_) {
-    if (!(p->flags & FP_FLAG_KERNEL_TIMING)) return;
+    if (!(p->flags & FP_FLAG_KERNEL_TIMING) && !((p->flags & FP_FLAG_TIME_TRACE) && kind == FP_KERNEL_TRACE))
+      return;
     auto &t = p->timers[kind];
     if (t.used == t.ev.size()) {
       cudaEvent_t a, b;
@@ -817,7 +818,8 @@ uint64_t fp_kernel_launches(const fp_plan *p) { return p ? p->launches : 0; }
 
 fp_status fp_kernel_time(fp_plan *p, int32_t kind, double *total_ms, uint64_t *launches) {
   if (!p || kind < 0 || kind > 2) return FP_ERR_INVALID_ARG;
-  if (!(p->flags & FP_FLAG_KERNEL_TIMING)) return fail(p, FP_ERR_STATE, "plan created without FP_FLAG_KERNEL_TIMING");
+  if (!(p->flags & FP_FLAG_KERNEL_TIMING) && !((p->flags & FP_FLAG_TIME_TRACE) && kind == FP_KERNEL_TRACE))
+    return fail(p, FP_ERR_STATE, "kernel kind %d is not timed (FP_FLAG_KERNEL_TIMING / FP_FLAG_TIME_TRACE)", kind);
   DeviceGuard g(p->device);
   auto &t = p->timers[kind];
   double tot = 0.0;
