@@ -67,13 +67,18 @@ def _rank(rank, world, port, name, n, flags, q):
         edges, cnt, mass = fp.sweep_histogram(plan)
         counts = fp.route_batch(plan, d, 8192, 16384, 65536)
         info = fp.fleet_plan_info(plan)
+        # the bench's step on this rank's shard: split picked across ranks on the
+        # device (sliced grid: all-gather + k_pick_route), packed or byte bins
+        dec = torch.zeros(count, dtype=torch.uint8, device="cuda")
+        sbest, _ = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec)
         q.put((rank, res.tobytes(), best.tobytes(), cnt.tobytes(), mass.tobytes(), counts,
-               info["cand_first"], info["cand_count"], None))
+               info["cand_first"], info["cand_count"], None,
+               (first, dec.cpu().numpy().tobytes(), sbest.tobytes() if sbest is not None else None)))
         fp.fleet_plan_destroy(plan)
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover
         import traceback
-        q.put((rank, None, None, None, None, None, 0, 0, traceback.format_exc()))
+        q.put((rank, None, None, None, None, None, 0, 0, traceback.format_exc(), None))
 
 
 @pytest.mark.parametrize("name,n,replicated", [("C5", 2_000_003, False), ("C3", 300_001, False),
@@ -94,7 +99,7 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
     for p in procs:
         p.join(timeout=120)
     for o in out:
-        assert o[-1] is None, o[-1]
+        assert o[8] is None, o[8]
     cfg = configs.CONFIGS[name]().with_n(n)
     L = generate_host(cfg.shape, cfg.seed, 0, n)
     allc, obest = oracle.sweep(cfg, L)
@@ -117,3 +122,12 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
         _, oc = oracle.route_batch(L, 8192, 16384, 65536, want_decisions=False)
         assert [o[5][k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
             [int(x) for x in oc]
+    # sweep_and_route: every rank routes its shard with the global best split
+    b = obest[0]
+    odec, _ = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    for o in out:
+        first, dec, sbest = o[9]
+        if sbest is not None:
+            assert sbest == obest.tobytes()
+        got = np.frombuffer(dec, dtype=np.uint8)
+        assert np.array_equal(got, odec[first:first + got.size])
