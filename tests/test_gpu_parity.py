@@ -368,3 +368,37 @@ def test_divisions_random_mu_and_rates(rate):
     o3, ob3 = oracle.sweep3(cfg, L)
     assert r3.tobytes() == o3.tobytes()
     assert b3.tobytes() == ob3.tobytes()
+
+
+@pytest.mark.slow
+def test_full_size_c5_step_against_oracle():
+    """The bench's step at its full size and launch configuration (C5, 1e9
+    requests, sweep_and_route with 6-bit packed bins): every candidate record of
+    the 1e9-request sweep and the per-model best splits equal the oracle's over
+    the whole trace (the oracle's definition loop takes ~10 s on the box's
+    cores), the histogram equals count_le at every edge, and sampled windows of
+    the decision bytes equal the oracle's Alg. 1 for the chosen split."""
+    cfg = configs.c5()
+    n = cfg.n_requests
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    d = generate_device(cfg.shape, cfg.seed, 0, n)
+    plan = _plan(cfg)
+    dec = torch.empty(n, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec)
+    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    allc, obest = oracle.sweep(cfg, L)
+    _compare_records(res, allc, "C5 full")
+    assert best.tobytes() == obest.tobytes()
+    edges, cnt, mass = fp.sweep_histogram(plan)
+    ocnt, omass = oracle.count_le(L, edges)
+    assert np.array_equal(np.cumsum(cnt)[:-1], ocnt) and int(cnt.sum()) == n
+    assert np.array_equal(np.cumsum(mass)[:-1], omass)
+    b = obest[0]
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
+        [int(b["n_short"]), int(b["n_long"]), int(b["n_reject"]), int(b["mass_short"]), int(b["mass_long"])]
+    rng = np.random.default_rng(3)
+    for first in list(rng.integers(0, n - (1 << 24), 3)) + [0, n - (1 << 24)]:
+        first = int(first)
+        odec, _ = oracle.route_batch(L[first:first + (1 << 24)], int(b["b_short"]), int(b["c_short"]),
+                                     int(b["c_long"]))
+        assert np.array_equal(dec[first:first + (1 << 24)].cpu().numpy(), odec), f"decisions @{first}"
