@@ -589,13 +589,6 @@ __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__
 // of 1 B. Launched with the trace pass's own grid x block: thread t reads its
 // chunks with one 8-B and one 4-B coalesced load per 16 requests and writes
 // 4 decision words (each warp store 128 B contiguous).
-__device__ __forceinline__ uint32_t unplane6(uint32_t lo16, uint32_t hi8) {
-  uint32_t n = (lo16 | (lo16 << 8)) & 0x00FF00FFu;
-  n = (n | (n << 4)) & 0x0F0F0F0Fu;             // nibble e -> byte e
-  uint32_t c = (hi8 | (hi8 << 12)) & 0x000F000Fu;
-  c = (c | (c << 6)) & 0x03030303u;             // crumb e -> byte e
-  return n | (c << 4);
-}
 
 template <bool VEC>
 __global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long *__restrict__ lo,
@@ -625,8 +618,13 @@ __global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long 
       q[0] = (uint8_t)d; q[1] = (uint8_t)(d >> 8); q[2] = (uint8_t)(d >> 16); q[3] = (uint8_t)(d >> 24);
     }
   };
+  // K1's pack_step layout: bins (u, e) -> byte e of word u, low nibble from the
+  // u-th nibble lane of lo, high 2 bits from bits 2u of byte e of hi
   auto word = [&](unsigned long long l, uint32_t c, int u) {
-    return dec_word_swar(unplane6((uint32_t)(l >> (16 * u)) & 0xFFFFu, (c >> (8 * u)) & 0xFFu), sk);
+    const uint32_t half = (uint32_t)(l >> (32 * (u >> 1)));
+    const uint32_t n = (half >> (4 * (u & 1))) & 0x0F0F0F0Fu;
+    const uint32_t h = (u == 3 ? (c >> 2) : (c << (4 - 2 * u))) & 0x30303030u;
+    return dec_word_swar(n | h, sk);
   };
   const uint64_t ustride = 4 * S;                 // bytes between a chunk's uint4 u and u + 1
   // full steps: four steps' chunks in flight per thread (48 B of loads), no bounds checks

@@ -176,25 +176,19 @@ struct SrcRaw {
   __device__ __forceinline__ uint32_t load1(uint64_t i) const { return estimate_l_total(body[i], mo[i], cat[i], tab); }
 };
 
-// Four bins packed in bytes (each < 64) -> the two parts of the 6-bit
-// packing: low nibbles as 16 bits (bin e at bits 4e) and high 2-bit parts as
-// 8 bits (bin e at bits 2e). ALU only (no shuffles: the hot loop's
-// shared-memory atomics already load the MIO pipe).
-__device__ __forceinline__ void split6(uint32_t w, uint32_t &lo16, uint32_t &hi8) {
-  uint32_t t = w & 0x0F0F0F0Fu;
-  t |= t >> 4;                                   // byte 0 = n1 n0, byte 2 = n3 n2
-  lo16 = __byte_perm(t, 0u, 0x4420);             // bytes 0, 2
-  uint32_t h = (w >> 4) & 0x03030303u;
-  h |= h >> 6;                                   // byte 0 = c1 c0 (4 bits), byte 2 = c3 c2
-  hi8 = (h & 0xFu) | ((h >> 12) & 0xF0u);
-}
-
-// accumulate uint4 u of this thread's step into the chunk words
-__device__ __forceinline__ void pack_into(uint32_t w, int u, unsigned long long &lo, uint32_t &hi) {
-  uint32_t l, h;
-  split6(w, l, h);
-  lo |= (unsigned long long)l << (16 * u);
-  hi |= h << (8 * u);
+// The 6-bit packing of a thread's step (4 words w_u of 4 byte-bins each,
+// every bin < 64), SIMD within the words -- no per-bin extraction:
+//   lo (u64) = (w0 & 0x0F..) | (w1 & 0x0F..) << 4  |  ((w2 & 0x0F..) | (w3 & 0x0F..) << 4) << 32
+//   hi (u32) = sum_u ((w_u >> 4) & 0x03030303) << 2u
+// i.e. byte e of each half of lo holds the low nibbles of bins (u, e) and
+// (u + 1, e), byte e of hi the high 2-bit parts of bins (0..3, e). ALU only
+// (no shuffles: the hot loop's shared-memory atomics already load the MIO pipe).
+__device__ __forceinline__ void pack_step(const uint32_t (&w)[4], unsigned long long &lo, uint32_t &hi) {
+  const uint32_t l01 = (w[0] & 0x0F0F0F0Fu) | ((w[1] & 0x0F0F0F0Fu) << 4);
+  const uint32_t l23 = (w[2] & 0x0F0F0F0Fu) | ((w[3] & 0x0F0F0F0Fu) << 4);
+  lo = (unsigned long long)l01 | ((unsigned long long)l23 << 32);
+  hi = ((w[0] >> 4) & 0x03030303u) | (((w[1] >> 4) & 0x03030303u) << 2) | (((w[2] >> 4) & 0x03030303u) << 4) |
+       (((w[3] >> 4) & 0x03030303u) << 6);
 }
 
 __device__ __forceinline__ void store_chunk(const TraceArgs &a, uint64_t c, unsigned long long lo, uint32_t hi) {
@@ -301,28 +295,36 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
         uint4 v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) v[u] = RAW ? sr.load4(body, base + u * S) : sp.load4(body, base + u * S);
-        unsigned long long plo = 0ull;
-        uint32_t phi = 0u;
+        uint32_t pw[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
-          if (BINS && PACK) pack_into(w, u, plo, phi);
+          if (BINS && PACK) pw[u & 3] = w;
           else if (BINS) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(w) : "memory");
         }
-        if (BINS && PACK) store_chunk(a, k * S + me, plo, phi);
+        if (BINS && PACK) {
+          unsigned long long plo;
+          uint32_t phi;
+          pack_step(pw, plo, phi);
+          store_chunk(a, k * S + me, plo, phi);
+        }
       } else {
-        unsigned long long plo = 0ull;
-        uint32_t phi = 0u;
+        uint32_t pw[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const uint64_t j = base + u * S;
           if (j < n4) {
             const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, j) : sp.load4(body, j));
-            if (BINS && PACK) pack_into(w, u, plo, phi);
+            if (BINS && PACK) pw[u & 3] = w;
             else if (BINS) bins4[j] = w;
           }
         }
-        if (BINS && PACK) store_chunk(a, k * S + me, plo, phi);
+        if (BINS && PACK) {
+          unsigned long long plo;
+          uint32_t phi;
+          pack_step(pw, plo, phi);
+          store_chunk(a, k * S + me, plo, phi);
+        }
       }
       maybe_flush(a.flush_iters);
     }
