@@ -38,7 +38,7 @@ namespace fp {
 namespace {
 
 constexpr int kCalBlock = 256;
-constexpr int kRound = 16;                 // records per segment per round
+constexpr int kRound = 8;                  // records per segment per round
 
 __device__ __forceinline__ uint64_t umin(uint64_t x, uint64_t y) { return x < y ? x : y; }
 
@@ -148,62 +148,81 @@ struct UVec<NC, false> {
 };
 
 // ---- coalesced staging of per-thread segments ---------------------------------
-// bytes / tokens [segment][16] u32 with 16-B groups swizzled by (segment >> 1) & 3,
-// categories [segment][16] u8
+// Rounds of kRound = 8 records per segment, 256 segments per block, double-
+// buffered: while round r is consumed, round r + 1 is copied global -> shared
+// by cp.async (no registers held, unlike a register prefetch, which kept the
+// kernels at 80 registers and 3 blocks per SM). bytes / tokens [segment][8]
+// u32 with the two 16-B groups swizzled by (segment >> 2) & 1 (each thread
+// then reads its own records conflict-free), categories [segment][8] u8.
 struct StageSmem {
   uint32_t *b, *t, *c;
 };
 
 constexpr size_t kStageBytes = (size_t)kCalBlock * kRound * 4 * 2 + (size_t)kCalBlock * kRound;
 constexpr size_t kScanBytes = 32 * sizeof(Aff);
+constexpr int kParts = kRound / 4;           // 16-B groups per segment per round
+static_assert(kRound == 8, "the swizzle below is for two 16-B groups");
 
 __device__ __forceinline__ uint32_t swz(uint32_t seg, uint32_t group) {
-  return seg * kRound + ((group ^ ((seg >> 1) & 3u)) << 2);
+  return seg * kRound + ((group ^ ((seg >> 2) & 1u)) << 2);
 }
 
-struct Pieces {              // the next round, held in registers while the current one runs
-  uint4 b[4], t[4], c;
-};
-
-__device__ __forceinline__ uint4 load4(const uint32_t *p, uint64_t g, uint64_t end, bool vec) {
-  if (vec && g + 4 <= end) return __ldcs(reinterpret_cast<const uint4 *>(p + g));
-  uint4 v;
-  v.x = g + 0 < end ? p[g + 0] : 0u;
-  v.y = g + 1 < end ? p[g + 1] : 0u;
-  v.z = g + 2 < end ? p[g + 2] : 0u;
-  v.w = g + 3 < end ? p[g + 3] : 0u;
-  return v;
+__device__ __forceinline__ StageSmem stage_at(unsigned char *smem, uint32_t i) {
+  StageSmem st;
+  st.b = reinterpret_cast<uint32_t *>(smem + i * kStageBytes);
+  st.t = st.b + kCalBlock * kRound;
+  st.c = st.t + kCalBlock * kRound;
+  return st;
 }
 
-__device__ __forceinline__ void fetch(const CalibArgs &a, uint64_t t0, uint64_t r, Pieces &pc) {
+__device__ __forceinline__ void cp_async(void *dst, const void *src, int bytes) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  if (bytes == 16) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+  else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+// full blocks (every segment complete, 16-B aligned columns): round r by cp.async
+__device__ __forceinline__ void issue_round(const CalibArgs &a, uint64_t t0, uint64_t r, const StageSmem &st) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q >> 2, part = q & 3u;
+  for (int i = 0; i < kParts; ++i) {
+    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q / kParts, part = q % kParts;
+    const uint64_t g = (t0 + seg) * a.seg + r * kRound + part * 4;
+    cp_async(st.b + swz(seg, part), a.bytes + g, 16);
+    cp_async(st.t + swz(seg, part), a.tokens + g, 16);
+  }
+  cp_async(st.c + threadIdx.x * (kRound / 4), a.cat + (t0 + threadIdx.x) * a.seg + r * kRound, 8);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t load1(const uint32_t *p, uint64_t g, uint64_t end) {
+  return g < end ? p[g] : 0u;
+}
+
+// partial blocks: round r synchronously, element by element (records past a
+// segment's end are staged with prompt_tokens = 0, which the update skips)
+__device__ __forceinline__ void stage_sync(const CalibArgs &a, uint64_t t0, uint64_t r, const StageSmem &st) {
+#pragma unroll
+  for (int i = 0; i < kParts; ++i) {
+    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q / kParts, part = q % kParts;
     const uint64_t base = (t0 + seg) * a.seg, end = umin(a.n, base + a.seg);
     const uint64_t g = base + r * kRound + part * 4;
-    pc.b[i] = load4(a.bytes, g, end, a.vec_bt);
-    pc.t[i] = load4(a.tokens, g, end, a.vec_bt);
+    uint4 vb, vt;
+    vb.x = load1(a.bytes, g, end); vb.y = load1(a.bytes, g + 1, end);
+    vb.z = load1(a.bytes, g + 2, end); vb.w = load1(a.bytes, g + 3, end);
+    vt.x = load1(a.tokens, g, end); vt.y = load1(a.tokens, g + 1, end);
+    vt.z = load1(a.tokens, g + 2, end); vt.w = load1(a.tokens, g + 3, end);
+    *reinterpret_cast<uint4 *>(st.b + swz(seg, part)) = vb;
+    *reinterpret_cast<uint4 *>(st.t + swz(seg, part)) = vt;
   }
   const uint64_t base = (t0 + threadIdx.x) * a.seg, end = umin(a.n, base + a.seg);
   const uint64_t g = base + r * kRound;
-  if (a.vec_c && g + kRound <= end) {
-    pc.c = __ldcs(reinterpret_cast<const uint4 *>(a.cat + g));
-  } else {
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
-    for (int j = 0; j < kRound; ++j)
-      if (g + j < end) w[j >> 2] |= (uint32_t)a.cat[g + j] << (8 * (j & 3));
-    pc.c = make_uint4(w[0], w[1], w[2], w[3]);
-  }
-}
-
-__device__ __forceinline__ void put(const StageSmem &st, const Pieces &pc) {
+  uint32_t w0 = 0u, w1 = 0u;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q >> 2, part = q & 3u;
-    *reinterpret_cast<uint4 *>(st.b + swz(seg, part)) = pc.b[i];
-    *reinterpret_cast<uint4 *>(st.t + swz(seg, part)) = pc.t[i];
+  for (int j = 0; j < kRound; ++j) {
+    const uint32_t v = g + j < end ? (uint32_t)a.cat[g + j] << (8 * (j & 3)) : 0u;
+    if (j < 4) w0 |= v; else w1 |= v;
   }
-  *reinterpret_cast<uint4 *>(st.c + threadIdx.x * 4) = pc.c;
+  *reinterpret_cast<uint2 *>(st.c + threadIdx.x * (kRound / 4)) = make_uint2(w0, w1);
 }
 
 __device__ __forceinline__ uint32_t get(const uint4 &v, int e) {
@@ -232,12 +251,12 @@ __device__ __forceinline__ double ratio(uint32_t num, uint32_t den) {
 
 template <typename Body>
 __device__ __forceinline__ void consume(const StageSmem &st, uint32_t last, Body &body) {
-  const uint4 cc = *reinterpret_cast<const uint4 *>(st.c + threadIdx.x * 4);
+  const uint2 cc = *reinterpret_cast<const uint2 *>(st.c + threadIdx.x * (kRound / 4));
 #pragma unroll
-  for (int gi = 0; gi < 4; ++gi) {
+  for (int gi = 0; gi < kParts; ++gi) {
     const uint4 vb = *reinterpret_cast<const uint4 *>(st.b + swz(threadIdx.x, gi));
     const uint4 vt = *reinterpret_cast<const uint4 *>(st.t + swz(threadIdx.x, gi));
-    const uint32_t cw = get(cc, gi);
+    const uint32_t cw = gi == 0 ? cc.x : cc.y;
     double o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) o[e] = ratio(get(vb, e), get(vt, e) | (get(vt, e) == 0u));
@@ -250,19 +269,31 @@ __device__ __forceinline__ void consume(const StageSmem &st, uint32_t last, Body
 }
 
 // Runs body(c_obs, category) over this thread's segment in order (valid records only).
+// Stage buffers 0 and 1 at smem + {0, kStageBytes}.
 template <typename Body>
-__device__ __forceinline__ void for_segment(const CalibArgs &a, const StageSmem &st, Body body) {
+__device__ __forceinline__ void for_segment(const CalibArgs &a, unsigned char *smem, Body body) {
   const uint64_t t0 = (uint64_t)blockIdx.x * kCalBlock;
   const uint64_t rounds = (a.seg + kRound - 1) / kRound;
   const uint32_t last = a.n_cats - 1;
-  Pieces pc;
-  fetch(a, t0, 0, pc);
-  for (uint64_t r = 0; r < rounds; ++r) {
-    __syncthreads();                 // previous round consumed
-    put(st, pc);
-    __syncthreads();
-    if (r + 1 < rounds) fetch(a, t0, r + 1, pc);
-    consume(st, last, body);
+  const bool full = a.vec_bt && a.vec_c && (t0 + kCalBlock) * a.seg <= a.n;
+  if (full) {
+    issue_round(a, t0, 0, stage_at(smem, 0));
+    for (uint64_t r = 0; r < rounds; ++r) {
+      if (r + 1 < rounds) issue_round(a, t0, r + 1, stage_at(smem, (uint32_t)(r + 1) & 1u));
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncthreads();
+      consume(stage_at(smem, (uint32_t)r & 1u), last, body);
+      __syncthreads();                 // buffer r & 1 is refilled at round r + 2
+    }
+  } else {
+    const StageSmem st = stage_at(smem, 0);
+    for (uint64_t r = 0; r < rounds; ++r) {
+      __syncthreads();                 // previous round consumed
+      stage_sync(a, t0, r, st);
+      __syncthreads();
+      consume(st, last, body);
+    }
   }
 }
 
@@ -278,7 +309,6 @@ __device__ __forceinline__ double pow_n(double beta, uint32_t n) {
 }
 
 struct Smem {
-  StageSmem st;
   Aff *scan;
   double *d0, *d1;      // [NC][kCalBlock]: d0 shared-memory state only, d1 always (sigma maps)
   uint32_t *u0, *u1;
@@ -286,11 +316,8 @@ struct Smem {
 
 __device__ __forceinline__ Smem smem_layout(unsigned char *smem, uint32_t nc, bool reg) {
   Smem s;
-  s.st.b = reinterpret_cast<uint32_t *>(smem);
-  s.st.t = s.st.b + kCalBlock * kRound;
-  s.st.c = s.st.t + kCalBlock * kRound;
-  s.scan = reinterpret_cast<Aff *>(smem + kStageBytes);
-  s.d0 = reinterpret_cast<double *>(smem + kStageBytes + kScanBytes);
+  s.scan = reinterpret_cast<Aff *>(smem + 2 * kStageBytes);
+  s.d0 = reinterpret_cast<double *>(smem + 2 * kStageBytes + kScanBytes);
   s.d1 = s.d0 + (reg ? 0 : nc * kCalBlock);
   s.u0 = reinterpret_cast<uint32_t *>(s.d1 + nc * kCalBlock);
   s.u1 = s.u0 + (reg ? 0 : nc * kCalBlock);
@@ -299,7 +326,7 @@ __device__ __forceinline__ Smem smem_layout(unsigned char *smem, uint32_t nc, bo
 
 // C1: per-thread c_hat maps -> within-block exclusive prefixes + block totals
 template <int NC, bool REG>
-__global__ void __launch_bounds__(kCalBlock, 3) c1_maps(CalibArgs a) {
+__global__ void __launch_bounds__(kCalBlock, 4) c1_maps(CalibArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem sm = smem_layout(smem, NC, REG);
   Vec<NC, REG> b;
@@ -308,7 +335,7 @@ __global__ void __launch_bounds__(kCalBlock, 3) c1_maps(CalibArgs a) {
   n.bind(sm.u0);
   for (uint32_t k = 0; k < NC; ++k) { b.set(k, 0.0); n.set(k, 0u); }
   const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
-  for_segment(a, sm.st, [&](double c, uint32_t k) {
+  for_segment(a, smem, [&](double c, uint32_t k) {
     b.set(k, __fma_rn(beta, b.get(k), __dmul_rn(w, c)));
     n.inc(k);
   });
@@ -365,7 +392,7 @@ __global__ void __launch_bounds__(1024) c2_scan(CalibArgs a, int which) {
 
 // C3: replay each segment from its c_hat start state; sigma maps; snapshots
 template <int NC, bool REG>
-__global__ void __launch_bounds__(kCalBlock, 3) c3_replay(CalibArgs a) {
+__global__ void __launch_bounds__(kCalBlock, 4) c3_replay(CalibArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const Smem sm = smem_layout(smem, NC, REG);
   Vec<NC, REG> c;
@@ -396,7 +423,7 @@ __global__ void __launch_bounds__(kCalBlock, 3) c3_replay(CalibArgs a) {
   }
   const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
   uint32_t snapped = 0u;          // bit k: this thread holds category k's snapshot
-  for_segment(a, sm.st, [&](double o, uint32_t k) {
+  for_segment(a, smem, [&](double o, uint32_t k) {
     const double prev = c.get(k);
     const double cn = __fma_rn(beta, prev, __dmul_rn(w, o));
     c.set(k, cn);
@@ -438,7 +465,7 @@ __global__ void c4_snap(CalibArgs a) {
 }
 
 size_t calib_smem(uint32_t nc, bool reg) {
-  return kStageBytes + kScanBytes + (size_t)nc * kCalBlock * 8 + (reg ? 0 : (size_t)nc * kCalBlock * (8 + 4 * 2));
+  return 2 * kStageBytes + kScanBytes + (size_t)nc * kCalBlock * 8 + (reg ? 0 : (size_t)nc * kCalBlock * (8 + 4 * 2));
 }
 
 template <int NC, bool REG>
