@@ -340,7 +340,13 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
   // this block's copy of the global accumulators: with one copy, 444 blocks x
   // 2 |E| same-address u64 atomics serialise at a few L2 slices (~35 ns per
   // block on C2; the C2 step's K1 fell from 33 to 23 us with 148 blocks)
-  unsigned long long *g_cnt = a.g_cnt + (size_t)(blockIdx.x % a.hist_copies) * 2 * nbins;
+  // (the block index is re-read here by a volatile asm, which the compiler
+  // cannot hoist above the main loop's volatile loads: computed up front, the
+  // copy address stayed live through the loop and cost a spill and ~7% on the
+  // raw-column trace pass)
+  uint32_t bx;
+  asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(bx));
+  unsigned long long *g_cnt = a.g_cnt + (size_t)(bx & (a.hist_copies - 1u)) * 2 * nbins;
   unsigned long long *g_mass = g_cnt + nbins;
   if constexpr (R == 32) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
