@@ -402,3 +402,29 @@ def test_full_size_c5_step_against_oracle():
         odec, _ = oracle.route_batch(L[first:first + (1 << 24)], int(b["b_short"]), int(b["c_short"]),
                                      int(b["c_long"]))
         assert np.array_equal(dec[first:first + (1 << 24)].cpu().numpy(), odec), f"decisions @{first}"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_size_configs_against_oracle(name):
+    """C2 (10.3M), C3 (1e8) and C4 (1e8) at the sizes BASELINE.json names: every
+    candidate record (up to 30,720) byte-identical to the oracle's sweep of the
+    whole trace, and the step (sweep_and_route) routes with the oracle's best
+    split -- decisions equal to Alg. 1 on sampled windows."""
+    cfg = configs.CONFIGS[name]()
+    n = cfg.n_requests
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    d = generate_device(cfg.shape, cfg.seed, 0, n)
+    plan = _plan(cfg)
+    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    allc, obest = oracle.sweep(cfg, L)
+    _compare_records(res, allc, f"{name} full")
+    assert fp.best_split(plan).tobytes() == obest.tobytes()
+    dec = torch.empty(n, dtype=torch.uint8, device="cuda")
+    best, _ = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[0]
+    win = min(n, 1 << 22)
+    for first in (0, n // 2, n - win):
+        odec, _ = oracle.route_batch(L[first:first + win], int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+        assert np.array_equal(dec[first:first + win].cpu().numpy(), odec), f"{name} decisions @{first}"
