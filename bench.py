@@ -330,9 +330,19 @@ def run_ours(args, cfg):
     # stream time, and timing K3 and K4 too would add ~16 us to every step
     # (1.5% of C5's, a third of C2's); the per-kernel breakdown is a second loop
     coll = fp.FP_FLAG_COLLECTIVES if multi else 0
+    if multi and args.p2p:
+        coll |= fp.FP_FLAG_P2P
+
+    def p2p_setup(pl):
+        # FP_FLAG_P2P: all-gather the ranks' IPC handles, open the peers' buffers
+        if coll & fp.FP_FLAG_P2P:
+            handles = [None] * world
+            dist.all_gather_object(handles, fp.fp_p2p_export(pl))
+            fp.fp_p2p_import(pl, handles)
     plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
                                 nccl_unique_id=uid,
                                 flags=(0 if args.no_kernel_events else fp.FP_FLAG_TIME_TRACE) | coll)
+    p2p_setup(plan)
     info = fp.fleet_plan_info(plan)
     # this rank's shard of the global trace: requests [rank*n, (rank+1)*n)
     d_len = generate_device(cfg.shape, cfg.seed, first, n)
@@ -375,6 +385,7 @@ def run_ours(args, cfg):
     plan_b = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
                                   nccl_unique_id=_bcast_uid(fp, dist, rank) if multi else None,
                                   flags=fp.FP_FLAG_KERNEL_TIMING | coll)
+    p2p_setup(plan_b)
     for _ in range(2):
         step(d_len, pl=plan_b)
     barrier()
@@ -507,6 +518,8 @@ def run_ours(args, cfg):
             "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
     if multi and world == 1:
         line["config"]["parallelism"] += "; --collectives: one-rank NCCL communicator in the step"
+    if coll & fp.FP_FLAG_P2P:
+        line["config"]["parallelism"] += "; --p2p: histogram sum over peer memory in K3 (no all-reduce)"
     if world == 1 and args.k3_grid:
         line["k3_large_grid"] = k3_large_grid(fp, generate_device)
     if world == 1 and args.next4:
@@ -554,6 +567,8 @@ def main():
                     help="strong scaling: split the config's trace over the ranks (default: weak, n per rank)")
     ap.add_argument("--collectives", action="store_true",
                     help="take the multi-GPU code path even at world 1 (NCCL group of one; for testing)")
+    ap.add_argument("--p2p", action="store_true",
+                    help="multi-rank: the histogram exchange through peer memory (FP_FLAG_P2P) instead of NCCL")
     ap.add_argument("--no-next2", dest="next2", action="store_false",
                     help="skip the three-pool (NEXT-2) measurement")
     ap.add_argument("--no-next1", dest="next1", action="store_false",

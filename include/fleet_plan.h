@@ -104,6 +104,17 @@ typedef struct fp_grid {
 #define FP_FLAG_TIME_TRACE 0x20u     /* record CUDA events around the trace-pass kernel
                                         only (each event pair costs a few us of stream
                                         time; timing K3/K4 too adds ~16 us per step)    */
+#define FP_FLAG_P2P 0x40u            /* world > 1 (or FP_FLAG_COLLECTIVES): the sweep's
+                                        histogram exchange goes through peer memory --
+                                        each rank's K1 accumulators are read by every
+                                        rank's K3 over NVLink (CUDA IPC), no all-reduce;
+                                        implies FP_FLAG_REPLICATED_GRID (no all-gather).
+                                        Needs fp_p2p_export / fp_p2p_import before the
+                                        first sweep; NCCL or the hooks still serve
+                                        route_batch, calibrate_replay, peak windows.
+                                        Every rank must issue the same sequence of
+                                        sweeps: a rank's K3 waits on the device for
+                                        every peer's K1 of the same step. world <= 64 */
 #define FP_FLAG_COLLECTIVES 0x10u    /* run the cross-rank steps even when world == 1
                                         (a one-rank NCCL communicator or the hooks): the
                                         multi-rank code path on a single GPU, for tests  */
@@ -390,6 +401,18 @@ fp_status sweep_histogram(fp_plan *plan, uint32_t *h_edges, uint64_t *h_bin_cnt,
 /* Writes a fresh 128-byte ncclUniqueId (for rank 0 to broadcast before
  * fleet_plan_create with world > 1). FP_ERR_NCCL if NCCL cannot be loaded. */
 fp_status fp_nccl_get_unique_id(void *out128);
+
+/* FP_FLAG_P2P: the 64-byte CUDA IPC handle of this rank's exchange buffer
+ * (K1 accumulators, two step parities, and the rank's arrival flag).
+ * Every rank all-gathers the handles (any host transport) and passes the
+ * [world][64] array, in rank order, to fp_p2p_import, which opens the peers'
+ * buffers (cudaIpcOpenMemHandle; NVLink peer access on an 8-GPU box; also
+ * works for processes sharing one device). FP_ERR_STATE without FP_P2P or on
+ * a second import; FP_ERR_CUDA if a handle cannot be opened. A sweep on a
+ * FP_P2P plan before the import fails with FP_ERR_STATE. */
+#define FP_P2P_HANDLE_BYTES 64
+fp_status fp_p2p_export(fp_plan *plan, void *handle_out);
+fp_status fp_p2p_import(fp_plan *plan, const void *handles);
 
 fp_status fleet_plan_info(const fp_plan *plan, fp_plan_info *out);
 

@@ -21,6 +21,8 @@ FP_FLAG_KERNEL_TIMING = 0x4
 FP_FLAG_CHECK_ORDER = 0x8
 FP_FLAG_COLLECTIVES = 0x10
 FP_FLAG_TIME_TRACE = 0x20
+FP_FLAG_P2P = 0x40
+FP_P2P_HANDLE_BYTES = 64
 FP_KERNEL_TRACE, FP_KERNEL_EVAL, FP_KERNEL_ROUTE = 0, 1, 2
 FP_CAND_VALID, FP_CAND_FEASIBLE, FP_CAND_HOMO_FEASIBLE = 1, 2, 4
 STATUS = ["FP_OK", "FP_ERR_INVALID_ARG", "FP_ERR_CONFIG", "FP_ERR_EMPTY_TRACE", "FP_ERR_ALIGNMENT",
@@ -30,7 +32,7 @@ EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split"
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
             "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
             "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools", "calibrate_replay",
-            "sweep_peak_windows"]
+            "sweep_peak_windows", "fp_p2p_export", "fp_p2p_import"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -164,6 +166,8 @@ def _load():
         "fp_candidate_range": (None, [c_u64, c_i32, c_i32, ctypes.POINTER(c_u64), ctypes.POINTER(c_u64)]),
         "fp_merge_best": (None, [c_vp, c_i32, c_u32, c_vp]),
         "fp_nccl_get_unique_id": (c_i32, [c_vp]),
+        "fp_p2p_export": (c_i32, [c_vp, c_vp]),
+        "fp_p2p_import": (c_i32, [c_vp, c_vp]),
         "fp_kernel_time": (c_i32, [c_vp, c_i32, ctypes.POINTER(c_dbl), ctypes.POINTER(c_u64)]),
         "fp_kernel_time_reset": (c_i32, [c_vp]),
         "sweep_thresholds_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_dbl,
@@ -400,6 +404,21 @@ def fp_nccl_get_unique_id():
     if st != 0:
         raise FleetPlanError(st, "ncclGetUniqueId failed")
     return buf.raw
+
+
+def fp_p2p_export(plan):
+    """This rank's CUDA IPC handle (FP_P2P_HANDLE_BYTES bytes) of its histogram exchange buffer."""
+    buf = ctypes.create_string_buffer(FP_P2P_HANDLE_BYTES)
+    _check(lib.fp_p2p_export(plan.handle, buf), plan)
+    return buf.raw
+
+
+def fp_p2p_import(plan, handles):
+    """Open every rank's exchange buffer; `handles` = the ranks' fp_p2p_export bytes in rank order."""
+    blob = b"".join(handles)
+    assert len(blob) == len(handles) * FP_P2P_HANDLE_BYTES
+    buf = ctypes.create_string_buffer(blob, len(blob))
+    _check(lib.fp_p2p_import(plan.handle, buf), plan)
 
 
 def fp_kernel_time(plan, kind):

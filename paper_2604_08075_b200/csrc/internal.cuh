@@ -102,6 +102,13 @@ struct EvalArgs {
   const unsigned long long *hist_cnt;   // [copies][2][nbins] per-bin counts (global, all ranks), copy 0
   const unsigned long long *hist_mass;  // = hist_cnt + nbins
   uint32_t hist_copies = 1;             // K3 sums the copies (K1's spread atomics)
+  // FP_FLAG_P2P: the histogram is the sum over ranks r of peer_hist[r] + p2p_off
+  // (each rank's K1 copies, this step's parity), read once every peer_flag[r]
+  // has reached p2p_epoch (no all-reduce)
+  const unsigned long long *const *peer_hist = nullptr;
+  const unsigned int *const *peer_flag = nullptr;
+  uint32_t p2p_world = 0, p2p_epoch = 0;
+  uint64_t p2p_off = 0;                 // u64 elements: parity * copies * 2 * nbins
   unsigned long long *hist_out = nullptr;  // [2][nbins] the summed histogram (written by block (0, 0))
   uint32_t nbins;                       // |E| + 1
   const uint32_t *b, *cs, *cl;          // grid values
@@ -149,6 +156,8 @@ struct EvalArgs {
   unsigned int *done_pk = nullptr;
 };
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
+// FP_FLAG_P2P: release this rank's accumulators of step `epoch` to its peers
+cudaError_t launch_p2p_signal(unsigned int *flag, unsigned int epoch, cudaStream_t s);
 cudaError_t launch_capacity(const EvalArgs &a, unsigned long long *cap, cudaStream_t s);  // fills cap_nseq
 cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);

@@ -304,6 +304,37 @@ __global__ void __launch_bounds__(256, 3) k3_eval(EvalArgs a) {
   // ---- prologue: K2 scan + capacity table for model m ----
   // sum K1's accumulator copies; block (0, 0) also publishes the summed
   // histogram (sweep_histogram, best_split's empty-trace check)
+  if (a.p2p_world) {
+    // peer-memory exchange (FP_FLAG_P2P): wait until every rank has released
+    // this step's accumulators (its K1 done, fenced system-wide), then read
+    // all ranks' copies directly -- the cross-rank sum fused into this prologue
+    if (threadIdx.x < a.p2p_world) {
+      const unsigned int *f = a.peer_flag[threadIdx.x];
+      unsigned int v;
+      for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int)(v - a.p2p_epoch) >= 0) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < a.nbins; j += blockDim.x) {
+      unsigned long long cnt = 0, mass = 0;
+      for (uint32_t r = 0; r < a.p2p_world; ++r) {
+        const unsigned long long *h = a.peer_hist[r] + a.p2p_off;
+        for (uint32_t c = 0; c < a.hist_copies; ++c) {
+          cnt += __ldcv(h + (size_t)c * 2 * a.nbins + j);
+          mass += __ldcv(h + (size_t)c * 2 * a.nbins + a.nbins + j);
+        }
+      }
+      sh.cnt_le[j] = cnt;
+      sh.mass_le[j] = mass;
+      if (a.hist_out && blockIdx.x == 0 && blockIdx.y == 0) {
+        a.hist_out[j] = cnt;
+        a.hist_out[a.nbins + j] = mass;
+      }
+    }
+  } else
   for (uint32_t j = threadIdx.x; j < a.nbins; j += blockDim.x) {
     unsigned long long cnt = 0, mass = 0;
     if (a.hist_copies == 16) {
@@ -603,6 +634,20 @@ cudaError_t eval_prepare() {
 cudaError_t launch_capacity(const EvalArgs &a, unsigned long long *cap, cudaStream_t s) {
   const uint64_t n = (uint64_t)a.n_models * a.n_gpus * a.n_windows;
   k_capacity<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, cap);
+  return cudaGetLastError();
+}
+
+namespace {
+// after K1 (stream order): make this rank's accumulators visible system-wide,
+// then publish the step's epoch (release) for the peers' K3 prologues
+__global__ void k_p2p_signal(unsigned int *flag, unsigned int epoch) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
+}  // namespace
+
+cudaError_t launch_p2p_signal(unsigned int *flag, unsigned int epoch, cudaStream_t s) {
+  k_p2p_signal<<<1, 1, 0, s>>>(flag, epoch);
   return cudaGetLastError();
 }
 

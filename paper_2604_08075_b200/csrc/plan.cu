@@ -101,6 +101,16 @@ struct fp_plan {
   unsigned long long *d_hist = nullptr;    // [2][nbins] summed histogram (written by K3)
   unsigned long long *d_hcopies = nullptr; // [hist_copies][2][nbins] K1's accumulators
   uint32_t hist_copies = 1;
+  // FP_FLAG_P2P: exchange buffer [2 parities][copies][2][nbins] u64 + the arrival flag,
+  // the peers' buffers opened by CUDA IPC, and device tables of their addresses
+  unsigned long long *d_xbuf = nullptr;
+  unsigned int *d_xflag = nullptr;
+  size_t xbuf_elems = 0;                    // u64 elements per parity
+  std::vector<void *> peer_open;            // opened IPC mappings (closed at destroy)
+  unsigned long long **d_peer_hist = nullptr;
+  unsigned int **d_peer_flag = nullptr;
+  bool p2p_ready = false;
+  uint32_t p2p_epoch = 0;
   unsigned long long *d_rcounts = nullptr; // [8]: route counts [5], mis-routes [2] (or the picked split)
   unsigned long long *d_cap = nullptr;     // [M][G][W] N_seq
   double *d_calib = nullptr;               // [256][2] estimator snapshot
@@ -230,6 +240,11 @@ fp_status validate_and_copy(fp_plan *p, const fp_plan_desc *d) {
   p->rank = d->rank;
   p->world = d->world;
   p->dist = d->world > 1 || (d->flags & FP_FLAG_COLLECTIVES);
+  if (p->flags & FP_FLAG_P2P) {
+    if (!p->dist) return fail(p, FP_ERR_CONFIG, "FP_FLAG_P2P needs world > 1 or FP_FLAG_COLLECTIVES");
+    if (d->world > 64) return fail(p, FP_ERR_CONFIG, "FP_FLAG_P2P: world > 64");
+    p->flags |= FP_FLAG_REPLICATED_GRID;   // every rank sums all ranks' histograms: no all-gather
+  }
 
   for (auto &m : p->models) {
     if (!m.n_layers || !m.n_kv_heads || !m.head_dim ||
@@ -402,6 +417,13 @@ fp_status upload(fp_plan *p) {
   p->hist_copies = p->nbins <= 256 ? 16u : 1u;
   CUDA_TRY(p, cudaMalloc(&p->d_hcopies, (size_t)p->hist_copies * 2 * p->nbins * 8), "cudaMalloc hist copies");
   CUDA_TRY(p, cudaMemset(p->d_hcopies, 0, (size_t)p->hist_copies * 2 * p->nbins * 8), "memset hist copies");
+  if (p->flags & FP_FLAG_P2P) {
+    p->xbuf_elems = (size_t)p->hist_copies * 2 * p->nbins;
+    const size_t bytes = 2 * p->xbuf_elems * 8 + 256;
+    CUDA_TRY(p, cudaMalloc(&p->d_xbuf, bytes), "cudaMalloc p2p exchange");
+    CUDA_TRY(p, cudaMemset(p->d_xbuf, 0, bytes), "memset p2p exchange");
+    p->d_xflag = reinterpret_cast<unsigned int *>(p->d_xbuf + 2 * p->xbuf_elems);
+  }
   CUDA_TRY(p, cudaMalloc(&p->d_rcounts, 8 * 8), "cudaMalloc counts");
   CUDA_TRY(p, cudaMalloc(&p->d_best, (size_t)p->world * M * sizeof(fp_candidate)), "cudaMalloc best");
   CUDA_TRY(p, cudaMemset(p->d_best, 0, (size_t)p->world * M * sizeof(fp_candidate)), "memset best");
@@ -716,6 +738,45 @@ fp_status fp_nccl_get_unique_id(void *out128) {
   return FP_OK;
 }
 
+fp_status fp_p2p_export(fp_plan *p, void *handle_out) {
+  if (!p || !handle_out) return FP_ERR_INVALID_ARG;
+  if (!(p->flags & FP_FLAG_P2P) || !p->d_xbuf) return fail(p, FP_ERR_STATE, "plan created without FP_FLAG_P2P");
+  static_assert(sizeof(cudaIpcMemHandle_t) == FP_P2P_HANDLE_BYTES, "IPC handle size");
+  DeviceGuard g(p->device);
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(p, cudaIpcGetMemHandle(&h, p->d_xbuf), "cudaIpcGetMemHandle");
+  memcpy(handle_out, &h, sizeof h);
+  return FP_OK;
+}
+
+fp_status fp_p2p_import(fp_plan *p, const void *handles) {
+  if (!p || !handles) return FP_ERR_INVALID_ARG;
+  if (!(p->flags & FP_FLAG_P2P) || !p->d_xbuf) return fail(p, FP_ERR_STATE, "plan created without FP_FLAG_P2P");
+  if (p->p2p_ready) return fail(p, FP_ERR_STATE, "fp_p2p_import called twice");
+  DeviceGuard g(p->device);
+  std::vector<unsigned long long *> hist(p->world);
+  std::vector<unsigned int *> flag(p->world);
+  for (int r = 0; r < p->world; ++r) {
+    unsigned long long *base = p->d_xbuf;
+    if (r != p->rank) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, static_cast<const unsigned char *>(handles) + (size_t)r * FP_P2P_HANDLE_BYTES, sizeof h);
+      void *q = nullptr;
+      CUDA_TRY(p, cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      p->peer_open.push_back(q);
+      base = static_cast<unsigned long long *>(q);
+    }
+    hist[r] = base;
+    flag[r] = reinterpret_cast<unsigned int *>(base + 2 * p->xbuf_elems);
+  }
+  CUDA_TRY(p, cudaMalloc(&p->d_peer_hist, p->world * sizeof(void *)), "cudaMalloc peer table");
+  CUDA_TRY(p, cudaMalloc(&p->d_peer_flag, p->world * sizeof(void *)), "cudaMalloc peer table");
+  CUDA_TRY(p, cudaMemcpy(p->d_peer_hist, hist.data(), p->world * sizeof(void *), cudaMemcpyHostToDevice), "H2D");
+  CUDA_TRY(p, cudaMemcpy(p->d_peer_flag, flag.data(), p->world * sizeof(void *), cudaMemcpyHostToDevice), "H2D");
+  p->p2p_ready = true;
+  return FP_OK;
+}
+
 fp_status fleet_plan_create(const fp_plan_desc *desc, fp_plan **out) {
   if (!out) return FP_ERR_INVALID_ARG;
   *out = nullptr;
@@ -766,6 +827,10 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_blob);
     cudaFree(p->d_hist);
     cudaFree(p->d_hcopies);
+    for (void *q : p->peer_open) cudaIpcCloseMemHandle(q);
+    cudaFree(p->d_peer_hist);
+    cudaFree(p->d_peer_flag);
+    cudaFree(p->d_xbuf);
     cudaFree(p->d_rcounts);
     cudaFree(p->d_cap);
     cudaFree(p->d_best);
@@ -1143,13 +1208,22 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   if (!p->dist && n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace (S:170)");
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  // FP_FLAG_P2P: this step's accumulators are this rank's exchange buffer of
+  // parity epoch & 1 (a peer may still be reading the other parity's)
+  const bool p2p = (p->flags & FP_FLAG_P2P) != 0;
+  if (p2p && !p->p2p_ready) return fail(p, FP_ERR_STATE, "FP_FLAG_P2P plan: call fp_p2p_import first");
+  const uint32_t epoch = p2p ? ++p->p2p_epoch : 0u;
+  unsigned long long *acc = p2p ? p->d_xbuf + (size_t)(epoch & 1u) * p->xbuf_elems : p->d_hcopies;
   // K1: trace pass into the global bin histogram
-  CUDA_TRY(p, cudaMemsetAsync(p->d_hcopies, 0, (size_t)p->hist_copies * 2 * p->nbins * 8, s), "memset hist");
+  CUDA_TRY(p, cudaMemsetAsync(acc, 0, (size_t)p->hist_copies * 2 * p->nbins * 8, s), "memset hist");
   fp_status st = FP_OK;
   if (raw) {
     if (n_local) {
       LaunchTimer lt(p, FP_KERNEL_TRACE, s);
-      cudaError_t e = launch_trace(*raw, p->k1_grid, p->k1_block, p->k1_smem, s);
+      TraceArgs r = *raw;
+      r.g_cnt = acc;
+      r.g_mass = acc + p->nbins;
+      cudaError_t e = launch_trace(r, p->k1_grid, p->k1_block, p->k1_smem, s);
       if (e != cudaSuccess) return cuda_fail(p, e, "trace pass (raw) launch");
       ++p->launches;
     }
@@ -1157,6 +1231,8 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
     TraceArgs t = p->ta;
     t.len = ptr;
     t.n = n;
+    t.g_cnt = acc;
+    t.g_mass = acc + p->nbins;
     // packed bins: this chunk's body starts at global uint4 off / 4 (chunks are
     // whole multiples of 4 elements except the last, and have no head)
     t.bins_out = bins ? bins + (bins_side ? 0 : off) : nullptr;   // packed: device traces (one call, off = 0)
@@ -1170,8 +1246,13 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
     return FP_OK;
   }, resident);
   if (st != FP_OK) return st;
-  // C1: sum the per-rank histograms
-  if (p->dist) {
+  // C1: sum the per-rank histograms -- through peer memory in K3's prologue
+  // (FP_FLAG_P2P: release this rank's accumulators), else an all-reduce
+  if (p2p) {
+    cudaError_t e = launch_p2p_signal(p->d_xflag, epoch, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "p2p signal launch");
+    ++p->launches;
+  } else if (p->dist) {
     st = all_reduce_u64(p, p->d_hcopies, (size_t)p->hist_copies * 2 * p->nbins, s, "all-reduce(histogram)");
     if (st != FP_OK) return st;
   }
@@ -1181,6 +1262,13 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   EvalArgs ea = p->ea;
   ea.rate = rate_rps;
   ea.results = h_results ? p->d_results : nullptr;
+  if (p2p) {
+    ea.peer_hist = p->d_peer_hist;
+    ea.peer_flag = p->d_peer_flag;
+    ea.p2p_world = (uint32_t)p->world;
+    ea.p2p_epoch = epoch;
+    ea.p2p_off = (size_t)(epoch & 1u) * p->xbuf_elems;
+  }
   ea.route_out = route_out;
   ea.route_model = route_model;
   cudaError_t e;
@@ -1245,6 +1333,11 @@ fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_r
     CUDA_TRY(p, cudaMemcpy(p->d_p3 + off_bw, bw.data(), nb * 2, cudaMemcpyHostToDevice), "H2D b_win3");
     CUDA_TRY(p, cudaMemset(p->d_p3 + off_done, 0, M * sizeof(unsigned int)), "memset done3");
     p->ea3 = p->ea;
+    // the last sweep's summed histogram (K3 of that sweep published it)
+    p->ea3.hist_cnt = p->d_hist;
+    p->ea3.hist_mass = p->d_hist + p->nbins;
+    p->ea3.hist_copies = 1;
+    p->ea3.hist_out = nullptr;
     p->ea3.pairs = reinterpret_cast<const uint32_t *>(p->d_p3);
     p->ea3.n_pairs = (uint32_t)pairs.size();
     p->ea3.b_win3 = reinterpret_cast<const uint16_t *>(p->d_p3 + off_bw);

@@ -62,6 +62,11 @@ def _rank(rank, world, port, name, n, flags, q):
             torch.zeros(0, dtype=torch.int32, device="cuda")
         plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=0, rank=rank, world=world,
                                     flags=flags, collectives=GlooCollectives(world))
+        if flags & fp.FP_FLAG_P2P:
+            # exchange the IPC handles of the K1 accumulators (any host transport)
+            handles = [None] * world
+            dist.all_gather_object(handles, fp.fp_p2p_export(plan))
+            fp.fp_p2p_import(plan, handles)
         res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
         best = fp.best_split(plan)
         edges, cnt, mass = fp.sweep_histogram(plan)
@@ -82,13 +87,18 @@ def _rank(rank, world, port, name, n, flags, q):
 
 
 @pytest.mark.parametrize("name,n,replicated", [("C5", 2_000_003, False), ("C3", 300_001, False),
-                                               ("C4", 500_000, True), ("C1", 1000, False)])
+                                               ("C4", 500_000, True), ("C1", 1000, False),
+                                               ("C5", 1_500_001, "p2p"), ("C1", 1000, "p2p")])
 def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
+    """replicated="p2p": the histogram sum goes through peer memory (FP_FLAG_P2P,
+    CUDA IPC between the two processes sharing cuda:0), grid replicated."""
     import oracle
     import paper_2604_08075_b200 as fp
     from synth import configs
     from synth.gen import generate_host
     flags = fp.FP_FLAG_REPLICATED_GRID if replicated else 0
+    if replicated == "p2p":
+        flags |= fp.FP_FLAG_P2P
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

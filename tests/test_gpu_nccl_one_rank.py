@@ -118,3 +118,48 @@ def test_calibration_and_peak_through_nccl():
     oall, obest = oracle.sweep_peak(cfg, L, arr, 10**9)
     assert res.tobytes() == oall.tobytes()
     assert best.tobytes() == obest.tobytes()
+
+
+def test_p2p_exchange_one_rank():
+    """FP_FLAG_P2P on one rank: K3 reads the accumulators through the peer
+    table (its own buffer), the flag protocol advances one epoch per sweep, and
+    alternating parities give the oracle's result every step."""
+    import oracle
+    import paper_2604_08075_b200 as fp
+    from synth import configs
+    from synth.gen import generate_device, generate_host
+    cfg = configs.c5().with_n(700_001)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    d = generate_device(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    allc, obest = oracle.sweep(cfg, L)
+    plan = _nccl_plan(fp, cfg, fp.FP_FLAG_P2P)
+    with pytest.raises(fp.FleetPlanError):
+        fp.sweep_thresholds(plan, d, cfg.rate_rps)          # before the import
+    fp.fp_p2p_import(plan, [fp.fp_p2p_export(plan)])
+    with pytest.raises(fp.FleetPlanError):
+        fp.fp_p2p_import(plan, [fp.fp_p2p_export(plan)])    # twice
+    for _ in range(3):
+        res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+        assert res.tobytes() == allc.tobytes()
+        assert fp.best_split(plan).tobytes() == obest.tobytes()
+    dec = torch.empty(cfg.n_requests, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec, want_best=False)
+    assert fp.best_split(plan).tobytes() == obest.tobytes()
+    b = obest[0]
+    odec, _ = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec.cpu().numpy(), odec)
+    _, cnt, mass = fp.sweep_histogram(plan)
+    assert int(cnt.sum()) == cfg.n_requests
+    fp.fleet_plan_destroy(plan)
+
+
+def test_p2p_needs_a_multi_rank_plan():
+    import paper_2604_08075_b200 as fp
+    from synth import configs
+    with pytest.raises(fp.FleetPlanError):
+        fp.fleet_plan_create(**fp.desc_from_config(configs.c1()), device=0, flags=fp.FP_FLAG_P2P)
+    plan = fp.fleet_plan_create(**fp.desc_from_config(configs.c1()), device=0)
+    with pytest.raises(fp.FleetPlanError):
+        fp.fp_p2p_export(plan)
+    fp.fleet_plan_destroy(plan)
