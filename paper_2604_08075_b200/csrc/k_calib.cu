@@ -109,6 +109,14 @@ struct Vec<NC, true> {
 #pragma unroll
     for (int j = 0; j < NC; ++j) v[j] = k == (uint32_t)j ? x : v[j];
   }
+  // v[k] = beta v[k] + x as NC predicated DFMAs (no select chains: a double
+  // select is two FSELs per category, more issue slots than the DFMAs)
+  __device__ __forceinline__ void ema(uint32_t k, double beta, double x) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j)
+      asm("{\n\t.reg .pred p;\n\tsetp.eq.u32 p, %1, %2;\n\t@p fma.rn.f64 %0, %3, %0, %4;\n\t}"
+          : "+d"(v[j]) : "r"(k), "r"((uint32_t)j), "d"(beta), "d"(x));
+  }
 };
 
 template <int NC>
@@ -117,6 +125,7 @@ struct Vec<NC, false> {
   __device__ __forceinline__ void bind(double *q) { p = q; }
   __device__ __forceinline__ double get(uint32_t k) const { return p[k * kCalBlock + threadIdx.x]; }
   __device__ __forceinline__ void set(uint32_t k, double x) { p[k * kCalBlock + threadIdx.x] = x; }
+  __device__ __forceinline__ void ema(uint32_t k, double beta, double x) { set(k, __fma_rn(beta, get(k), x)); }
 };
 
 template <int NC, bool REG>
@@ -336,7 +345,7 @@ __global__ void __launch_bounds__(kCalBlock, 4) c1_maps(CalibArgs a) {
   for (uint32_t k = 0; k < NC; ++k) { b.set(k, 0.0); n.set(k, 0u); }
   const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
   for_segment(a, smem, [&](double c, uint32_t k) {
-    b.set(k, __fma_rn(beta, b.get(k), __dmul_rn(w, c)));
+    b.ema(k, beta, __dmul_rn(w, c));
     n.inc(k);
   });
   const uint64_t t = (uint64_t)blockIdx.x * kCalBlock + threadIdx.x;
