@@ -71,3 +71,23 @@ def test_unsorted_arrivals_are_rejected():
     _, best = fp.sweep_peak_windows(checked, d_len, torch.from_numpy(arr.view(np.int64)).cuda(), 10**8)
     _, obest = oracle.sweep_peak(cfg, L, arr, 10**8)
     assert best.tobytes() == obest.tobytes()
+
+
+@pytest.mark.parametrize("name,window_ns", [("C5", 3 * 10**8), ("C5", 5 * 10**8), ("C5", 2 * 10**9),
+                                            ("C3", 5 * 10**8), ("C2", 4 * 10**8)])
+def test_windows_of_a_few_thousand_requests(name, window_ns):
+    """Windows of ~1K-20K requests (bursty arrivals: sizes vary by phase), so
+    K1w switches between its per-window shared histogram (flush per window) and
+    the global-atomic path for windows under 2,048 requests inside one block's
+    slice; C3 (259 bins) and C2 (65) for wider histograms."""
+    n = 3_000_001
+    cfg = configs.CONFIGS[name]().with_n(n)
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    arr = arrivals_host(cfg.seed, n, 10_000.0)
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg))
+    res, best = fp.sweep_peak_windows(plan, _dev(L), torch.from_numpy(arr.view(np.int64)).cuda(), window_ns,
+                                      want_results=True)
+    oall, obest = oracle.sweep_peak(cfg, L, arr, window_ns)
+    assert res.tobytes() == oall.tobytes()
+    assert best.tobytes() == obest.tobytes()
+    fp.fleet_plan_destroy(plan)
