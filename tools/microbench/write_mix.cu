@@ -60,6 +60,42 @@ __global__ void mixv(const unsigned long long *lo, const uint32_t *hi, uint4 *ou
     }
   }
 }
+// K1's mix: per thread-step 4 uint4 loads (16 requests) and one 8-B + one 4-B
+// store (the packed bins), chunks c = k*S + t as in K1
+template <int U>
+__global__ void k1mix(const uint4 *in, unsigned long long *lo, uint32_t *hi, uint64_t nchunks) {
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t c = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += U * S) {
+    uint4 v[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        v[u][j] = c + u * S < nchunks ? __ldcs(in + 4 * (c + u * S) + j) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (c + u * S >= nchunks) continue;
+      uint32_t x = 0, y = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) { x ^= v[u][j].x + v[u][j].y; y ^= v[u][j].z + v[u][j].w; }
+      __stcs(lo + c + u * S, ((unsigned long long)x << 32) | y);
+      __stcs(hi + c + u * S, x ^ y);
+    }
+  }
+}
+template <int U>
+__global__ void ronly(const uint4 *in, uint32_t *out, uint64_t n4) {
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  uint32_t acc = 0;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += U * S) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = i + u * S < n4 ? __ldcs(in + i + u * S) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += v[u].x ^ v[u].y ^ v[u].z ^ v[u].w;
+  }
+  if (acc == 0x9e3779b9u) out[0] = acc;
+}
 template <class F> float best(F f) {
   cudaEvent_t a, b; CK(cudaEventCreate(&a)); CK(cudaEventCreate(&b));
   f(); CK(cudaDeviceSynchronize());
@@ -85,6 +121,22 @@ int main() {
   printf("copy uint4 1:1: %.3f ms, %.0f GB/s\n", t, chunks * 32.0 / t / 1e6);
   t = best([&] { wonly<<<148 * 8, 256>>>(out, chunks); });
   printf("write-only uint4 (1184x256): %.3f ms, %.0f GB/s\n", t, chunks * 16.0 / t / 1e6);
+  {
+    uint4 *trace;                          // 1e9 requests x 4 B
+    CK(cudaMalloc(&trace, chunks * 64));
+    CK(cudaMemset(trace, 5, chunks * 64));
+    float t1 = best([&] { k1mix<1><<<grid, block>>>(trace, lo, hi, chunks); });
+    printf("K1 mix U1 (64 B in, 12 B out per 16 requests) 444x512: %.3f ms, %.0f GB/s\n", t1, chunks * 76.0 / t1 / 1e6);
+    t1 = best([&] { k1mix<2><<<grid, block>>>(trace, lo, hi, chunks); });
+    printf("K1 mix U2 444x512: %.3f ms, %.0f GB/s\n", t1, chunks * 76.0 / t1 / 1e6);
+    t1 = best([&] { k1mix<1><<<148 * 4, 512>>>(trace, lo, hi, chunks); });
+    printf("K1 mix U1 592x512: %.3f ms, %.0f GB/s\n", t1, chunks * 76.0 / t1 / 1e6);
+    t1 = best([&] { ronly<4><<<grid, block>>>(trace, hi, chunks * 4); });
+    printf("read-only 4 GB U4 444x512: %.3f ms, %.0f GB/s\n", t1, chunks * 64.0 / t1 / 1e6);
+    t1 = best([&] { ronly<8><<<grid, block>>>(trace, hi, chunks * 4); });
+    printf("read-only 4 GB U8 444x512: %.3f ms, %.0f GB/s\n", t1, chunks * 64.0 / t1 / 1e6);
+    CK(cudaFree(trace));
+  }
   int bps = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, copyv<4, false>, 256, 0));
   const int g2 = 148 * bps;
