@@ -200,6 +200,7 @@ struct CalibArgs {
   uint64_t threads, blocks, seg;    // thread t owns [t*seg, (t+1)*seg); seg % 16 == 0; 256 threads / block
   double *thrA, *thrB;              // [n_cats][threads] within-block exclusive c_hat maps
   uint32_t *thrN;
+  uint32_t *thrC;                   // [n_cats][threads] observations in each thread's own segment
   double *blkA, *blkB;              // [n_cats][blocks] c_hat block totals -> exclusive prefixes
   unsigned long long *blkN;
   double *sblkA, *sblkB;            // [n_cats][blocks] sigma block totals -> exclusive prefixes

@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(kCalBlock, 4) c1_maps(CalibArgs a) {
     a.thrA[k * a.threads + t] = ex.a;
     a.thrB[k * a.threads + t] = ex.b;
     a.thrN[k * a.threads + t] = (uint32_t)ex.n;
+    a.thrC[k * a.threads + t] = nk;
     if (threadIdx.x == 0) {
       a.blkA[k * a.blocks + blockIdx.x] = tot.a;
       a.blkB[k * a.blocks + blockIdx.x] = tot.b;
@@ -432,20 +433,33 @@ __global__ void __launch_bounds__(kCalBlock, 4) c3_replay(CalibArgs a) {
   }
   const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
   uint32_t snapped = 0u;          // bit k: this thread holds category k's snapshot
-  for_segment(a, smem, [&](double o, uint32_t k) {
-    const double prev = c.get(k);
-    const double cn = __fma_rn(beta, prev, __dmul_rn(w, o));
-    c.set(k, cn);
-    const double sn = __fma_rn(beta, sb.get(k), __dmul_rn(w, fabs(__dsub_rn(o, prev))));
-    sb.set(k, sn);
-    n.inc(k);
-    if (n.eq(k, target)) {
-      a.snap_c[k] = cn;
-      a.snap_sa[k] = pow_n(beta, target.get(k));
-      a.snap_sb[k] = sn;
-      snapped |= 1u << k;
-    }
-  });
+  // Only the blocks holding a snapshot count observations per record; the
+  // others take each segment's counts from C1 (thrC) and skip the counters
+  bool mine = false;
+  for (uint32_t k = 0; k < a.n_cats; ++k) mine |= target.get(k) != 0u;
+  if (__syncthreads_or(mine)) {
+    for_segment(a, smem, [&](double o, uint32_t k) {
+      const double prev = c.get(k);
+      const double cn = __fma_rn(beta, prev, __dmul_rn(w, o));
+      c.set(k, cn);
+      const double sn = __fma_rn(beta, sb.get(k), __dmul_rn(w, fabs(__dsub_rn(o, prev))));
+      sb.set(k, sn);
+      n.inc(k);
+      if (n.eq(k, target)) {
+        a.snap_c[k] = cn;
+        a.snap_sa[k] = pow_n(beta, target.get(k));
+        a.snap_sb[k] = sn;
+        snapped |= 1u << k;
+      }
+    });
+  } else {
+    for_segment(a, smem, [&](double o, uint32_t k) {
+      const double prev = c.get(k);
+      c.set(k, __fma_rn(beta, prev, __dmul_rn(w, o)));
+      sb.set(k, __fma_rn(beta, sb.get(k), __dmul_rn(w, fabs(__dsub_rn(o, prev)))));
+    });
+    for (uint32_t k = 0; k < a.n_cats; ++k) n.set(k, a.thrC[k * a.threads + t]);
+  }
   for (uint32_t k = 0; k < a.n_cats; ++k) {
     const uint32_t nk = n.get(k);
     Aff ex, tot;
@@ -515,9 +529,9 @@ cudaError_t launch_replay(const CalibArgs &a, cudaStream_t s) {
 }  // namespace
 
 size_t calib_scratch_bytes(uint64_t blocks, uint32_t n_cats) {
-  // thrA, thrB (double), thrN (u32) per (category, thread); blkA, blkB, sblkA,
-  // sblkB (double), blkN (u64) per (category, block)
-  return (size_t)blocks * n_cats * ((size_t)kCalBlock * (8 * 2 + 4) + 8 * 5);
+  // thrA, thrB (double), thrN, thrC (u32) per (category, thread); blkA, blkB,
+  // sblkA, sblkB (double), blkN (u64) per (category, block)
+  return (size_t)blocks * n_cats * ((size_t)kCalBlock * (8 * 2 + 4 * 2) + 8 * 5);
 }
 
 int calib_blocks_per_sm(uint32_t n_cats) {

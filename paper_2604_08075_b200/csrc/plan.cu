@@ -1439,6 +1439,7 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   a.sblkB = a.sblkA + KB;
   a.blkN = reinterpret_cast<unsigned long long *>(a.sblkB + KB);
   a.thrN = reinterpret_cast<uint32_t *>(a.blkN + KB);
+  a.thrC = a.thrN + KT;
   // 16 slots of 16 doubles; slots 3-5 and 10-13 / 14-15 are the exchange records
   double *sm = reinterpret_cast<double *>(base + scratch);
   auto slot = [&](int i) { return sm + 16 * i; };

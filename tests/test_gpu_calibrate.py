@@ -30,7 +30,8 @@ def _close(a, b, rel=1e-12):
 
 
 @pytest.mark.parametrize("n,ncat,snap", [(1, 4, 1), (37, 4, 5), (100_003, 4, 50), (5_000_000, 4, 1000),
-                                         (2_000_001, 3, 50), (300_000, 16, 7)])
+                                         (2_000_001, 3, 50), (300_000, 16, 7),
+                                         (3_000_001, 4, 400_000), (1_000_003, 16, 30_000)])
 def test_replay_matches_sequential(n, ncat, snap):
     body, mo, cat, tp = generate_raw_host("MIX", 13, 0, n)
     if ncat == 16:
