@@ -190,11 +190,13 @@ __device__ __forceinline__ void cp_async(void *dst, const void *src, int bytes) 
   else asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
 }
 
-// full blocks (every segment complete, 16-B aligned columns): round r by cp.async
+// full blocks (every segment complete, 16-B aligned columns): round r by
+// cp.async; each warp stages its own 32 segments, so a round needs only
+// __syncwarp, not a block barrier
 __device__ __forceinline__ void issue_round(const CalibArgs &a, uint64_t t0, uint64_t r, const StageSmem &st) {
 #pragma unroll
   for (int i = 0; i < kParts; ++i) {
-    const uint32_t q = threadIdx.x + kCalBlock * i, seg = q / kParts, part = q % kParts;
+    const uint32_t q = (threadIdx.x & 31u) + 32u * i, seg = (threadIdx.x & ~31u) + q / kParts, part = q % kParts;
     const uint64_t g = (t0 + seg) * a.seg + r * kRound + part * 4;
     cp_async(st.b + swz(seg, part), a.bytes + g, 16);
     cp_async(st.t + swz(seg, part), a.tokens + g, 16);
@@ -291,9 +293,9 @@ __device__ __forceinline__ void for_segment(const CalibArgs &a, unsigned char *s
       if (r + 1 < rounds) issue_round(a, t0, r + 1, stage_at(smem, (uint32_t)(r + 1) & 1u));
       else asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group 1;" ::: "memory");
-      __syncthreads();
+      __syncwarp();
       consume(stage_at(smem, (uint32_t)r & 1u), last, body);
-      __syncthreads();                 // buffer r & 1 is refilled at round r + 2
+      __syncwarp();                    // buffer r & 1 is refilled at round r + 2
     }
   } else {
     const StageSmem st = stage_at(smem, 0);
