@@ -134,6 +134,157 @@ __global__ void __launch_bounds__(kHistBlock) k1w_hist(PeakArgs a) {
   }
 }
 
+// K1w, per-warp form (small E): every warp streams its own contiguous slice
+// into a warp-private lane-column histogram [nbins][32 lanes], so a window
+// boundary costs that warp alone a flush -- no block barrier anywhere in the
+// loop. Tiles of 32 lanes x kWU quads, the next tile's loads in flight. A tile
+// inside one window adds every request to the histogram; a tile with <= 3
+// boundaries makes one predicated pass per window it touches and flushes each
+// window that ends in it; a tile with more boundaries (windows of < ~128
+// requests) goes to global atomics.
+constexpr int kWarpBlock = 256;
+constexpr int kWU = 4;
+
+// last window w with start[w] <= i, searching w in [lo, hi] (start[lo] <= i)
+__device__ __forceinline__ uint64_t window_of(const uint64_t *start, uint64_t i, uint64_t lo, uint64_t hi) {
+  uint64_t n = hi - lo + 1;
+  while (n > 0) {
+    const uint64_t half = n >> 1;
+    if (start[lo + half] <= i) { lo += half + 1; n -= half + 1; } else { n = half; }
+  }
+  return lo - 1;
+}
+
+template <int LUTW>
+__global__ void __launch_bounds__(kWarpBlock, 3) k1w_hist_warp(PeakArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t nbins = a.nbins;
+  uint32_t lut_bytes = LUTW ? a.lut_cells * LUTW : (nbins - 1) * 4;
+  lut_bytes = (lut_bytes + 15u) & ~15u;
+  unsigned char *lut = smem;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t *acc_all = reinterpret_cast<uint32_t *>(smem + lut_bytes);  // [warps][nbins][32]
+  {
+    const uint32_t *src = LUTW ? reinterpret_cast<const uint32_t *>(a.lut) : a.edges;
+    for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(lut)[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < (blockDim.x >> 5) * nbins * 32; i += blockDim.x) acc_all[i] = 0u;
+  }
+  __syncthreads();
+  uint32_t *acc = acc_all + warp * nbins * 32;
+  const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc) + lane * 4u;
+  const uint32_t clampv = a.clampv, round = a.round, shift = a.shift, ne = nbins - 1;
+  const uint32_t *len = a.len;
+  const uint64_t *start = a.start;
+  const uint32_t n = (uint32_t)a.n, nw = (uint32_t)a.n_windows;   // < 2^32, <= 2^26 (host checks)
+  auto bin = [&](uint32_t L) { return bin_of<LUTW>(L, lut, clampv, round, shift, ne); };
+  auto inc = [&](uint32_t L) { asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(acc_s + bin(L) * 128u) : "memory"); };
+  auto global_add = [&](uint32_t w, uint32_t L) { atomicAdd(a.hist2d + (size_t)w * nbins + bin(L), 1u); };
+  const uint32_t off = min(n, (uint32_t)(((16u - ((uintptr_t)len & 15u)) & 15u) >> 2));
+  const uint32_t nq = (n - off) >> 2;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + warp, W = gridDim.x * (blockDim.x >> 5);
+  if (gw == 0) {      // requests before the first aligned address and after the last full quad
+    for (uint32_t i = lane; i < off; i += 32) global_add((uint32_t)window_of(start, i, 0, nw), __ldcs(len + i));
+    for (uint32_t i = off + 4 * nq + lane; i < n; i += 32) global_add((uint32_t)window_of(start, i, 0, nw), __ldcs(len + i));
+  }
+  const uint32_t per = (nq + W - 1) / W;
+  const uint32_t qlo = min(gw * per, nq), qhi = min(qlo + per, nq);
+  if (qlo >= qhi) return;
+  // window f's lane columns -> one global row; lane j sums bin j's 32 columns
+  // (8 x 16-B loads, rotated so the lanes of a phase hit distinct banks)
+  auto flush = [&](uint32_t f) {
+    __syncwarp();
+    uint32_t *row = a.hist2d + (size_t)f * nbins;
+    for (uint32_t j = lane; j < nbins; j += 32) {
+      uint4 *r = reinterpret_cast<uint4 *>(acc + j * 32);
+      uint32_t c = 0;
+#pragma unroll
+      for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t kk = (k + j) & 7u;
+        const uint4 x = r[kk];
+        r[kk] = make_uint4(0u, 0u, 0u, 0u);
+        c += x.x + x.y + x.z + x.w;
+      }
+      if (c) atomicAdd(row + j, c);
+    }
+    __syncwarp();
+  };
+  const uint4 *v = reinterpret_cast<const uint4 *>(len + off);
+  constexpr uint32_t kT = 32u * kWU;
+  uint32_t w = (uint32_t)window_of(start, off + 4ull * qlo, 0, nw);
+  uint32_t nb = w < nw ? (uint32_t)__ldg(start + w + 1) : n;      // first request of window w + 1
+  uint4 cur[kWU], nxt[kWU];
+#pragma unroll
+  for (int k = 0; k < kWU; ++k) {
+    const uint32_t q = qlo + lane + 32u * k;
+    cur[k] = q < qhi ? __ldcs(v + q) : make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (uint32_t q0 = qlo; q0 < qhi; q0 += kT) {
+    const uint32_t q1 = min(q0 + kT, qhi);
+    if (q1 < qhi) {
+#pragma unroll
+      for (int k = 0; k < kWU; ++k) {
+        const uint32_t q = q1 + lane + 32u * k;
+        nxt[k] = q < qhi ? __ldcs(v + q) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    const uint32_t e1 = off + 4 * q1;
+    if (e1 <= nb) {                                    // the tile lies in window w
+#pragma unroll
+      for (int k = 0; k < kWU; ++k)
+        if (q0 + lane + 32u * k < q1) { inc(cur[k].x); inc(cur[k].y); inc(cur[k].z); inc(cur[k].w); }
+    } else {
+      // windows w .. wl touch the tile; their starts (warp-uniform loads)
+      uint32_t bs[4];                                  // bs[d] = start[w + 1 + d]
+      bs[0] = nb;
+      uint32_t wl = w;
+#pragma unroll
+      for (int d = 1; d < 4; ++d) bs[d] = (w + 1 + d <= nw) ? (uint32_t)__ldg(start + w + 1 + d) : n;
+      while (wl - w < 4 && bs[wl - w] < e1) ++wl;     // wl - w boundaries inside the tile (capped at 4)
+      if (wl - w < 4) {
+        for (uint32_t d = 0; d <= wl - w; ++d) {
+          const uint32_t lo = d ? bs[d - 1] : 0u, hi = bs[d];   // window w + d = [lo, hi)
+#pragma unroll
+          for (int k = 0; k < kWU; ++k) {
+            const uint32_t q = q0 + lane + 32u * k;
+            if (q < q1) {
+              const uint32_t i0 = off + 4 * q;
+              const uint32_t x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+#pragma unroll
+              for (int c = 0; c < 4; ++c)
+                if (i0 + c >= lo && (d == wl - w || i0 + c < hi)) inc(x[c]);
+            }
+          }
+          if (d < wl - w) flush(w + d);
+        }
+        w = wl;
+      } else {
+        // more than 3 boundaries: flush w, then global atomics for the tile
+        flush(w);
+        const uint32_t wlast = (uint32_t)window_of(start, e1 - 1, w, nw);
+#pragma unroll
+        for (int k = 0; k < kWU; ++k) {
+          const uint32_t q = q0 + lane + 32u * k;
+          if (q < q1) {
+            const uint32_t x[4] = {cur[k].x, cur[k].y, cur[k].z, cur[k].w};
+            uint32_t ww = (uint32_t)window_of(start, off + 4 * q, w, wlast);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t i = off + 4 * q + c;
+              while (ww < wlast && __ldg(start + ww + 1) <= i) ++ww;
+              global_add(ww, x[c]);
+            }
+          }
+        }
+        w = wlast;
+      }
+      nb = w < nw ? (uint32_t)__ldg(start + w + 1) : n;
+    }
+#pragma unroll
+    for (int k = 0; k < kWU; ++k) cur[k] = nxt[k];
+  }
+  flush(w);
+}
+
 // K2w: inclusive scan of each window's row in shared memory, then the window
 // maxima per bin and per (B, C_L) pair; one atomicMax per entry per block
 __global__ void __launch_bounds__(256) k2w_peaks(PeakArgs a) {
@@ -211,6 +362,24 @@ size_t peak_scan_smem_bytes(const PeakArgs &a) {
   return ((size_t)a.rows * a.nbins + (size_t)a.n_b * a.n_cl + a.nbins) * 4;
 }
 
+size_t warp_hist_smem(const PeakArgs &a) {
+  const size_t lut = a.lutw ? (size_t)a.lut_cells * a.lutw : (size_t)(a.nbins - 1) * 4;
+  return ((lut + 15) & ~size_t(15)) + (size_t)(kWarpBlock / 32) * a.nbins * 32 * 4;
+}
+
+template <int LUTW>
+cudaError_t launch_hist_warp(const PeakArgs &a, int sm_count, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k1w_hist_warp<LUTW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1w_hist_warp<LUTW>, kWarpBlock, smem);
+  if (e != cudaSuccess) return e;
+  const uint64_t want = (uint64_t)sm_count * (uint64_t)std::max(per_sm, 1);
+  const uint64_t useful = std::max<uint64_t>(1, (a.n + 4095) / 4096);
+  k1w_hist_warp<LUTW><<<(unsigned)std::min(want, useful), kWarpBlock, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
   cudaError_t e;
   if (a.check_order) {
@@ -219,6 +388,12 @@ cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
   }
   k0w_bounds<<<(unsigned)((a.n_windows + 1 + 255) / 256), 256, 0, s>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  // per-warp histograms while they fit 3 blocks per SM (|E| + 1 <= ~140 bins)
+  const size_t wsmem = warp_hist_smem(a);
+  if (wsmem <= 72 * 1024)
+    return a.lutw == 1 ? launch_hist_warp<1>(a, sm_count, wsmem, s)
+           : a.lutw == 2 ? launch_hist_warp<2>(a, sm_count, wsmem, s)
+                         : launch_hist_warp<0>(a, sm_count, wsmem, s);
   const size_t smem = peak_smem_bytes(a);
   e = a.lutw == 1 ? launch_hist<1>(a, sm_count, smem, s)
       : a.lutw == 2 ? launch_hist<2>(a, sm_count, smem, s)
