@@ -28,6 +28,8 @@ namespace {
 constexpr int kHistBlock = 512;
 constexpr uint64_t kSmallSegment = 2048;   // below this a window goes to global atomics
 
+// one thread per window: binary search (30 dependent loads at n = 1e9; used
+// for many windows, where the loads of other windows hide the latency)
 __global__ void k0w_bounds(PeakArgs a) {
   const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (w > a.n_windows) return;
@@ -38,6 +40,38 @@ __global__ void k0w_bounds(PeakArgs a) {
     if (a.arrival[lo + half] < t) { lo += half + 1; n -= half + 1; } else { n = half; }
   }
   a.start[w] = w == a.n_windows ? a.n : lo;
+}
+
+// one warp per window: a 32-way search (each round 32 probes, one ballot),
+// so the dependent chain is ~log32(n) = 6 loads instead of log2(n) = 30 --
+// for few windows (the chain is the whole kernel); 6x the probes of the
+// binary search, so many windows take k0w_bounds
+__global__ void k0w_bounds_warp(PeakArgs a) {
+  const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (w > a.n_windows) return;                 // warp-uniform
+  if (w == a.n_windows) {
+    if (lane == 0) a.start[w] = a.n;
+    return;
+  }
+  const uint64_t t = w * a.window_ns;          // no overflow: checked on the host
+  // lower_bound(arrival, t) lies in [lo, hi]: arrival[lo - 1] < t (or lo = 0),
+  // arrival[hi] >= t (or hi = n)
+  uint64_t lo = 0, hi = a.n;
+  while (hi - lo > 32) {
+    const uint64_t step = (hi - lo + 31) / 32;
+    const uint64_t idx = min(lo + (lane + 1) * step - 1, hi - 1);
+    const bool below = __ldg(a.arrival + idx) < t;
+    const uint32_t c = __popc(__ballot_sync(0xffffffffu, below));   // probes below t: a prefix
+    const uint64_t nlo = c ? min(lo + c * step - 1, hi - 1) + 1 : lo;
+    const uint64_t nhi = c < 32 ? min(lo + (c + 1) * step - 1, hi - 1) : hi;
+    lo = nlo;
+    hi = nhi;
+  }
+  const uint64_t idx = lo + lane;
+  const bool below = idx < hi && __ldg(a.arrival + idx) < t;
+  const uint32_t c = __popc(__ballot_sync(0xffffffffu, below));
+  if (lane == 0) a.start[w] = lo + c;
 }
 
 __global__ void kc_check_order(PeakArgs a) {
@@ -300,7 +334,20 @@ __global__ void __launch_bounds__(256) k2w_peaks(PeakArgs a) {
     const uint32_t rn = (uint32_t)min((uint64_t)R, a.n_windows - w0);
     __syncthreads();
     const uint32_t *src = a.hist2d + w0 * nbins;
-    for (uint32_t i = threadIdx.x; i < rn * nbins; i += blockDim.x) rows[i] = src[i];
+    // 8 independent loads in flight per thread (the rows come from L2)
+    for (uint32_t base = threadIdx.x; base < rn * nbins; base += 8 * blockDim.x) {
+      uint32_t v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = base + k * blockDim.x;
+        v[k] = i < rn * nbins ? __ldcg(src + i) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t i = base + k * blockDim.x;
+        if (i < rn * nbins) rows[i] = v[k];
+      }
+    }
     __syncthreads();
     for (uint32_t r = warp; r < rn; r += nwarps) {
       uint32_t *row = rows + r * nbins, carry = 0;
@@ -386,7 +433,10 @@ cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
     kc_check_order<<<sm_count * 4, 512, 0, s>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  k0w_bounds<<<(unsigned)((a.n_windows + 1 + 255) / 256), 256, 0, s>>>(a);
+  if (a.n_windows < 16384)
+    k0w_bounds_warp<<<(unsigned)((a.n_windows + 1 + 7) / 8), 256, 0, s>>>(a);   // one warp per window
+  else
+    k0w_bounds<<<(unsigned)((a.n_windows + 1 + 255) / 256), 256, 0, s>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // per-warp histograms while they fit 3 blocks per SM (|E| + 1 <= ~140 bins)
   const size_t wsmem = warp_hist_smem(a);
