@@ -358,10 +358,24 @@ __global__ void __launch_bounds__(512, 2) k4_route_raw(RouteRawArgs a) {
     const uint32_t *c4 = reinterpret_cast<const uint32_t *>(a.cat + head);
     uint32_t *d4 = DEC ? reinterpret_cast<uint32_t *>(a.decision + head) : nullptr;
     uint4 *l4 = LT ? reinterpret_cast<uint4 *>(a.l_total + head) : nullptr;
-    for (uint64_t i = me; i < n4; i += S) {
-      const uint4 b = ldg_stream(b4 + i), m = ldg_stream(m4 + i);
-      const uint4 t = TRUE_TOK ? ldg_stream(t4 + i) : make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t k = __ldg(c4 + i);
+    // two quads per thread per iteration, both loaded before either is routed
+    // (twice the bytes in flight; the second may be past the end)
+    for (uint64_t i0 = me; i0 < n4; i0 += 2 * S) {
+      const bool has2 = i0 + S < n4;
+      const uint64_t i1 = has2 ? i0 + S : i0;
+      const uint4 b0 = ldg_stream(b4 + i0), m0 = ldg_stream(m4 + i0);
+      const uint4 t0 = TRUE_TOK ? ldg_stream(t4 + i0) : make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t k0 = __ldg(c4 + i0);
+      const uint4 b1 = ldg_stream(b4 + i1), m1 = ldg_stream(m4 + i1);
+      const uint4 t1 = TRUE_TOK ? ldg_stream(t4 + i1) : make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t k1 = __ldg(c4 + i1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+      if (h == 1 && !has2) break;
+      const uint64_t i = h ? i1 : i0;
+      const uint4 b = h ? b1 : b0, m = h ? m1 : m0;
+      const uint4 t = h ? t1 : t0;
+      const uint32_t k = h ? k1 : k0;
       const uint4 L = make_uint4(estimate_l_total(b.x, m.x, k & 0xFFu, cst),
                                  estimate_l_total(b.y, m.y, (k >> 8) & 0xFFu, cst),
                                  estimate_l_total(b.z, m.z, (k >> 16) & 0xFFu, cst),
@@ -384,6 +398,7 @@ __global__ void __launch_bounds__(512, 2) k4_route_raw(RouteRawArgs a) {
       }
       if (DEC) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(d4 + i), "r"(w) : "memory");
       if (LT) l4[i] = L;
+      }
     }
   }
   // counts: short, long, rejected, mass short, mass long, mis-routes short, long
