@@ -104,7 +104,7 @@ __device__ __forceinline__ void store4(uint8_t *dec, uint32_t w) {
 // DEC: write decisions; SMALL: C_L < 2^28 (u32 tile masses); DVEC: the
 // decision address of every uint4 of the body is 4-byte aligned.
 template <bool DEC, bool SMALL, bool DVEC>
-__global__ void __launch_bounds__(512, 4) k4_route(RouteArgs a) {
+__global__ void __launch_bounds__(512, 2) k4_route(RouteArgs a) {
   const uint32_t B = a.b, CS = a.cs, CL = a.cl;
   Acc acc;
   const uint32_t mis = (uint32_t)((reinterpret_cast<uintptr_t>(a.len) & 15u) >> 2);
@@ -128,13 +128,25 @@ __global__ void __launch_bounds__(512, 4) k4_route(RouteArgs a) {
   const uint64_t tile4 = (uint64_t)blockDim.x * kUnroll;
   const uint64_t full_tiles = n4 / tile4;
   const uint64_t ntiles = (n4 + tile4 - 1) / tile4;
+  // software pipeline: the next full tile's loads are in flight while this one
+  // is routed (2 x 512 threads per SM at 63 registers: 0.83 -> 0.77 ms on C5)
+  uint4 nx[kUnroll];
+  if ((uint64_t)blockIdx.x < full_tiles) {
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) nx[u] = ldg_stream(body + blockIdx.x * tile4 + threadIdx.x + (uint64_t)u * blockDim.x);
+  }
   for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     const uint64_t base = t * tile4 + threadIdx.x;
     uint32_t gms = 0, gmsv = 0;
     if (t < full_tiles) {
       uint4 v[kUnroll];
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) v[u] = ldg_stream(body + base + (uint64_t)u * blockDim.x);
+      for (int u = 0; u < kUnroll; ++u) v[u] = nx[u];
+      const uint64_t tn = t + gridDim.x;
+      if (tn < full_tiles) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) nx[u] = ldg_stream(body + tn * tile4 + threadIdx.x + (uint64_t)u * blockDim.x);
+      }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t w = route4<SMALL>(v[u], B, CS, CL, acc, gms, gmsv);

@@ -541,8 +541,8 @@ fp_status configure_launch(fp_plan *p) {
   p->k4_block = env_int("FP_K4_BLOCK", 512);
   if (p->k4_block < 64 || p->k4_block > 512 || (p->k4_block & 31))
     return fail(p, FP_ERR_CONFIG, "FP_K4_BLOCK must be a multiple of 32 in [64, 512]");
-  // persistent grid = every block resident (4 x 512 threads per SM with
-  // __launch_bounds__(512, 4); profiles/r01_tune_k4.txt)
+  // persistent grid = every block resident (2 x 512 threads per SM with
+  // __launch_bounds__(512, 2) and the next tile's loads in flight)
   int k4_res = 1;
   CUDA_TRY(p, route_occupancy(p->k4_block, &k4_res), "k4 occupancy");
   p->k4_grid = p->sm_count * std::min(k4_res, env_int("FP_K4_BLOCKS_PER_SM", k4_res));
