@@ -151,7 +151,15 @@ def test_p2p_exchange_one_rank():
     assert np.array_equal(dec.cpu().numpy(), odec)
     _, cnt, mass = fp.sweep_histogram(plan)
     assert int(cnt.sum()) == cfg.n_requests
+    # NEXT-2 reuses the last sweep's summed histogram (K3 publishes it; the
+    # P2P accumulators themselves alternate between parities)
+    _, best3 = fp.sweep_three_pools(plan, cfg.rate_rps)
     fp.fleet_plan_destroy(plan)
+    ref = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=0)
+    fp.sweep_thresholds(ref, d, cfg.rate_rps)
+    _, ref3 = fp.sweep_three_pools(ref, cfg.rate_rps)
+    fp.fleet_plan_destroy(ref)
+    assert best3.tobytes() == ref3.tobytes()
 
 
 def test_p2p_needs_a_multi_rank_plan():
