@@ -3,10 +3,39 @@
 // for the kernels.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include "fleet_plan.h"
 
 namespace fp {
+
+// programmatic dependent launch: the kernel may start while the previous
+// kernel in the stream drains; it must execute griddepcontrol.wait before
+// touching that kernel's outputs. FP_NO_PDL=1 falls back to plain launches.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char *v = getenv("FP_NO_PDL");
+    return !(v && v[0] == '1');
+  }();
+  return on;
+}
+
+template <typename... Params, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(Params...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr int kMaxEdges = 4096;          // |E| limit (K3 scans |E|+1 bins in smem)
 constexpr int kLutMaxCells = 16384;      // above this: binary search over E

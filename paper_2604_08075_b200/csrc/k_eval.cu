@@ -302,6 +302,16 @@ __global__ void __launch_bounds__(256, 3) k3_eval(EvalArgs a) {
   sh.rmu = sh.mu + (size_t)a.n_gpus * a.n_windows;
 
   // ---- prologue: K2 scan + capacity table for model m ----
+  // the plan's tables first: they do not depend on the trace pass, so with a
+  // programmatic (PDL) launch they load while K1's last blocks drain
+  for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
+    sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    const double mu = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
+    sh.mu[j] = mu;
+    sh.rmu[j] = mrcp(mu);
+  }
+  // K1's histogram is complete and visible after this (no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // sum K1's accumulator copies; block (0, 0) also publishes the summed
   // histogram (sweep_histogram, best_split's empty-trace check)
   if (a.p2p_world) {
@@ -359,12 +369,6 @@ __global__ void __launch_bounds__(256, 3) k3_eval(EvalArgs a) {
       a.hist_out[j] = cnt;
       a.hist_out[a.nbins + j] = mass;
     }
-  }
-  for (uint32_t j = threadIdx.x; j < a.n_gpus * a.n_windows; j += blockDim.x) {
-    sh.nseq[j] = a.cap_nseq[(uint64_t)m * a.n_gpus * a.n_windows + j];
-    const double mu = a.mu[(uint64_t)m * a.n_gpus * a.n_windows + j];
-    sh.mu[j] = mu;
-    sh.rmu[j] = mrcp(mu);
   }
   __syncthreads();
   block_scan_inclusive(sh.cnt_le, a.nbins, warp_tot);
@@ -651,10 +655,12 @@ cudaError_t launch_p2p_signal(unsigned int *flag, unsigned int epoch, cudaStream
   return cudaGetLastError();
 }
 
+// K3 after K1 as a programmatic dependent launch: its blocks are scheduled as
+// K1's blocks exit and wait (griddepcontrol.wait) only before the histogram
+// reads, which hides the launch latency and the table loads (FP_NO_PDL=1: a
+// plain launch)
 cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {
-  dim3 grid(grid_x, a.n_models);
-  k3_eval<false><<<grid, block, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k3_eval<false>, dim3(grid_x, a.n_models), dim3(block), smem, s, a);
 }
 
 cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {

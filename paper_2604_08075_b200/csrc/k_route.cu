@@ -570,6 +570,7 @@ __global__ void k_pick_route(const fp_candidate *recs, int ranks, uint32_t n_mod
 template <bool VEC, bool SWAR>
 __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__ bins, uint8_t *__restrict__ dec,
                                                       uint64_t n, const uint32_t *__restrict__ route) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // K3's split (PDL launch)
   const uint4 rt = *reinterpret_cast<const uint4 *>(route);
   if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
   const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
@@ -622,6 +623,7 @@ __global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long 
                                                        const uint32_t *__restrict__ hi,
                                                        const uint8_t *__restrict__ side, uint8_t *__restrict__ dec,
                                                        uint64_t n, uint32_t head, const uint32_t *__restrict__ route) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // K3's split (PDL launch)
   const uint4 rt = *reinterpret_cast<const uint4 *>(route);
   if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
   const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
@@ -697,9 +699,10 @@ cudaError_t launch_route_packed(const uint8_t *lo, const uint8_t *hi, const uint
   const bool vec = (reinterpret_cast<uintptr_t>(decision + h) & 3u) == 0;
   const auto *l8 = reinterpret_cast<const unsigned long long *>(lo);
   const auto *h4 = reinterpret_cast<const uint32_t *>(hi);
-  if (vec) k4_route_packed<true><<<k1_grid, k1_block, 0, s>>>(l8, h4, side, decision, n, head, route);
-  else k4_route_packed<false><<<k1_grid, k1_block, 0, s>>>(l8, h4, side, decision, n, head, route);
-  return cudaGetLastError();
+  return vec ? launch_pdl(k4_route_packed<true>, dim3(k1_grid), dim3(k1_block), 0, s, l8, h4, side, decision, n, head,
+                          (const uint32_t *)route)
+             : launch_pdl(k4_route_packed<false>, dim3(k1_grid), dim3(k1_block), 0, s, l8, h4, side, decision, n, head,
+                          (const uint32_t *)route);
 }
 
 cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
@@ -714,10 +717,10 @@ cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n
   const int g = (int)std::min<uint64_t>((uint64_t)grid, std::max<uint64_t>(1, need));
   // SWAR needs every bin < 128: bins go up to |E|, and j = iB, iCS, iCL < |E|
   const bool swar = n_edges < 128;
-  if (vec && swar) k4_route_bins<true, true><<<g, block, 0, s>>>(bins, decision, n, route);
-  else if (vec) k4_route_bins<true, false><<<g, block, 0, s>>>(bins, decision, n, route);
-  else k4_route_bins<false, false><<<g, block, 0, s>>>(bins, decision, n, route);
-  return cudaGetLastError();
+  const uint32_t *rt = route;
+  if (vec && swar) return launch_pdl(k4_route_bins<true, true>, dim3(g), dim3(block), 0, s, bins, decision, n, rt);
+  if (vec) return launch_pdl(k4_route_bins<true, false>, dim3(g), dim3(block), 0, s, bins, decision, n, rt);
+  return launch_pdl(k4_route_bins<false, false>, dim3(g), dim3(block), 0, s, bins, decision, n, rt);
 }
 
 }  // namespace fp
