@@ -161,6 +161,11 @@ struct EvalArgs {
   fp_candidate *best_out;               // [n_models] (this rank's)
   BlockBest *block_best;                // [n_models][grid_x]
   unsigned int *done;                   // [n_models] last-block-done counters (self-resetting)
+  // non-null: the block that reads K1's accumulator copies last (counter
+  // read_done, self-resetting) zeroes them for the next sweep, replacing the
+  // memset before K1
+  unsigned long long *zero_copies = nullptr;
+  unsigned int *read_done = nullptr;
   // sweep_and_route (one rank's grid is the whole grid): the last block of
   // model route_model also writes {iB, iCS, iCL, ok} of its best split
   const uint32_t *edges = nullptr;

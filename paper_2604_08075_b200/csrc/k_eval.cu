@@ -291,7 +291,7 @@ __global__ void __launch_bounds__(256, 3) k3_eval(EvalArgs a) {
   __shared__ double red_c[32];
   __shared__ uint32_t red_i[32], red_v[32];
   __shared__ uint32_t route_v[4];
-  __shared__ bool is_last;
+  __shared__ bool is_last, zero_last;
   const uint32_t m = blockIdx.y;
 
   Shared sh;
@@ -371,6 +371,20 @@ __global__ void __launch_bounds__(256, 3) k3_eval(EvalArgs a) {
     }
   }
   __syncthreads();
+  if (a.zero_copies) {
+    // every block has its sums in shared memory now; the last one to get here
+    // zeroes the copies (stream order puts this before the next sweep's K1)
+    if (threadIdx.x == 0) {
+      __threadfence();
+      zero_last = atomicAdd(a.read_done, 1u) == gridDim.x * gridDim.y - 1;
+    }
+    __syncthreads();
+    if (zero_last) {
+      const size_t total = (size_t)a.hist_copies * 2 * a.nbins;
+      for (size_t i = threadIdx.x; i < total; i += blockDim.x) a.zero_copies[i] = 0ull;
+      if (threadIdx.x == 0) *a.read_done = 0u;
+    }
+  }
   block_scan_inclusive(sh.cnt_le, a.nbins, warp_tot);
   block_scan_inclusive(sh.mass_le, a.nbins, warp_tot);
   sh.rN = mrcp(u2d(sh.cnt_le[a.nbins - 1]));

@@ -118,6 +118,8 @@ struct fp_plan {
   fp_candidate *d_results = nullptr;       // [cand_count] (lazy)
   BlockBest *d_block_best = nullptr;
   unsigned int *d_done = nullptr;
+  unsigned int *d_read_done = nullptr;     // K3's copy-reader counter (zeroing protocol)
+  bool copies_clean = true;                // d_hcopies is zero (or will be, stream-ordered)
   int k3_grid_x = 1, k3_block = 256;
   // host streaming
   uint32_t *d_stage[2] = {nullptr, nullptr};
@@ -513,6 +515,8 @@ fp_status upload(fp_plan *p) {
   CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * p->k3_grid_x * sizeof(BlockBest)), "cudaMalloc block_best");
   CUDA_TRY(p, cudaMalloc(&p->d_done, M * sizeof(unsigned int)), "cudaMalloc done");
   CUDA_TRY(p, cudaMemset(p->d_done, 0, M * sizeof(unsigned int)), "memset done");
+  CUDA_TRY(p, cudaMalloc(&p->d_read_done, sizeof(unsigned int)), "cudaMalloc read_done");
+  CUDA_TRY(p, cudaMemset(p->d_read_done, 0, sizeof(unsigned int)), "memset read_done");
   ea.block_best = p->d_block_best;
   ea.done = p->d_done;
   p->k3_smem = eval_smem_bytes(ea, p->k3_block);
@@ -837,6 +841,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_results);
     cudaFree(p->d_block_best);
     cudaFree(p->d_done);
+    cudaFree(p->d_read_done);
     cudaFree(p->d_resident);
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
@@ -1214,8 +1219,12 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   if (p2p && !p->p2p_ready) return fail(p, FP_ERR_STATE, "FP_FLAG_P2P plan: call fp_p2p_import first");
   const uint32_t epoch = p2p ? ++p->p2p_epoch : 0u;
   unsigned long long *acc = p2p ? p->d_xbuf + (size_t)(epoch & 1u) * p->xbuf_elems : p->d_hcopies;
-  // K1: trace pass into the global bin histogram
-  CUDA_TRY(p, cudaMemsetAsync(acc, 0, (size_t)p->hist_copies * 2 * p->nbins * 8, s), "memset hist");
+  // K1: trace pass into the global bin histogram. The copies are zeroed by
+  // the previous sweep's K3 (see zero_copies below); a memset only if that
+  // sweep did not get to launch K3, and always for the P2P parity buffers
+  if (p2p || !p->copies_clean)
+    CUDA_TRY(p, cudaMemsetAsync(acc, 0, (size_t)p->hist_copies * 2 * p->nbins * 8, s), "memset hist");
+  if (!p2p) p->copies_clean = false;
   fp_status st = FP_OK;
   if (raw) {
     if (n_local) {
@@ -1262,6 +1271,10 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   EvalArgs ea = p->ea;
   ea.rate = rate_rps;
   ea.results = h_results ? p->d_results : nullptr;
+  if (!p2p) {
+    ea.zero_copies = p->d_hcopies;
+    ea.read_done = p->d_read_done;
+  }
   if (p2p) {
     ea.peer_hist = p->d_peer_hist;
     ea.peer_flag = p->d_peer_flag;
@@ -1277,6 +1290,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
     e = launch_eval(ea, p->k3_grid_x, p->k3_block, p->k3_smem, s);
   }
   if (e != cudaSuccess) return cuda_fail(p, e, "candidate evaluation launch");
+  if (!p2p) p->copies_clean = true;        // K3 zeroes them after its last read
   ++p->launches;
   // C2: gather every rank's per-model best
   if (p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID)) {
@@ -1338,6 +1352,8 @@ fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_r
     p->ea3.hist_mass = p->d_hist + p->nbins;
     p->ea3.hist_copies = 1;
     p->ea3.hist_out = nullptr;
+    p->ea3.zero_copies = nullptr;
+    p->ea3.read_done = nullptr;
     p->ea3.pairs = reinterpret_cast<const uint32_t *>(p->d_p3);
     p->ea3.n_pairs = (uint32_t)pairs.size();
     p->ea3.b_win3 = reinterpret_cast<const uint16_t *>(p->d_p3 + off_bw);
