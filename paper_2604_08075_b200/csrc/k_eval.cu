@@ -575,6 +575,7 @@ __global__ void __launch_bounds__(256) k3_peak(EvalArgs a) {
     sh.mu[j] = mu;
     sh.rmu[j] = mrcp(mu);
   }
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // K2w's window maxima (PDL launch)
   __syncthreads();
   const uint64_t lo = (uint64_t)m * a.per_model, hi = lo + a.per_model;
   double bc = 0.0;
@@ -634,9 +635,7 @@ __global__ void __launch_bounds__(256) k3_peak(EvalArgs a) {
 cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k3_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   if (e != cudaSuccess) return e;
-  dim3 grid(grid_x, a.n_models);
-  k3_peak<<<grid, block, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k3_peak, dim3(grid_x, a.n_models), dim3(block), smem, s, a);
 }
 
 size_t eval_smem_bytes(const EvalArgs &a, int) {

@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(kWarpBlock, 3) k1w_hist_warp(PeakArgs a) {
     for (uint32_t i = threadIdx.x; i < lut_bytes / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(lut)[i] = src[i];
     for (uint32_t i = threadIdx.x; i < (blockDim.x >> 5) * nbins * 32; i += blockDim.x) acc_all[i] = 0u;
   }
+  // K0w's window starts (and the memset of the 2-D histogram before it) are
+  // complete past this point; the LUT and counter setup above overlap K0w
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   uint32_t *acc = acc_all + warp * nbins * 32;
   const uint32_t acc_s = (uint32_t)__cvta_generic_to_shared(acc) + lane * 4u;
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(256) k2w_peaks(PeakArgs a) {
   uint32_t *cmax = pmax + n_pairs;            // [nbins]
   for (uint32_t i = threadIdx.x; i < n_pairs; i += blockDim.x) pmax[i] = 0u;
   for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) cmax[i] = 0u;
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // K1w's 2-D histogram (PDL launch)
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   for (uint64_t w0 = (uint64_t)blockIdx.x * R; w0 < a.n_windows; w0 += (uint64_t)gridDim.x * R) {
     const uint32_t rn = (uint32_t)min((uint64_t)R, a.n_windows - w0);
@@ -423,8 +427,7 @@ cudaError_t launch_hist_warp(const PeakArgs &a, int sm_count, size_t smem, cudaS
   if (e != cudaSuccess) return e;
   const uint64_t want = (uint64_t)sm_count * (uint64_t)std::max(per_sm, 1);
   const uint64_t useful = std::max<uint64_t>(1, (a.n + 4095) / 4096);
-  k1w_hist_warp<LUTW><<<(unsigned)std::min(want, useful), kWarpBlock, smem, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k1w_hist_warp<LUTW>, dim3((unsigned)std::min(want, useful)), dim3(kWarpBlock), smem, s, a);
 }
 
 cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
@@ -457,8 +460,8 @@ cudaError_t launch_peak_scan(const PeakArgs &a, int sm_count, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k2w_peaks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   if (e != cudaSuccess) return e;
   const uint64_t chunks = (a.n_windows + a.rows - 1) / a.rows;
-  k2w_peaks<<<(unsigned)std::min<uint64_t>(chunks, (uint64_t)sm_count * 4), 256, smem2, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k2w_peaks, dim3((unsigned)std::min<uint64_t>(chunks, (uint64_t)sm_count * 4)), dim3(256), smem2, s,
+                    a);
 }
 
 }  // namespace fp
