@@ -34,6 +34,11 @@
  *     descriptor (NCCL collective semantics).
  *   - There is no CPU fallback: without a usable CUDA device every compute
  *     call fails with FP_ERR_CUDA.
+ *   - Kernels that follow another kernel of the same call are issued as
+ *     programmatic dependent launches (they wait on the device for their
+ *     predecessor's results); environment FP_NO_PDL=1 issues plain launches.
+ *     Either way the results are identical and the calls stay stream-ordered
+ *     with respect to the caller's other work on `stream`.
  * ======================================================================== */
 #ifndef FLEET_PLAN_H
 #define FLEET_PLAN_H
