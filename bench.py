@@ -332,6 +332,11 @@ def run_ours(args, cfg):
     coll = fp.FP_FLAG_COLLECTIVES if multi else 0
     if multi and args.p2p:
         coll |= fp.FP_FLAG_P2P
+    # small grids (C5: 4,096 candidates) are evaluated whole on every rank: K3
+    # is latency-bound there, so slicing it only adds the all-gather of the
+    # ranks' best records and the pick kernel to the step
+    if multi and not args.sliced_grid and cfg.n_candidates() <= 100_000:
+        coll |= fp.FP_FLAG_REPLICATED_GRID
 
     def p2p_setup(pl):
         # FP_FLAG_P2P: all-gather the ranks' IPC handles, open the peers' buffers
@@ -520,6 +525,8 @@ def run_ours(args, cfg):
         line["config"]["parallelism"] += "; --collectives: one-rank NCCL communicator in the step"
     if coll & fp.FP_FLAG_P2P:
         line["config"]["parallelism"] += "; --p2p: histogram sum over peer memory in K3 (no all-reduce)"
+    if coll & fp.FP_FLAG_REPLICATED_GRID:
+        line["config"]["parallelism"] += "; candidate grid replicated on every rank (no all-gather)"
     if world == 1 and args.k3_grid:
         line["k3_large_grid"] = k3_large_grid(fp, generate_device)
     if world == 1 and args.next4:
@@ -567,6 +574,8 @@ def main():
                     help="strong scaling: split the config's trace over the ranks (default: weak, n per rank)")
     ap.add_argument("--collectives", action="store_true",
                     help="take the multi-GPU code path even at world 1 (NCCL group of one; for testing)")
+    ap.add_argument("--sliced-grid", action="store_true",
+                    help="multi-rank: split the candidate grid over the ranks even when it is small")
     ap.add_argument("--p2p", action="store_true",
                     help="multi-rank: the histogram exchange through peer memory (FP_FLAG_P2P) instead of NCCL")
     ap.add_argument("--no-next2", dest="next2", action="store_false",
