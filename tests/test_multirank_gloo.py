@@ -71,12 +71,14 @@ def _worker(rank, world, port, name, n_total, q):
         q.put((rank, False, False, repr(e)))
 
 
-@pytest.mark.parametrize("name,n", [("C5", 100_003), ("C3", 50_001), ("C4", 64)])
-def test_two_rank_protocol_equals_single_process(name, n):
+@pytest.mark.parametrize("name,n,world", [("C5", 100_003, 2), ("C3", 50_001, 2), ("C4", 64, 2), ("C5", 100_003, 4),
+                                          ("C4", 7, 4)])
+def test_two_rank_protocol_equals_single_process(name, n, world):
+    """World 2 and 4 (shard invariance; C4 with 7 requests leaves ranks empty)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, name, n, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, n, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in procs]
