@@ -1,4 +1,4 @@
-"""Multi-rank parity on ONE GPU: two processes, each a rank of a world-2 plan
+"""Multi-rank parity on ONE GPU: two (or four) processes, each a rank of a world-2 (or 4) plan
 on cuda:0, with the library's host-collective hooks carried by a gloo process
 group (127.0.0.1) instead of NCCL (which refuses two ranks on one device).
 This runs the whole world > 1 path of libfleetplan.so -- shard-local K1,
@@ -86,10 +86,11 @@ def _rank(rank, world, port, name, n, flags, q):
         q.put((rank, None, None, None, None, None, 0, 0, traceback.format_exc(), None))
 
 
-@pytest.mark.parametrize("name,n,replicated", [("C5", 2_000_003, False), ("C3", 300_001, False),
-                                               ("C4", 500_000, True), ("C1", 1000, False),
-                                               ("C5", 1_500_001, "p2p"), ("C1", 1000, "p2p")])
-def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
+@pytest.mark.parametrize("name,n,replicated,world", [("C5", 2_000_003, False, 2), ("C3", 300_001, False, 2),
+                                                     ("C4", 500_000, True, 2), ("C1", 1000, False, 2),
+                                                     ("C5", 1_500_001, "p2p", 2), ("C1", 1000, "p2p", 2),
+                                                     ("C5", 1_000_003, False, 4), ("C5", 1_000_003, "p2p", 4)])
+def test_two_ranks_one_gpu_match_oracle(name, n, replicated, world):
     """replicated="p2p": the histogram sum goes through peer memory (FP_FLAG_P2P,
     CUDA IPC between the two processes sharing cuda:0), grid replicated."""
     import oracle
@@ -102,7 +103,7 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank, args=(r, 2, port, name, n, flags, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank, args=(r, world, port, name, n, flags, q)) for r in range(world)]
     for p in procs:
         p.start()
     out = sorted(q.get(timeout=600) for _ in procs)
@@ -119,7 +120,8 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated):
         for r in recs:
             assert r.tobytes() == allc.tobytes()
     else:
-        assert out[0][6] == 0 and out[0][7] + out[1][7] == cfg.n_candidates()
+        assert out[0][6] == 0 and sum(o[7] for o in out) == cfg.n_candidates()
+        assert all(out[r][6] + out[r][7] == out[r + 1][6] for r in range(world - 1))
         assert np.concatenate(recs).tobytes() == allc.tobytes()
     for o in out:
         assert o[2] == obest.tobytes()                      # same best split on every rank
