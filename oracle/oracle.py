@@ -1,7 +1,7 @@
 """ctypes front end of the plain-C oracle (TEST INFRASTRUCTURE ONLY).
 
 Argument marshalling only; every number is computed in fleet_oracle.c.
-Functions without a pin are listed in DESIGN.md "Parity pins" (none today).
+Every output field is named next to its pin in DESIGN.md §2 "Parity pins, field by field".
 """
 from __future__ import annotations
 

@@ -309,3 +309,19 @@ def test_count_le_invariants():
     assert c_all[0] == L.size and int(m_all[0]) == int(L.astype(np.int64).sum())   # alpha(inf) = 1
     perm = rng.permutation(L)
     assert all(np.array_equal(a, b) for a, b in zip((cnt, mass), oracle.count_le(perm, x)))
+
+
+# --------------------------------------------------------- fragmentation ----
+
+
+def test_fragmentation_worst_case(golden):
+    """Effect 3 (P:625-629): 16-token blocks waste up to 15 tokens per sequence;
+    with 128 short sequences at Qwen3's per-token per-GPU KV bytes (Eq. 1 / TP)
+    that is ~46 MB. (The paper's "0.03% of MI300X HBM" is 0.024%: prose, R18.)"""
+    g = golden["fragmentation"]
+    a = golden["kv_per_token_per_gpu_qwen3"]["args"]
+    per_tok, rem = oracle.kv_bytes_per_token_per_gpu(a["n_l"], a["n_h"], a["d_h"], a["b"], a["tp"])
+    assert per_tok == g["per_token"] and rem == 0
+    waste = g["n_seqs"] * (g["block"] - 1) * per_tok
+    assert round(waste / 1e6) == g["mb_approx"]
+    assert waste / 192e9 < 0.0003

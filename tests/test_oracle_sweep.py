@@ -157,6 +157,16 @@ def test_config_sweeps_invariants(name):
     allc, best = oracle.sweep(cfg, L)
     assert len(allc) == cfg.n_candidates()
     assert np.array_equal(allc["index"], np.arange(len(allc), dtype=np.uint32))
+    # flat order (m, g, C_L, C_S, B), B fastest (R12): the record's own fields
+    nb, ncs, ncl, ng = len(cfg.b_short), cfg.n_cs_eff(), len(cfg.c_long), len(cfg.gpus)
+    i = np.arange(len(allc))
+    kb, ks, kl = i % nb, (i // nb) % ncs, (i // (nb * ncs)) % ncl
+    assert np.array_equal(allc["b_short"], np.array(cfg.b_short, np.uint32)[kb])
+    cs = np.array(cfg.c_short, np.uint32)[ks] if cfg.c_short else allc["b_short"]
+    assert np.array_equal(allc["c_short"], cs)
+    assert np.array_equal(allc["c_long"], np.array(cfg.c_long, np.uint32)[kl])
+    assert np.array_equal(allc["gpu"], (i // (nb * ncs * ncl)) % ng)
+    assert np.array_equal(allc["model"], i // (nb * ncs * ncl * ng))
     v = (allc["flags"] & 1) != 0
     assert np.all(allc["n_short"][v] + allc["n_long"][v] + allc["n_reject"][v] == cfg.n_requests)
     assert np.all(allc["b_short"][v] <= allc["c_short"][v]) and np.all(allc["c_short"][v] <= allc["c_long"][v])
