@@ -110,13 +110,42 @@ class ClockSampler:
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def _workload(cfg, n_per_rank, world):
+def _l2_bytes(dev=None):
+    import torch
+    try:
+        return int(torch.cuda.get_device_properties(dev or 0).L2_cache_size)
+    except Exception:
+        return 126 * 2 ** 20
+
+
+def _l2_label(trace_bytes, l2, flushed):
+    if flushed:
+        return (f"L2 flushed before every timed step (a {2 * l2 / 1e6:.0f} MB write = 2 x L2) -- the trace "
+                f"({trace_bytes / 1e6:.3g} MB) would otherwise stay in the {l2 / 1e6:.0f} MB L2")
+    return (f"inputs larger than L2: {trace_bytes / 1e9:.3g} GB trace per GPU > 2 x {l2 / 1e6:.0f} MB L2 "
+            f"(no flush needed)")
+
+
+def _workload(cfg, n_per_rank, world, l2_label=None):
     return {"workload": f"{cfg.name}: {cfg.description}", "name": cfg.name,
             "trace": cfg.shape, "seed": cfg.seed, "n_requests_per_gpu": n_per_rank,
             "n_requests_total": n_per_rank * world, "n_candidates": cfg.n_candidates(),
             "rate_rps": cfg.rate_rps,
-            "l2": f"inputs larger than L2 (4 B x {n_per_rank:.3g} = {4 * n_per_rank / 1e9:.3g} GB per GPU > 126 MB)",
+            "l2": l2_label or f"inputs larger than L2 (4 B x {n_per_rank:.3g} = {4 * n_per_rank / 1e9:.3g} GB per GPU)",
             "parallelism": f"dp{world} (trace sharded by global request index)"}
+
+
+def _host_cpu():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count()}
 
 
 # ------------------------------------------------------------------ CPU oracle ----
@@ -131,10 +160,8 @@ def oracle_step(cfg, L):
     return best
 
 
-def cpu_baseline(cfg, target_s=12.0):
-    import oracle
+def _time_oracle(cfg, target_s, n0=1 << 20):
     from synth.gen import generate_host
-    n0 = 1 << 20
     L = generate_host(cfg.shape, cfg.seed, 0, n0)
     t = time.perf_counter()
     oracle_step(cfg.with_n(n0), L)
@@ -143,10 +170,26 @@ def cpu_baseline(cfg, target_s=12.0):
     L = generate_host(cfg.shape, cfg.seed, 0, n)
     t = time.perf_counter()
     oracle_step(cfg.with_n(n), L)
-    dt = time.perf_counter() - t
-    return {"value": n / dt, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+    return n, time.perf_counter() - t
+
+
+def cpu_baseline(cfg, target_s=10.0, target_1t_s=8.0):
+    """The oracle as it stands on this host: all cores (OpenMP over requests)
+    and one thread, each on a bounded sample of the same workload."""
+    import oracle
+    cores = oracle.num_threads()
+    n, dt = _time_oracle(cfg, target_s)
+    oracle.set_num_threads(1)
+    try:
+        n1, dt1 = _time_oracle(cfg, target_1t_s, n0=1 << 18)
+    finally:
+        oracle.set_num_threads(cores)
+    return {"value": n / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"first {n:,} requests of the {cfg.name} trace (one oracle step: sweep of all "
-                      f"{cfg.n_candidates()} candidates + argmin + Alg. 1 route), {dt:.1f} s"}
+                      f"{cfg.n_candidates()} candidates + argmin + Alg. 1 route), {dt:.1f} s on {cores} threads",
+            "single_thread": {"value": n1 / dt1, "unit": UNIT, "cores": 1,
+                              "sample": f"first {n1:,} requests, {dt1:.1f} s on 1 thread"},
+            "host_cpu": _host_cpu()}
 
 
 def run_reference(args, cfg):
@@ -295,8 +338,138 @@ def _bcast_uid(fp, dist, rank):
     return obj[0]
 
 
+def _timed_steps(step, steps, stream, flush=None):
+    """Device time of `steps` calls of step() on `stream` (ms, list per step when
+    flushing). With `flush` (a tensor of 2 x L2) the L2 is overwritten before
+    every step, outside the timed events."""
+    import torch
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k)
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+    ev[-1][1].synchronize()
+    per = [a.elapsed_time(b) for a, b in ev]
+    return sum(per), per
+
+
+def config_results(fp, names, steps, warmup):
+    """BASELINE.json's other configurations (C1-C4) at their full sizes on this
+    GPU, the same step (sweep_and_route, asynchronous) timed per step with CUDA
+    events, the L2 flushed before every step when the trace would fit in it."""
+    import torch
+    from synth import configs
+    from synth.gen import generate_device
+    l2 = _l2_bytes()
+    peak = _peaks()[0]
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(2 * l2 // 4, dtype=torch.int32, device="cuda")
+    out = {}
+    for name in names:
+        cfg = configs.CONFIGS[name]()
+        n = cfg.n_requests
+        d = generate_device(cfg.shape, cfg.seed, 0, n)
+        dec = torch.empty(n, dtype=torch.uint8, device="cuda")
+        plan = fp.fleet_plan_create(**fp.desc_from_config(cfg))
+        step = lambda: fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec,  # noqa: E731
+                                          stream=stream, want_best=False)
+        for _ in range(warmup):
+            step()
+        needs_flush = 4 * n < 2 * l2
+        l0 = fp.fp_kernel_launches(plan)
+        total, per = _timed_steps(step, steps, stream, flush if needs_flush else None)
+        launches = fp.fp_kernel_launches(plan) - l0
+        best = fp.best_split(plan)
+        info = fp.fleet_plan_info(plan)
+        fp.fleet_plan_destroy(plan)
+        if per is None:
+            per = [total / steps] * steps
+        per = sorted(per)
+        med = per[len(per) // 2]
+        ms = total / steps
+        # the bytes the step must move at least: the trace read once, one decision byte written
+        out[name] = {
+            "workload": f"{cfg.name}: {cfg.description}", "n_requests": n, "n_candidates": cfg.n_candidates(),
+            "ms_per_step": ms, "ms_p10_p50_p90": [per[int(0.1 * (steps - 1))], med, per[int(0.9 * (steps - 1))]],
+            "requests_per_s": n / (ms / 1e3), "candidates_per_s_step": cfg.n_candidates() / (ms / 1e3),
+            "step_min_bytes_per_request": 5.0,
+            "step_frac_min_bytes": 5.0 * n / (ms / 1e3) / 1e9 / peak,
+            "l2": _l2_label(4 * n, l2, needs_flush), "gpu_launches_per_step": launches / steps,
+            "k3_shape": ["cluster", "factored", "grid"][info["k3_shape"]],
+            "best_model0": {"index": int(best[0]["index"]), "b_short": int(best[0]["b_short"]),
+                            "c_short": int(best[0]["c_short"]), "c_long": int(best[0]["c_long"]),
+                            "savings": float(best[0]["savings"])}}
+        del d, dec
+        torch.cuda.empty_cache()
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps, warmup):
+    """The multi-GPU step under each exchange / grid mode, weak (n_weak
+    requests per rank) and strong (the config's trace split over the ranks):
+    NCCL all-reduce with the grid replicated or sliced across ranks (+ the
+    all-gather of best records), and the peer-memory exchange (FP_FLAG_P2P,
+    grid replicated). Device time, max over ranks."""
+    import torch
+    from synth.gen import generate_device
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    out = []
+    for strong in (False, True):
+        if strong:
+            first, n = fp.fp_shard_range(cfg.n_requests, rank, world)
+        else:
+            first, n = rank * n_weak, n_weak
+        c = cfg.with_n(n)
+        d = generate_device(c.shape, c.seed, first, n)
+        dec = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+        for mode in ("nccl-replicated", "nccl-sliced", "p2p"):
+            flags = fp.FP_FLAG_COLLECTIVES
+            if mode != "nccl-sliced":
+                flags |= fp.FP_FLAG_REPLICATED_GRID
+            if mode == "p2p":
+                flags |= fp.FP_FLAG_P2P
+            plan = fp.fleet_plan_create(**fp.desc_from_config(c), device=local, rank=rank, world=world,
+                                        nccl_unique_id=_bcast_uid(fp, dist, rank), flags=flags)
+            if mode == "p2p":
+                handles = [None] * world
+                dist.all_gather_object(handles, fp.fp_p2p_export(plan))
+                fp.fp_p2p_import(plan, handles)
+            step = lambda: fp.sweep_and_route(plan, d, c.rate_rps, route_model=0, decision=dec,  # noqa: E731
+                                              stream=stream, want_best=False)
+            for _ in range(warmup):
+                step()
+            dist.barrier(device_ids=[local])
+            torch.cuda.synchronize(dev)
+            ms, _ = _timed_steps(step, steps, stream)
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms_step = float(t.item()) / steps
+            best = fp.best_split(plan)
+            dist.barrier(device_ids=[local])       # peers may still read a P2P buffer
+            fp.fleet_plan_destroy(plan)
+            total = cfg.n_requests if strong else n_weak * world
+            out.append({"scaling": "strong" if strong else "weak", "exchange": mode, "n_gpus": world,
+                        "ms_per_step": ms_step, "requests_per_s": total / (ms_step / 1e3),
+                        "best_index_model0": int(best[0]["index"])})
+        del d, dec
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, cfg):
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -322,6 +495,7 @@ def run_ours(args, cfg):
         first, n = fp.fp_shard_range(n, rank, world)
     else:
         first = rank * n
+    n_weak = args.n or cfg.n_requests
     cfg = cfg.with_n(n)
 
     uid = _bcast_uid(fp, dist, rank) if multi else None
@@ -349,10 +523,16 @@ def run_ours(args, cfg):
                                 flags=(0 if args.no_kernel_events else fp.FP_FLAG_TIME_TRACE) | coll)
     p2p_setup(plan)
     info = fp.fleet_plan_info(plan)
+    if multi:
+        print(f"[bench] rank {rank}/{world}: NCCL communicator of {info['nccl_comm_size']} ranks "
+              f"(device {local})", file=sys.stderr, flush=True)
     # this rank's shard of the global trace: requests [rank*n, (rank+1)*n)
     d_len = generate_device(cfg.shape, cfg.seed, first, n)
     d_dec = torch.empty(n, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
+    l2 = _l2_bytes(local)
+    needs_flush = 4 * n < 2 * l2
+    flush = torch.empty(2 * l2 // 4, dtype=torch.int32, device=dev) if needs_flush else None
 
     def step(lengths, want_best=False, pl=None):
         # sweep_thresholds -> per-model argmin -> route_batch(model 0's best split), one ABI call;
@@ -371,18 +551,13 @@ def run_ours(args, cfg):
     if not args.no_kernel_events:
         fp.fp_kernel_time_reset(plan)
     l0 = fp.fp_kernel_launches(plan)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        for k in range(args.steps):
-            step(d_len)
-        e1.record(stream)
+        ms_local, _ = _timed_steps(lambda: step(d_len), args.steps, stream, flush)
         torch.cuda.synchronize(dev)
     barrier()
     best = fp.best_split(plan)                  # the records of the last timed step
     launches = fp.fp_kernel_launches(plan) - l0
-    ms_local = e0.elapsed_time(e1)
     k1_time = (0.0, 0) if args.no_kernel_events else fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
 
     # ---- per-kernel breakdown and per-step spread: a second loop on a plan that
@@ -428,6 +603,9 @@ def run_ours(args, cfg):
                  "best_savings_three_pools": [float(x) for x in best3["savings"]],
                  "note": "P:1099-1100 claims ~2% marginal savings for a third pool; under the stated "
                          "uncapped pow23 mu the gain is larger (it depends on mu saturation, not stated)"}
+    if multi:
+        barrier()
+    fp.fleet_plan_destroy(plan_b)
 
     # ---- e2e: the same step through the C ABI with HOST (pinned) buffers ----
     e2e = None
@@ -445,12 +623,21 @@ def run_ours(args, cfg):
         e2e = {"value": total_requests * args.e2e_steps / float(dt.item()), "unit": UNIT,
                "h2d_bytes_per_step": 4 * n,   # the pinned trace crosses PCIe once per step
                "d2h_bytes_per_step": best.nbytes + 5 * 8,
-               "note": "sweep_and_route on a pinned host trace: 128 MB chunks DMA'd into a device copy "
-                       "while K1 consumes them, K4 reads the device copy; best records + route counts "
-                       "to host"}
+               "note": "sweep_and_route on a pinned host trace: 128 MB chunks DMA'd into the device while K1 "
+                       "consumes them (bins written on the device), K4 routes from the bins; best records + "
+                       "route counts to host every step"}
         del h_len
 
+    # ---- the multi-GPU exchange / grid variants (N > 1, or --collectives at N = 1) ----
+    variants = None
+    if multi and args.variants:
+        barrier()
+        variants = multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps=max(5, args.steps // 2),
+                                  warmup=3)
+
     if rank != 0:
+        barrier()
+        fp.fleet_plan_destroy(plan)
         if multi:
             dist.destroy_process_group()
         return
@@ -459,39 +646,45 @@ def run_ours(args, cfg):
     peak, peak_src = _peaks()
     shares = {k: v[0] for k, v in ktime.items()}
     dom = max(shares, key=shares.get)
-    # algorithmic bytes per step of each kernel as designed: with
-    # the bin pass (|E| < 255, u8 LUT) the trace pass reads 4 B and writes a 1-B
-    # bin per request and the routing pass maps 1 B of bins to 1 B of decisions;
-    # otherwise the routing pass re-reads the 4-B L_total and writes 1 B.
-    # With |E| + 1 <= 64 bins (C5: 56) and a device trace the bins are 6-bit
-    # packed: 0.75 B per request written and read back.
+    # bytes each kernel moves per step as designed: with the bin
+    # pass (|E| < 255, u8 LUT) the trace pass reads 4 B and writes a bin per
+    # request (6-bit packed: 0.75 B; else 1 B) and the routing pass maps the
+    # bins to 1-B decisions; otherwise the routing pass re-reads L_total.
     bin_pass = info["lut_cells"] > 0 and info["n_edges"] < 255
     packed = bin_pass and info["n_edges"] + 1 <= 64
     bin_bytes = 0.75 if packed else 1.0
-    algo_bytes = ({"trace": (4.0 + bin_bytes) * n, "route": (bin_bytes + 1.0) * n, "eval": 0.0} if bin_pass
-                  else {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0})
-    # the dominant kernel's launches inside the timed region (k1_time); the
-    # other kernels' numbers come from the breakdown loop
+    moved = ({"trace": (4.0 + bin_bytes) * n, "route": (bin_bytes + 1.0) * n, "eval": 0.0} if bin_pass
+             else {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0})
+    # SURVEY §8(d)'s algorithmic bytes: the sweep pass reads 4 B per request;
+    # route_batch reads 4 B and writes 1 B (the bins are this design's, not the method's)
+    algo = {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0}
     kms, kcount = k1_time if dom == "trace" else ktime[dom]
     per_launch_ms = kms / max(kcount, 1)
-    per_launch_bytes = algo_bytes[dom] / max(1.0, kcount / args.steps)   # bytes per step / launches per step
+    per_launch_bytes = algo[dom] / max(1.0, kcount / args.steps)   # bytes per step / launches per step
     achieved = per_launch_bytes / (per_launch_ms / 1e3) / 1e9 if per_launch_ms > 0 else float("nan")
-    k_gbs = {k: (algo_bytes[k] * args.steps / (ktime[k][0] / 1e3) / 1e9 if ktime[k][0] and algo_bytes[k] else None)
+    moved_gbs = moved[dom] / max(1.0, kcount / args.steps) / (per_launch_ms / 1e3) / 1e9 if per_launch_ms else None
+    k_gbs = {k: (moved[k] * args.steps / (ktime[k][0] / 1e3) / 1e9 if ktime[k][0] and moved[k] else None)
              for k in ktime}
     kname = {"trace": "K1 k1_trace" + ((" (6-bit packed bin pass)" if packed else " (bin pass)") if bin_pass else ""),
              "route": ("K4p k4_route_packed" if packed else "K4b k4_route_bins") if bin_pass else "K4 k4_route"}
+    # the step's DRAM traffic as ncu measured it (profiles/ncu_traffic.json, --set full)
+    step_dram = None
+    if all(_traffic(cfg.name, k) for k in ("trace", "route")):
+        step_dram = sum(_traffic(cfg.name, k) or 0.0 for k in ("trace", "route", "eval"))
     roof = {"bound": "hbm", "kernel": kname.get(dom, dom),
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "frac_of_nominal_7700": achieved / 7700.0,
             "traffic": _traffic(cfg.name, dom), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": per_launch_bytes,
-            "per_kernel_GBps": k_gbs,
+            "algorithmic_bytes_per_request": algo[dom] / n,
+            "algorithmic_bytes_note": "SURVEY §8(d): the sweep's trace pass reads 4 B per request",
+            "bytes_moved_per_request": moved[dom] / n,
+            "achieved_bytes_moved": moved_gbs, "frac_bytes_moved": moved_gbs / peak if moved_gbs else None,
+            "frac_of_nominal_7700": achieved / 7700.0,
+            "per_kernel_GBps_bytes_moved": k_gbs,
             "step_share": {k: v / sum(per_step) for k, v in shares.items()},   # breakdown loop
-            # the whole step against the SURVEY §8(d) per-request figures of the
-            # path it replaces (4 B sweep read + 4 B route read + 1 B decision)
-            "step_paper_bytes_per_request": 9.0,
-            "step_GBps_paper_bytes": 9.0 * n * world / (ms_step / 1e3) / 1e9 / world,
-            "step_frac_paper_bytes": 9.0 * n / (ms_step / 1e3) / 1e9 / peak}
+            "step_dram_bytes_per_request_ncu": step_dram / 1e9 if step_dram and cfg.n_requests == 10**9 else None,
+            "step_frac_dram_ncu": (step_dram / (ms_step / 1e3) / 1e9 / peak
+                                   if step_dram and n == 10**9 else None)}
     cand_per_s = cfg.n_candidates() * args.steps / (ktime["eval"][0] / 1e3) if ktime["eval"][0] else None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -503,7 +696,8 @@ def run_ours(args, cfg):
             "step": "sweep_and_route: K1 trace pass (+6-bit packed bins) -> K3 sweep + per-model argmin -> device "
                     "split pick -> K4p routing pass, stream-ordered with no host round trip; the best records stay "
                     "on the device and are read once after the timed loop (e2e reads them every step)",
-            "config": dict(_workload(cfg, n, world), n_requests_total=total_requests),
+            "config": dict(_workload(cfg, n, world, _l2_label(4 * n, l2, needs_flush)),
+                           n_requests_total=total_requests),
             "candidates_per_s": cand_per_s,
             "candidates_per_s_step": cfg.n_candidates() / (ms_step / 1e3),
             "kernel_ms_per_step": {k: v[0] / args.steps for k, v in ktime.items()},
@@ -513,26 +707,39 @@ def run_ours(args, cfg):
                               "per step)"),
             "roofline": roof,
             "gpu_launches": launches,
+            "k3_shape": ["cluster", "factored", "grid"][info["k3_shape"]],
             "next2_three_pools": next2,
             "clocks": clk.summary(),
             "e2e": e2e,
+            "variants": variants,
+            "configs": None,
             "best_split_model0": {k: (int(best[0][k]) if k not in ("cost_dual", "savings", "predicted_savings")
                                       else float(best[0][k]))
                                   for k in ("index", "b_short", "c_short", "c_long", "gpus_dual", "gpus_homo",
                                             "cost_dual", "savings", "predicted_savings")},
-            "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count")}}
+            "plan": {k: info[k] for k in ("n_edges", "lut_shift", "lut_cells", "k1_grid", "k1_block", "sm_count",
+                                          "nccl_comm_size", "k3_blocks_per_model")}}
     if multi and world == 1:
         line["config"]["parallelism"] += "; --collectives: one-rank NCCL communicator in the step"
     if coll & fp.FP_FLAG_P2P:
         line["config"]["parallelism"] += "; --p2p: histogram sum over peer memory in K3 (no all-reduce)"
     if coll & fp.FP_FLAG_REPLICATED_GRID:
         line["config"]["parallelism"] += "; candidate grid replicated on every rank (no all-gather)"
+    if multi:
+        barrier()
+    fp.fleet_plan_destroy(plan)
+    del d_dec
     if world == 1 and args.k3_grid:
         line["k3_large_grid"] = k3_large_grid(fp, generate_device)
     if world == 1 and args.next4:
         line["next4_peak_windows"] = next4_peak_windows(fp, cfg, n, d_len)
+    if world == 1 and args.configs:
+        del d_len
+        torch.cuda.empty_cache()
+        line["configs"] = config_results(fp, [c for c in ("C1", "C2", "C3", "C4") if c != cfg.name],
+                                         steps=max(10, args.steps), warmup=args.warmup)
     if world == 1 and args.next1:
-        del d_len, d_dec
+        d_len = None
         torch.cuda.empty_cache()
         line["next1_fused_estimation"] = next1_fused_estimation(fp, cfg, n)
     if world == 1 and not args.no_cpu_baseline:
@@ -554,11 +761,47 @@ def emit(line):
     out.flush()
 
 
+def _free_port():
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def _spawn_ranks(gpus):
+    """`bench.py --gpus N` (N > 1) without a launcher: re-run this command as N
+    ranks under torch.distributed.run (127.0.0.1 rendezvous); rank 0 prints the
+    line. Returns the launcher's exit code."""
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print("[bench] spawning: " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.call(cmd)
+
+
+def run_plumbing_check(args):
+    """CPU check of the multi-rank plumbing the GPU arm uses (launcher, env,
+    process group on 127.0.0.1, max over ranks, rank-0-only output) with gloo."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dist.init_process_group("gloo")
+    t = torch.tensor([float(rank + 1)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ranks = [None] * world
+    dist.all_gather_object(ranks, {"rank": rank, "local_rank": int(os.environ.get("LOCAL_RANK", "0"))})
+    if rank == 0:
+        emit({"plumbing": "ok", "n_gpus": world, "max_over_ranks": float(t.item()), "ranks": ranks})
+    dist.destroy_process_group()
+
+
 def main():
     global _JSON_OUT
-    sys.stdout.flush()
-    _JSON_OUT = os.fdopen(os.dup(1), "w")
-    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
@@ -578,6 +821,10 @@ def main():
                     help="multi-rank: split the candidate grid over the ranks even when it is small")
     ap.add_argument("--p2p", action="store_true",
                     help="multi-rank: the histogram exchange through peer memory (FP_FLAG_P2P) instead of NCCL")
+    ap.add_argument("--no-variants", dest="variants", action="store_false",
+                    help="multi-rank: skip the NCCL/P2P x replicated/sliced x weak/strong variant timings")
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the C1-C4 per-configuration results")
     ap.add_argument("--no-next2", dest="next2", action="store_false",
                     help="skip the three-pool (NEXT-2) measurement")
     ap.add_argument("--no-next1", dest="next1", action="store_false",
@@ -588,9 +835,19 @@ def main():
                     help="skip the 2^24-candidate K3 measurement")
     ap.add_argument("--ref-sample", type=int, default=10_000_000,
                     help="requests per reference (oracle) step")
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="CPU: exercise the multi-rank launch / gloo / rank-0 output path only")
     args = ap.parse_args()
     if args.warmup < 3:
         raise SystemExit("--warmup must be >= 3")
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(_spawn_ranks(args.gpus))
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+    if args.plumbing_check:
+        run_plumbing_check(args)
+        return
     from synth import configs
     cfg = configs.CONFIGS[args.config]()
     if args.impl == "reference":

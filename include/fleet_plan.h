@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define FP_ABI_VERSION 1u
+#define FP_ABI_VERSION 2u
 #define FP_NAME_LEN 32
 
 typedef enum fp_status {
@@ -111,9 +111,16 @@ typedef struct fp_grid {
                                         time; timing K3/K4 too adds ~16 us per step)    */
 #define FP_FLAG_P2P 0x40u            /* world > 1 (or FP_FLAG_COLLECTIVES): the sweep's
                                         histogram exchange goes through peer memory --
-                                        each rank's K1 accumulators are read by every
-                                        rank's K3 over NVLink (CUDA IPC), no all-reduce;
-                                        implies FP_FLAG_REPLICATED_GRID (no all-gather).
+                                        each rank folds its K1 accumulators into one
+                                        histogram and publishes it; every rank's K3
+                                        reads all of them over NVLink (CUDA IPC), no
+                                        all-reduce; implies FP_FLAG_REPLICATED_GRID.
+                                        K3's wait for a peer is bounded (env
+                                        FP_P2P_TIMEOUT_MS, default 10000): on timeout
+                                        the sweep's results are invalid and the next
+                                        synchronising call (best_split,
+                                        sweep_histogram, a sweep with h_results)
+                                        returns FP_ERR_NCCL.
                                         Needs fp_p2p_export / fp_p2p_import before the
                                         first sweep; NCCL or the hooks still serve
                                         route_batch, calibrate_replay, peak windows.
@@ -201,6 +208,10 @@ typedef struct fp_plan_info {
   int32_t device, rank, world;
   uint32_t sm_count;
   uint32_t k1_grid, k1_block;   /* trace-pass launch configuration                */
+  int32_t nccl_comm_size;       /* ranks in the plan's NCCL communicator (0: none) */
+  uint32_t k3_shape;            /* K3 launch shape of the sweep: 0 cluster (paper-size
+                                   grids), 1 factored (large grids), 2 grid-stride */
+  uint32_t k3_blocks_per_model; /* K3 blocks per model (the cluster size for shape 0) */
 } fp_plan_info;
 
 typedef struct fp_plan fp_plan; /* opaque */
@@ -418,6 +429,10 @@ fp_status fp_nccl_get_unique_id(void *out128);
 #define FP_P2P_HANDLE_BYTES 64
 fp_status fp_p2p_export(fp_plan *plan, void *handle_out);
 fp_status fp_p2p_import(fp_plan *plan, const void *handles);
+/* Teardown of a FP_P2P plan: a peer's K3 may still be reading this rank's
+ * exchange buffer after this rank's last sweep returns. All ranks must
+ * synchronise (e.g. a barrier after best_split) before any of them calls
+ * fleet_plan_destroy, which frees the exported buffer. */
 
 fp_status fleet_plan_info(const fp_plan *plan, fp_plan_info *out);
 
@@ -432,8 +447,10 @@ uint64_t fp_kernel_launches(const fp_plan *plan);
 /* With FP_FLAG_KERNEL_TIMING (every kind) or FP_FLAG_TIME_TRACE (FP_KERNEL_TRACE
  * only): total device time (ms, CUDA events recorded on the launch stream
  * around each launch) and launch count of kernel `kind` since the last
- * fp_kernel_time_reset (or creation). Synchronizes those events. FP_ERR_STATE
- * when the kind is not timed by the plan's flags. */
+ * fp_kernel_time_reset (or creation). Synchronizes those events. The plan
+ * keeps at most 256 event pairs per kind: older launches are folded into the
+ * running total as new ones are recorded (bounded memory in long-running
+ * processes). FP_ERR_STATE when the kind is not timed by the plan's flags. */
 fp_status fp_kernel_time(fp_plan *plan, int32_t kind, double *total_ms, uint64_t *launches);
 fp_status fp_kernel_time_reset(fp_plan *plan);
 

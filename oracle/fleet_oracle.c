@@ -302,6 +302,15 @@ int or_num_threads(void) {
 #endif
 }
 
+/* Thread count of the OpenMP loops (bench.py's single-thread timing). */
+void or_set_num_threads(int n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+#else
+  (void)n;
+#endif
+}
+
 /* ==========================================================================
  * Token-budget estimation (NEXT-1; TEST INFRASTRUCTURE like the rest).
  * ========================================================================== */

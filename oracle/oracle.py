@@ -75,6 +75,7 @@ def lib():
         "or_sweep": (ctypes.c_int, [VP, U64, U32, VP, U32, VP, VP, VP, VP, U32, VP, U32, VP, U32,
                                     VP, U32, VP, F64, F64, VP, VP]),
         "or_num_threads": (ctypes.c_int, []),
+        "or_set_num_threads": (None, [ctypes.c_int]),
         "or_route_ratio": (F64, [F64, F64, F64, F64]),
         "or_pool3_size": (U32, []),
         "or_peak_size": (U32, []),
@@ -164,6 +165,10 @@ def cost(gpus, price, hours):
 
 def num_threads():
     return int(lib().or_num_threads())
+
+
+def set_num_threads(n):
+    lib().or_set_num_threads(int(n))
 
 
 # ---- the sweep -------------------------------------------------------------------

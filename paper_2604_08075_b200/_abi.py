@@ -14,7 +14,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FLEETPLAN_LIB") or os.path.join(_HERE, "lib", "libfleetplan.so")
 
-FP_ABI_VERSION = 1
+FP_ABI_VERSION = 2
 FP_FLAG_NO_MASS = 0x1
 FP_FLAG_REPLICATED_GRID = 0x2
 FP_FLAG_KERNEL_TIMING = 0x4
@@ -102,7 +102,8 @@ class fp_plan_info(ctypes.Structure):
     _fields_ = [("n_candidates", c_u64), ("cand_first", c_u64), ("cand_count", c_u64),
                 ("n_edges", c_u32), ("lut_shift", c_u32), ("lut_cells", c_u32), ("n_windows", c_u32),
                 ("device", c_i32), ("rank", c_i32), ("world", c_i32),
-                ("sm_count", c_u32), ("k1_grid", c_u32), ("k1_block", c_u32)]
+                ("sm_count", c_u32), ("k1_grid", c_u32), ("k1_block", c_u32),
+                ("nccl_comm_size", c_i32), ("k3_shape", c_u32), ("k3_blocks_per_model", c_u32)]
 
 
 # fp_candidate (192 bytes) as a numpy record, field order of fleet_plan.h

@@ -138,7 +138,7 @@ struct EvalArgs {
   const unsigned int *const *peer_flag = nullptr;
   uint32_t p2p_world = 0, p2p_epoch = 0;
   uint64_t p2p_off = 0;                 // u64 elements: parity * copies * 2 * nbins
-  unsigned long long *hist_out = nullptr;  // [2][nbins] the summed histogram (written by block (0, 0))
+  unsigned long long *hist_out = nullptr;  // [2][nbins] the summed histogram (written by one block)
   uint32_t nbins;                       // |E| + 1
   const uint32_t *b, *cs, *cl;          // grid values
   const uint16_t *b_edge, *cl_edge;     // index in E of each B / C_L
@@ -154,6 +154,9 @@ struct EvalArgs {
   const uint32_t *windows;              // [n_windows]
   const double *mu;                     // [m][g][w]
   const unsigned long long *cap_nseq = nullptr;  // [m][g][w] N_seq (Eq. 2), computed once per plan
+  const double *rmu = nullptr;          // [m][g][w] RN(1/mu) (0 outside mdiv's range), once per plan
+  unsigned int *err_word = nullptr;     // device error word (P2P wait timed out: 1 | peer << 8)
+  unsigned long long p2p_timeout_ns = 10000000000ull;
   double rate, hours;
   uint64_t per_model;                   // candidates per model
   uint64_t cand_first, cand_count;      // this rank's slice
@@ -161,11 +164,10 @@ struct EvalArgs {
   fp_candidate *best_out;               // [n_models] (this rank's)
   BlockBest *block_best;                // [n_models][grid_x]
   unsigned int *done;                   // [n_models] last-block-done counters (self-resetting)
-  // non-null: the block that reads K1's accumulator copies last (counter
-  // read_done, self-resetting) zeroes them for the next sweep, replacing the
-  // memset before K1
+  // non-null: the other parity's accumulator copies [copies][2][nbins], zeroed
+  // by one block for the next sweep (its last reader, the previous sweep's K3
+  // or fold kernel, completed before this sweep's plain-launched trace pass)
   unsigned long long *zero_copies = nullptr;
-  unsigned int *read_done = nullptr;
   // sweep_and_route (one rank's grid is the whole grid): the last block of
   // model route_model also writes {iB, iCS, iCL, ok} of its best split
   const uint32_t *edges = nullptr;
@@ -189,13 +191,27 @@ struct EvalArgs {
   BlockBest *block_best_pk = nullptr;
   unsigned int *done_pk = nullptr;
 };
-cudaError_t launch_eval(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
-// FP_FLAG_P2P: release this rank's accumulators of step `epoch` to its peers
-cudaError_t launch_p2p_signal(unsigned int *flag, unsigned int epoch, cudaStream_t s);
-cudaError_t launch_capacity(const EvalArgs &a, unsigned long long *cap, cudaStream_t s);  // fills cap_nseq
+// K3 launch shape (chosen once per plan)
+enum { kK3Cluster = 0, kK3Factored = 1, kK3Grid = 2 };
+struct EvalLaunch {
+  int shape = kK3Grid;
+  int grid_x = 1, block = 256;   // blocks per model (cluster size for kK3Cluster)
+  size_t smem = 0;
+};
+cudaError_t launch_eval(const EvalArgs &a, const EvalLaunch &L, cudaStream_t s);
+// sum the trace pass's accumulator copies into one [2][nbins] histogram; with
+// flag (FP_FLAG_P2P) also fence system-wide and publish `epoch` for the peers
+cudaError_t launch_fold(const unsigned long long *copies, uint32_t n_copies, uint32_t nbins, unsigned long long *out,
+                        unsigned int *flag, unsigned int epoch, cudaStream_t s);
+// fills cap_nseq and rmu
+cudaError_t launch_capacity(const EvalArgs &a, unsigned long long *cap, double *rmu, cudaStream_t s);
 cudaError_t launch_eval3(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
-cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, size_t smem, cudaStream_t s);
+cudaError_t launch_eval_peak(const EvalArgs &a, int grid_x, int block, cudaStream_t s);
 size_t eval_smem_bytes(const EvalArgs &a, int block);
+size_t eval_factored_smem_bytes(const EvalArgs &a);
+size_t eval_peak_smem_bytes(const EvalArgs &a);
+uint32_t eval_factored_blocks_per_model(const EvalArgs &a);
+int eval_max_cluster(int block, size_t smem);
 cudaError_t eval_prepare();
 
 // NEXT-4: peak-window provisioning (k_peak.cu + the k3 peak kernel)

@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 using namespace fp;
@@ -36,6 +38,8 @@ struct NcclApi {
   int (*AllGather)(const void *, void *, size_t, int, NcclComm, cudaStream_t) = nullptr;
   int (*CommDestroy)(NcclComm) = nullptr;
   const char *(*GetErrorString)(int) = nullptr;
+  int (*CommCount)(NcclComm, int *) = nullptr;
+  int (*CommGetAsyncError)(NcclComm, int *) = nullptr;
 };
 
 bool load_nccl(NcclApi &api, std::string &err) {
@@ -55,6 +59,8 @@ bool load_nccl(NcclApi &api, std::string &err) {
   FP_SYM(AllGather, "ncclAllGather");
   FP_SYM(CommDestroy, "ncclCommDestroy");
   FP_SYM(GetErrorString, "ncclGetErrorString");
+  FP_SYM(CommCount, "ncclCommCount");
+  FP_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef FP_SYM
   return true;
 }
@@ -99,10 +105,17 @@ struct fp_plan {
   TraceArgs ta{};
   EvalArgs ea{};
   unsigned long long *d_hist = nullptr;    // [2][nbins] summed histogram (written by K3)
-  unsigned long long *d_hcopies = nullptr; // [hist_copies][2][nbins] K1's accumulators
+  // K1's accumulators [2 parities][hist_copies][2][nbins]: sweep number q uses
+  // parity q & 1, and its K3 zeroes the other parity for sweep q + 1
+  unsigned long long *d_hcopies = nullptr;
   uint32_t hist_copies = 1;
-  // FP_FLAG_P2P: exchange buffer [2 parities][copies][2][nbins] u64 + the arrival flag,
-  // the peers' buffers opened by CUDA IPC, and device tables of their addresses
+  size_t copies_elems = 0;                  // u64 elements per parity
+  uint64_t sweep_seq = 0;
+  bool parity_clean[2] = {true, true};      // that parity's copies are zero (stream-ordered)
+  unsigned long long *d_fold = nullptr;     // dist (NCCL / hooks): [2][nbins] folded histogram, all-reduced
+  // FP_FLAG_P2P: exchange buffer [2 parities][2][nbins] u64 (each rank's folded
+  // histogram) + the arrival flag, the peers' buffers opened by CUDA IPC, and
+  // device tables of their addresses
   unsigned long long *d_xbuf = nullptr;
   unsigned int *d_xflag = nullptr;
   size_t xbuf_elems = 0;                    // u64 elements per parity
@@ -113,14 +126,16 @@ struct fp_plan {
   uint32_t p2p_epoch = 0;
   unsigned long long *d_rcounts = nullptr; // [8]: route counts [5], mis-routes [2] (or the picked split)
   unsigned long long *d_cap = nullptr;     // [M][G][W] N_seq
+  double *d_rmu = nullptr;                 // [M][G][W] RN(1/mu)
+  unsigned int *d_err = nullptr;           // device error word (P2P wait timeout)
   double *d_calib = nullptr;               // [256][2] estimator snapshot
   fp_candidate *d_best = nullptr;          // [world][n_models]
   fp_candidate *d_results = nullptr;       // [cand_count] (lazy)
   BlockBest *d_block_best = nullptr;
   unsigned int *d_done = nullptr;
-  unsigned int *d_read_done = nullptr;     // K3's copy-reader counter (zeroing protocol)
-  bool copies_clean = true;                // d_hcopies is zero (or will be, stream-ordered)
-  int k3_grid_x = 1, k3_block = 256;
+  EvalLaunch k3a;                          // K3 launch, argmin only (the step's)
+  EvalLaunch k3r;                          // K3 launch with every record (want_results)
+  int k3_grid_x = 1;                       // blocks per model of the grid-stride shape
   // host streaming
   uint32_t *d_stage[2] = {nullptr, nullptr};
   cudaStream_t copy_stream = nullptr;
@@ -151,11 +166,16 @@ struct fp_plan {
   NcclComm comm = nullptr;
   fp_collectives coll{};                   // host hooks replacing NCCL (optional)
   bool has_coll = false;
-  // per-kernel event timing (FP_FLAG_KERNEL_TIMING)
+  // per-kernel event timing (FP_FLAG_KERNEL_TIMING): a ring of event pairs;
+  // the oldest pending pair is folded into the running total when the ring is
+  // full, so a long-running process keeps a bounded number of events
   struct Timer {
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-    size_t used = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;   // ring
+    size_t head = 0, pending = 0;
+    double total_ms = 0.0;
+    uint64_t launches = 0;
   } timers[3];
+  cudaEvent_t ev_order = nullptr;          // orders a call on another stream after the last sweep
   // state
   bool have_sweep = false;
   cudaStream_t last_stream = nullptr;
@@ -190,6 +210,13 @@ fp_status cuda_fail(fp_plan *p, cudaError_t e, const char *what) {
   } while (0)
 
 fp_status nccl_check(fp_plan *p, int r, const char *what) {
+  // a communicator failure raised asynchronously (a peer died, a network
+  // error) is reported by the next collective's check
+  constexpr int kNcclInProgress = 7;
+  if (r == 0 && p && p->comm && g_nccl.CommGetAsyncError) {
+    int ae = 0;
+    if (g_nccl.CommGetAsyncError(p->comm, &ae) == 0 && ae != 0 && ae != kNcclInProgress) r = ae;
+  }
   if (r == 0) return FP_OK;
   return fail(p, FP_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
 }
@@ -417,10 +444,16 @@ fp_status upload(fp_plan *p) {
   // K1's accumulator copies: 16 for small |E| (a few KB), one for large ones
   // (K3 sums them per block)
   p->hist_copies = p->nbins <= 256 ? 16u : 1u;
-  CUDA_TRY(p, cudaMalloc(&p->d_hcopies, (size_t)p->hist_copies * 2 * p->nbins * 8), "cudaMalloc hist copies");
-  CUDA_TRY(p, cudaMemset(p->d_hcopies, 0, (size_t)p->hist_copies * 2 * p->nbins * 8), "memset hist copies");
+  p->copies_elems = (size_t)p->hist_copies * 2 * p->nbins;
+  CUDA_TRY(p, cudaMalloc(&p->d_hcopies, 2 * p->copies_elems * 8), "cudaMalloc hist copies");
+  CUDA_TRY(p, cudaMemset(p->d_hcopies, 0, 2 * p->copies_elems * 8), "memset hist copies");
+  if (p->dist && !(p->flags & FP_FLAG_P2P)) {
+    CUDA_TRY(p, cudaMalloc(&p->d_fold, 2ull * p->nbins * 8), "cudaMalloc folded histogram");
+  }
+  CUDA_TRY(p, cudaMalloc(&p->d_err, 16), "cudaMalloc error word");
+  CUDA_TRY(p, cudaMemset(p->d_err, 0, 16), "memset error word");
   if (p->flags & FP_FLAG_P2P) {
-    p->xbuf_elems = (size_t)p->hist_copies * 2 * p->nbins;
+    p->xbuf_elems = 2ull * p->nbins;
     const size_t bytes = 2 * p->xbuf_elems * 8 + 256;
     CUDA_TRY(p, cudaMalloc(&p->d_xbuf, bytes), "cudaMalloc p2p exchange");
     CUDA_TRY(p, cudaMemset(p->d_xbuf, 0, bytes), "memset p2p exchange");
@@ -440,7 +473,7 @@ fp_status upload(fp_plan *p) {
   ta.n_edges = (uint32_t)p->edges.size();
   ta.max_edge = p->max_edge;
   ta.want_mass = !(p->flags & FP_FLAG_NO_MASS);
-  ta.g_cnt = p->d_hcopies;
+  ta.g_cnt = p->d_hcopies;              // (per sweep: the sweep's parity)
   ta.g_mass = p->d_hcopies + p->nbins;
   ta.hist_copies = p->hist_copies;
 
@@ -484,14 +517,18 @@ fp_status upload(fp_plan *p) {
   ea.best_out = p->d_best + (size_t)((p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID)) ? p->rank : 0) * M;
   ea.edges = ta.edges;
   ea.n_edges = ta.n_edges;
-  // capacity table N_seq[m][g][w] (Eq. 2): plan data only, computed once here
+  // capacity table N_seq[m][g][w] (Eq. 2) and RN(1/mu): plan data only, computed once here
   CUDA_TRY(p, cudaMalloc(&p->d_cap, (size_t)M * G * W * 8), "cudaMalloc capacity table");
+  CUDA_TRY(p, cudaMalloc(&p->d_rmu, (size_t)M * G * W * 8), "cudaMalloc reciprocal table");
   {
-    cudaError_t e = launch_capacity(ea, p->d_cap, 0);
+    cudaError_t e = launch_capacity(ea, p->d_cap, p->d_rmu, 0);
     if (e != cudaSuccess) return cuda_fail(p, e, "capacity table launch");
     CUDA_TRY(p, cudaDeviceSynchronize(), "capacity table");
   }
   ea.cap_nseq = p->d_cap;
+  ea.rmu = p->d_rmu;
+  ea.err_word = p->d_err;
+  ea.p2p_timeout_ns = (unsigned long long)std::max(1, env_int("FP_P2P_TIMEOUT_MS", 10000)) * 1000000ull;
 
   // K3 grid: enough blocks for the largest per-model part of this rank's slice
   uint64_t widest = 0;
@@ -500,28 +537,60 @@ fp_status upload(fp_plan *p) {
     uint64_t hi = std::min<uint64_t>((uint64_t)(m + 1) * p->per_model, p->cand_first + p->cand_count);
     if (hi > lo) widest = std::max(widest, hi - lo);
   }
-  // one thread per candidate up to ~8 blocks per SM in total, then grid-stride
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, p->device);
+  CUDA_TRY(p, eval_prepare(), "k3 attributes");
+  const size_t tab_smem = eval_smem_bytes(ea, 256);
+  if (tab_smem > 190 * 1024)
+    return fail(p, FP_ERR_CONFIG, "histogram + capacity table need %zu B of shared memory", tab_smem);
+  // grid-stride shape (full records of large grids): one thread per candidate
+  // up to ~8 blocks per SM in total, then grid-stride
   const uint64_t cap = std::max<uint64_t>(1, (uint64_t)sms * 8 / M);
-  // block size: small grids (the paper's) are latency-bound -> more, smaller blocks
-  p->k3_block = env_int("FP_K3_BLOCK", widest <= (uint64_t)sms * 128 ? 128 : 256);
-  if (p->k3_block < 32 || p->k3_block > 256 || (p->k3_block & 31))
-    return fail(p, FP_ERR_CONFIG, "FP_K3_BLOCK must be a multiple of 32 in [32, 256]");
-  p->k3_grid_x = (int)std::min<uint64_t>(cap * (256 / p->k3_block),
-                                         std::max<uint64_t>(1, (widest + p->k3_block - 1) / p->k3_block));
+  p->k3_grid_x = (int)std::min<uint64_t>(cap, std::max<uint64_t>(1, (widest + 255) / 256));
   p->k3_grid_x = std::max(1, std::min(p->k3_grid_x, env_int("FP_K3_GRID", p->k3_grid_x)));
   if (p->k3_grid_x > 65535 * 64) return fail(p, FP_ERR_CONFIG, "candidate grid too large for one launch");
-  CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * p->k3_grid_x * sizeof(BlockBest)), "cudaMalloc block_best");
+  EvalLaunch grid;
+  grid.shape = kK3Grid;
+  grid.grid_x = p->k3_grid_x;
+  grid.block = 256;
+  grid.smem = tab_smem;
+  // cluster shape: the paper-size grids, one cluster per model reduced in DSMEM
+  // (<= 4 candidates per thread); FP_K3_SHAPE=grid|factored|cluster forces a shape
+  const char *force = getenv("FP_K3_SHAPE");
+  const int max_cl = eval_max_cluster(256, tab_smem);
+  EvalLaunch clu;
+  clu.shape = kK3Cluster;
+  clu.block = widest <= 512 ? 128 : 256;
+  clu.grid_x = (int)std::min<uint64_t>(max_cl, std::max<uint64_t>(1, (widest + clu.block - 1) / clu.block));
+  clu.smem = tab_smem;
+  const bool cluster_ok = widest <= (uint64_t)clu.grid_x * clu.block * 4;
+  // factored shape: large grids, argmin only
+  EvalLaunch fac;
+  fac.shape = kK3Factored;
+  fac.grid_x = (int)eval_factored_blocks_per_model(ea);
+  fac.block = 256;
+  fac.smem = eval_factored_smem_bytes(ea);
+  const bool fac_ok = fac.smem <= 190 * 1024 && fac.grid_x <= 65535 * 64;
+  if (force && !strcmp(force, "grid")) {
+    p->k3a = grid;
+    p->k3r = grid;
+  } else if (force && !strcmp(force, "factored") && fac_ok) {
+    p->k3a = fac;
+    p->k3r = grid;
+  } else if (cluster_ok && !(force && !strcmp(force, "factored"))) {
+    p->k3a = clu;
+    p->k3r = clu;
+  } else {
+    p->k3a = fac_ok ? fac : grid;
+    p->k3r = grid;
+  }
+  const int bb_blocks = std::max(p->k3_grid_x, p->k3a.shape == kK3Factored ? p->k3a.grid_x : 1);
+  CUDA_TRY(p, cudaMalloc(&p->d_block_best, (size_t)M * bb_blocks * sizeof(BlockBest)), "cudaMalloc block_best");
   CUDA_TRY(p, cudaMalloc(&p->d_done, M * sizeof(unsigned int)), "cudaMalloc done");
   CUDA_TRY(p, cudaMemset(p->d_done, 0, M * sizeof(unsigned int)), "memset done");
-  CUDA_TRY(p, cudaMalloc(&p->d_read_done, sizeof(unsigned int)), "cudaMalloc read_done");
-  CUDA_TRY(p, cudaMemset(p->d_read_done, 0, sizeof(unsigned int)), "memset read_done");
   ea.block_best = p->d_block_best;
   ea.done = p->d_done;
-  p->k3_smem = eval_smem_bytes(ea, p->k3_block);
-  if (p->k3_smem > 190 * 1024)
-    return fail(p, FP_ERR_CONFIG, "histogram + capacity table need %zu B of shared memory", p->k3_smem);
+  p->k3_smem = tab_smem;
   return FP_OK;
 }
 
@@ -550,7 +619,6 @@ fp_status configure_launch(fp_plan *p) {
   int k4_res = 1;
   CUDA_TRY(p, route_occupancy(p->k4_block, &k4_res), "k4 occupancy");
   p->k4_grid = p->sm_count * std::min(k4_res, env_int("FP_K4_BLOCKS_PER_SM", k4_res));
-  CUDA_TRY(p, eval_prepare(), "k3 attributes");
   // pinned host mirrors for the small synchronous results
   CUDA_TRY(p, cudaMallocHost(&p->h_best, (size_t)p->world * p->models.size() * sizeof(fp_candidate)),
            "cudaMallocHost best");
@@ -558,7 +626,20 @@ fp_status configure_launch(fp_plan *p) {
   return FP_OK;
 }
 
-// Record an event pair around one launch of kernel `kind` (timing flag only).
+constexpr size_t kTimerRing = 256;
+
+// Fold the oldest pending event pair of `t` into its running total.
+void timer_fold_one(fp_plan::Timer &t) {
+  const size_t i = (t.head + t.ev.size() - t.pending) % t.ev.size();
+  float ms = 0.f;
+  if (cudaEventSynchronize(t.ev[i].second) == cudaSuccess &&
+      cudaEventElapsedTime(&ms, t.ev[i].first, t.ev[i].second) == cudaSuccess)
+    t.total_ms += ms;
+  cudaGetLastError();
+  --t.pending;
+}
+
+// Record an event pair around one launch of kernel `kind` (timing flags only).
 struct LaunchTimer {
   fp_plan *p;
   cudaStream_t s;
@@ -567,12 +648,20 @@ struct LaunchTimer {
     if (!(p->flags & FP_FLAG_KERNEL_TIMING) && !((p->flags & FP_FLAG_TIME_TRACE) && kind == FP_KERNEL_TRACE))
       return;
     auto &t = p->timers[kind];
-    if (t.used == t.ev.size()) {
-      cudaEvent_t a, b;
-      if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { cudaGetLastError(); return; }
-      t.ev.emplace_back(a, b);
+    if (t.pending == t.ev.size()) {
+      if (t.ev.size() < kTimerRing) {
+        // grow the ring: the new slot goes right after the newest pending pair
+        cudaEvent_t a, b;
+        if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) { cudaGetLastError(); return; }
+        t.ev.insert(t.ev.begin() + t.head, std::make_pair(a, b));
+      } else {
+        timer_fold_one(t);               // ring full: fold the oldest (long finished) launch
+      }
     }
-    auto &pr = t.ev[t.used++];
+    auto &pr = t.ev[t.head];
+    t.head = (t.head + 1) % t.ev.size();
+    ++t.pending;
+    ++t.launches;
     cudaEventRecord(pr.first, s);
     stop = pr.second;
   }
@@ -580,6 +669,27 @@ struct LaunchTimer {
     if (stop) cudaEventRecord(stop, s);
   }
 };
+
+// NVTX range around a host-side phase (header-only NVTX3: a no-op unless a
+// tool such as Nsight injects itself)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// The device error word (the P2P wait's timeout), read at the synchronising calls.
+fp_status check_device_error(fp_plan *p) {
+  unsigned int *h = reinterpret_cast<unsigned int *>(p->h_small + 2ull * p->nbins + 7);
+  CUDA_TRY(p, cudaMemcpy(h, p->d_err, 4, cudaMemcpyDeviceToHost), "D2H error word");
+  if (*h) {
+    const unsigned int v = *h;
+    CUDA_TRY(p, cudaMemset(p->d_err, 0, 4), "clear error word");
+    return fail(p, FP_ERR_NCCL, "P2P exchange: rank %u did not publish its histogram within %d ms (a peer "
+                "failed or stopped sweeping); results of that sweep are invalid", v >> 8,
+                std::max(1, env_int("FP_P2P_TIMEOUT_MS", 10000)));
+  }
+  return FP_OK;
+}
 
 fp_status ensure_staging(fp_plan *p) {
   if (p->d_stage[0]) return FP_OK;
@@ -841,7 +951,10 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_results);
     cudaFree(p->d_block_best);
     cudaFree(p->d_done);
-    cudaFree(p->d_read_done);
+    cudaFree(p->d_fold);
+    cudaFree(p->d_rmu);
+    cudaFree(p->d_err);
+    if (p->ev_order) cudaEventDestroy(p->ev_order);
     cudaFree(p->d_resident);
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
@@ -881,6 +994,13 @@ fp_status fleet_plan_info(const fp_plan *p, fp_plan_info *o) {
   o->sm_count = (uint32_t)p->sm_count;
   o->k1_grid = (uint32_t)p->k1_grid;
   o->k1_block = (uint32_t)p->k1_block;
+  o->nccl_comm_size = 0;
+  if (p->comm && g_nccl.CommCount) {
+    int n = 0;
+    if (g_nccl.CommCount(p->comm, &n) == 0) o->nccl_comm_size = n;
+  }
+  o->k3_shape = (uint32_t)p->k3a.shape;
+  o->k3_blocks_per_model = (uint32_t)p->k3a.grid_x;
   return FP_OK;
 }
 
@@ -892,21 +1012,20 @@ fp_status fp_kernel_time(fp_plan *p, int32_t kind, double *total_ms, uint64_t *l
     return fail(p, FP_ERR_STATE, "kernel kind %d is not timed (FP_FLAG_KERNEL_TIMING / FP_FLAG_TIME_TRACE)", kind);
   DeviceGuard g(p->device);
   auto &t = p->timers[kind];
-  double tot = 0.0;
-  for (size_t i = 0; i < t.used; ++i) {
-    CUDA_TRY(p, cudaEventSynchronize(t.ev[i].second), "event sync");
-    float ms = 0.f;
-    CUDA_TRY(p, cudaEventElapsedTime(&ms, t.ev[i].first, t.ev[i].second), "event elapsed");
-    tot += ms;
-  }
-  if (total_ms) *total_ms = tot;
-  if (launches) *launches = t.used;
+  while (t.pending) timer_fold_one(t);
+  if (total_ms) *total_ms = t.total_ms;
+  if (launches) *launches = t.launches;
   return FP_OK;
 }
 
 fp_status fp_kernel_time_reset(fp_plan *p) {
   if (!p) return FP_ERR_INVALID_ARG;
-  for (auto &t : p->timers) t.used = 0;
+  DeviceGuard g(p->device);
+  for (auto &t : p->timers) {
+    while (t.pending) timer_fold_one(t);
+    t.total_ms = 0.0;
+    t.launches = 0;
+  }
   return FP_OK;
 }
 
@@ -1213,87 +1332,105 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   if (!p->dist && n_local == 0) return fail(p, FP_ERR_EMPTY_TRACE, "empty trace (S:170)");
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
-  // FP_FLAG_P2P: this step's accumulators are this rank's exchange buffer of
-  // parity epoch & 1 (a peer may still be reading the other parity's)
+  // this sweep's accumulator parity (its K3 clears the other one for the next sweep)
+  const uint32_t par = (uint32_t)(p->sweep_seq & 1u);
+  unsigned long long *acc = p->d_hcopies + par * p->copies_elems;
+  unsigned long long *other = p->d_hcopies + (par ^ 1u) * p->copies_elems;
+  // a memset only when an earlier sweep failed before its K3 ran
+  if (!p->parity_clean[par])
+    CUDA_TRY(p, cudaMemsetAsync(acc, 0, p->copies_elems * 8, s), "memset hist");
   const bool p2p = (p->flags & FP_FLAG_P2P) != 0;
   if (p2p && !p->p2p_ready) return fail(p, FP_ERR_STATE, "FP_FLAG_P2P plan: call fp_p2p_import first");
-  const uint32_t epoch = p2p ? ++p->p2p_epoch : 0u;
-  unsigned long long *acc = p2p ? p->d_xbuf + (size_t)(epoch & 1u) * p->xbuf_elems : p->d_hcopies;
-  // K1: trace pass into the global bin histogram. The copies are zeroed by
-  // the previous sweep's K3 (see zero_copies below); a memset only if that
-  // sweep did not get to launch K3, and always for the P2P parity buffers
-  if (p2p || !p->copies_clean)
-    CUDA_TRY(p, cudaMemsetAsync(acc, 0, (size_t)p->hist_copies * 2 * p->nbins * 8, s), "memset hist");
-  if (!p2p) p->copies_clean = false;
+  // FP_FLAG_P2P: the step's epoch is committed only once this rank has
+  // published it (a failure before that leaves the peers waiting for the same
+  // epoch, which a retried sweep then publishes)
+  const uint32_t epoch = p2p ? p->p2p_epoch + 1u : 0u;
+  p->parity_clean[par] = false;
   fp_status st = FP_OK;
-  if (raw) {
-    if (n_local) {
+  {
+    NvtxRange r("fp:K1 trace pass");
+    if (raw) {
+      if (n_local) {
+        LaunchTimer lt(p, FP_KERNEL_TRACE, s);
+        TraceArgs t = *raw;
+        t.g_cnt = acc;
+        t.g_mass = acc + p->nbins;
+        cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
+        if (e != cudaSuccess) return cuda_fail(p, e, "trace pass (raw) launch");
+        ++p->launches;
+      }
+    } else st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t off) {
+      TraceArgs t = p->ta;
+      t.len = ptr;
+      t.n = n;
+      t.g_cnt = acc;
+      t.g_mass = acc + p->nbins;
+      // packed bins: this chunk's body starts at global uint4 off / 4 (chunks are
+      // whole multiples of 4 elements except the last, and have no head)
+      t.bins_out = bins ? bins + (bins_side ? 0 : off) : nullptr;   // packed: device traces (one call, off = 0)
+      t.bins_hi = bins_hi;
+      t.bins_pack = bins_side ? 1u : 0u;
+      t.bins_side = bins_side;
       LaunchTimer lt(p, FP_KERNEL_TRACE, s);
-      TraceArgs r = *raw;
-      r.g_cnt = acc;
-      r.g_mass = acc + p->nbins;
-      cudaError_t e = launch_trace(r, p->k1_grid, p->k1_block, p->k1_smem, s);
-      if (e != cudaSuccess) return cuda_fail(p, e, "trace pass (raw) launch");
+      cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
+      if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");
       ++p->launches;
-    }
-  } else st = over_trace(p, d_len, n_local, s, [&](const uint32_t *ptr, uint64_t n, uint64_t off) {
-    TraceArgs t = p->ta;
-    t.len = ptr;
-    t.n = n;
-    t.g_cnt = acc;
-    t.g_mass = acc + p->nbins;
-    // packed bins: this chunk's body starts at global uint4 off / 4 (chunks are
-    // whole multiples of 4 elements except the last, and have no head)
-    t.bins_out = bins ? bins + (bins_side ? 0 : off) : nullptr;   // packed: device traces (one call, off = 0)
-    t.bins_hi = bins_hi;
-    t.bins_pack = bins_side ? 1u : 0u;
-    t.bins_side = bins_side;
-    LaunchTimer lt(p, FP_KERNEL_TRACE, s);
-    cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
-    if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");
-    ++p->launches;
-    return FP_OK;
-  }, resident);
+      return FP_OK;
+    }, resident);
+  }
   if (st != FP_OK) return st;
-  // C1: sum the per-rank histograms -- through peer memory in K3's prologue
-  // (FP_FLAG_P2P: release this rank's accumulators), else an all-reduce
-  if (p2p) {
-    cudaError_t e = launch_p2p_signal(p->d_xflag, epoch, s);
-    if (e != cudaSuccess) return cuda_fail(p, e, "p2p signal launch");
-    ++p->launches;
-  } else if (p->dist) {
-    st = all_reduce_u64(p, p->d_hcopies, (size_t)p->hist_copies * 2 * p->nbins, s, "all-reduce(histogram)");
-    if (st != FP_OK) return st;
-  }
-  // K2 + K3: scan, evaluate this rank's candidates, per-model argmin
-  if (h_results && !p->d_results && p->cand_count)
-    CUDA_TRY(p, cudaMalloc(&p->d_results, p->cand_count * sizeof(fp_candidate)), "cudaMalloc results");
+  // C1: sum the per-rank histograms. The accumulator copies are folded into
+  // one [2][nbins] histogram first (one small kernel), then either published
+  // to the peers (FP_FLAG_P2P: K3's prologue reads every rank's over NVLink)
+  // or all-reduced (2 (|E| + 1) u64).
   EvalArgs ea = p->ea;
-  ea.rate = rate_rps;
-  ea.results = h_results ? p->d_results : nullptr;
-  if (!p2p) {
-    ea.zero_copies = p->d_hcopies;
-    ea.read_done = p->d_read_done;
-  }
   if (p2p) {
+    NvtxRange r("fp:C1 p2p publish");
+    unsigned long long *xb = p->d_xbuf + (size_t)(epoch & 1u) * p->xbuf_elems;
+    cudaError_t e = launch_fold(acc, p->hist_copies, p->nbins, xb, p->d_xflag, epoch, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "p2p fold/publish launch");
+    ++p->launches;
+    p->p2p_epoch = epoch;
     ea.peer_hist = p->d_peer_hist;
     ea.peer_flag = p->d_peer_flag;
     ea.p2p_world = (uint32_t)p->world;
     ea.p2p_epoch = epoch;
     ea.p2p_off = (size_t)(epoch & 1u) * p->xbuf_elems;
+  } else if (p->dist) {
+    NvtxRange r("fp:C1 all-reduce(histogram)");
+    cudaError_t e = launch_fold(acc, p->hist_copies, p->nbins, p->d_fold, nullptr, 0, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "fold launch");
+    ++p->launches;
+    st = all_reduce_u64(p, p->d_fold, 2ull * p->nbins, s, "all-reduce(histogram)");
+    if (st != FP_OK) return st;
+    ea.hist_cnt = p->d_fold;
+    ea.hist_mass = p->d_fold + p->nbins;
+    ea.hist_copies = 1;
+  } else {
+    ea.hist_cnt = acc;
+    ea.hist_mass = acc + p->nbins;
   }
+  // K2 + K3: scan, evaluate this rank's candidates, per-model argmin
+  if (h_results && !p->d_results && p->cand_count)
+    CUDA_TRY(p, cudaMalloc(&p->d_results, p->cand_count * sizeof(fp_candidate)), "cudaMalloc results");
+  ea.rate = rate_rps;
+  ea.results = h_results ? p->d_results : nullptr;
+  ea.zero_copies = other;
   ea.route_out = route_out;
   ea.route_model = route_model;
   cudaError_t e;
   {
+    NvtxRange r("fp:K3 candidate evaluation");
     LaunchTimer lt(p, FP_KERNEL_EVAL, s);
-    e = launch_eval(ea, p->k3_grid_x, p->k3_block, p->k3_smem, s);
+    e = launch_eval(ea, h_results ? p->k3r : p->k3a, s);
   }
   if (e != cudaSuccess) return cuda_fail(p, e, "candidate evaluation launch");
-  if (!p2p) p->copies_clean = true;        // K3 zeroes them after its last read
+  p->parity_clean[par ^ 1u] = true;        // K3 zeroes them (stream-ordered)
+  ++p->sweep_seq;
   ++p->launches;
   // C2: gather every rank's per-model best
   if (p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID)) {
+    NvtxRange r("fp:C2 all-gather(best)");
     const size_t bytes = p->models.size() * sizeof(fp_candidate);
     st = all_gather_bytes(p, p->d_best + (size_t)p->rank * p->models.size(), p->d_best, bytes, s,
                           "all-gather(best)");
@@ -1306,6 +1443,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
                                 cudaMemcpyDeviceToHost, s),
              "D2H results");
     CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    if (p2p) return check_device_error(p);
   }
   return FP_OK;
 }
@@ -1353,7 +1491,7 @@ fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_r
     p->ea3.hist_copies = 1;
     p->ea3.hist_out = nullptr;
     p->ea3.zero_copies = nullptr;
-    p->ea3.read_done = nullptr;
+    p->ea3.p2p_world = 0;
     p->ea3.pairs = reinterpret_cast<const uint32_t *>(p->d_p3);
     p->ea3.n_pairs = (uint32_t)pairs.size();
     p->ea3.b_win3 = reinterpret_cast<const uint16_t *>(p->d_p3 + off_bw);
@@ -1365,6 +1503,12 @@ fp_status sweep_three_pools(fp_plan *p, double rate_rps, fp_pool3_candidate *h_r
   }
   if (h_results && !p->d_results3)
     CUDA_TRY(p, cudaMalloc(&p->d_results3, p->n_cand3 * sizeof(fp_pool3_candidate)), "cudaMalloc results3");
+  // the last sweep's histogram was written on last_stream: order this call after it
+  if (p->last_stream != s) {
+    if (!p->ev_order) CUDA_TRY(p, cudaEventCreateWithFlags(&p->ev_order, cudaEventDisableTiming), "event");
+    CUDA_TRY(p, cudaEventRecord(p->ev_order, p->last_stream), "record order");
+    CUDA_TRY(p, cudaStreamWaitEvent(s, p->ev_order, 0), "wait order");
+  }
   EvalArgs ea = p->ea3;
   ea.rate = rate_rps;
   ea.results3 = h_results ? p->d_results3 : nullptr;
@@ -1745,7 +1889,7 @@ fp_status sweep_peak_windows(fp_plan *p, const uint32_t *d_len, const uint64_t *
   ea.results_pk = h_results ? p->d_results_pk : nullptr;
   {
     LaunchTimer lt(p, FP_KERNEL_EVAL, s);
-    cudaError_t e = launch_eval_peak(ea, grid_x, 256, (size_t)ea.n_gpus * ea.n_windows * 24, s);
+    cudaError_t e = launch_eval_peak(ea, grid_x, 256, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "peak evaluation launch");
   }
   ++p->launches;
@@ -1773,6 +1917,10 @@ fp_status best_split(fp_plan *p, fp_candidate *h_best) {
   CUDA_TRY(p, cudaMemcpyAsync(p->h_small, p->d_hist, p->nbins * 8, cudaMemcpyDeviceToHost, p->last_stream),
            "D2H hist");
   CUDA_TRY(p, cudaStreamSynchronize(p->last_stream), "sync");
+  if (p->flags & FP_FLAG_P2P) {
+    fp_status st = check_device_error(p);
+    if (st != FP_OK) return st;
+  }
   unsigned long long total = 0;
   for (uint32_t j = 0; j < p->nbins; ++j) total += p->h_small[j];
   if (total == 0) return fail(p, FP_ERR_EMPTY_TRACE, "global trace is empty");
@@ -1785,6 +1933,10 @@ fp_status sweep_histogram(fp_plan *p, uint32_t *h_edges, uint64_t *h_bin_cnt, ui
   if (!p->have_sweep) return fail(p, FP_ERR_STATE, "sweep_histogram before sweep_thresholds");
   DeviceGuard g(p->device);
   CUDA_TRY(p, cudaStreamSynchronize(p->last_stream), "sync");
+  if (p->flags & FP_FLAG_P2P) {
+    fp_status st = check_device_error(p);
+    if (st != FP_OK) return st;
+  }
   if (h_edges) memcpy(h_edges, p->edges.data(), p->edges.size() * 4);
   if (h_bin_cnt) CUDA_TRY(p, cudaMemcpy(h_bin_cnt, p->d_hist, p->nbins * 8, cudaMemcpyDeviceToHost), "D2H hist");
   if (h_bin_mass)

@@ -258,4 +258,17 @@ def k3_large(n: int = 1_000_000) -> Config:
                        description="2^24-candidate ALU-regime grid on a 1e6 MIX trace")
 
 
-CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "K3L": k3_large}
+def k3_factored(n: int = 400_003) -> Config:
+    """Test grid just above the cluster K3 shape's reach (2 models x 2 GPUs x
+    96 B x 16 C_S x 20 C_L = 122,880 candidates; > 8,192 per model), so the
+    factored K3 shape runs; C_S values are not B or C_L values (extra edges).
+    Not a paper workload."""
+    b = [64 * k for k in range(1, 97)]
+    cs = [6144 + 512 * k for k in range(1, 17)]
+    cl = [8192 + 4096 * k for k in range(0, 20)]
+    return make_config("K3F", "MIX", SEED0 + 7, n, 10000.0, ["llama3-8b", "qwen3-235b-a22b"],
+                       ["b200-180g", "mi300x-192g"], b, cs, cl,
+                       description="122,880-candidate factored-shape test grid")
+
+
+CONFIGS = {"C1": c1, "C2": c2, "C3": c3, "C4": c4, "C5": c5, "K3L": k3_large, "K3F": k3_factored}

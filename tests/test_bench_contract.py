@@ -39,3 +39,16 @@ def test_warmup_below_three_is_rejected():
     r = _bench("--impl", "reference", "--steps", "1", "--warmup", "1", "--ref-sample", "1000", timeout=120)
     assert r.returncode != 0
     assert "warmup" in r.stderr
+
+
+def test_self_spawn_two_ranks_gloo():
+    """`bench.py --gpus 2` without torchrun re-launches itself as two ranks
+    (torch.distributed.run, 127.0.0.1); the plumbing check runs the same launch,
+    process group, max-over-ranks and rank-0-only output path on gloo."""
+    r = _bench("--gpus", "2", "--plumbing-check", timeout=240)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["plumbing"] == "ok" and d["n_gpus"] == 2 and d["max_over_ranks"] == 2.0
+    assert sorted(x["rank"] for x in d["ranks"]) == [0, 1]

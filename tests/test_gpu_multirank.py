@@ -89,7 +89,8 @@ def _rank(rank, world, port, name, n, flags, q):
 @pytest.mark.parametrize("name,n,replicated,world", [("C5", 2_000_003, False, 2), ("C3", 300_001, False, 2),
                                                      ("C4", 500_000, True, 2), ("C1", 1000, False, 2),
                                                      ("C5", 1_500_001, "p2p", 2), ("C1", 1000, "p2p", 2),
-                                                     ("C5", 1_000_003, False, 4), ("C5", 1_000_003, "p2p", 4)])
+                                                     ("C5", 1_000_003, False, 4), ("C5", 1_000_003, "p2p", 4),
+                                                     ("K3F", 200_003, False, 2), ("K3F", 200_003, "p2p", 2)])
 def test_two_ranks_one_gpu_match_oracle(name, n, replicated, world):
     """replicated="p2p": the histogram sum goes through peer memory (FP_FLAG_P2P,
     CUDA IPC between the two processes sharing cuda:0), grid replicated."""
@@ -127,7 +128,7 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated, world):
         assert o[2] == obest.tobytes()                      # same best split on every rank
         cnt = np.frombuffer(o[3], dtype=np.uint64)
         mass = np.frombuffer(o[4], dtype=np.uint64)
-        edges = np.array(sorted(set(cfg.b_short) | set(cfg.c_long)), dtype=np.uint32)
+        edges = np.array(sorted(set(cfg.b_short) | set(cfg.c_short) | set(cfg.c_long)), dtype=np.uint32)
         ocnt, omass = oracle.count_le(L, edges)
         assert np.array_equal(np.cumsum(cnt)[:-1], ocnt) and int(cnt.sum()) == n
         assert np.array_equal(np.cumsum(mass)[:-1], omass)
@@ -143,3 +144,60 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated, world):
             assert sbest == obest.tobytes()
         got = np.frombuffer(dec, dtype=np.uint8)
         assert np.array_equal(got, odec[first:first + got.size])
+
+
+def _silent_peer(rank, world, port, q):
+    """Rank 1 opens the exchange but never sweeps; rank 0's K3 must give up
+    waiting (FP_P2P_TIMEOUT_MS) and report FP_ERR_NCCL instead of hanging."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        os.environ["FP_P2P_TIMEOUT_MS"] = "1500"
+        import time
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2604_08075_b200 as fp
+        from synth import configs
+        from synth.gen import generate_device
+        cfg = configs.c5().with_n(100_000)
+        plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=0, rank=rank, world=world,
+                                    flags=fp.FP_FLAG_P2P, collectives=GlooCollectives(world))
+        handles = [None] * world
+        dist.all_gather_object(handles, fp.fp_p2p_export(plan))
+        fp.fp_p2p_import(plan, handles)
+        status = None
+        if rank == 0:
+            d = generate_device(cfg.shape, cfg.seed, 0, cfg.n_requests)
+            t0 = time.time()
+            fp.sweep_thresholds(plan, d, cfg.rate_rps)
+            try:
+                fp.best_split(plan)
+                status = "no error"
+            except fp.FleetPlanError as e:
+                status = (e.status, time.time() - t0)
+            # the error word is cleared: the plan reports it once
+        dist.barrier()
+        fp.fleet_plan_destroy(plan)
+        dist.destroy_process_group()
+        q.put((rank, status, None))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, None, traceback.format_exc()))
+
+
+def test_p2p_wait_is_bounded():
+    import paper_2604_08075_b200 as fp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_silent_peer, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for o in out:
+        assert o[2] is None, o[2]
+    status, dt = out[0][1]
+    assert status == fp.STATUS.index("FP_ERR_NCCL") and 1.0 < dt < 60.0

@@ -370,61 +370,110 @@ def test_divisions_random_mu_and_rates(rate):
     assert b3.tobytes() == ob3.tobytes()
 
 
-@pytest.mark.slow
-def test_full_size_c5_step_against_oracle():
-    """The bench's step at its full size and launch configuration (C5, 1e9
-    requests, sweep_and_route with 6-bit packed bins): every candidate record of
-    the 1e9-request sweep and the per-model best splits equal the oracle's over
-    the whole trace (the oracle's definition loop takes ~10 s on the box's
-    cores), the histogram equals count_le at every edge, and sampled windows of
-    the decision bytes equal the oracle's Alg. 1 for the chosen split."""
-    cfg = configs.c5()
+def _all_decisions_equal(dec, L, b, what, chunk=1 << 26):
+    """Every decision byte of the step against the oracle's Alg. 1 for split b,
+    chunk by chunk (no sampling)."""
+    n = L.size
+    for first in range(0, n, chunk):
+        last = min(n, first + chunk)
+        odec, _ = oracle.route_batch(L[first:last], int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+        got = dec[first:last].cpu().numpy()
+        if not np.array_equal(got, odec):
+            bad = np.nonzero(got != odec)[0]
+            raise AssertionError(f"{what}: {bad.size} decisions differ in [{first}, {last}), first at {first + bad[0]}")
+
+
+def _step_against_oracle(cfg, flags=0):
+    """The bench's step (sweep_and_route in its asynchronous form, the launch
+    configuration bench.py times) at the config's full size, checked
+    completely: the step's own histogram (read right after the step, before
+    any other sweep) equals count_le at every edge, its best records equal the
+    oracle's, and every one of its decision bytes equals Alg. 1 for the
+    oracle's best split. Then every candidate record of a records sweep."""
     n = cfg.n_requests
     L = generate_host(cfg.shape, cfg.seed, 0, n)
     d = generate_device(cfg.shape, cfg.seed, 0, n)
-    plan = _plan(cfg)
+    plan = _plan(cfg, flags=flags)
     dec = torch.empty(n, dtype=torch.uint8, device="cuda")
-    best, counts = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec)
-    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
-    allc, obest = oracle.sweep(cfg, L)
-    _compare_records(res, allc, "C5 full")
-    assert best.tobytes() == obest.tobytes()
-    edges, cnt, mass = fp.sweep_histogram(plan)
+    assert fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec, want_best=False) == (None, None)
+    edges, cnt, mass = fp.sweep_histogram(plan)                    # the step's own K1 histogram
+    best = fp.best_split(plan)
     ocnt, omass = oracle.count_le(L, edges)
     assert np.array_equal(np.cumsum(cnt)[:-1], ocnt) and int(cnt.sum()) == n
     assert np.array_equal(np.cumsum(mass)[:-1], omass)
-    b = obest[0]
-    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
-        [int(b["n_short"]), int(b["n_long"]), int(b["n_reject"]), int(b["mass_short"]), int(b["mass_long"])]
-    rng = np.random.default_rng(3)
-    for first in list(rng.integers(0, n - (1 << 24), 3)) + [0, n - (1 << 24)]:
-        first = int(first)
-        odec, _ = oracle.route_batch(L[first:first + (1 << 24)], int(b["b_short"]), int(b["c_short"]),
-                                     int(b["c_long"]))
-        assert np.array_equal(dec[first:first + (1 << 24)].cpu().numpy(), odec), f"decisions @{first}"
+    allc, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    _all_decisions_equal(dec, L, obest[0], cfg.name)
+    del dec
+    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    _compare_records(res, allc, f"{cfg.name} full")
+    return plan
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_size_c5_step_against_oracle():
+    """C5 (1e9 requests, 4,096 candidates, 6-bit packed bins) -- the bench's
+    workload -- on a plan with the bench's flags: all 1e9 decision bytes, the
+    step's histogram and best records, then all 4,096 records."""
+    _step_against_oracle(configs.c5(), flags=fp.FP_FLAG_TIME_TRACE)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
 def test_full_size_configs_against_oracle(name):
-    """C2 (10.3M), C3 (1e8) and C4 (1e8) at the sizes BASELINE.json names: every
-    candidate record (up to 30,720) byte-identical to the oracle's sweep of the
-    whole trace, and the step (sweep_and_route) routes with the oracle's best
-    split -- decisions equal to Alg. 1 on sampled windows."""
-    cfg = configs.CONFIGS[name]()
-    n = cfg.n_requests
-    L = generate_host(cfg.shape, cfg.seed, 0, n)
-    d = generate_device(cfg.shape, cfg.seed, 0, n)
+    """C1 (1,000), C2 (10.3M), C3 (1e8) and C4 (1e8) at the sizes BASELINE.json
+    names, checked as completely as C5: every decision byte of the step, its
+    histogram and best records, and every candidate record (up to 30,720)."""
+    _step_against_oracle(configs.CONFIGS[name]())
+
+
+def _big_grid_cfg(tie_mu=False):
+    """configs.k3_factored: a grid above the cluster shape's reach (per model >
+    8 x 256 x 4), i.e. the factored K3 shape. With tie_mu every window gets the
+    same mu, so many candidates tie on cost and the lowest index must win."""
+    cfg = configs.k3_factored()
+    if tie_mu:
+        from dataclasses import replace
+        vals = {(m.name, g.name, int(w)): 5.0 for m in cfg.models for g in cfg.gpus for w in cfg.windows()}
+        cfg = replace(cfg, mu_mode="table", mu_values=vals)
+    return cfg
+
+
+@pytest.mark.parametrize("tie_mu", [False, True])
+def test_factored_k3_matches_oracle(tie_mu, monkeypatch):
+    """The factored K3 shape (per-tile instance tables, argmin only) against the
+    oracle's argmin and against the grid-stride shape's records; the route
+    split it picks drives the step's decisions."""
+    cfg = _big_grid_cfg(tie_mu=tie_mu)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    d = _dev(L)
     plan = _plan(cfg)
-    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    assert fp.fleet_plan_info(plan)["k3_shape"] == 1                  # factored
+    fp.sweep_thresholds(plan, d, cfg.rate_rps)
+    best = fp.best_split(plan)
     allc, obest = oracle.sweep(cfg, L)
-    _compare_records(res, allc, f"{name} full")
+    _compare_records(best, obest.view(fp.FP_CANDIDATE), "factored best")
+    dec = torch.zeros(L.size, dtype=torch.uint8, device="cuda")
+    b2, _ = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=1, decision=dec)
+    assert b2.tobytes() == obest.tobytes()
+    _all_decisions_equal(dec, L, obest[1], "factored step")
+    # records through the grid-stride shape of the same plan
+    res = fp.sweep_thresholds(plan, d, cfg.rate_rps, want_results=True)
+    _compare_records(res, allc.view(fp.FP_CANDIDATE), "factored plan records")
+    if tie_mu:
+        feas = allc[(allc["model"] == 0) & ((allc["flags"] & 2) != 0)]
+        assert (feas["cost_dual"] == feas["cost_dual"].min()).sum() > 1      # real ties exercised
+
+
+@pytest.mark.parametrize("shape", ["grid", "factored", "cluster"])
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_forced_k3_shapes_agree(shape, name, monkeypatch):
+    """Every K3 shape (FP_K3_SHAPE forces one at plan creation) gives the
+    oracle's best records on the paper-size grids."""
+    monkeypatch.setenv("FP_K3_SHAPE", shape)
+    cfg = configs.CONFIGS[name]().with_n(300_007)
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    fp.sweep_thresholds(plan, _dev(L), cfg.rate_rps)
+    _, obest = oracle.sweep(cfg, L, want_all=False)
     assert fp.best_split(plan).tobytes() == obest.tobytes()
-    dec = torch.empty(n, dtype=torch.uint8, device="cuda")
-    best, _ = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec)
-    assert best.tobytes() == obest.tobytes()
-    b = obest[0]
-    win = min(n, 1 << 22)
-    for first in (0, n // 2, n - win):
-        odec, _ = oracle.route_batch(L[first:first + win], int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
-        assert np.array_equal(dec[first:first + win].cpu().numpy(), odec), f"{name} decisions @{first}"

@@ -72,9 +72,10 @@ def _worker(rank, world, port, name, n_total, q):
 
 
 @pytest.mark.parametrize("name,n,world", [("C5", 100_003, 2), ("C3", 50_001, 2), ("C4", 64, 2), ("C5", 100_003, 4),
-                                          ("C4", 7, 4)])
+                                          ("C4", 7, 4), ("C5", 100_003, 8), ("C1", 1000, 8)])
 def test_two_rank_protocol_equals_single_process(name, n, world):
-    """World 2 and 4 (shard invariance; C4 with 7 requests leaves ranks empty)."""
+    """World 2, 4 and 8 -- the 8-GPU box of SURVEY §8(e) -- (shard invariance;
+    C4 with 7 requests leaves ranks empty)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
