@@ -142,6 +142,7 @@ struct EvalArgs {
   uint32_t nbins;                       // |E| + 1
   const uint32_t *b, *cs, *cl;          // grid values
   const uint16_t *b_edge, *cl_edge;     // index in E of each B / C_L
+  const uint16_t *cs_edge = nullptr;    // index in E of each C_S
   const uint16_t *b_win, *cs_win, *cl_win;  // index in windows of each B / C_S / C_L
   uint32_t n_b, n_cs, n_cl, n_cs_eff;
   // exact 32-bit division by n_b, n_cs_eff, n_cl, n_gpus: q = umul64hi(x, mul) (mul = ceil(2^64 / d), 0 for d = 1)
@@ -157,6 +158,7 @@ struct EvalArgs {
   const double *rmu = nullptr;          // [m][g][w] RN(1/mu) (0 outside mdiv's range), once per plan
   unsigned int *err_word = nullptr;     // device error word (P2P wait timed out: 1 | peer << 8)
   unsigned long long p2p_timeout_ns = 10000000000ull;
+  unsigned long long *phase_ts = nullptr;  // diagnostic (env FP_K3_PHASES): %globaltimer at K3's phases
   double rate, hours;
   uint64_t per_model;                   // candidates per model
   uint64_t cand_first, cand_count;      // this rank's slice
@@ -168,6 +170,7 @@ struct EvalArgs {
   // by one block for the next sweep (its last reader, the previous sweep's K3
   // or fold kernel, completed before this sweep's plain-launched trace pass)
   unsigned long long *zero_copies = nullptr;
+  size_t zero_elems = 0;                // u64 elements of zero_copies (every copy, whatever hist_copies says)
   // sweep_and_route (one rank's grid is the whole grid): the last block of
   // model route_model also writes {iB, iCS, iCL, ok} of its best split
   const uint32_t *edges = nullptr;
@@ -266,6 +269,23 @@ struct CalibArgs {
   unsigned long long *snap_block;   // [n_cats] (~0: no snapshot)
   bool vec_bt, vec_c;               // 16-B aligned columns: vector loads
 };
+// one-rank single-pass replay (k_calib.cu c_single): tiles of 4,096 records
+// in ticket order, decoupled look-back over tiles
+struct CalibTileArgs {
+  const uint32_t *bytes, *tokens;
+  const uint8_t *cat;
+  uint64_t n, n_tiles;
+  uint32_t n_cats;                  // <= 16
+  double beta;
+  const double *c0, *s0;            // device [n_cats] initial state
+  unsigned int *ticket;             // [1] tile ticket (zeroed before the launch)
+  unsigned int *cflag, *sflag;      // [n_tiles] look-back flags (zeroed before the launch)
+  void *cdesc, *sdesc;              // [n_tiles][2][NC] published affine maps (k_calib.cu Aff, 24 B)
+  uint64_t snap_at;
+  double *out;                      // [80]: c_hat[16], sigma[16], n_obs[16] (u64), snap_c[16], snap_s[16]
+};
+uint64_t calib_tiles(uint64_t n);
+cudaError_t launch_calib_tile(const CalibTileArgs &a, int sm_count, cudaStream_t s);
 size_t calib_scratch_bytes(uint64_t blocks, uint32_t n_cats);
 int calib_blocks_per_sm(uint32_t n_cats);
 cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s);        // C1 C2 C3 C2 C4 (one rank)

@@ -30,6 +30,7 @@
 // prompt_tokens = 0, which the update skips.
 // The composition reassociates the fp64 sums, so results agree with the
 // sequential oracle to rounding (tests: <= 1e-12 relative), not bit for bit.
+#include <algorithm>
 #include <cmath>
 #include "internal.cuh"
 
@@ -488,6 +489,371 @@ __global__ void c4_snap(CalibArgs a) {
   const double s_start = __fma_rn(a.sblkA[k * a.blocks + j], a.s0[k], a.sblkB[k * a.blocks + j]);
   a.snap_s[k] = __fma_rn(a.snap_sa[k], s_start, a.snap_sb[k]);
 }
+
+
+// ============================================================================
+// One rank, single pass: every record is read from HBM once.
+//
+// The stream is cut into tiles of 4,096 records taken in order by a ticket.
+// A block stages its tile in shared memory as c_obs (fp64; dropped feedback
+// has no category) and lists, per category, the positions of its
+// observations in tile order (ballot masks, popcount ranks): a category's
+// observations are then read through that list without per-record category
+// dispatch. The block's 256 threads form per-category worker groups in
+// proportion to the category counts (balanced for any mix); worker j of
+// category k owns the j-th slice of k's list.
+//   pass A  each worker composes the c_hat maps (Eq. `ema`) of its slice; a
+//           scan inside each group gives every worker its exclusive map and
+//           the tile's per-category aggregate
+//   look-back (decoupled single-pass scan over tiles; block-wide: 256
+//           predecessors per round) -> the tile's exact exclusive prefix
+//   pass B  each worker replays its slice from its exact start state (tile
+//           prefix, then group prefix, applied to c_0) -- the sequential
+//           update -- which yields c_hat(before) for every observation and so
+//           the sigma maps (R26); the snapshot at the snap_at-th observation;
+//           group scan and a second look-back for sigma
+// The last tile writes the final state. Reassociation: within 1e-12 of the
+// sequential oracle, like the multi-rank kernels above.
+// ============================================================================
+constexpr uint32_t kTileRecs = 4096;
+constexpr uint32_t kTileWords = kTileRecs / 32;
+constexpr uint32_t kTileThreads = 256;
+constexpr uint32_t kTileWarps = kTileThreads / 32;
+
+template <int NC>
+struct TileLayout {
+  static constexpr size_t o = 0;                                          // double [4096]
+  static constexpr size_t mask = o + kTileRecs * 8;                       // u32 [NC][128]
+  static constexpr size_t wpre = mask + (size_t)NC * kTileWords * 4;      // u32 [NC][129]
+  static constexpr size_t pos = wpre + (size_t)NC * (kTileWords + 1) * 4; // u16 [4096]
+  static constexpr size_t cat = pos + kTileRecs * 2;                      // u8 [4096] (0xFF: dropped)
+  static constexpr size_t wmap = (cat + kTileRecs + 15) & ~size_t(15);    // Aff [256]
+  static constexpr size_t bytes = wmap + kTileThreads * sizeof(Aff);
+};
+
+__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ Aff ld_aff(const Aff *p) {
+  return Aff{__ldcg(&p->a), __ldcg(&p->b), __ldcg(&p->n)};
+}
+
+// Per-category exclusive scan of the worker maps wm[g0 .. g0 + P) of each
+// group (one warp per group); the group total -> tot[k].
+__device__ void group_scan(Aff *wm, const uint32_t *gstart, uint32_t n_cats, Aff *tot) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t k = warp; k < n_cats; k += kTileWarps) {
+    const uint32_t g0 = gstart[k], P = gstart[k + 1] - g0;
+    const uint32_t q = (P + 31) / 32, lo = min(P, lane * q), hi = min(P, lo + q);
+    Aff run = aff_id();
+    for (uint32_t i = lo; i < hi; ++i) run = compose(run, wm[g0 + i]);
+    const Aff inc = warp_inclusive(run, lane);
+    Aff cur = shfl_up(inc, 1);
+    if (lane == 0) cur = aff_id();
+    for (uint32_t i = lo; i < hi; ++i) {
+      const Aff x = wm[g0 + i];
+      wm[g0 + i] = cur;
+      cur = compose(cur, x);
+    }
+    if (lane == 31) tot[k] = inc;
+  }
+}
+
+template <int NC>
+struct TileSm {                           // static shared state of one tile
+  Aff tot[NC], excl[NC], sexcl[NC], part[NC];
+  Aff red[NC][kTileWarps];                // look-back: per-warp partial compositions
+  double snapv[NC];
+  uint32_t gstart[NC + 1], cbase[NC + 1], snap_w[NC];
+  uint32_t tile, last[2];
+};
+
+struct TileBuf {
+  double *o;
+  uint32_t *mask, *wpre;
+  uint16_t *pos;
+  uint8_t *cat;
+  Aff *wm;
+};
+
+template <int NC>
+__device__ __forceinline__ TileBuf tile_buf(unsigned char *smem) {
+  using L = TileLayout<NC>;
+  return TileBuf{reinterpret_cast<double *>(smem + L::o), reinterpret_cast<uint32_t *>(smem + L::mask),
+                 reinterpret_cast<uint32_t *>(smem + L::wpre), reinterpret_cast<uint16_t *>(smem + L::pos),
+                 reinterpret_cast<uint8_t *>(smem + L::cat), reinterpret_cast<Aff *>(smem + L::wmap)};
+}
+
+// Stage tile `tile`: c_obs and categories, masks, per-category word prefixes,
+// worker groups, per-category position lists. Returns this thread's slice
+// [r0, r1) of category kw's list (kw == n_cats: no work).
+template <int NC>
+__device__ void stage_tile(const CalibTileArgs &a, const TileBuf &X, TileSm<NC> &S, uint32_t tile, uint32_t &kw,
+                           uint32_t &r0, uint32_t &r1) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t nc = a.n_cats, last_cat = nc - 1;
+  const uint64_t base = (uint64_t)tile * kTileRecs;
+  // warp w stages words 16 w .. 16 w + 15 (coalesced 128-B column loads per word)
+#pragma unroll 1
+  for (uint32_t i0 = 0; i0 < 16; i0 += 4) {
+    uint32_t vb[4], vt[4], vc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint64_t i = base + (uint64_t)(warp * 16 + i0 + u) * 32 + lane;
+      const bool in = i < a.n;
+      vb[u] = in ? __ldcs(a.bytes + i) : 0u;
+      vt[u] = in ? __ldcs(a.tokens + i) : 0u;
+      vc[u] = in ? (uint32_t)__ldcs(a.cat + i) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t word = warp * 16 + i0 + u, r = word * 32 + lane;
+      const bool valid = vt[u] != 0u;                           // zero-token feedback is dropped
+      const uint32_t k = vc[u] < last_cat ? vc[u] : last_cat;   // R23
+      X.o[r] = ratio(vb[u], vt[u] | (vt[u] == 0u));
+      X.cat[r] = valid ? (uint8_t)k : (uint8_t)0xFF;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        if (j < (int)nc) {
+          const unsigned mk = __ballot_sync(0xffffffffu, valid && k == (uint32_t)j);
+          if (lane == (uint32_t)j) X.mask[j * kTileWords + word] = mk;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // per category: exclusive prefix of the observation counts over words
+  for (uint32_t k = warp; k < nc; k += kTileWarps) {
+    const uint32_t *mk = X.mask + k * kTileWords;
+    uint32_t c[4], run = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { c[u] = __popc(mk[lane * 4 + u]); run += c[u]; }
+    uint32_t inc = run;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= (uint32_t)off) inc += y;
+    }
+    uint32_t ex = inc - run;
+    uint32_t *wp = X.wpre + k * (kTileWords + 1);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) { wp[lane * 4 + u] = ex; ex += c[u]; }
+    if (lane == 31) wp[kTileWords] = inc;
+  }
+  __syncthreads();
+  // list offsets and worker groups in proportion to the category counts
+  if (threadIdx.x == 0) {
+    uint32_t total = 0, nonempty = 0, big = 0, bigc = 0;
+    for (uint32_t k = 0; k < nc; ++k) {
+      const uint32_t ck = X.wpre[k * (kTileWords + 1) + kTileWords];
+      S.cbase[k] = total;
+      total += ck;
+      nonempty += ck ? 1u : 0u;
+      if (ck > bigc) { big = k; bigc = ck; }
+    }
+    S.cbase[nc] = total;
+    uint32_t used = 0;
+    for (uint32_t k = 0; k < nc; ++k) {
+      const uint32_t ck = X.wpre[k * (kTileWords + 1) + kTileWords];
+      used += ck ? 1u + (uint32_t)((uint64_t)ck * (kTileThreads - nonempty) / total) : 0u;
+    }
+    const uint32_t extra = total ? kTileThreads - used : 0u;
+    uint32_t g0 = 0;
+    for (uint32_t k = 0; k < nc; ++k) {
+      const uint32_t ck = X.wpre[k * (kTileWords + 1) + kTileWords];
+      S.gstart[k] = g0;
+      g0 += (ck ? 1u + (uint32_t)((uint64_t)ck * (kTileThreads - nonempty) / total) : 0u) + (k == big ? extra : 0u);
+    }
+    S.gstart[nc] = g0;
+  }
+  __syncthreads();
+  // position lists: record r of category k -> pos[cbase[k] + rank of r in k]
+#pragma unroll 4
+  for (uint32_t i = 0; i < 16; ++i) {
+    const uint32_t word = warp * 16 + i, r = word * 32 + lane;
+    const uint32_t k = X.cat[r];
+    if (k != 0xFFu) {
+      const uint32_t below = X.mask[k * kTileWords + word] & ((1u << lane) - 1u);
+      X.pos[S.cbase[k] + X.wpre[k * (kTileWords + 1) + word] + __popc(below)] = (uint16_t)r;
+    }
+  }
+  kw = 0;
+  while (kw < nc && S.gstart[kw + 1] <= threadIdx.x) ++kw;
+  r0 = r1 = 0;
+  if (kw < nc) {
+    const uint32_t P = S.gstart[kw + 1] - S.gstart[kw], j = threadIdx.x - S.gstart[kw];
+    const uint32_t ck = S.cbase[kw + 1] - S.cbase[kw];
+    r0 = S.cbase[kw] + ck * j / P;
+    r1 = S.cbase[kw] + ck * (j + 1) / P;
+  }
+  __syncthreads();
+}
+
+// Decoupled look-back over the whole block (one predecessor per thread, 256
+// per round): publish this tile's aggregates (flag 1), compose the
+// predecessors' aggregates / inclusive prefixes into the exclusive prefix
+// excl[k], publish the inclusive prefix (flag 2). A round covers 256 tiles,
+// so the walk back to the nearest inclusive prefix stays about one round deep
+// at the stream's tile rate. Flags are polled relaxed (no L1 invalidation per
+// poll); one fence after they are seen orders the map reads.
+// desc: [tile][2 (aggregate, inclusive)][NC] maps.
+template <int NC>
+__device__ void look_back_block(uint32_t tile, uint32_t n_cats, unsigned int *flags, Aff *desc, const Aff *agg,
+                                Aff *excl, TileSm<NC> &S) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Aff *mine = desc + (size_t)tile * 2 * NC;
+  if (threadIdx.x < n_cats) {
+    mine[threadIdx.x] = agg[threadIdx.x];
+    if (tile == 0) mine[NC + threadIdx.x] = agg[threadIdx.x];
+    excl[threadIdx.x] = aff_id();
+  }
+  if (threadIdx.x == 0) { S.last[0] = 0xffffffffu; S.last[1] = 0u; }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(flags + tile, tile == 0 ? 2u : 1u);
+  if (tile == 0) return;
+  int64_t top = (int64_t)tile - 1;
+  for (;;) {
+    const int64_t p = top - (int64_t)threadIdx.x;
+    unsigned int f = 0;
+    if (p >= 0) {
+      for (;;) {
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flags + p) : "memory");
+        if (f) break;
+        __nanosleep(20);
+      }
+    }
+    __threadfence();                     // acquire: the maps published before the flag
+    // the nearest predecessor with an inclusive prefix (lowest thread), else the oldest valid one
+    const unsigned inc_w = __ballot_sync(0xffffffffu, p >= 0 && f == 2u);
+    const unsigned val_w = __ballot_sync(0xffffffffu, p >= 0);
+    if (lane == 0 && inc_w) atomicMin(&S.last[0], warp * 32 + (uint32_t)__ffs(inc_w) - 1);
+    if (lane == 0 && val_w) atomicMax(&S.last[1], warp * 32 + 31 - (uint32_t)__clz(val_w));
+    __syncthreads();
+    const bool found = S.last[0] != 0xffffffffu;
+    const uint32_t last = found ? S.last[0] : S.last[1];
+    // every category at once: warp-ordered reductions, then one thread per category
+    for (uint32_t k = 0; k < n_cats; ++k) {
+      Aff x = aff_id();
+      if (threadIdx.x <= last)
+        x = ld_aff(desc + ((size_t)p * 2 + ((threadIdx.x == last && f == 2u) ? 1 : 0)) * NC + k);
+      // older predecessors (higher threads) are applied first
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const Aff y = Aff{__shfl_down_sync(0xffffffffu, x.a, o), __shfl_down_sync(0xffffffffu, x.b, o),
+                          __shfl_down_sync(0xffffffffu, x.n, o)};
+        if ((lane & (2 * o - 1)) == 0) x = compose(y, x);
+      }
+      if (lane == 0) S.red[k][warp] = x;
+    }
+    __syncthreads();
+    if (threadIdx.x < n_cats) {
+      const uint32_t k = threadIdx.x;
+      Aff acc = S.red[k][kTileWarps - 1];
+      for (int w = (int)kTileWarps - 2; w >= 0; --w) acc = compose(acc, S.red[k][w]);
+      excl[k] = compose(acc, excl[k]);
+    }
+    if (found) break;
+    __syncthreads();
+    if (threadIdx.x == 0) { S.last[0] = 0xffffffffu; S.last[1] = 0u; }
+    __syncthreads();
+    top -= (int64_t)kTileThreads;
+  }
+  __syncwarp();
+  if (threadIdx.x < n_cats) mine[NC + threadIdx.x] = compose(excl[threadIdx.x], agg[threadIdx.x]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(flags + tile, 2u);
+}
+
+template <int NC>
+__global__ void __launch_bounds__(kTileThreads, NC <= 4 ? 4 : 3) c_single(CalibTileArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ TileSm<NC> S;
+  const TileBuf X = tile_buf<NC>(smem);
+  const uint32_t nc = a.n_cats;
+  if (threadIdx.x == 0) S.tile = atomicAdd(a.ticket, 1u);
+  if (threadIdx.x < NC) S.snap_w[threadIdx.x] = 0xffffffffu;
+  __syncthreads();
+  const uint32_t tile = S.tile;
+  Aff *cdesc = static_cast<Aff *>(a.cdesc), *sdesc = static_cast<Aff *>(a.sdesc);
+  const double beta = a.beta, wgt = __dsub_rn(1.0, a.beta);
+  uint32_t kw, r0, r1;
+  stage_tile<NC>(a, X, S, tile, kw, r0, r1);
+  // ---- pass A: c_hat maps ----
+  {
+    double b = 0.0;
+    for (uint32_t r = r0; r < r1; ++r) b = __fma_rn(beta, b, __dmul_rn(wgt, X.o[X.pos[r]]));
+    X.wm[threadIdx.x] = Aff{pow_n(beta, r1 - r0), b, (unsigned long long)(r1 - r0)};
+  }
+  __syncthreads();
+  group_scan(X.wm, S.gstart, nc, S.tot);
+  __syncthreads();
+  look_back_block<NC>(tile, nc, a.cflag, cdesc, S.tot, S.excl, S);
+  __syncthreads();
+  // ---- pass B: replay from the exact start state; sigma maps; snapshot ----
+  double sb = 0.0;
+  if (r1 > r0) {
+    const Aff p0 = compose(S.excl[kw], X.wm[threadIdx.x]);
+    double cv = apply(p0, a.c0[kw]);
+    const unsigned long long before = p0.n;
+    const uint64_t target = (a.snap_at > before && a.snap_at - before <= r1 - r0) ? a.snap_at - before : 0ull;
+    for (uint32_t r = r0; r < r1; ++r) {
+      const double x = X.o[X.pos[r]];
+      const double prev = cv;
+      cv = __fma_rn(beta, prev, __dmul_rn(wgt, x));
+      sb = __fma_rn(beta, sb, __dmul_rn(wgt, fabs(__dsub_rn(x, prev))));
+      if (r - r0 + 1 == target) {
+        S.snapv[kw] = cv;
+        S.part[kw] = Aff{pow_n(beta, (uint32_t)target), sb, 0ull};
+        S.snap_w[kw] = threadIdx.x;
+      }
+    }
+  }
+  __syncthreads();                                   // every worker has read its c map
+  X.wm[threadIdx.x] = Aff{pow_n(beta, r1 - r0), sb, 0ull};
+  __syncthreads();
+  group_scan(X.wm, S.gstart, nc, S.tot);
+  __syncthreads();
+  look_back_block<NC>(tile, nc, a.sflag, sdesc, S.tot, S.sexcl, S);
+  __syncthreads();
+  if (threadIdx.x < nc) {
+    const uint32_t k = threadIdx.x;
+    if (S.snap_w[k] != 0xffffffffu) {                // the snap_at-th observation of category k is here
+      const Aff m = compose(S.sexcl[k], compose(X.wm[S.snap_w[k]], S.part[k]));
+      a.out[48 + k] = S.snapv[k];
+      a.out[64 + k] = apply(m, a.s0[k]);
+    }
+    if (tile == a.n_tiles - 1) {                     // the last tile: the final state
+      const Aff ci = ld_aff(cdesc + ((size_t)tile * 2 + 1) * NC + k);
+      const Aff si = compose(S.sexcl[k], S.tot[k]);
+      a.out[k] = apply(ci, a.c0[k]);
+      a.out[16 + k] = apply(si, a.s0[k]);
+      reinterpret_cast<unsigned long long *>(a.out)[32 + k] = ci.n;
+    }
+  }
+}
+
+template <int NC>
+cudaError_t launch_single(const CalibTileArgs &a, cudaStream_t s) {
+  const size_t smem = TileLayout<NC>::bytes;
+  cudaError_t e = cudaFuncSetAttribute(c_single<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  c_single<NC><<<(unsigned)a.n_tiles, kTileThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+uint64_t calib_tiles(uint64_t n) { return (n + kTileRecs - 1) / kTileRecs; }
+
+cudaError_t launch_calib_tile(const CalibTileArgs &a, int, cudaStream_t s) {
+  return a.n_cats <= 4 ? launch_single<4>(a, s) : launch_single<16>(a, s);
+}
+
+
+
+namespace {
 
 size_t calib_smem(uint32_t nc, bool reg) {
   return 2 * kStageBytes + kScanBytes + (size_t)nc * kCalBlock * 8 + (reg ? 0 : (size_t)nc * kCalBlock * (8 + 4 * 2));

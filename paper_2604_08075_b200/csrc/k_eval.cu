@@ -30,6 +30,7 @@
 //    one candidate per thread, grid-stride, arrival protocol.
 #include <cfloat>
 #include <cmath>
+#include <type_traits>
 #include "internal.cuh"
 
 namespace fp {
@@ -38,6 +39,7 @@ namespace {
 
 constexpr double kInf = __builtin_huge_val();
 constexpr unsigned long long kNoPool = 1ull << 62;   // factored tables: infeasible / invalid pool
+constexpr unsigned long long kNoGpu = 1ull << 63;    // factored GPU-count tables: infeasible / invalid
 
 // ---- shared-memory tables of one model ---------------------------------------
 struct Tab {
@@ -47,12 +49,12 @@ struct Tab {
   unsigned long long *gpi;                // [G] GPUs per instance
   double *price;                          // [G]
   uint32_t *b, *cs, *cl;                  // grid values
-  uint16_t *b_edge, *cl_edge, *b_win, *cs_win, *cl_win;
+  uint16_t *b_edge, *cl_edge, *b_win, *cs_win, *cl_win, *cs_edge;
   double rN;                              // RN(1/N) or 0
 };
 
 struct TabLayout {
-  size_t cnt, mass, nseq, mu, rmu, gpi, price, b, cs, cl, be, ce, bw, sw, lw, bytes;
+  size_t cnt, mass, nseq, mu, rmu, gpi, price, b, cs, cl, be, ce, bw, sw, lw, se, bytes;
 };
 
 __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -76,6 +78,7 @@ __host__ __device__ inline TabLayout tab_layout(const EvalArgs &a, bool hist) {
   L.bw = o; o += al16((size_t)a.n_b * 2);
   L.sw = o; o += al16((size_t)a.n_cs * 2);
   L.lw = o; o += al16((size_t)a.n_cl * 2);
+  L.se = o; o += al16((size_t)a.n_cs * 2);
   L.bytes = o;
   return L;
 }
@@ -98,6 +101,7 @@ __device__ Tab tab_bind(const EvalArgs &a, unsigned char *smem, bool hist) {
   T.b_win = reinterpret_cast<uint16_t *>(smem + L.bw);
   T.cs_win = reinterpret_cast<uint16_t *>(smem + L.sw);
   T.cl_win = reinterpret_cast<uint16_t *>(smem + L.lw);
+  T.cs_edge = reinterpret_cast<uint16_t *>(smem + L.se);
   T.rN = 0.0;
   return T;
 }
@@ -123,6 +127,7 @@ __device__ void load_plan_tables(const EvalArgs &a, const Tab &T, uint32_t m) {
   for (uint32_t j = threadIdx.x; j < a.n_cs; j += blockDim.x) {
     T.cs[j] = a.cs[j];
     T.cs_win[j] = a.cs_win[j];
+    T.cs_edge[j] = a.cs_edge[j];
   }
   for (uint32_t j = threadIdx.x; j < a.n_cl; j += blockDim.x) {
     T.cl[j] = a.cl[j];
@@ -341,20 +346,26 @@ __device__ __forceinline__ void better(double &c0, uint32_t &i0, uint32_t &v0, d
   if (take) { c0 = c1; i0 = i1; v0 = v1; }
 }
 
-__device__ __forceinline__ void warp_argmin(double &c, uint32_t &i, uint32_t &v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double c1 = __shfl_down_sync(0xffffffffu, c, o);
-    uint32_t i1 = __shfl_down_sync(0xffffffffu, i, o);
-    uint32_t v1 = __shfl_down_sync(0xffffffffu, v, o);
-    better(c, i, v, c1, i1, v1);
-  }
+// (cost, index) argmin of a warp by three 32-bit min reductions (REDUX):
+// costs are >= +0 (GPUs x price x hours, price >= 0, hours > 0) or +inf, and
+// the IEEE bit patterns of non-negative doubles order like their values, so
+// (cost bits, index) compares lexicographically as (hi word, lo word, index).
+// Non-candidates (v = 0) carry the all-ones key. Every lane gets the result.
+__device__ __forceinline__ void warp_argmin_key(double &c, uint32_t &i, uint32_t &v) {
+  const unsigned long long bits = v ? (unsigned long long)__double_as_longlong(c) : ~0ull;
+  const uint32_t hi = (uint32_t)(bits >> 32), lo = (uint32_t)bits, ix = v ? i : 0xffffffffu;
+  const uint32_t mh = __reduce_min_sync(0xffffffffu, hi);
+  const uint32_t ml = __reduce_min_sync(0xffffffffu, hi == mh ? lo : 0xffffffffu);
+  const uint32_t mi = __reduce_min_sync(0xffffffffu, (hi == mh && lo == ml) ? ix : 0xffffffffu);
+  v = __reduce_or_sync(0xffffffffu, (v && hi == mh && lo == ml && ix == mi) ? 1u : 0u);
+  c = __longlong_as_double((long long)(((unsigned long long)mh << 32) | ml));
+  i = mi;
 }
 
-// block-wide (cost, index) argmin; the result is valid in thread 0
+// block-wide (cost, index) argmin; the result is valid in warp 0 (every lane)
 __device__ void block_argmin(double &bc, uint32_t &bi, uint32_t &bv, double *red_c, uint32_t *red_i,
                              uint32_t *red_v) {
-  warp_argmin(bc, bi, bv);
+  warp_argmin_key(bc, bi, bv);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
   if (lane == 0) { red_c[w] = bc; red_i[w] = bi; red_v[w] = bv; }
   __syncthreads();
@@ -362,7 +373,7 @@ __device__ void block_argmin(double &bc, uint32_t &bi, uint32_t &bv, double *red
     bc = lane < nw ? red_c[lane] : 0.0;
     bi = lane < nw ? red_i[lane] : 0xffffffffu;
     bv = lane < nw ? red_v[lane] : 0u;
-    warp_argmin(bc, bi, bv);
+    warp_argmin_key(bc, bi, bv);
   }
 }
 
@@ -404,19 +415,26 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+// diagnostic phase stamps of block (0, 0), thread 0 (EvalArgs::phase_ts, env FP_K3_PHASES)
+__device__ __forceinline__ void phase(const EvalArgs &a, int i) {
+  if (a.phase_ts && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) a.phase_ts[i] = globaltimer();
+}
+
 // Prologue shared by every K3 shape: the plan tables (before the PDL wait),
 // the histogram of this sweep, its scan and RN(1/N). `first` marks the one
 // block that publishes the summed histogram and clears the other parity's
 // accumulator copies (last read by the previous sweep, which completed
 // before this sweep's trace pass started: the trace pass is a plain launch).
 __device__ void prologue(const EvalArgs &a, Tab &T, uint32_t m, bool first, unsigned long long *warp_tot) {
+  phase(a, 0);
   load_plan_tables(a, T, m);
   if (first && a.zero_copies) {
-    const size_t total = (size_t)a.hist_copies * 2 * a.nbins;
-    for (size_t i = threadIdx.x; i < total; i += blockDim.x) a.zero_copies[i] = 0ull;
+    for (size_t i = threadIdx.x; i < a.zero_elems; i += blockDim.x) a.zero_copies[i] = 0ull;
   }
+  phase(a, 1);
   // the trace pass's histogram is complete and visible after this (no-op without PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  phase(a, 2);
   if (a.p2p_world) {
     // peer-memory exchange (FP_FLAG_P2P): wait until every rank has published
     // this step's folded histogram (its K1 done, fenced system-wide), then
@@ -481,43 +499,73 @@ __device__ void prologue(const EvalArgs &a, Tab &T, uint32_t m, bool first, unsi
     }
   }
   __syncthreads();
-  block_scan_inclusive(T.cnt_le, a.nbins, warp_tot);
-  block_scan_inclusive(T.mass_le, a.nbins, warp_tot);
-  __syncthreads();
-  // every thread forms RN(1/N) itself (one DDIV; no extra barrier)
-  T.rN = mrcp(u2d(T.cnt_le[a.nbins - 1]));
-}
-
-// The winner's record (evaluated in full by one thread) and, in
-// sweep_and_route, the split's edge indices #{e in E : e < v} for B, C_S, C_L.
-__device__ void emit_winner(const EvalArgs &a, const Tab &T, uint32_t m, double bc, uint32_t bi, uint32_t bv,
-                            uint32_t *route_v) {
-  // thread 0 only
-  fp_candidate c;
-  if (bv) {
-    evaluate<true>(a, T, m, bi, c);
+  phase(a, 3);
+  if (a.nbins <= 256) {
+    // one warp scans both arrays (<= 8 contiguous bins per lane): no block barriers
+    if (threadIdx.x < 32) {
+      const uint32_t lane = threadIdx.x, per = (a.nbins + 31) / 32;
+      const uint32_t lo = min(a.nbins, lane * per), hi = min(a.nbins, lo + per);
+      unsigned long long rc = 0, rm = 0;
+      for (uint32_t j = lo; j < hi; ++j) { rc += T.cnt_le[j]; rm += T.mass_le[j]; }
+      unsigned long long xc = rc, xm = rm;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long yc = __shfl_up_sync(0xffffffffu, xc, o);
+        const unsigned long long ym = __shfl_up_sync(0xffffffffu, xm, o);
+        if (lane >= (uint32_t)o) { xc += yc; xm += ym; }
+      }
+      unsigned long long oc = xc - rc, om = xm - rm;
+      for (uint32_t j = lo; j < hi; ++j) {
+        oc += T.cnt_le[j]; T.cnt_le[j] = oc;
+        om += T.mass_le[j]; T.mass_le[j] = om;
+      }
+      // N = the last lane's inclusive count; RN(1/N) formed once, shared below
+      const unsigned long long N = __shfl_sync(0xffffffffu, xc, 31);
+      if (lane == 0) warp_tot[0] = (unsigned long long)__double_as_longlong(mrcp(u2d(N)));
+    }
   } else {
-    memset(&c, 0, sizeof c);
-    c.index = 0xffffffffu;
-    c.model = m;
-    c.cost_dual = c.cost_homo = kInf;
+    block_scan_inclusive(T.cnt_le, a.nbins, warp_tot);
+    __syncthreads();
+    block_scan_inclusive(T.mass_le, a.nbins, warp_tot);
+    __syncthreads();
+    if (threadIdx.x == 0) warp_tot[0] = (unsigned long long)__double_as_longlong(mrcp(u2d(T.cnt_le[a.nbins - 1])));
   }
-  a.best_out[m] = c;
-  route_v[0] = c.b_short; route_v[1] = c.c_short; route_v[2] = c.c_long;
-  route_v[3] = (c.flags & FP_CAND_FEASIBLE) ? 1u : 0u;
+  __syncthreads();
+  T.rN = __longlong_as_double((long long)warp_tot[0]);
+  __syncthreads();                       // warp_tot is reused by the caller
+  phase(a, 4);
 }
 
-__device__ void emit_route(const EvalArgs &a, const uint32_t *route_v) {
-  // warp 0; E is read from global memory (L2), only in the routing model's block
-  const int lane = threadIdx.x & 31;
-  uint32_t nb = 0, ns = 0, nl = 0;
-  for (uint32_t base = 0; base < a.n_edges; base += 32) {
-    const uint32_t e = base + lane < a.n_edges ? a.edges[base + lane] : 0xffffffffu;
-    nb += __popc(__ballot_sync(0xffffffffu, e < route_v[0]));
-    ns += __popc(__ballot_sync(0xffffffffu, e < route_v[1]));
-    nl += __popc(__ballot_sync(0xffffffffu, e < route_v[2]));
+// The empty record of a model without a feasible candidate.
+__device__ void no_winner(fp_candidate &c, uint32_t m) {
+  memset(&c, 0, sizeof c);
+  c.index = 0xffffffffu;
+  c.model = m;
+  c.cost_dual = c.cost_homo = kInf;
+}
+
+// sweep_and_route: the routed split's edge indices #{e in E : e < v} for its
+// B, C_S, C_L -- the positions of those values in E (they are edges), read
+// from the plan's index tables -- and whether it is feasible.
+__device__ void emit_route(const EvalArgs &a, const Tab &T, uint32_t bi, uint32_t bv) {
+  uint4 v = make_uint4(0u, 0u, 0u, 0u);
+  if (bv) {
+    uint32_t r = bi, k, s, l;
+    r = divmod(r, a.n_b, a.div_b, k);
+    r = divmod(r, a.n_cs_eff, a.div_cs, s);
+    divmod(r, a.n_cl, a.div_cl, l);
+    v = make_uint4(T.b_edge[k], a.n_cs ? T.cs_edge[s] : T.b_edge[k], T.cl_edge[l], 1u);
   }
-  if (lane == 0) *reinterpret_cast<uint4 *>(a.route_out) = make_uint4(nb, ns, nl, route_v[3]);
+  *reinterpret_cast<uint4 *>(a.route_out) = v;
+}
+
+// The winner's record, evaluated in full by one thread (grid-stride shapes).
+__device__ void emit_winner(const EvalArgs &a, const Tab &T, uint32_t m, uint32_t bi, uint32_t bv) {
+  fp_candidate c;
+  if (bv) evaluate<true>(a, T, m, bi, c);
+  else no_winner(c, m);
+  a.best_out[m] = c;
+  if (a.route_out && m == a.route_model) emit_route(a, T, bi, bv);
 }
 
 // ---- cluster-scope helpers (PTX) ------------------------------------------------
@@ -538,8 +586,17 @@ __device__ __forceinline__ uint32_t ld_dsmem_u32(uint32_t addr) {
   asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_dsmem_u64(uint32_t addr) {
+  unsigned long long v;
+  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+  return v;
+}
 
 // ---- latency shape: one cluster of gridDim.x blocks per model -------------------
+// Every thread evaluates its (<= 4) candidates in full and keeps its best
+// record in its shared-memory slot; the blocks' winners meet in rank 0 through
+// DSMEM after one cluster barrier, and rank 0 copies the winning record out of
+// its owner's slot (the owner follows from the index: no re-evaluation).
 template <bool RESULTS>
 __global__ void __launch_bounds__(256) k3_cluster(EvalArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -548,9 +605,9 @@ __global__ void __launch_bounds__(256) k3_cluster(EvalArgs a) {
   __shared__ uint32_t red_i[32], red_v[32];
   __shared__ double win_c;
   __shared__ uint32_t win_i, win_v;
-  __shared__ uint32_t route_v[4];
   const uint32_t m = blockIdx.y, rank = blockIdx.x;   // cluster (gridDim.x, 1, 1): rank = blockIdx.x
   Tab T = tab_bind(a, smem, true);
+  fp_candidate *slot = reinterpret_cast<fp_candidate *>(smem + tab_layout(a, true).bytes);
   prologue(a, T, m, rank == 0 && m == 0, warp_tot);
 
   const uint64_t m_lo = (uint64_t)m * a.per_model, m_hi = m_lo + a.per_model;
@@ -560,16 +617,22 @@ __global__ void __launch_bounds__(256) k3_cluster(EvalArgs a) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t idx = lo + (uint64_t)rank * blockDim.x + threadIdx.x; idx < hi; idx += stride) {
     fp_candidate c;
-    evaluate<RESULTS>(a, T, m, idx, c);
+    evaluate<true>(a, T, m, idx, c);
     if (RESULTS) a.results[idx - a.cand_first] = c;
     // indices increase along the loop, so strict '<' keeps the lowest index on ties
-    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || c.cost_dual < bc)) { bc = c.cost_dual; bi = c.index; bv = 1; }
+    if ((c.flags & FP_CAND_FEASIBLE) && (!bv || c.cost_dual < bc)) {
+      bc = c.cost_dual; bi = c.index; bv = 1;
+      slot[threadIdx.x] = c;
+    }
   }
+  phase(a, 5);
   block_argmin(bc, bi, bv, red_c, red_i, red_v);
   if (threadIdx.x == 0) { win_c = bc; win_i = bi; win_v = bv; }
-  // every block's winner is in its shared memory: one cluster barrier
+  phase(a, 6);
+  // every block's winner (and its record) is in its shared memory: one cluster barrier
   cluster_arrive();
   cluster_wait();
+  phase(a, 7);
   if (rank != 0) {
     // keep this block's shared memory alive until rank 0 has read it
     cluster_arrive();
@@ -580,19 +643,31 @@ __global__ void __launch_bounds__(256) k3_cluster(EvalArgs a) {
     const uint32_t lane = threadIdx.x;
     double c = 0.0;
     uint32_t i = 0xffffffffu, v = 0;
-    for (uint32_t r = lane; r < gridDim.x; r += 32) {
-      better(c, i, v, ld_dsmem_f64(dsmem_addr(&win_c, r)), ld_dsmem_u32(dsmem_addr(&win_i, r)),
-             ld_dsmem_u32(dsmem_addr(&win_v, r)));
+    if (lane < gridDim.x) {
+      c = ld_dsmem_f64(dsmem_addr(&win_c, lane));
+      i = ld_dsmem_u32(dsmem_addr(&win_i, lane));
+      v = ld_dsmem_u32(dsmem_addr(&win_v, lane));
     }
-    warp_argmin(c, i, v);
-    if (lane == 0) { bc = c; bi = i; bv = v; }
+    warp_argmin_key(c, i, v);
+    phase(a, 8);
+    // the record: owner block and thread from the loop's index mapping
+    constexpr uint32_t kWords = sizeof(fp_candidate) / 8;
+    if (v) {
+      const uint64_t off = (uint64_t)i - lo;
+      const uint32_t r = (uint32_t)(off % stride), owner = r / blockDim.x, t = r % blockDim.x;
+      if (lane < kWords) {
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(&slot[t]) + lane;
+        reinterpret_cast<unsigned long long *>(a.best_out + m)[lane] = ld_dsmem_u64(dsmem_addr(src, owner));
+      }
+    } else if (lane == 0) {
+      fp_candidate e;
+      no_winner(e, m);
+      a.best_out[m] = e;
+    }
+    if (lane == 0 && a.route_out && m == a.route_model) emit_route(a, T, i, v);
   }
+  phase(a, 9);
   cluster_arrive();                     // the other blocks may exit now
-  if (threadIdx.x == 0) emit_winner(a, T, m, bc, bi, bv, route_v);
-  if (a.route_out && m == a.route_model) {
-    __syncthreads();
-    if (threadIdx.x < 32) emit_route(a, route_v);
-  }
   cluster_wait();
 }
 
@@ -636,7 +711,6 @@ __global__ void __launch_bounds__(256, 3) k3_grid(EvalArgs a) {
   __shared__ unsigned long long warp_tot[32];
   __shared__ double red_c[32];
   __shared__ uint32_t red_i[32], red_v[32];
-  __shared__ uint32_t route_v[4];
   const uint32_t m = blockIdx.y;
   Tab T = tab_bind(a, smem, true);
   prologue(a, T, m, blockIdx.x == 0 && m == 0, warp_tot);
@@ -686,11 +760,7 @@ __global__ void __launch_bounds__(256, 3) k3_grid(EvalArgs a) {
       a.best3[m] = c;
     }
   } else {
-    if (threadIdx.x == 0) emit_winner(a, T, m, bc, bi, bv, route_v);
-    if (a.route_out && m == a.route_model) {
-      __syncthreads();
-      if (threadIdx.x < 32) emit_route(a, route_v);
-    }
+    if (threadIdx.x == 0) emit_winner(a, T, m, bi, bv);
   }
 }
 
@@ -727,7 +797,6 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
   __shared__ unsigned long long warp_tot[32];
   __shared__ double red_c[32];
   __shared__ uint32_t red_i[32], red_v[32];
-  __shared__ uint32_t route_v[4];
   const uint32_t m = blockIdx.y;
   Tab T = tab_bind(a, smem, true);
   unsigned long long *Is = reinterpret_cast<unsigned long long *>(smem + tab_layout(a, true).bytes);
@@ -740,49 +809,64 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t k = kt * 32 + lane;
   const bool kin = k < a.n_b;
-  // the instance tables of this tile
+  const unsigned long long gpi = T.gpi[g];
+  // the GPU-count tables of this tile: gpi x I_short, gpi x I_long, bit 63 set
+  // when the pool is infeasible (or B > C_S). gpi x I <= 2^9 x 2^53, so a
+  // valid entry never has bit 63; gpi (I_s + I_l) = gpi I_s + gpi I_l mod 2^64
+  // as in the per-candidate evaluation
   for (uint32_t e = threadIdx.x; e < a.n_cs_eff * 32; e += blockDim.x) {
     const uint32_t kk = kt * 32 + (e & 31);
-    Is[e] = kk < a.n_b ? short_instances(a, T, g, e >> 5, kk) : kNoPool;
+    const unsigned long long v = kk < a.n_b ? short_instances(a, T, g, e >> 5, kk) : kNoPool;
+    Is[e] = v == kNoPool ? kNoGpu : gpi * v;
   }
   for (uint32_t e = threadIdx.x; e < nl * 32; e += blockDim.x) {
     const uint32_t kk = kt * 32 + (e & 31);
-    Il[e] = kk < a.n_b ? long_instances(a, T, g, l0 + (e >> 5), kk) : kNoPool;
+    const unsigned long long v = kk < a.n_b ? long_instances(a, T, g, l0 + (e >> 5), kk) : kNoPool;
+    Il[e] = v == kNoPool ? kNoGpu : gpi * v;
   }
   __syncthreads();
 
   const uint64_t m_lo = (uint64_t)m * a.per_model;
   const uint64_t lo = max(m_lo, a.cand_first), hi = min(m_lo + a.per_model, a.cand_first + a.cand_count);
-  const unsigned long long gpi = T.gpi[g];
   const double price = T.price[g], hours = a.hours;
   const uint32_t B = kin ? T.b[k] : 0xffffffffu;
-  double bc = 0.0;
-  uint32_t bi = 0xffffffffu, bv = 0;
-  // (l, s) pairs over the warps in increasing order: for a fixed lane (k) the
-  // flat index increases along the loop, so strict '<' keeps the lowest index
-  // flat index = idx0 + q n_b with q = li n_cs' + s (the pair counter)
-  const uint32_t ncs = a.n_cs_eff, npairs = nl * ncs;
+  // flat index = idx0 + q n_b, q = li n_cs' + s; for a fixed lane (k) the
+  // loops below visit q in increasing order, so strict '<' keeps the lowest index
+  const uint32_t ncs = a.n_cs_eff;
   const uint64_t idx0 = m_lo + ((uint64_t)g * a.n_cl + l0) * ncs * a.n_b + k;
-  uint32_t li = w / ncs, s = w - (w / ncs) * ncs;
-  for (uint32_t q = w; q < npairs; q += nw) {
-    const uint32_t CL = T.cl[l0 + li];
-    const uint32_t CS = a.n_cs ? T.cs[s] : B;
-    const unsigned long long S = Is[s * 32 + lane] + Il[li * 32 + lane];
-    const uint64_t idx = idx0 + (uint64_t)q * a.n_b;
-    if (kin && S < kNoPool && CS <= CL && idx >= lo && idx < hi) {
-      const double cost = __dmul_rn(__dmul_rn(u2d(gpi * S), price), hours);
-      if (!bv || cost < bc) { bc = cost; bi = (uint32_t)idx; bv = 1; }
+  const uint64_t tile_lo = idx0 - lane, tile_hi = tile_lo + ((uint64_t)nl * ncs - 1) * a.n_b + 31;
+  const bool whole = tile_lo >= lo && tile_hi < hi;      // no per-candidate slice check
+  double bc = 0.0;
+  uint32_t bq = 0, bv = 0;
+  auto scan = [&](auto check) {
+    for (uint32_t li = w; li < nl; li += nw) {
+      const unsigned long long gl = Il[li * 32 + lane];
+      if (gl >> 63) continue;
+      const uint32_t CL = T.cl[l0 + li], qb = li * ncs;
+#pragma unroll 4
+      for (uint32_t s = 0; s < ncs; ++s) {
+        const unsigned long long gs = Is[s * 32 + lane];
+        const uint32_t CS = a.n_cs ? T.cs[s] : B;
+        bool ok = !(gs >> 63) && CS <= CL;
+        if (decltype(check)::value) {
+          const uint64_t idx = idx0 + (uint64_t)(qb + s) * a.n_b;
+          ok = ok && idx >= lo && idx < hi;
+        }
+        if (ok) {
+          const double cost = __dmul_rn(__dmul_rn(u2d(gs + gl), price), hours);
+          if (!bv || cost < bc) { bc = cost; bq = qb + s; bv = 1; }
+        }
+      }
     }
-    s += nw;
-    while (s >= ncs) { s -= ncs; ++li; }
+  };
+  if (kin) {
+    if (whole) scan(std::false_type{});
+    else scan(std::true_type{});
   }
+  uint32_t bi = bv ? (uint32_t)(idx0 + (uint64_t)bq * a.n_b) : 0xffffffffu;
   block_argmin(bc, bi, bv, red_c, red_i, red_v);
   if (!arrive_last(a.block_best, a.done, m, bc, bi, bv, red_c, red_i, red_v)) return;
-  if (threadIdx.x == 0) emit_winner(a, T, m, bc, bi, bv, route_v);
-  if (a.route_out && m == a.route_model) {
-    __syncthreads();
-    if (threadIdx.x < 32) emit_route(a, route_v);
-  }
+  if (threadIdx.x == 0) emit_winner(a, T, m, bi, bv);
 }
 
 // N_seq (Eq. 2) and RN(1/mu) for every (model, GPU, window): plan data only, computed once

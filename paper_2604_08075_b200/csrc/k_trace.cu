@@ -204,6 +204,10 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
   // raw: 3 columns per request (36 B per uint4 step in flight), 2 steps per
   // thread at 3 x 512 threads/SM keep ~110 KB/SM in flight within 42 registers
   constexpr int U = RAW ? 2 : kUnroll;
+  // a programmatic dependent (K3, or the fold kernel) may be scheduled right
+  // away into the room this grid leaves on each SM: it loads the plan's tables
+  // and then waits (griddepcontrol.wait) for this grid to complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t nbins = a.n_edges + 1;
   uint32_t lut_bytes = (LUTW == 0) ? a.n_edges * 4 : a.lut_cells * LUTW;

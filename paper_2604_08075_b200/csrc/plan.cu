@@ -133,6 +133,9 @@ struct fp_plan {
   fp_candidate *d_results = nullptr;       // [cand_count] (lazy)
   BlockBest *d_block_best = nullptr;
   unsigned int *d_done = nullptr;
+  unsigned long long *h_phase = nullptr;   // diagnostic K3 phase stamps (env FP_K3_PHASES, mapped host)
+  double phase_sum[16] = {0};
+  uint64_t phase_n = 0;
   EvalLaunch k3a;                          // K3 launch, argmin only (the step's)
   EvalLaunch k3r;                          // K3 launch with every record (want_results)
   int k3_grid_x = 1;                       // blocks per model of the grid-stride shape
@@ -397,12 +400,15 @@ fp_status upload(fp_plan *p) {
   size_t off_b = put(p->b.data(), p->b.size() * 4);
   size_t off_cs = put(p->cs.data(), p->cs.size() * 4);
   size_t off_cl = put(p->cl.data(), p->cl.size() * 4);
-  std::vector<uint16_t> b_edge, cl_edge, b_win, cs_win, cl_win;
+  std::vector<uint16_t> b_edge, cs_edge, cl_edge, b_win, cs_win, cl_win;
   for (uint32_t v : p->b) {
     b_edge.push_back((uint16_t)index_of(p->edges, v));
     b_win.push_back(p->cs.empty() ? (uint16_t)index_of(p->windows, v) : 0);
   }
-  for (uint32_t v : p->cs) cs_win.push_back((uint16_t)index_of(p->windows, v));
+  for (uint32_t v : p->cs) {
+    cs_win.push_back((uint16_t)index_of(p->windows, v));
+    cs_edge.push_back((uint16_t)index_of(p->edges, v));
+  }
   for (uint32_t v : p->cl) {
     cl_edge.push_back((uint16_t)index_of(p->edges, v));
     cl_win.push_back((uint16_t)index_of(p->windows, v));
@@ -412,6 +418,7 @@ fp_status upload(fp_plan *p) {
   size_t off_ce = put(cl_edge.data(), cl_edge.size() * 2);
   size_t off_bw = put(b_win.data(), b_win.size() * 2);
   size_t off_sw = put(cs_win.data(), cs_win.size() * 2);
+  size_t off_se = put(cs_edge.data(), cs_edge.size() * 2);
   size_t off_lw = put(cl_win.data(), cl_win.size() * 2);
   std::vector<uint32_t> arch;
   for (auto &m : p->models) {
@@ -490,6 +497,7 @@ fp_status upload(fp_plan *p) {
   ea.cl_edge = reinterpret_cast<const uint16_t *>(B0 + off_ce);
   ea.b_win = reinterpret_cast<const uint16_t *>(B0 + off_bw);
   ea.cs_win = reinterpret_cast<const uint16_t *>(B0 + off_sw);
+  ea.cs_edge = reinterpret_cast<const uint16_t *>(B0 + off_se);
   ea.cl_win = reinterpret_cast<const uint16_t *>(B0 + off_lw);
   ea.n_b = (uint32_t)p->b.size();
   ea.n_cs = (uint32_t)p->cs.size();
@@ -528,6 +536,13 @@ fp_status upload(fp_plan *p) {
   ea.cap_nseq = p->d_cap;
   ea.rmu = p->d_rmu;
   ea.err_word = p->d_err;
+  if (env_int("FP_K3_PHASES", 0)) {
+    CUDA_TRY(p, cudaHostAlloc(&p->h_phase, 16 * 8, cudaHostAllocMapped), "cudaHostAlloc phases");
+    memset(p->h_phase, 0, 16 * 8);
+    unsigned long long *dptr = nullptr;
+    CUDA_TRY(p, cudaHostGetDevicePointer(&dptr, p->h_phase, 0), "phase pointer");
+    ea.phase_ts = dptr;
+  }
   ea.p2p_timeout_ns = (unsigned long long)std::max(1, env_int("FP_P2P_TIMEOUT_MS", 10000)) * 1000000ull;
 
   // K3 grid: enough blocks for the largest per-model part of this rank's slice
@@ -557,13 +572,16 @@ fp_status upload(fp_plan *p) {
   // cluster shape: the paper-size grids, one cluster per model reduced in DSMEM
   // (<= 4 candidates per thread); FP_K3_SHAPE=grid|factored|cluster forces a shape
   const char *force = getenv("FP_K3_SHAPE");
-  const int max_cl = eval_max_cluster(256, tab_smem);
+  // 128-thread blocks when <= 2 candidates per thread: they fit beside the
+  // trace pass's 3 x 512 threads on an SM, so the early-launched K3 loads its
+  // tables while K1 drains; each thread keeps its best full record in shared memory
   EvalLaunch clu;
   clu.shape = kK3Cluster;
-  clu.block = widest <= 512 ? 128 : 256;
+  clu.block = widest <= 2048 ? 128 : 256;
+  clu.smem = tab_smem + (size_t)clu.block * sizeof(fp_candidate);
+  const int max_cl = eval_max_cluster(clu.block, clu.smem);
   clu.grid_x = (int)std::min<uint64_t>(max_cl, std::max<uint64_t>(1, (widest + clu.block - 1) / clu.block));
-  clu.smem = tab_smem;
-  const bool cluster_ok = widest <= (uint64_t)clu.grid_x * clu.block * 4;
+  const bool cluster_ok = widest <= (uint64_t)clu.grid_x * clu.block * 4 && clu.smem <= 190 * 1024;
   // factored shape: large grids, argmin only
   EvalLaunch fac;
   fac.shape = kK3Factored;
@@ -627,6 +645,15 @@ fp_status configure_launch(fp_plan *p) {
 }
 
 constexpr size_t kTimerRing = 256;
+
+// The trace pass's grid for n requests: the plan's resident grid, but no more
+// blocks than there is work for (16 requests per thread per grid-stride step),
+// so a small trace does not pay 444 block prologues and flushes.
+int k1_grid_for(const fp_plan *p, uint64_t n) {
+  const uint64_t per_block = (uint64_t)p->k1_block * 16;
+  const uint64_t want = std::max<uint64_t>(1, (n + per_block - 1) / per_block);
+  return (int)std::min<uint64_t>((uint64_t)p->k1_grid, want);
+}
 
 // Fold the oldest pending event pair of `t` into its running total.
 void timer_fold_one(fp_plan::Timer &t) {
@@ -970,6 +997,14 @@ void fleet_plan_destroy(fp_plan *p) {
       if (p->ev_used[i]) cudaEventDestroy(p->ev_used[i]);
     }
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+    if (p->h_phase) {
+      if (p->phase_n) {
+        fprintf(stderr, "[fp] K3 phases over %llu sweeps (us after entry): ", (unsigned long long)p->phase_n);
+        for (int i = 1; i <= 10; ++i) fprintf(stderr, "%d:%.2f ", i, p->phase_sum[i] / p->phase_n / 1e3);
+        fprintf(stderr, "\n");
+      }
+      cudaFreeHost(p->h_phase);
+    }
     if (p->h_best) cudaFreeHost(p->h_best);
     if (p->h_small) cudaFreeHost(p->h_small);
     for (auto &t : p->timers)
@@ -1126,7 +1161,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
         TraceArgs tq = p->ta;
         tq.bins_out = reinterpret_cast<uint8_t *>(16);   // any non-null: the bin variant's grid
         tq.bins_pack = 1;
-        k1_grid_used = trace_grid(tq, p->k1_grid, p->k1_block);
+        k1_grid_used = trace_grid(tq, k1_grid_for(p, n_local), p->k1_block);
         const uint64_t S = (uint64_t)k1_grid_used * p->k1_block;
         const uint64_t n4 = (n_local - std::min<uint64_t>(n_local, head_phase)) / 4;
         chunks = std::max<uint64_t>(1, (n4 + 4 * S - 1) / (4 * S)) * S;
@@ -1355,7 +1390,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
         TraceArgs t = *raw;
         t.g_cnt = acc;
         t.g_mass = acc + p->nbins;
-        cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
+        cudaError_t e = launch_trace(t, k1_grid_for(p, n_local), p->k1_block, p->k1_smem, s);
         if (e != cudaSuccess) return cuda_fail(p, e, "trace pass (raw) launch");
         ++p->launches;
       }
@@ -1372,7 +1407,8 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
       t.bins_pack = bins_side ? 1u : 0u;
       t.bins_side = bins_side;
       LaunchTimer lt(p, FP_KERNEL_TRACE, s);
-      cudaError_t e = launch_trace(t, p->k1_grid, p->k1_block, p->k1_smem, s);
+      // packed bins: the grid the routing pass will use (bins_pack: one piece, n_local)
+      cudaError_t e = launch_trace(t, k1_grid_for(p, bins_side ? n_local : n), p->k1_block, p->k1_smem, s);
       if (e != cudaSuccess) return cuda_fail(p, e, "trace pass launch");
       ++p->launches;
       return FP_OK;
@@ -1416,6 +1452,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   ea.rate = rate_rps;
   ea.results = h_results ? p->d_results : nullptr;
   ea.zero_copies = other;
+  ea.zero_elems = p->copies_elems;
   ea.route_out = route_out;
   ea.route_model = route_model;
   cudaError_t e;
@@ -1561,6 +1598,79 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   if (bad) n = 0;
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
+  if (!p->dist && env_int("FP_CALIB_SINGLE", 0)) {
+    // one rank, FP_CALIB_SINGLE=1: the single-pass tile kernel (every record read once;
+    // k_calib.cu c_single, decoupled look-back over tiles). Correct, but slower than the
+    // two-pass kernels below on a B200 (the look-back chain over 244K tiles of 4,096
+    // records does not keep up with the stream: DESIGN.md §10)
+    const uint64_t tiles = calib_tiles(n);
+    const size_t nc = n_cats <= 4 ? 4 : 16;
+    const size_t desc = tiles * 2 * nc * 24;           // one [tile][2][NC] array of maps (24 B)
+    const size_t flag_bytes = ((2 * tiles + 4) * 4 + 255) & ~size_t(255);
+    const size_t need = 16 * 16 * 8 + flag_bytes + 2 * desc + 256;
+    if (p->calib_cap < need) {
+      cudaFree(p->d_calib_scratch);
+      p->d_calib_scratch = nullptr;
+      p->calib_cap = 0;
+      CUDA_TRY(p, cudaMalloc(&p->d_calib_scratch, need), "cudaMalloc calibration scratch");
+      p->calib_cap = need;
+    }
+    unsigned char *base = p->d_calib_scratch;
+    double *sm = reinterpret_cast<double *>(base);                       // 16 slots of 16 doubles
+    unsigned int *flags = reinterpret_cast<unsigned int *>(base + 16 * 16 * 8);   // [2][tiles] + ticket
+    unsigned char *descs = base + 16 * 16 * 8 + flag_bytes;
+    CalibTileArgs a{};
+    a.bytes = d_body_bytes;
+    a.tokens = d_prompt_tokens;
+    a.cat = d_category;
+    a.n = n;
+    a.n_tiles = tiles;
+    a.n_cats = n_cats;
+    a.beta = beta;
+    double *c0 = sm + 16 * 8, *s0 = sm + 16 * 9;
+    a.c0 = c0;
+    a.s0 = s0;
+    a.cflag = flags;
+    a.sflag = flags + tiles;
+    a.ticket = flags + 2 * tiles;
+    a.cdesc = descs;
+    a.sdesc = descs + desc;
+    a.snap_at = snap_at;
+    a.out = sm;
+    std::vector<double> init_c(16, 0.0), init_s(16, 0.0), outv(80, 0.0);
+    for (uint32_t k = 0; k < n_cats; ++k) {
+      init_c[k] = init[k].c_hat;
+      init_s[k] = init[k].sigma_hat;
+      outv[k] = init[k].c_hat;                          // the final state of an empty stream
+      outv[16 + k] = init[k].sigma_hat;
+    }
+    for (int k = 48; k < 80; ++k) outv[k] = std::nan("");
+    CUDA_TRY(p, cudaMemcpyAsync(c0, init_c.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
+    CUDA_TRY(p, cudaMemcpyAsync(s0, init_s.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
+    CUDA_TRY(p, cudaMemcpyAsync(sm, outv.data(), 80 * 8, cudaMemcpyHostToDevice, s), "H2D outputs");
+    CUDA_TRY(p, cudaMemsetAsync(flags, 0, (2 * tiles + 1) * 4, s), "memset look-back flags");
+    if (tiles) {
+      LaunchTimer lt(p, FP_KERNEL_EVAL, s);
+      cudaError_t e = launch_calib_tile(a, p->sm_count, s);
+      if (e != cudaSuccess) return cuda_fail(p, e, "calibration replay launch");
+      ++p->launches;
+    }
+    std::vector<double> h(80);
+    CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 80 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");
+    CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+    for (uint32_t k = 0; k < n_cats; ++k) {
+      uint64_t nobs;
+      memcpy(&nobs, &h[32 + k], 8);
+      h_final[k].c_hat = h[k];
+      h_final[k].sigma_hat = h[16 + k];
+      h_n_obs[k] = nobs;
+      if (h_snap) {
+        h_snap[k].c_hat = h[48 + k];
+        h_snap[k].sigma_hat = h[64 + k];
+      }
+    }
+    return FP_OK;
+  }
   // one contiguous segment per thread (a multiple of 16 records), one resident wave
   const int bps = calib_blocks_per_sm(n_cats);
   if (bps < 1) return fail(p, FP_ERR_CUDA, "calibration kernels do not fit an SM");
@@ -1920,6 +2030,11 @@ fp_status best_split(fp_plan *p, fp_candidate *h_best) {
   if (p->flags & FP_FLAG_P2P) {
     fp_status st = check_device_error(p);
     if (st != FP_OK) return st;
+  }
+  if (p->h_phase && p->h_phase[0]) {
+    for (int i = 1; i <= 10; ++i)
+      if (p->h_phase[i] >= p->h_phase[0]) p->phase_sum[i] += (double)(p->h_phase[i] - p->h_phase[0]);
+    ++p->phase_n;
   }
   unsigned long long total = 0;
   for (uint32_t j = 0; j < p->nbins; ++j) total += p->h_small[j];

@@ -75,3 +75,29 @@ def test_replay_misaligned_columns(shift):
     assert np.array_equal(g["n_obs"], o["n_obs"])
     assert _close(g["c_hat"], o["c_hat"]) and _close(g["sigma"], o["sigma"])
     assert _close(g["snap_c"], o["snap_c"]) and _close(g["snap_sigma"], o["snap_sigma"])
+
+
+@pytest.mark.parametrize("single", [False, True])
+@pytest.mark.parametrize("mode", ["skew", "dropped", "empty", "one_cat", "mixed"])
+def test_replay_edge_cases(mode, single, monkeypatch):
+    """A 99%-one-category mix, a stream whose feedback is all dropped, an empty
+    stream, one category, a plain mix -- through the two-pass kernels (the
+    default) and the single-pass look-back kernel (FP_CALIB_SINGLE=1: its
+    per-category worker groups and position lists)."""
+    n = 0 if mode == "empty" else 777_777
+    body, mo, cat, tp = generate_raw_host("MIX", 29, 0, max(n, 1))
+    body, cat, tp = body[:n], cat[:n], tp[:n]
+    ncat = 1 if mode == "one_cat" else 4
+    if mode == "skew":
+        cat = np.where(np.arange(n) % 101 == 0, cat, 2).astype(np.uint8)
+    if mode == "dropped":
+        tp = np.zeros_like(tp)
+    if single:
+        monkeypatch.setenv("FP_CALIB_SINGLE", "1")
+    init = [(4.0, 0.5)] * ncat
+    plan = fp.fleet_plan_create(**fp.desc_from_config(configs.c1()))
+    g = fp.calibrate_replay(plan, _dev(body), _dev(tp), _dev(cat), init, beta=0.95, snap_at=50)
+    o = oracle.calibrate(body, tp, cat, ncat, beta=0.95, c0=4.0, s0=0.5, snap_at=50)
+    assert np.array_equal(g["n_obs"], o["n_obs"])
+    assert _close(g["c_hat"], o["c_hat"]) and _close(g["sigma"], o["sigma"])
+    assert _close(g["snap_c"], o["snap_c"]) and _close(g["snap_sigma"], o["snap_sigma"])
