@@ -506,10 +506,12 @@ def run_ours(args, cfg):
     coll = fp.FP_FLAG_COLLECTIVES if multi else 0
     if multi and args.p2p:
         coll |= fp.FP_FLAG_P2P
-    # small grids (C5: 4,096 candidates) are evaluated whole on every rank: K3
-    # is latency-bound there, so slicing it only adds the all-gather of the
-    # ranks' best records and the pick kernel to the step
-    if multi and not args.sliced_grid and cfg.n_candidates() <= 100_000:
+    # the north star's split: the candidate grid is sliced over the ranks and
+    # the per-model winners are gathered (argmin reduce). --replicated-grid
+    # evaluates the whole (small) grid on every rank instead -- K3 is latency-
+    # bound at C5's 4,096 candidates, so that skips the all-gather and the
+    # pick kernel; the variants block times both
+    if multi and args.replicated_grid:
         coll |= fp.FP_FLAG_REPLICATED_GRID
 
     def p2p_setup(pl):
@@ -817,8 +819,11 @@ def main():
                     help="strong scaling: split the config's trace over the ranks (default: weak, n per rank)")
     ap.add_argument("--collectives", action="store_true",
                     help="take the multi-GPU code path even at world 1 (NCCL group of one; for testing)")
+    ap.add_argument("--replicated-grid", action="store_true",
+                    help="multi-rank: evaluate the whole candidate grid on every rank (no all-gather) "
+                         "instead of the default split + argmin gather")
     ap.add_argument("--sliced-grid", action="store_true",
-                    help="multi-rank: split the candidate grid over the ranks even when it is small")
+                    help="(the default at N > 1; kept for compatibility)")
     ap.add_argument("--p2p", action="store_true",
                     help="multi-rank: the histogram exchange through peer memory (FP_FLAG_P2P) instead of NCCL")
     ap.add_argument("--no-variants", dest="variants", action="store_false",

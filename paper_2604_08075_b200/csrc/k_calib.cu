@@ -261,7 +261,10 @@ __device__ __forceinline__ double ratio(uint32_t num, uint32_t den) {
   return __dmul_rn(u2d(num), y);
 }
 
-template <typename Body>
+// PRED: body(c_obs, k) for every staged record, k = n_cats for dropped feedback
+// (the bodies below then update a scratch slot: no branch, no select of
+// the whole update); otherwise body is called for valid records only.
+template <bool PRED, typename Body>
 __device__ __forceinline__ void consume(const StageSmem &st, uint32_t last, Body &body) {
   const uint2 cc = *reinterpret_cast<const uint2 *>(st.c + threadIdx.x * (kRound / 4));
 #pragma unroll
@@ -275,14 +278,15 @@ __device__ __forceinline__ void consume(const StageSmem &st, uint32_t last, Body
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t cat = (cw >> (8 * e)) & 0xffu;
-      if (get(vt, e) != 0u) body(o[e], cat < last ? cat : last);   // S:240 drop; R23
+      if (PRED) body(o[e], get(vt, e) != 0u ? (cat < last ? cat : last) : last + 1u);
+      else if (get(vt, e) != 0u) body(o[e], cat < last ? cat : last);   // S:240 drop; R23
     }
   }
 }
 
 // Runs body(c_obs, category) over this thread's segment in order (valid records only).
 // Stage buffers 0 and 1 at smem + {0, kStageBytes}.
-template <typename Body>
+template <bool PRED = false, typename Body>
 __device__ __forceinline__ void for_segment(const CalibArgs &a, unsigned char *smem, Body body) {
   const uint64_t t0 = (uint64_t)blockIdx.x * kCalBlock;
   const uint64_t rounds = (a.seg + kRound - 1) / kRound;
@@ -295,7 +299,7 @@ __device__ __forceinline__ void for_segment(const CalibArgs &a, unsigned char *s
       else asm volatile("cp.async.commit_group;" ::: "memory");
       asm volatile("cp.async.wait_group 1;" ::: "memory");
       __syncwarp();
-      consume(stage_at(smem, (uint32_t)r & 1u), last, body);
+      consume<PRED>(stage_at(smem, (uint32_t)r & 1u), last, body);
       __syncwarp();                    // buffer r & 1 is refilled at round r + 2
     }
   } else {
@@ -304,7 +308,7 @@ __device__ __forceinline__ void for_segment(const CalibArgs &a, unsigned char *s
       __syncthreads();                 // previous round consumed
       stage_sync(a, t0, r, st);
       __syncthreads();
-      consume(st, last, body);
+      consume<PRED>(st, last, body);
     }
   }
 }
@@ -319,6 +323,21 @@ __device__ __forceinline__ double pow_n(double beta, uint32_t n) {
   }
   return r;
 }
+
+// ---- NC <= 4 fast paths: scaled recurrences ---------------------------------------
+// The recurrences run on state scaled by 1 / w (w = 1 - beta), one FMA per update:
+//   C1  b~ <- beta b~ + c_obs                   (the map's offset = w b~)
+//   C3  c~ <- beta c~ + c_obs                   (c_hat = w c~)
+//       s~ <- beta s~ + |c_obs - c_hat(before)|,  c_obs - c_hat = fma(-w, c~, c_obs)   (R26)
+// -- the oracle's sums with each term rounded once more by the final scaling,
+// within the replay's reassociation tolerance (1e-12 relative). Category state
+// is indexed where a register select chain would cost more issue slots:
+// ptxas turns a predicated DFMA into an unconditional DFMA + two FSELs per
+// category, so C1's b~ lives in shared memory rows [k][thread] (one LDS.64 +
+// STS.64 per record, no select) with the counters packed in one u64; C3 keeps
+// c~ in registers (read and written through select chains) and s~ in shared
+// memory. (Both states in shared memory -- 64- or 128-bit rows -- measured
+// slower: the MIO queue saturates, profiles/r02/r02_next3_variants.md.)
 
 struct Smem {
   Aff *scan;
@@ -347,10 +366,32 @@ __global__ void __launch_bounds__(kCalBlock, 4) c1_maps(CalibArgs a) {
   n.bind(sm.u0);
   for (uint32_t k = 0; k < NC; ++k) { b.set(k, 0.0); n.set(k, 0u); }
   const double beta = a.beta, w = __dsub_rn(1.0, a.beta);
-  for_segment(a, smem, [&](double c, uint32_t k) {
-    b.ema(k, beta, __dmul_rn(w, c));
-    n.inc(k);
-  });
+  if constexpr (REG) {
+    // scaled b~ indexed in shared memory (d1 rows [k][thread]; row n_cats
+    // takes dropped feedback): one LDS.64 + STS.64 per record instead of NC
+    // DFMAs and 2 NC FSELs; the NC 16-bit counters packed in one u64
+    // (shl.b64 by 16 k >= 64 adds nothing: dropped feedback)
+    double *bk = sm.d1 + threadIdx.x;
+    for (uint32_t j = 0; j <= a.n_cats; ++j) bk[j * kCalBlock] = 0.0;
+    unsigned long long cnt = 0ull;
+    for_segment<true>(a, smem, [&](double c, uint32_t k) {
+      double *p = bk + k * kCalBlock;
+      *p = __fma_rn(beta, *p, c);
+      unsigned long long inc;
+      asm("shl.b64 %0, %1, %2;" : "=l"(inc) : "l"(1ull), "r"(16u * k));
+      cnt += inc;
+    });
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      b.set(j, j < (int)a.n_cats ? __dmul_rn(w, bk[j * kCalBlock]) : 0.0);
+      n.set(j, (uint32_t)(cnt >> (16 * j)) & 0xffffu);
+    }
+  } else {
+    for_segment(a, smem, [&](double c, uint32_t k) {
+      b.ema(k, beta, __dmul_rn(w, c));
+      n.inc(k);
+    });
+  }
   const uint64_t t = (uint64_t)blockIdx.x * kCalBlock + threadIdx.x;
   for (uint32_t k = 0; k < a.n_cats; ++k) {
     const uint32_t nk = n.get(k);
@@ -456,11 +497,28 @@ __global__ void __launch_bounds__(kCalBlock, 4) c3_replay(CalibArgs a) {
       }
     });
   } else {
-    for_segment(a, smem, [&](double o, uint32_t k) {
-      const double prev = c.get(k);
-      c.set(k, __fma_rn(beta, prev, __dmul_rn(w, o)));
-      sb.set(k, __fma_rn(beta, sb.get(k), __dmul_rn(w, fabs(__dsub_rn(o, prev)))));
-    });
+    if constexpr (REG) {
+      // scaled c~ in registers (select chains), scaled s~ in shared memory
+      // (row n_cats <= NC takes dropped feedback)
+      sb.set(a.n_cats, 0.0);
+      const double neg_w = -w;
+      Vec<NC, true> cs;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) cs.v[j] = __ddiv_rn(c.get(j), w);
+      for_segment<true>(a, smem, [&](double o, uint32_t k) {
+        const double prev = cs.get(k);
+        const double d = __fma_rn(neg_w, prev, o);
+        cs.set(k, __fma_rn(beta, prev, o));
+        sb.set(k, __fma_rn(beta, sb.get(k), fabs(d)));
+      });
+      for (uint32_t k = 0; k < a.n_cats; ++k) sb.set(k, __dmul_rn(w, sb.get(k)));
+    } else {
+      for_segment(a, smem, [&](double o, uint32_t k) {
+        const double prev = c.get(k);
+        c.set(k, __fma_rn(beta, prev, __dmul_rn(w, o)));
+        sb.set(k, __fma_rn(beta, sb.get(k), __dmul_rn(w, fabs(__dsub_rn(o, prev)))));
+      });
+    }
     for (uint32_t k = 0; k < a.n_cats; ++k) n.set(k, a.thrC[k * a.threads + t]);
   }
   for (uint32_t k = 0; k < a.n_cats; ++k) {
@@ -856,7 +914,9 @@ cudaError_t launch_calib_tile(const CalibTileArgs &a, int, cudaStream_t s) {
 namespace {
 
 size_t calib_smem(uint32_t nc, bool reg) {
-  return 2 * kStageBytes + kScanBytes + (size_t)nc * kCalBlock * 8 + (reg ? 0 : (size_t)nc * kCalBlock * (8 + 4 * 2));
+  // reg: d1 = [nc + 1][256] (row nc: C3's scratch row for dropped feedback)
+  return 2 * kStageBytes + kScanBytes + (size_t)(nc + (reg ? 1 : 0)) * kCalBlock * 8 +
+         (reg ? 0 : (size_t)nc * kCalBlock * (8 + 4 * 2));
 }
 
 template <int NC, bool REG>

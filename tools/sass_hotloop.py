@@ -16,6 +16,7 @@ import argparse
 import collections
 import os
 import re
+import signal
 import subprocess
 import sys
 
@@ -83,6 +84,7 @@ def mnemonic(text):
 
 
 def main():
+    signal.signal(signal.SIGPIPE, signal.SIG_DFL)
     ap = argparse.ArgumentParser()
     ap.add_argument("--kernel", required=True, help="substring of the mangled name")
     ap.add_argument("--marker", default=r"LDG\.E\S*\.128", help="regex counted to pick the hot loop")
