@@ -649,10 +649,11 @@ def run_ours(args, cfg):
     shares = {k: v[0] for k, v in ktime.items()}
     dom = max(shares, key=shares.get)
     # bytes each kernel moves per step as designed: with the bin
-    # pass (|E| < 255, u8 LUT) the trace pass reads 4 B and writes a bin per
-    # request (6-bit packed: 0.75 B; else 1 B) and the routing pass maps the
-    # bins to 1-B decisions; otherwise the routing pass re-reads L_total.
-    bin_pass = info["lut_cells"] > 0 and info["n_edges"] < 255
+    # pass (a fine-cell LUT and a device trace: u8 bins for |E| < 256, clamped
+    # bytes above) the trace pass reads 4 B and writes a bin per request
+    # (6-bit packed: 0.75 B; else 1 B) and the routing pass maps the bins to
+    # 1-B decisions; otherwise the routing pass re-reads L_total.
+    bin_pass = info["lut_cells"] > 0
     packed = bin_pass and info["n_edges"] + 1 <= 64
     bin_bytes = 0.75 if packed else 1.0
     moved = ({"trace": (4.0 + bin_bytes) * n, "route": (bin_bytes + 1.0) * n, "eval": 0.0} if bin_pass

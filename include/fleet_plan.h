@@ -266,6 +266,10 @@ fp_status best_split(fp_plan *plan, fp_candidate *h_best);
  * pass consumes each chunk, and the routing pass reads the device copy.
  * With |E| < 256 (u8 LUT) the trace pass also writes each request's 1-B bin
  * and the split is picked and applied on the device (no host round trip).
+ * With a fine-cell LUT and |E| >= 256 (u16 LUT) and a DEVICE trace the same
+ * holds with clamped bins (min(bin, 255)): the routing pass reads `len` back
+ * for requests whose byte is 255 when the split has an edge index >= 255, so
+ * `len` must stay unchanged until the call's work has completed on `stream`.
  * Synchronizes -- except in that bin mode with a device trace when h_best and
  * h_counts are both NULL: then the call is stream-ordered and asynchronous,
  * the records stay on the device for a later best_split, and a model without

@@ -111,10 +111,12 @@ struct RouteRawArgs {
 cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStream_t s);
 
 // K4b: decisions from per-request bins (sweep_and_route): with iB, iCS, iCL
-// the indices in E of B, C_S, C_L, L <= e_j <=> bin <= j.
+// the indices in E of B, C_S, C_L, L <= e_j <=> bin <= j. With n_edges >= 255
+// the bins are clamped bytes and len (the device trace, element i = bin i) is
+// read back for byte 255 when the split has an edge index >= 255.
 cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
                               int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,
-                              uint32_t *route, int grid, int block, cudaStream_t s);
+                              uint32_t *route, int grid, int block, cudaStream_t s, const uint32_t *len);
 // K4p: the same from K1's 6-bit packed bins (TraceArgs::bins_pack), launched
 // with the trace pass's grid x block (k1_grid x k1_block) so thread t reads
 // the chunks it wrote

@@ -506,11 +506,6 @@ __device__ __forceinline__ uint32_t dec_byte(uint32_t b, uint32_t iB, uint32_t i
 // Four packed bins -> four decision bytes. SWAR when every bin < 128: adding
 // 0x7F - j to a byte sets its top bit iff the byte is > j (no carry out of
 // any byte), so a word compare costs one add and one and.
-__device__ __forceinline__ uint32_t dec_word(uint32_t w, uint32_t iB, uint32_t iCS, uint32_t iCL) {
-  return dec_byte(w & 0xFFu, iB, iCS, iCL) | (dec_byte((w >> 8) & 0xFFu, iB, iCS, iCL) << 8) |
-         (dec_byte((w >> 16) & 0xFFu, iB, iCS, iCL) << 16) | (dec_byte(w >> 24, iB, iCS, iCL) << 24);
-}
-
 struct SwarK {
   uint32_t kB, kCS, kCL;   // (0x7F - j) replicated in every byte
 };
@@ -520,6 +515,38 @@ __device__ __forceinline__ uint32_t dec_word_swar(uint32_t w, const SwarK &k) {
   const uint32_t gS = (w + k.kCS) & 0x80808080u;
   const uint32_t gL = (w + k.kCL) & 0x80808080u;
   return (gB >> 7) + (gS >> 5) + (gL >> 7) * 9u;     // a + 4 b + 9 c per byte
+}
+
+// SWAR for full bytes (bins up to 255): b > j <=> b >= y, y = j + 1 <= 255.
+// d = (b | 0x80) - (y & 0x7F) per byte never borrows across bytes, and its top
+// bit is [b & 0x7F >= y & 0x7F]; then b >= y is (b7 | d7) when y < 128 and
+// (b7 & d7) when y >= 128: ((b & d) | ((b | d) & o)) & 0x80 with o = 0x80 or 0.
+// j >= 255 (only with the routing pass's escapes, which rewrite byte 255) is
+// taken as j = 254.
+struct SwarU {
+  uint32_t ylow[3], o[3];
+};
+
+__device__ __forceinline__ SwarU swar_u(uint32_t iB, uint32_t iCS, uint32_t iCL) {
+  SwarU k;
+  const uint32_t j[3] = {iB, iCS, iCL};
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t y = (j[t] < 254u ? j[t] : 254u) + 1u;
+    k.ylow[t] = (y & 0x7Fu) * 0x01010101u;
+    k.o[t] = y < 128u ? 0x80808080u : 0u;
+  }
+  return k;
+}
+
+__device__ __forceinline__ uint32_t dec_word_u8(uint32_t w, const SwarU &k) {
+  uint32_t g[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    const uint32_t d = (w | 0x80808080u) - k.ylow[t];
+    g[t] = (((w & d) | ((w | d) & k.o[t])) >> 7) & 0x01010101u;
+  }
+  return g[0] + g[1] * 4u + g[2] * 9u;                // a + 4 b + 9 c per byte
 }
 
 // The split to route with, picked on the device so that the step needs no
@@ -567,41 +594,83 @@ __global__ void k_pick_route(const fp_candidate *recs, int ranks, uint32_t n_mod
   if (lane == 0) { out[0] = nb; out[1] = ns; out[2] = nl; out[3] = 1u; }
 }
 
+// Clamped bytes (|E| >= 255, k1_trace bin_byte): byte 255 = "bin >= 255". When
+// every edge index of the split is < 255 that byte is above all three and the
+// decision needs nothing else; otherwise (esc) such requests read L_total back
+// from the trace and compare it with the split's edge values: a stand-in bin
+// with the same order relations to iB <= iCS <= iCL (rare: L above the 255th
+// edge).
+__device__ __forceinline__ uint32_t escape_bin(uint32_t L, uint32_t iB, uint32_t iCS, uint32_t iCL,
+                                               const uint32_t *edges) {
+  uint32_t fb = 0;
+  if (L > __ldg(edges + iB)) fb = iB + 1;
+  if (L > __ldg(edges + iCS)) fb = iCS + 1;
+  if (L > __ldg(edges + iCL)) fb = iCL + 1;
+  return fb;
+}
+
+// byte 0xFF in any lane of w
+__device__ __forceinline__ bool has_ff(uint32_t w) { return ((~w - 0x01010101u) & w & 0x80808080u) != 0u; }
+
 template <bool VEC, bool SWAR>
 __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__ bins, uint8_t *__restrict__ dec,
-                                                      uint64_t n, const uint32_t *__restrict__ route) {
+                                                      uint64_t n, const uint32_t *__restrict__ route,
+                                                      const uint32_t *__restrict__ len, const uint32_t *__restrict__ edges) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // K3's split (PDL launch)
   const uint4 rt = *reinterpret_cast<const uint4 *>(route);
   if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
   const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
+  const bool esc = len && iCL >= 255u;      // iB <= iCS <= iCL
+  // the decision of request i from its byte b
+  auto one = [&](uint64_t i, uint32_t b) {
+    return dec_byte(esc && b == 255u ? escape_bin(__ldg(len + i), iB, iCS, iCL, edges) : b, iB, iCS, iCL);
+  };
   const SwarK sk{(0x7Fu - (iB < 0x7Fu ? iB : 0x7Fu)) * 0x01010101u, (0x7Fu - (iCS < 0x7Fu ? iCS : 0x7Fu)) * 0x01010101u,
                  (0x7Fu - (iCL < 0x7Fu ? iCL : 0x7Fu)) * 0x01010101u};
-  auto word = [&](uint32_t w) { return SWAR ? dec_word_swar(w, sk) : dec_word(w, iB, iCS, iCL); };
+  const SwarU su = swar_u(iB, iCS, iCL);
+  auto word = [&](uint32_t w) { return SWAR ? dec_word_swar(w, sk) : dec_word_u8(w, su); };
   const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t me = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if constexpr (!VEC) {
-    for (uint64_t i = me; i < n; i += S) dec[i] = (uint8_t)dec_byte(bins[i], iB, iCS, iCL);
+    for (uint64_t i = me; i < n; i += S) dec[i] = (uint8_t)one(i, bins[i]);
   } else {
     const uint32_t mis = (uint32_t)(reinterpret_cast<uintptr_t>(bins) & 15u);
     const uint64_t head = mis ? (n < 16u - mis ? n : 16u - mis) : 0u;
     const uint64_t n16 = (n - head) >> 4;
     const uint64_t tail_first = head + (n16 << 4);
-    if (blockIdx.x == 0 && threadIdx.x < head) dec[threadIdx.x] = (uint8_t)dec_byte(bins[threadIdx.x], iB, iCS, iCL);
+    if (blockIdx.x == 0 && threadIdx.x < head) dec[threadIdx.x] = (uint8_t)one(threadIdx.x, bins[threadIdx.x]);
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < n - tail_first) {
       const uint64_t i = tail_first + threadIdx.x;
-      dec[i] = (uint8_t)dec_byte(bins[i], iB, iCS, iCL);
+      dec[i] = (uint8_t)one(i, bins[i]);
     }
     const uint4 *b16 = reinterpret_cast<const uint4 *>(bins + head);
     uint4 *d16 = reinterpret_cast<uint4 *>(dec + head);
+    // 16 decisions from 16 bytes; escapes (esc only, warp-uniform) one by one
+    auto sixteen = [&](uint64_t q, const uint4 &v) {
+      uint4 o = make_uint4(word(v.x), word(v.y), word(v.z), word(v.w));
+      if (esc && (has_ff(v.x) | has_ff(v.y) | has_ff(v.z) | has_ff(v.w))) {
+        uint32_t *ow = &o.x;
+        const uint32_t *vw = &v.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (((vw[k] >> (8 * e)) & 0xFFu) == 0xFFu) {
+              const uint32_t d = one(head + 16 * q + 4 * k + e, 255u);
+              ow[k] = (ow[k] & ~(0xFFu << (8 * e))) | (d << (8 * e));
+            }
+      }
+      return o;
+    };
     for (uint64_t i = me; i < n16; i += 2 * S) {
       const bool two = i + S < n16;
       const uint4 v = ldg_stream(b16 + i);
       const uint4 v2 = two ? ldg_stream(b16 + i + S) : make_uint4(0u, 0u, 0u, 0u);
-      const uint4 o = make_uint4(word(v.x), word(v.y), word(v.z), word(v.w));
+      const uint4 o = sixteen(i, v);
       asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w)
                    : "memory");
       if (two) {
-        const uint4 o2 = make_uint4(word(v2.x), word(v2.y), word(v2.z), word(v2.w));
+        const uint4 o2 = sixteen(i + S, v2);
         asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i + S), "r"(o2.x), "r"(o2.y), "r"(o2.z),
                      "r"(o2.w)
                      : "memory");
@@ -707,7 +776,7 @@ cudaError_t launch_route_packed(const uint8_t *lo, const uint8_t *hi, const uint
 
 cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n, const fp_candidate *recs,
                               int ranks, uint32_t n_models, uint32_t model, const uint32_t *edges, uint32_t n_edges,
-                              uint32_t *route, int grid, int block, cudaStream_t s) {
+                              uint32_t *route, int grid, int block, cudaStream_t s, const uint32_t *len) {
   // recs == NULL: K3 already wrote route (one rank's grid is the whole grid)
   if (recs) k_pick_route<<<1, 32, 0, s>>>(recs, ranks, n_models, model, edges, n_edges, route);
   cudaError_t e = cudaGetLastError();
@@ -718,9 +787,11 @@ cudaError_t launch_route_bins(const uint8_t *bins, uint8_t *decision, uint64_t n
   // SWAR needs every bin < 128: bins go up to |E|, and j = iB, iCS, iCL < |E|
   const bool swar = n_edges < 128;
   const uint32_t *rt = route;
-  if (vec && swar) return launch_pdl(k4_route_bins<true, true>, dim3(g), dim3(block), 0, s, bins, decision, n, rt);
-  if (vec) return launch_pdl(k4_route_bins<true, false>, dim3(g), dim3(block), 0, s, bins, decision, n, rt);
-  return launch_pdl(k4_route_bins<false, false>, dim3(g), dim3(block), 0, s, bins, decision, n, rt);
+  // clamped bytes (n_edges >= 255): escapes may read the trace (len, device)
+  const uint32_t *lv = n_edges >= 255 ? len : nullptr;
+  if (vec && swar) return launch_pdl(k4_route_bins<true, true>, dim3(g), dim3(block), 0, s, bins, decision, n, rt, lv, edges);
+  if (vec) return launch_pdl(k4_route_bins<true, false>, dim3(g), dim3(block), 0, s, bins, decision, n, rt, lv, edges);
+  return launch_pdl(k4_route_bins<false, false>, dim3(g), dim3(block), 0, s, bins, decision, n, rt, lv, edges);
 }
 
 }  // namespace fp

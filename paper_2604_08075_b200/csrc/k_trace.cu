@@ -107,13 +107,20 @@ __device__ __forceinline__ uint32_t add_one(const K1Ctx &c, uint32_t L) {
   return b;
 }
 
-// returns the four bins packed in bytes (meaningful when |E| < 256)
+// the byte a request's bin is stored as: the bin itself when |E| < 256 (u8
+// LUT), else min(bin, 255) -- 255 then stands for "bin >= 255" (the routing
+// pass reads L_total back for such requests only when the routed split has an
+// edge index >= 255)
+template <int LUTW>
+__device__ __forceinline__ uint32_t bin_byte(uint32_t b) { return LUTW == 1 ? b : min(b, 255u); }
+
+// returns the four bins packed in bytes (bin_byte)
 template <int LUTW, int R, bool SPLIT, bool MASS>
 __device__ __forceinline__ uint32_t add_four(const K1Ctx &c, const uint4 &v) {
-  const uint32_t b0 = add_one<LUTW, R, SPLIT, MASS>(c, v.x);
-  const uint32_t b1 = add_one<LUTW, R, SPLIT, MASS>(c, v.y);
-  const uint32_t b2 = add_one<LUTW, R, SPLIT, MASS>(c, v.z);
-  const uint32_t b3 = add_one<LUTW, R, SPLIT, MASS>(c, v.w);
+  const uint32_t b0 = bin_byte<LUTW>(add_one<LUTW, R, SPLIT, MASS>(c, v.x));
+  const uint32_t b1 = bin_byte<LUTW>(add_one<LUTW, R, SPLIT, MASS>(c, v.y));
+  const uint32_t b2 = bin_byte<LUTW>(add_one<LUTW, R, SPLIT, MASS>(c, v.z));
+  const uint32_t b3 = bin_byte<LUTW>(add_one<LUTW, R, SPLIT, MASS>(c, v.w));
   return b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
 }
 
@@ -275,13 +282,13 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
   } else {
     if (blockIdx.x == 0 && threadIdx.x < head) {
       const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
-      if (BINS) (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)b;
+      if (BINS) (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)bin_byte<LUTW>(b);
     }
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
       const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
       if (BINS) {
         if (PACK) a.bins_side[4 + threadIdx.x] = (uint8_t)b;
-        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)b;
+        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)bin_byte<LUTW>(b);
       }
     }
     uint32_t *bins4 = (BINS && !PACK) ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
@@ -442,15 +449,23 @@ void *pick_kernel_src(const Variant &v) {
   return nullptr;
 }
 
-// the bin-writing variants exist for the plain u8-LUT path only (|E| < 256)
+// the bin-writing variants exist for the plain LUT paths: u8 LUT (|E| < 256;
+// 6-bit packed when |E| < 64) and u16 LUT (clamped bytes, bin_byte)
+template <int L, bool PACK>
+void *pick_kernel_bins_w(const Variant &v) {
+  if (!v.mass)
+    return v.R == 32 ? kernel_ptr<L, 32, false, false, false, true, PACK>() : kernel_ptr<L, 1, false, false, false, true, PACK>();
+  if (v.R == 32)
+    return v.split ? kernel_ptr<L, 32, true, true, false, true, PACK>() : kernel_ptr<L, 32, false, true, false, true, PACK>();
+  return v.split ? kernel_ptr<L, 1, true, true, false, true, PACK>() : kernel_ptr<L, 1, false, true, false, true, PACK>();
+}
+
 template <bool PACK>
 void *pick_kernel_bins(const Variant &v) {
-  if (v.raw || v.lutw != 1) return nullptr;
-  if (!v.mass)
-    return v.R == 32 ? kernel_ptr<1, 32, false, false, false, true, PACK>() : kernel_ptr<1, 1, false, false, false, true, PACK>();
-  if (v.R == 32)
-    return v.split ? kernel_ptr<1, 32, true, true, false, true, PACK>() : kernel_ptr<1, 32, false, true, false, true, PACK>();
-  return v.split ? kernel_ptr<1, 1, true, true, false, true, PACK>() : kernel_ptr<1, 1, false, true, false, true, PACK>();
+  if (v.raw) return nullptr;
+  if (v.lutw == 1) return pick_kernel_bins_w<1, PACK>(v);
+  if (v.lutw == 2 && !PACK) return pick_kernel_bins_w<2, false>(v);
+  return nullptr;
 }
 
 void *pick_kernel(const Variant &v) {

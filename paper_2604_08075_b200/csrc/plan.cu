@@ -1137,7 +1137,10 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   // the route counts are the best record's counts (same histogram). A host
   // trace then never needs a device copy. Otherwise: K4 re-reads L_total
   // (from a device copy for host traces).
-  const bool bin_pass = p->lut_cells && p->lut_u8;
+  // |E| >= 256 (u16 LUT): clamped bytes (k1_trace bin_byte) for device traces,
+  // the routing pass reading L_total back for requests above the 255th edge
+  // when the split needs it
+  const bool bin_pass = p->lut_cells && (p->lut_u8 || (len && !is_host_pointer(len)));
   // |E| + 1 <= 64 bins, device trace: 6-bit packed bins (0.75 B per request each way)
   const bool pack = bin_pass && p->nbins <= 64 && !(len && is_host_pointer(len));
   const uint32_t *src = len;
@@ -1212,7 +1215,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
                                    (uint32_t)p->models.size(), route_model, p->ta.edges, (uint32_t)p->edges.size(),
                                    route, k1_grid_used, p->k1_block, s)
              : launch_route_bins(bins, d_decision, n_local, recs, ranks, (uint32_t)p->models.size(), route_model,
-                                 p->ta.edges, (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s);
+                                 p->ta.edges, (uint32_t)p->edges.size(), route, p->k4_grid, p->k4_block, s, len);
     if (e != cudaSuccess) return cuda_fail(p, e, "route (bins) launch");
     p->launches += sliced ? 2 : 1;
   }

@@ -248,7 +248,7 @@ def test_sweep_and_route_equals_separate_calls(where):
 
 
 @pytest.mark.parametrize("off,doff", [(0, 0), (1, 0), (2, 5), (3, 3), (0, 7)])
-@pytest.mark.parametrize("name", ["C5", "C4", "C2"])
+@pytest.mark.parametrize("name", ["C5", "C4", "C2", "C3"])
 def test_sweep_and_route_bin_pass_misaligned(name, off, doff):
     # the bin pass (|E| < 256) at every pointer phase; C4 exercises C_S edges
     cfg = configs.CONFIGS[name]().with_n(1_000_003)
@@ -477,3 +477,34 @@ def test_forced_k3_shapes_agree(shape, name, monkeypatch):
     fp.sweep_thresholds(plan, _dev(L), cfg.rate_rps)
     _, obest = oracle.sweep(cfg, L, want_all=False)
     assert fp.best_split(plan).tobytes() == obest.tobytes()
+
+
+def _escape_cfg(n):
+    """|E| = 301 (u16 LUT: clamped-byte bin pass) with a trace almost entirely
+    above the 255th edge (65,280), so the best split's B has an edge index
+    >= 255 and the routing pass must read L_total back for byte 255."""
+    return make_config("ESC", "AZ", 7, n, 1000.0, ["llama3-70b"], ["b200-180g"],
+                       [256 * k for k in range(1, 301)], [], [131072])
+
+
+@pytest.mark.parametrize("off,doff", [(0, 0), (1, 3), (3, 0)])
+def test_sweep_and_route_clamped_bins_escape(off, doff):
+    n = 300_007
+    cfg = _escape_cfg(n)
+    rng = np.random.default_rng(11 + off)
+    full = rng.integers(65_281, 76_000, n + off, dtype=np.uint64).astype(np.uint32)
+    full[rng.random(n + off) < 0.02] = 100                     # a few short requests
+    full[rng.random(n + off) < 0.01] = 200_000                 # and rejections
+    L = full[off:]
+    plan = _plan(cfg)
+    assert fp.fleet_plan_info(plan)["n_edges"] >= 256
+    dec = torch.zeros(L.size + 16, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(full)[off:], cfg.rate_rps, route_model=0, decision=dec[doff:])
+    _, obest = oracle.sweep(cfg, L)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[0]
+    edges = sorted(set(cfg.b_short) | set(cfg.c_long))
+    assert edges.index(int(b["b_short"])) >= 255, "the split must exercise the escape path"
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec[doff:doff + L.size].cpu().numpy(), odec)
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
