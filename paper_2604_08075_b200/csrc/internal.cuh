@@ -147,6 +147,7 @@ struct EvalArgs {
   const uint16_t *cs_edge = nullptr;    // index in E of each C_S
   const uint16_t *b_win, *cs_win, *cl_win;  // index in windows of each B / C_S / C_L
   uint32_t n_b, n_cs, n_cl, n_cs_eff;
+  uint32_t fac_lc = 16;                 // k3_factored: C_L values per block (<= 64)
   // exact 32-bit division by n_b, n_cs_eff, n_cl, n_gpus: q = umul64hi(x, mul) (mul = ceil(2^64 / d), 0 for d = 1)
   unsigned long long div_b = 0, div_cs = 0, div_cl = 0, div_g = 0;
   uint32_t n_models, n_gpus, n_windows;

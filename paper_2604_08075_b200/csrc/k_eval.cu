@@ -766,11 +766,11 @@ __global__ void __launch_bounds__(256, 3) k3_grid(EvalArgs a) {
 
 // ---- factored shape: large grids, argmin only ------------------------------------------
 // blockIdx.x = (g * n_lc + lc) * n_kt + kt: B tile kt (32 values, one per
-// lane), C_L chunk lc (kLC values), GPU g; every C_S. Shared tables:
+// lane), C_L chunk lc (a.fac_lc values), GPU g; every C_S. Shared tables:
 //   Is[s][32] = I_short(g, C_S[s], B[k])   (kNoPool: infeasible or B > C_S)
 //   Il[lc][32] = I_long(g, C_L[l], B[k])   (kNoPool: infeasible)
 // built with the per-candidate evaluation's operations (identical values).
-constexpr int kLC = 16;
+constexpr int kMaxLC = 64;                 // EvalArgs::fac_lc <= kMaxLC
 
 __device__ __forceinline__ unsigned long long short_instances(const EvalArgs &a, const Tab &T, uint32_t g, uint32_t s,
                                                               uint32_t k) {
@@ -803,9 +803,10 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
   unsigned long long *Il = Is + (size_t)a.n_cs_eff * 32;
   prologue(a, T, m, blockIdx.x == 0 && m == 0, warp_tot);
 
-  const uint32_t n_kt = (a.n_b + 31) / 32, n_lc = (a.n_cl + kLC - 1) / kLC;
+  const uint32_t LC = a.fac_lc;
+  const uint32_t n_kt = (a.n_b + 31) / 32, n_lc = (a.n_cl + LC - 1) / LC;
   const uint32_t kt = blockIdx.x % n_kt, lc = (blockIdx.x / n_kt) % n_lc, g = blockIdx.x / (n_kt * n_lc);
-  const uint32_t l0 = lc * kLC, nl = min((uint32_t)kLC, a.n_cl - l0);
+  const uint32_t l0 = lc * LC, nl = min(LC, a.n_cl - l0);
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t k = kt * 32 + lane;
   const bool kin = k < a.n_b;
@@ -814,15 +815,38 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
   // when the pool is infeasible (or B > C_S). gpi x I <= 2^9 x 2^53, so a
   // valid entry never has bit 63; gpi (I_s + I_l) = gpi I_s + gpi I_l mod 2^64
   // as in the per-candidate evaluation
+  __shared__ uint32_t gmax_s, gmax_l, cs_unsorted, s_hi[kMaxLC];
+  if (threadIdx.x == 0) { gmax_s = 0u; gmax_l = 0u; cs_unsorted = 0u; }
+  __syncthreads();
+  unsigned long long ms = 0ull, ml = 0ull;       // largest feasible table entries
   for (uint32_t e = threadIdx.x; e < a.n_cs_eff * 32; e += blockDim.x) {
     const uint32_t kk = kt * 32 + (e & 31);
     const unsigned long long v = kk < a.n_b ? short_instances(a, T, g, e >> 5, kk) : kNoPool;
     Is[e] = v == kNoPool ? kNoGpu : gpi * v;
+    if (v != kNoPool) ms = max(ms, gpi * v);
   }
   for (uint32_t e = threadIdx.x; e < nl * 32; e += blockDim.x) {
     const uint32_t kk = kt * 32 + (e & 31);
     const unsigned long long v = kk < a.n_b ? long_instances(a, T, g, l0 + (e >> 5), kk) : kNoPool;
     Il[e] = v == kNoPool ? kNoGpu : gpi * v;
+    if (v != kNoPool) ml = max(ml, gpi * v);
+  }
+  // independent C_S grid: the C_S values <= C_L of chunk entry li are a prefix
+  // [0, s_hi[li]) when the grid is ascending (checked here)
+  if (a.n_cs) {
+    for (uint32_t s = threadIdx.x; s + 1 < a.n_cs; s += blockDim.x)
+      if (T.cs[s] > T.cs[s + 1]) cs_unsorted = 1u;
+    for (uint32_t li = threadIdx.x; li < nl; li += blockDim.x) {
+      uint32_t c = 0;
+      while (c < a.n_cs && T.cs[c] <= T.cl[l0 + li]) ++c;
+      s_hi[li] = c;
+    }
+  }
+  // block maxima, saturated to u32 (an upper bound is all the test below needs)
+  {
+    const uint32_t s32 = __reduce_max_sync(0xffffffffu, (uint32_t)min(ms, 0xffffffffull));
+    const uint32_t l32 = __reduce_max_sync(0xffffffffu, (uint32_t)min(ml, 0xffffffffull));
+    if ((threadIdx.x & 31) == 0) { atomicMax(&gmax_s, s32); atomicMax(&gmax_l, l32); }
   }
   __syncthreads();
 
@@ -859,7 +883,38 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
       }
     }
   };
-  if (kin) {
+  // Integer argmin. For this block's GPU the cost is RN(RN(G price) hours) of
+  // the candidate's GPU count G = gpi (I_short + I_long), monotone in G; it is
+  // STRICTLY monotone (distinct G -> distinct costs, so the (cost, index)
+  // argmin is the (G, index) argmin) when the products stay far from fp64's
+  // precision: price >= 1/32, hours >= 1, G price <= 2^40 and G price hours
+  // <= 2^44 for every G of this block (bounded by the tables' largest feasible
+  // entries) -- then RN(G2 p) - RN(G1 p) >= p - 2^-11 > 1/64 and the product
+  // with hours keeps a gap > 2 ulp(2^44) = 1/128. Each candidate is then one
+  // 64-bit add and compare on the integer pipes (an infeasible table entry
+  // carries bit 63, so its sum never beats the initial 2^63); the winner's
+  // cost is formed once, with the same operations as evaluate().
+  const double gbound = u2d((unsigned long long)gmax_s + gmax_l);
+  const bool int_argmin = !(a.n_cs && cs_unsorted) && price >= 0.03125 && hours >= 1.0 &&
+                          __dmul_rn(gbound, price) <= 1099511627776.0 &&
+                          __dmul_rn(__dmul_rn(gbound, price), hours) <= 17592186044416.0;
+  if (kin && whole && int_argmin) {
+    unsigned long long bg = kNoGpu;
+    for (uint32_t li = w; li < nl; li += nw) {
+      const unsigned long long gl = Il[li * 32 + lane];
+      if (gl >> 63) continue;
+      const uint32_t qb = li * ncs;
+      uint32_t s_end = ncs;
+      if (a.n_cs) s_end = s_hi[li];
+      else if (B > T.cl[l0 + li]) continue;        // C_S = B <= C_L
+#pragma unroll 8
+      for (uint32_t s = 0; s < s_end; ++s) {
+        const unsigned long long G = Is[s * 32 + lane] + gl;
+        if (G < bg) { bg = G; bq = qb + s; }
+      }
+    }
+    if (bg < kNoGpu) { bv = 1; bc = __dmul_rn(__dmul_rn(u2d(bg), price), hours); }
+  } else if (kin) {
     if (whole) scan(std::false_type{});
     else scan(std::true_type{});
   }
@@ -988,11 +1043,11 @@ __global__ void k_fold(const unsigned long long *copies, uint32_t n_copies, uint
 // ---- host side --------------------------------------------------------------------------
 size_t eval_smem_bytes(const EvalArgs &a, int) { return tab_layout(a, true).bytes; }
 size_t eval_factored_smem_bytes(const EvalArgs &a) {
-  return tab_layout(a, true).bytes + ((size_t)a.n_cs_eff + kLC) * 32 * 8;
+  return tab_layout(a, true).bytes + ((size_t)a.n_cs_eff + a.fac_lc) * 32 * 8;
 }
 size_t eval_peak_smem_bytes(const EvalArgs &a) { return tab_layout(a, false).bytes; }
 uint32_t eval_factored_blocks_per_model(const EvalArgs &a) {
-  return a.n_gpus * ((a.n_cl + kLC - 1) / kLC) * ((a.n_b + 31) / 32);
+  return a.n_gpus * ((a.n_cl + a.fac_lc - 1) / a.fac_lc) * ((a.n_b + 31) / 32);
 }
 
 cudaError_t eval_prepare() {

@@ -612,6 +612,22 @@ __device__ __forceinline__ uint32_t escape_bin(uint32_t L, uint32_t iB, uint32_t
 // byte 0xFF in any lane of w
 __device__ __forceinline__ bool has_ff(uint32_t w) { return ((~w - 0x01010101u) & w & 0x80808080u) != 0u; }
 
+// the decisions of the 0xFF bytes of v (requests len[0..16)) from L_total
+__device__ __noinline__ uint4 fix_escapes(uint4 v, uint4 o, const uint32_t *len, uint32_t iB, uint32_t iCS,
+                                          uint32_t iCL, const uint32_t *edges) {
+  uint32_t *ow = &o.x;
+  const uint32_t *vw = &v.x;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (((vw[k] >> (8 * e)) & 0xFFu) == 0xFFu) {
+        const uint32_t d = dec_byte(escape_bin(__ldg(len + 4 * k + e), iB, iCS, iCL, edges), iB, iCS, iCL);
+        ow[k] = (ow[k] & ~(0xFFu << (8 * e))) | (d << (8 * e));
+      }
+  return o;
+}
+
 template <bool VEC, bool SWAR>
 __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__ bins, uint8_t *__restrict__ dec,
                                                       uint64_t n, const uint32_t *__restrict__ route,
@@ -645,35 +661,29 @@ __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__
     }
     const uint4 *b16 = reinterpret_cast<const uint4 *>(bins + head);
     uint4 *d16 = reinterpret_cast<uint4 *>(dec + head);
-    // 16 decisions from 16 bytes; escapes (esc only, warp-uniform) one by one
+    // 16 decisions from 16 bytes; the rare escapes (esc only, warp-uniform)
+    // out of line so the streaming loop keeps its registers
     auto sixteen = [&](uint64_t q, const uint4 &v) {
       uint4 o = make_uint4(word(v.x), word(v.y), word(v.z), word(v.w));
-      if (esc && (has_ff(v.x) | has_ff(v.y) | has_ff(v.z) | has_ff(v.w))) {
-        uint32_t *ow = &o.x;
-        const uint32_t *vw = &v.x;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (((vw[k] >> (8 * e)) & 0xFFu) == 0xFFu) {
-              const uint32_t d = one(head + 16 * q + 4 * k + e, 255u);
-              ow[k] = (ow[k] & ~(0xFFu << (8 * e))) | (d << (8 * e));
-            }
-      }
+      if (esc && (has_ff(v.x) | has_ff(v.y) | has_ff(v.z) | has_ff(v.w)))
+        o = fix_escapes(v, o, len + head + 16 * q, iB, iCS, iCL, edges);
       return o;
     };
-    for (uint64_t i = me; i < n16; i += 2 * S) {
-      const bool two = i + S < n16;
-      const uint4 v = ldg_stream(b16 + i);
-      const uint4 v2 = two ? ldg_stream(b16 + i + S) : make_uint4(0u, 0u, 0u, 0u);
-      const uint4 o = sixteen(i, v);
-      asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i), "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w)
-                   : "memory");
-      if (two) {
-        const uint4 o2 = sixteen(i + S, v2);
-        asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i + S), "r"(o2.x), "r"(o2.y), "r"(o2.z),
-                     "r"(o2.w)
-                     : "memory");
+    // KQ quads in flight per thread (small traces are latency-bound: a 1e8-
+    // request pass needs ~10 MB in flight to reach the copy rate)
+    constexpr int KQ = 4;
+    for (uint64_t i = me; i < n16; i += KQ * S) {
+      uint4 v[KQ];
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) v[k] = i + k * S < n16 ? ldg_stream(b16 + i + k * S) : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+      for (int k = 0; k < KQ; ++k) {
+        if (i + k * S < n16) {
+          const uint4 o = sixteen(i + k * S, v[k]);
+          asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(d16 + i + k * S), "r"(o.x), "r"(o.y),
+                       "r"(o.z), "r"(o.w)
+                       : "memory");
+        }
       }
     }
   }

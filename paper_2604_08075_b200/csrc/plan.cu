@@ -583,6 +583,16 @@ fp_status upload(fp_plan *p) {
   clu.grid_x = (int)std::min<uint64_t>(max_cl, std::max<uint64_t>(1, (widest + clu.block - 1) / clu.block));
   const bool cluster_ok = widest <= (uint64_t)clu.grid_x * clu.block * 4 && clu.smem <= 190 * 1024;
   // factored shape: large grids, argmin only
+  // C_L values per block: the smallest power of two >= 16 whose grid fits in
+  // one resident wave (2 blocks per SM): fewer blocks rebuild the short-pool
+  // table fewer times, but a second partial wave costs more (2^24 grid:
+  // 16 -> 41.1 us, 32 -> 29.6 us, 64 -> 31.1 us; profiles/r02/k3_factored_lc.md)
+  {
+    uint32_t lc = 16;
+    const uint64_t kt = ((uint64_t)ea.n_b + 31) / 32;
+    while (lc < 64 && (uint64_t)ea.n_gpus * ((ea.n_cl + lc - 1) / lc) * kt * M > (uint64_t)sms * 2) lc *= 2;
+    ea.fac_lc = (uint32_t)std::max(1, std::min(64, env_int("FP_K3_LC", (int)lc)));
+  }
   EvalLaunch fac;
   fac.shape = kK3Factored;
   fac.grid_x = (int)eval_factored_blocks_per_model(ea);
