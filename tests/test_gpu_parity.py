@@ -487,6 +487,32 @@ def test_factored_k3_integer_argmin_fallbacks(variant):
     _compare_records(fp.best_split(plan), obest.view(fp.FP_CANDIDATE), f"factored {variant}")
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_factored_k3_random_prices_hours_mu(seed):
+    """Random GPU prices (some below 1/32), hours (1 .. 1e12), mu tables and
+    C_S orders: the factored shape picks the integer or the fp64 argmin per
+    block, and both must give the oracle's best records."""
+    from dataclasses import replace
+    rng = np.random.default_rng(1000 + seed)
+    cfg = configs.k3_factored(n=200_003)
+    gpus = tuple(replace(g, price_per_gpu_hour=float(rng.choice([0.01, 0.03, 0.04, 1.0, 3.67, 97.0])))
+                 for g in cfg.gpus)
+    cs = list(cfg.c_short)
+    if rng.random() < 0.5:
+        rng.shuffle(cs)
+    vals = {(m.name, g.name, int(w)): float(rng.uniform(0.5, 40.0))
+            for m in cfg.models for g in cfg.gpus for w in cfg.windows()}
+    cfg = replace(cfg, gpus=gpus, c_short=tuple(int(x) for x in cs), mu_mode="table", mu_values=vals,
+                  hours_per_year=float(rng.choice([1.0, 8760.0, 3.3e9, 1e12])),
+                  rate_rps=float(rng.choice([10.0, 1e4, 1e7])))
+    L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
+    plan = _plan(cfg)
+    assert fp.fleet_plan_info(plan)["k3_shape"] == 1                  # factored
+    fp.sweep_thresholds(plan, _dev(L), cfg.rate_rps)
+    _, obest = oracle.sweep(cfg, L, want_all=False)
+    _compare_records(fp.best_split(plan), obest.view(fp.FP_CANDIDATE), f"factored random {seed}")
+
+
 @pytest.mark.parametrize("shape", ["grid", "factored", "cluster"])
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
 def test_forced_k3_shapes_agree(shape, name, monkeypatch):
