@@ -28,24 +28,10 @@ namespace {
 constexpr int kHistBlock = 512;
 constexpr uint64_t kSmallSegment = 2048;   // below this a window goes to global atomics
 
-// one thread per window: binary search (30 dependent loads at n = 1e9; used
-// for many windows, where the loads of other windows hide the latency)
-__global__ void k0w_bounds(PeakArgs a) {
-  const uint64_t w = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w > a.n_windows) return;
-  const uint64_t t = w * a.window_ns;          // no overflow: checked on the host
-  uint64_t lo = 0, n = a.n;
-  while (n > 0) {
-    const uint64_t half = n >> 1;
-    if (a.arrival[lo + half] < t) { lo += half + 1; n -= half + 1; } else { n = half; }
-  }
-  a.start[w] = w == a.n_windows ? a.n : lo;
-}
-
 // one warp per window: a 32-way search (each round 32 probes, one ballot),
 // so the dependent chain is ~log32(n) = 6 loads instead of log2(n) = 30 --
 // for few windows (the chain is the whole kernel); 6x the probes of the
-// binary search, so many windows take k0w_bounds
+// binary search, so many windows take k0w_bounds_multi
 __global__ void k0w_bounds_warp(PeakArgs a) {
   const uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -72,6 +58,59 @@ __global__ void k0w_bounds_warp(PeakArgs a) {
   const bool below = idx < hi && __ldg(a.arrival + idx) < t;
   const uint32_t c = __popc(__ballot_sync(0xffffffffu, below));
   if (lane == 0) a.start[w] = lo + c;
+}
+
+// many windows: one warp per 32 consecutive windows. Shared 32-way rounds
+// narrow one range that holds all 32 answers (probes compared with the first
+// and the last target) while that still shrinks it; then every lane takes the
+// probe interval of its own target (32 ballots, no loads) and finishes with a
+// binary search inside it. ~4 shared rounds + log2(interval) dependent loads
+// instead of log2(n) = 30 (1-s windows on 1e9 requests: ~18).
+__global__ void k0w_bounds_multi(PeakArgs a) {
+  const uint64_t w0 = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) << 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (w0 > a.n_windows) return;                               // warp-uniform
+  const uint64_t w = w0 + lane;
+  const uint64_t last = min(w0 + 31, a.n_windows);            // the warp's last window (<= n_windows)
+  const uint64_t t = min(w, last) * a.window_ns;              // lanes past the end repeat the last target
+  const uint64_t tf = __shfl_sync(0xffffffffu, t, 0), tl = __shfl_sync(0xffffffffu, t, 31);
+  // every answer lower_bound(arrival, t_lane) lies in [lo, hi]
+  uint64_t lo = 0, hi = a.n;
+  uint64_t step = 0;
+  uint64_t pv = 0;                                            // this lane's probe value (last round)
+  uint64_t pidx = 0;
+  while (hi - lo > 32) {
+    step = (hi - lo + 31) / 32;
+    pidx = min(lo + (lane + 1) * step - 1, hi - 1);
+    pv = __ldg(a.arrival + pidx);
+    const uint32_t cf = __popc(__ballot_sync(0xffffffffu, pv < tf));
+    const uint32_t cl = __popc(__ballot_sync(0xffffffffu, pv < tl));
+    const uint64_t nlo = cf ? min(lo + cf * step - 1, hi - 1) + 1 : lo;
+    const uint64_t nhi = cl < 32 ? min(lo + (cl + 1) * step - 1, hi - 1) : hi;
+    if (nhi - nlo > (hi - lo) / 2) break;                     // the targets span the range: split per lane
+    lo = nlo;
+    hi = nhi;
+    step = 0;
+  }
+  uint64_t mlo = lo, mhi = hi;
+  if (step) {
+    // this lane's interval from the last round's probes (probe j at pidx_j)
+    uint32_t c = 0;
+    for (uint32_t j = 0; j < 32; ++j) {
+      const uint64_t tj = __shfl_sync(0xffffffffu, t, j);
+      const uint32_t cj = __popc(__ballot_sync(0xffffffffu, pv < tj));
+      if (lane == j) c = cj;
+    }
+    mlo = c ? min(lo + c * step - 1, hi - 1) + 1 : lo;
+    mhi = c < 32 ? min(lo + (c + 1) * step - 1, hi - 1) : hi;
+  }
+  // lower_bound(arrival, t) in [mlo, mhi]: arrival[mlo - 1] < t, arrival[mhi] >= t (or mhi = n)
+  uint64_t n = mhi - mlo;
+  while (n > 0) {
+    const uint64_t half = n >> 1;
+    if (__ldg(a.arrival + mlo + half) < t) { mlo += half + 1; n -= half + 1; } else { n = half; }
+  }
+  if (w <= a.n_windows) a.start[w] = w == a.n_windows ? a.n : mlo;
 }
 
 __global__ void kc_check_order(PeakArgs a) {
@@ -439,7 +478,7 @@ cudaError_t launch_peak_hist(const PeakArgs &a, int sm_count, cudaStream_t s) {
   if (a.n_windows < 16384)
     k0w_bounds_warp<<<(unsigned)((a.n_windows + 1 + 7) / 8), 256, 0, s>>>(a);   // one warp per window
   else
-    k0w_bounds<<<(unsigned)((a.n_windows + 1 + 255) / 256), 256, 0, s>>>(a);
+    k0w_bounds_multi<<<(unsigned)((a.n_windows + 1 + 255) / 256), 256, 0, s>>>(a);     // 32 windows per warp
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   // per-warp histograms while they fit 3 blocks per SM (|E| + 1 <= ~140 bins)
   const size_t wsmem = warp_hist_smem(a);
