@@ -504,6 +504,10 @@ def run_ours(args, cfg):
     # stream time, and timing K3 and K4 too would add ~16 us to every step
     # (1.5% of C5's, a third of C2's); the per-kernel breakdown is a second loop
     coll = fp.FP_FLAG_COLLECTIVES if multi else 0
+    # speculative routing (FP_FLAG_SPECULATE, fleet_plan.h): the library applies
+    # it where it can (one rank, device trace, |E| < 127, >= 2^26 requests) and
+    # falls back otherwise; results are identical either way
+    spec_flag = fp.FP_FLAG_SPECULATE if args.speculate else 0
     if multi and args.p2p:
         coll |= fp.FP_FLAG_P2P
     # the north star's split: the candidate grid is sliced over the ranks and
@@ -522,7 +526,7 @@ def run_ours(args, cfg):
             fp.fp_p2p_import(pl, handles)
     plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
                                 nccl_unique_id=uid,
-                                flags=(0 if args.no_kernel_events else fp.FP_FLAG_TIME_TRACE) | coll)
+                                flags=(0 if args.no_kernel_events else fp.FP_FLAG_TIME_TRACE) | coll | spec_flag)
     p2p_setup(plan)
     info = fp.fleet_plan_info(plan)
     if multi:
@@ -560,13 +564,14 @@ def run_ours(args, cfg):
     barrier()
     best = fp.best_split(plan)                  # the records of the last timed step
     launches = fp.fp_kernel_launches(plan) - l0
+    info = fp.fleet_plan_info(plan)             # (+ the speculation counters of the timed steps)
     k1_time = (0.0, 0) if args.no_kernel_events else fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
 
     # ---- per-kernel breakdown and per-step spread: a second loop on a plan that
     # times every kernel (not part of the headline value) ----
     plan_b = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=local, rank=rank, world=world,
                                   nccl_unique_id=_bcast_uid(fp, dist, rank) if multi else None,
-                                  flags=fp.FP_FLAG_KERNEL_TIMING | coll)
+                                  flags=fp.FP_FLAG_KERNEL_TIMING | coll | spec_flag)
     p2p_setup(plan_b)
     for _ in range(2):
         step(d_len, pl=plan_b)
@@ -654,10 +659,15 @@ def run_ours(args, cfg):
     # (6-bit packed: 0.75 B; else 1 B) and the routing pass maps the bins to
     # 1-B decisions; otherwise the routing pass re-reads L_total.
     bin_pass = info["lut_cells"] > 0
-    packed = bin_pass and info["n_edges"] + 1 <= 64
+    speculative = info["spec_calls"] > 0
+    packed = bin_pass and info["n_edges"] + 1 <= 64 and not speculative
     bin_bytes = 0.75 if packed else 1.0
     moved = ({"trace": (4.0 + bin_bytes) * n, "route": (bin_bytes + 1.0) * n, "eval": 0.0} if bin_pass
              else {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0})
+    if speculative:
+        # the full trace pass reads L_total and writes the decision byte; the
+        # verify kernel reads two 16-B splits (re-routing only on a miss)
+        moved = {"trace": 5.0 * n, "route": 0.0, "eval": 0.0}
     # SURVEY §8(d)'s algorithmic bytes: the sweep pass reads 4 B per request;
     # route_batch reads 4 B and writes 1 B (the bins are this design's, not the method's)
     algo = {"trace": 4.0 * n, "route": 5.0 * n, "eval": 0.0}
@@ -670,13 +680,16 @@ def run_ours(args, cfg):
              for k in ktime}
     kname = {"trace": "K1 k1_trace" + ((" (6-bit packed bin pass)" if packed else " (bin pass)") if bin_pass else ""),
              "route": ("K4p k4_route_packed" if packed else "K4b k4_route_bins") if bin_pass else "K4 k4_route"}
+    if speculative:
+        kname = {"trace": "K1 k1_trace (decision-writing pass for the sampled split)", "route": "K4v k4_route_verify"}
     # the step's DRAM traffic as ncu measured it (profiles/ncu_traffic.json, --set full)
     step_dram = None
-    if all(_traffic(cfg.name, k) for k in ("trace", "route")):
-        step_dram = sum(_traffic(cfg.name, k) or 0.0 for k in ("trace", "route", "eval"))
+    tkey = cfg.name + ("-spec" if speculative else "")     # ncu_traffic.json workload key
+    if all(_traffic(tkey, k) for k in ("trace", "route")):
+        step_dram = sum(_traffic(tkey, k) or 0.0 for k in ("trace", "route", "eval", "sample", "sample_eval"))
     roof = {"bound": "hbm", "kernel": kname.get(dom, dom),
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": _traffic(cfg.name, dom), "peak_source": peak_src,
+            "traffic": _traffic(tkey, dom), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": per_launch_bytes,
             "algorithmic_bytes_per_request": algo[dom] / n,
             "algorithmic_bytes_note": "SURVEY §8(d): the sweep's trace pass reads 4 B per request",
@@ -696,9 +709,17 @@ def run_ours(args, cfg):
             "ms_per_step_p10_p50_p90": [pct(0.1), pct(0.5), pct(0.9)],
             "vs_baseline": None, "dtype": "u32/f64",
             "data": "synthetic (seeded Philox MIX trace, generated on device; not timed)",
-            "step": "sweep_and_route: K1 trace pass (+6-bit packed bins) -> K3 sweep + per-model argmin -> device "
-                    "split pick -> K4p routing pass, stream-ordered with no host round trip; the best records stay "
-                    "on the device and are read once after the timed loop (e2e reads them every step)",
+            "step": (("sweep_and_route with speculative routing (FP_FLAG_SPECULATE): K1s sample pass (~2% of the "
+                      "trace in grid-wide stripes) -> K3s sampled split -> K1 full trace pass writing the decision "
+                      "bytes for it -> K3 sweep + per-model argmin -> K4v verify (re-routes every request from "
+                      "L_total if the split differs); results identical to the non-speculative step"
+                      if speculative else
+                      "sweep_and_route: K1 trace pass (+6-bit packed bins) -> K3 sweep + per-model argmin -> "
+                      "device split pick -> K4p routing pass")
+                     + ", stream-ordered with no host round trip; the best records stay on the device and are "
+                       "read once after the timed loop (e2e reads them every step)"),
+            "speculation": ({"calls": info["spec_calls"], "misses": info["spec_misses"]}
+                            if speculative else None),
             "config": dict(_workload(cfg, n, world, _l2_label(4 * n, l2, needs_flush)),
                            n_requests_total=total_requests),
             "candidates_per_s": cand_per_s,
@@ -820,6 +841,8 @@ def main():
                     help="strong scaling: split the config's trace over the ranks (default: weak, n per rank)")
     ap.add_argument("--collectives", action="store_true",
                     help="take the multi-GPU code path even at world 1 (NCCL group of one; for testing)")
+    ap.add_argument("--no-speculate", dest="speculate", action="store_false",
+                    help="no speculative routing (FP_FLAG_SPECULATE) in the step: the bin-pass step instead")
     ap.add_argument("--replicated-grid", action="store_true",
                     help="multi-rank: evaluate the whole candidate grid on every rank (no all-gather) "
                          "instead of the default split + argmin gather")

@@ -127,6 +127,19 @@ typedef struct fp_grid {
                                         Every rank must issue the same sequence of
                                         sweeps: a rank's K3 waits on the device for
                                         every peer's K1 of the same step. world <= 64 */
+#define FP_FLAG_SPECULATE 0x80u      /* sweep_and_route, one rank, device trace, |E| < 127,
+                                        >= 2^26 requests: speculative routing. A sample
+                                        pass (every ~6th grid-wide stripe of the trace,
+                                        ~2%) and its K3 pick a split; the full trace pass
+                                        then writes Alg. 1's decision bytes for that split
+                                        directly into d_decision (no bin round trip:
+                                        5 B/request instead of 6.5); the full K3 picks the
+                                        true split and a verify kernel re-routes every
+                                        request from L_total when the two differ. Results
+                                        are identical to the non-speculative call; only
+                                        the time depends on the sample. Difference: when
+                                        route_model has no feasible split, d_decision's
+                                        contents are unspecified (not left untouched)  */
 #define FP_FLAG_COLLECTIVES 0x10u    /* run the cross-rank steps even when world == 1
                                         (a one-rank NCCL communicator or the hooks): the
                                         multi-rank code path on a single GPU, for tests  */
@@ -212,6 +225,10 @@ typedef struct fp_plan_info {
   uint32_t k3_shape;            /* K3 launch shape of the sweep: 0 cluster (paper-size
                                    grids), 1 factored (large grids), 2 grid-stride */
   uint32_t k3_blocks_per_model; /* K3 blocks per model (the cluster size for shape 0) */
+  uint32_t spec_calls;          /* FP_FLAG_SPECULATE: speculative sweep_and_route calls */
+  uint32_t spec_misses;         /* ... whose sampled split was not the final one (the
+                                   verify kernel re-routed every request); reading it
+                                   synchronizes the plan's last stream             */
 } fp_plan_info;
 
 typedef struct fp_plan fp_plan; /* opaque */

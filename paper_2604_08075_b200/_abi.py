@@ -22,6 +22,7 @@ FP_FLAG_CHECK_ORDER = 0x8
 FP_FLAG_COLLECTIVES = 0x10
 FP_FLAG_TIME_TRACE = 0x20
 FP_FLAG_P2P = 0x40
+FP_FLAG_SPECULATE = 0x80
 FP_P2P_HANDLE_BYTES = 64
 FP_KERNEL_TRACE, FP_KERNEL_EVAL, FP_KERNEL_ROUTE = 0, 1, 2
 FP_CAND_VALID, FP_CAND_FEASIBLE, FP_CAND_HOMO_FEASIBLE = 1, 2, 4
@@ -103,7 +104,8 @@ class fp_plan_info(ctypes.Structure):
                 ("n_edges", c_u32), ("lut_shift", c_u32), ("lut_cells", c_u32), ("n_windows", c_u32),
                 ("device", c_i32), ("rank", c_i32), ("world", c_i32),
                 ("sm_count", c_u32), ("k1_grid", c_u32), ("k1_block", c_u32),
-                ("nccl_comm_size", c_i32), ("k3_shape", c_u32), ("k3_blocks_per_model", c_u32)]
+                ("nccl_comm_size", c_i32), ("k3_shape", c_u32), ("k3_blocks_per_model", c_u32),
+                ("spec_calls", c_u32), ("spec_misses", c_u32)]
 
 
 # fp_candidate (192 bytes) as a numpy record, field order of fleet_plan.h

@@ -76,6 +76,16 @@ struct TraceArgs {
   uint32_t bins_pack = 0;
   uint8_t *bins_hi = nullptr;
   uint8_t *bins_side = nullptr;
+  // speculative routing (FP_FLAG_SPECULATE, sweep_and_route):
+  //  step_stride > 1: a SAMPLE pass -- only the grid steps k = 0, stride, 2 stride, ...
+  //    (whole grid-wide stripes spread over the trace), no head / tail elements
+  //  dec_route != NULL (byte bin variant, |E| < 128): bins_out receives DECISION
+  //    bytes for the split {iB, iCS, iCL, ok} at dec_route (read after
+  //    griddepcontrol.wait; ok == 0: nothing is written), pdl: launch as a
+  //    programmatic dependent of the previous kernel
+  uint32_t step_stride = 1;
+  const uint32_t *dec_route = nullptr;
+  uint32_t pdl = 0;
 };
 cudaError_t launch_trace(const TraceArgs &a, int grid, int block, size_t smem, cudaStream_t s);
 // the grid launch_trace uses for `a` (the bin/raw variants are clamped to the resident grid)
@@ -125,6 +135,12 @@ cudaError_t launch_route_packed(const uint8_t *lo, const uint8_t *hi, const uint
                                 uint32_t model, const uint32_t *edges, uint32_t n_edges, uint32_t *route, int k1_grid,
                                 int k1_block, cudaStream_t s);
 cudaError_t route_occupancy(int block, int *per_sm);
+// FP_FLAG_SPECULATE: after the full K3 -- if the final split (route) differs
+// from the speculated one (spec), every decision byte is recomputed from
+// L_total (device trace len, decision[i] <-> len[i]) with the final split.
+cudaError_t launch_route_verify(const uint32_t *len, uint8_t *decision, uint64_t n, const uint32_t *spec,
+                                const uint32_t *route, const uint32_t *edges, unsigned int *misses, int grid,
+                                int block, cudaStream_t s);
 
 // ---- K3: candidate evaluation + argmin ---------------------------------------
 struct BlockBest { double cost; uint32_t index; uint32_t valid; };
@@ -174,6 +190,7 @@ struct EvalArgs {
   // or fold kernel, completed before this sweep's plain-launched trace pass)
   unsigned long long *zero_copies = nullptr;
   size_t zero_elems = 0;                // u64 elements of zero_copies (every copy, whatever hist_copies says)
+  unsigned long long *zero_copies2 = nullptr;   // FP_FLAG_SPECULATE: the sample's accumulators (zero_elems)
   // sweep_and_route (one rank's grid is the whole grid): the last block of
   // model route_model also writes {iB, iCS, iCL, ok} of its best split
   const uint32_t *edges = nullptr;

@@ -434,6 +434,12 @@ __device__ void prologue(const EvalArgs &a, Tab &T, uint32_t m, bool first, unsi
   phase(a, 1);
   // the trace pass's histogram is complete and visible after this (no-op without PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  // FP_FLAG_SPECULATE: the sample's accumulators, for the next step's sample
+  // pass. Only past the wait: this K3 may start while the full trace pass
+  // still waits for the sample's K3, which reads them
+  if (first && a.zero_copies2) {
+    for (size_t i = threadIdx.x; i < a.zero_elems; i += blockDim.x) a.zero_copies2[i] = 0ull;
+  }
   phase(a, 2);
   if (a.p2p_world) {
     // peer-memory exchange (FP_FLAG_P2P): wait until every rank has published
@@ -815,8 +821,8 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
   // when the pool is infeasible (or B > C_S). gpi x I <= 2^9 x 2^53, so a
   // valid entry never has bit 63; gpi (I_s + I_l) = gpi I_s + gpi I_l mod 2^64
   // as in the per-candidate evaluation
-  __shared__ uint32_t gmax_s, gmax_l, cs_unsorted, s_hi[kMaxLC];
-  if (threadIdx.x == 0) { gmax_s = 0u; gmax_l = 0u; cs_unsorted = 0u; }
+  __shared__ uint32_t gmax_s, gmax_l, gmax_big, cs_unsorted, s_hi[kMaxLC];
+  if (threadIdx.x == 0) { gmax_s = 0u; gmax_l = 0u; gmax_big = 0u; cs_unsorted = 0u; }
   __syncthreads();
   unsigned long long ms = 0ull, ml = 0ull;       // largest feasible table entries
   for (uint32_t e = threadIdx.x; e < a.n_cs_eff * 32; e += blockDim.x) {
@@ -842,11 +848,17 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
       s_hi[li] = c;
     }
   }
-  // block maxima, saturated to u32 (an upper bound is all the test below needs)
+  // block maxima in u32 (an upper bound is all the test below needs); an entry
+  // of 2^32 or more disables the integer argmin for the block
   {
     const uint32_t s32 = __reduce_max_sync(0xffffffffu, (uint32_t)min(ms, 0xffffffffull));
     const uint32_t l32 = __reduce_max_sync(0xffffffffu, (uint32_t)min(ml, 0xffffffffull));
-    if ((threadIdx.x & 31) == 0) { atomicMax(&gmax_s, s32); atomicMax(&gmax_l, l32); }
+    const bool big = __any_sync(0xffffffffu, (ms | ml) >> 32);
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(&gmax_s, s32);
+      atomicMax(&gmax_l, l32);
+      if (big) gmax_big = 1u;
+    }
   }
   __syncthreads();
 
@@ -895,7 +907,7 @@ __global__ void __launch_bounds__(256, 2) k3_factored(EvalArgs a) {
   // carries bit 63, so its sum never beats the initial 2^63); the winner's
   // cost is formed once, with the same operations as evaluate().
   const double gbound = u2d((unsigned long long)gmax_s + gmax_l);
-  const bool int_argmin = !(a.n_cs && cs_unsorted) && price >= 0.03125 && hours >= 1.0 &&
+  const bool int_argmin = !gmax_big && !(a.n_cs && cs_unsorted) && price >= 0.03125 && hours >= 1.0 &&
                           __dmul_rn(gbound, price) <= 1099511627776.0 &&
                           __dmul_rn(__dmul_rn(gbound, price), hours) <= 17592186044416.0;
   if (kin && whole && int_argmin) {

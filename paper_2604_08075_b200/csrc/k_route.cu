@@ -765,7 +765,33 @@ __global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long 
   }
 }
 
+// FP_FLAG_SPECULATE verify / fix-up: nothing to do when the speculated split
+// is the final one (the trace pass already wrote its decisions); otherwise
+// every request is re-routed from L_total with the final split (escape_bin's
+// stand-in bin has the same order relations to iB <= iCS <= iCL as the bin).
+__global__ void __launch_bounds__(512) k4_route_verify(const uint32_t *__restrict__ len, uint8_t *__restrict__ dec,
+                                                       uint64_t n, const uint32_t *__restrict__ spec,
+                                                       const uint32_t *__restrict__ route,
+                                                       const uint32_t *__restrict__ edges, unsigned int *misses) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the full K3's split (PDL launch)
+  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
+  const uint4 sp = *reinterpret_cast<const uint4 *>(spec);
+  if (!rt.w) return;                           // no feasible split: decisions unspecified (header)
+  if (sp.w && sp.x == rt.x && sp.y == rt.y && sp.z == rt.z) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && misses) atomicAdd(misses, 1u);
+  const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += S)
+    dec[i] = (uint8_t)dec_byte(escape_bin(__ldg(len + i), iB, iCS, iCL, edges), iB, iCS, iCL);
+}
+
 }  // namespace
+
+cudaError_t launch_route_verify(const uint32_t *len, uint8_t *decision, uint64_t n, const uint32_t *spec,
+                                const uint32_t *route, const uint32_t *edges, unsigned int *misses, int grid,
+                                int block, cudaStream_t s) {
+  return launch_pdl(k4_route_verify, dim3(grid), dim3(block), 0, s, len, decision, n, spec, route, edges, misses);
+}
 
 cudaError_t launch_route_packed(const uint8_t *lo, const uint8_t *hi, const uint8_t *side, uint32_t head,
                                 uint8_t *decision, uint64_t n, const fp_candidate *recs, int ranks, uint32_t n_models,

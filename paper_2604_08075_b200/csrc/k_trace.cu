@@ -107,6 +107,21 @@ __device__ __forceinline__ uint32_t add_one(const K1Ctx &c, uint32_t L) {
   return b;
 }
 
+// speculative routing: Alg. 1's decision byte from a bin for the split's edge
+// indices (pool + 4 stage, k_route.cu dec_byte), SWAR for bins < 128: adding
+// 0x7F - j sets a byte's top bit iff the byte is > j
+struct DecK {
+  uint32_t kB, kCS, kCL;
+};
+__device__ __forceinline__ DecK dec_k(uint32_t iB, uint32_t iCS, uint32_t iCL) {
+  auto r = [](uint32_t j) { return (0x7Fu - (j < 0x7Fu ? j : 0x7Fu)) * 0x01010101u; };
+  return DecK{r(iB), r(iCS), r(iCL)};
+}
+__device__ __forceinline__ uint32_t dec_word(uint32_t w, const DecK &k) {
+  const uint32_t gB = (w + k.kB) & 0x80808080u, gS = (w + k.kCS) & 0x80808080u, gL = (w + k.kCL) & 0x80808080u;
+  return (gB >> 7) + (gS >> 5) + (gL >> 7) * 9u;
+}
+
 // the byte a request's bin is stored as: the bin itself when |E| < 256 (u8
 // LUT), else min(bin, 255) -- 255 then stands for "bin >= 255" (the routing
 // pass reads L_total back for such requests only when the routed split has an
@@ -280,18 +295,32 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
       maybe_flush(a.flush_iters * 4u * kUnroll);
     }
   } else {
-    if (blockIdx.x == 0 && threadIdx.x < head) {
-      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
-      if (BINS) (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)bin_byte<LUTW>(b);
+    // speculative routing: the split to write decisions for (after the
+    // predecessor -- the sample's K3 -- has completed)
+    bool store = true;
+    DecK dk{0u, 0u, 0u};
+    if (BINS && !PACK && a.dec_route) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      uint4 rt;
+      asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(rt.x), "=r"(rt.y), "=r"(rt.z), "=r"(rt.w) : "l"(a.dec_route));
+      store = rt.w != 0u;
+      dk = dec_k(rt.x, rt.y, rt.z);
     }
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
+    const bool decm = BINS && !PACK && a.dec_route;
+    uint32_t *bins4 = (BINS && !PACK) ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
+    if (a.step_stride == 1u && blockIdx.x == 0 && threadIdx.x < head) {
+      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
+      if (BINS && store)
+        (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)(decm ? dec_word(b, dk) : bin_byte<LUTW>(b));
+    }
+    if (a.step_stride == 1u && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
       const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
-      if (BINS) {
+      if (BINS && store) {
         if (PACK) a.bins_side[4 + threadIdx.x] = (uint8_t)b;
-        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)bin_byte<LUTW>(b);
+        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)(decm ? dec_word(b, dk) : bin_byte<LUTW>(b));
       }
     }
-    uint32_t *bins4 = (BINS && !PACK) ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
     const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
     // grid-stride stripes: at every step the whole grid reads kUnroll contiguous
     // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
@@ -300,7 +329,7 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
     const uint64_t step4 = S * U;
     const uint64_t full_steps = n4 / step4;
     const uint64_t nsteps = (n4 + step4 - 1) / step4;
-    for (uint64_t k = 0; k < nsteps; ++k) {
+    for (uint64_t k = 0; k < nsteps; k += a.step_stride) {
       const uint64_t base = k * step4 + me;
       if (k < full_steps) {
         uint4 v[U];
@@ -311,7 +340,9 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
         for (int u = 0; u < U; ++u) {
           const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
           if (BINS && PACK) pw[u & 3] = w;
-          else if (BINS) asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(w) : "memory");
+          else if (BINS && store)
+            asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(decm ? dec_word(w, dk) : w)
+                         : "memory");
         }
         if (BINS && PACK) {
           unsigned long long plo;
@@ -327,7 +358,7 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
           if (j < n4) {
             const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, j) : sp.load4(body, j));
             if (BINS && PACK) pw[u & 3] = w;
-            else if (BINS) bins4[j] = w;
+            else if (BINS && store) bins4[j] = decm ? dec_word(w, dk) : w;
           }
         }
         if (BINS && PACK) {
@@ -537,7 +568,22 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
     }
     a.n = std::min<uint64_t>(cap, a0.n - off);
     void *args[] = {&a};
-    cudaError_t e = cudaLaunchKernel(k, dim3(grid), dim3(block), args, smem, s);
+    cudaError_t e;
+    if (a0.pdl && off == 0 && pdl_enabled()) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(block);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelExC(&cfg, k, args);
+    } else {
+      e = cudaLaunchKernel(k, dim3(grid), dim3(block), args, smem, s);
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

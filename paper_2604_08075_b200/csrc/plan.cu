@@ -113,6 +113,14 @@ struct fp_plan {
   uint64_t sweep_seq = 0;
   bool parity_clean[2] = {true, true};      // that parity's copies are zero (stream-ordered)
   unsigned long long *d_fold = nullptr;     // dist (NCCL / hooks): [2][nbins] folded histogram, all-reduced
+  // FP_FLAG_SPECULATE: the sample's accumulator copies (zeroed by the full K3),
+  // its best records, its split {iB, iCS, iCL, ok} and a miss counter
+  unsigned char *d_spec = nullptr;
+  unsigned long long *spec_acc = nullptr;
+  fp_candidate *spec_best = nullptr;
+  uint32_t *spec_route = nullptr;
+  unsigned int *spec_miss = nullptr;
+  uint64_t spec_calls = 0;
   // FP_FLAG_P2P: exchange buffer [2 parities][2][nbins] u64 (each rank's folded
   // histogram) + the arrival flag, the peers' buffers opened by CUDA IPC, and
   // device tables of their addresses
@@ -989,6 +997,7 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_block_best);
     cudaFree(p->d_done);
     cudaFree(p->d_fold);
+    cudaFree(p->d_spec);
     cudaFree(p->d_rmu);
     cudaFree(p->d_err);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
@@ -1046,6 +1055,15 @@ fp_status fleet_plan_info(const fp_plan *p, fp_plan_info *o) {
   }
   o->k3_shape = (uint32_t)p->k3a.shape;
   o->k3_blocks_per_model = (uint32_t)p->k3a.grid_x;
+  o->spec_calls = (uint32_t)p->spec_calls;
+  o->spec_misses = 0;
+  if (p->spec_miss) {
+    DeviceGuard g(p->device);
+    if (p->last_stream) cudaStreamSynchronize(p->last_stream);
+    unsigned int m = 0;
+    if (cudaMemcpy(&m, p->spec_miss, 4, cudaMemcpyDeviceToHost) == cudaSuccess) o->spec_misses = m;
+    cudaGetLastError();
+  }
   return FP_OK;
 }
 
@@ -1125,13 +1143,101 @@ namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident,
                      const TraceArgs *raw = nullptr, uint8_t *bins = nullptr, uint32_t *route_out = nullptr,
-                     uint32_t route_model = 0, uint8_t *bins_side = nullptr, uint8_t *bins_hi = nullptr);
+                     uint32_t route_model = 0, uint8_t *bins_side = nullptr, uint8_t *bins_hi = nullptr,
+                     const uint32_t *dec_route = nullptr, unsigned long long *zero2 = nullptr);
 }
 
 fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                            fp_candidate *h_results, void *stream) {
   return sweep_impl(p, d_len, n_local, rate_rps, h_results, stream, nullptr);
 }
+
+namespace {
+// FP_FLAG_SPECULATE path of sweep_and_route (preconditions checked by the caller).
+fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_local, double rate_rps,
+                                  uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
+                                  fp_route_counts *h_counts, cudaStream_t s) {
+  const size_t M = p->models.size();
+  if (!p->d_spec) {
+    const size_t acc_b = p->copies_elems * 8, best_b = M * sizeof(fp_candidate);
+    CUDA_TRY(p, cudaMalloc(&p->d_spec, acc_b + best_b + 32), "cudaMalloc speculation state");
+    CUDA_TRY(p, cudaMemset(p->d_spec, 0, acc_b + best_b + 32), "memset speculation state");
+    p->spec_acc = reinterpret_cast<unsigned long long *>(p->d_spec);
+    p->spec_best = reinterpret_cast<fp_candidate *>(p->d_spec + acc_b);
+    p->spec_route = reinterpret_cast<uint32_t *>(p->d_spec + acc_b + best_b);
+    p->spec_miss = reinterpret_cast<unsigned int *>(p->d_spec + acc_b + best_b + 16);
+  }
+  ++p->spec_calls;
+  // 1. the sample: every stride-th grid-wide stripe of the trace pass (~6 stripes)
+  {
+    NvtxRange r("fp:K1s sample pass");
+    TraceArgs t = p->ta;
+    t.len = len;
+    t.n = n_local;
+    t.g_cnt = p->spec_acc;
+    t.g_mass = p->spec_acc + p->nbins;
+    const int grid = k1_grid_for(p, n_local);
+    const uint64_t stripe = (uint64_t)grid * p->k1_block * 4;        // uint4 per grid step (kUnroll = 4)
+    const uint64_t nsteps = (n_local / 4 + stripe - 1) / stripe;
+    t.step_stride = (uint32_t)std::max<uint64_t>(1, nsteps / 6);
+    cudaError_t e = launch_trace(t, grid, p->k1_block, p->k1_smem, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "sample pass launch");
+    ++p->launches;
+  }
+  // 2. its K3: the speculated split of route_model
+  {
+    NvtxRange r("fp:K3s sample evaluation");
+    EvalArgs es = p->ea;
+    es.hist_cnt = p->spec_acc;
+    es.hist_mass = p->spec_acc + p->nbins;
+    es.hist_copies = p->hist_copies;
+    es.rate = rate_rps;
+    es.results = nullptr;
+    es.zero_copies = nullptr;
+    es.zero_copies2 = nullptr;
+    es.hist_out = nullptr;
+    es.best_out = p->spec_best;
+    es.route_out = p->spec_route;
+    es.route_model = route_model;
+    es.p2p_world = 0;
+    es.phase_ts = nullptr;
+    cudaError_t e = launch_eval(es, p->k3a, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "sample evaluation launch");
+    ++p->launches;
+  }
+  // 3. + 4. the full trace pass writing decisions for the speculated split, the full K3
+  uint32_t *route = reinterpret_cast<uint32_t *>(p->d_rcounts);
+  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, s, nullptr, nullptr, d_decision, route, route_model,
+                            nullptr, nullptr, p->spec_route, p->spec_acc);
+  if (st != FP_OK) return st;
+  // 5. verify: re-route from L_total when the final split differs
+  {
+    NvtxRange r("fp:K4v verify");
+    LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
+    cudaError_t e = launch_route_verify(len, d_decision, n_local, p->spec_route, route, p->ta.edges, p->spec_miss,
+                                        p->k4_grid, p->k4_block, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "verify launch");
+    ++p->launches;
+  }
+  p->last_stream = s;
+  if (!h_best && !h_counts) return FP_OK;
+  std::vector<fp_candidate> best(M);
+  st = best_split(p, best.data());
+  if (st != FP_OK) return st;
+  if (h_best) memcpy(h_best, best.data(), best.size() * sizeof(fp_candidate));
+  const fp_candidate &b = best[route_model];
+  if (!(b.flags & FP_CAND_FEASIBLE))
+    return fail(p, FP_ERR_STATE, "model %u has no feasible split to route with", route_model);
+  if (h_counts) {
+    h_counts->n_short = b.n_short;
+    h_counts->n_long = b.n_long;
+    h_counts->n_reject = b.n_reject;
+    h_counts->mass_short = b.mass_short;
+    h_counts->mass_long = b.mass_long;
+  }
+  return FP_OK;
+}
+}  // namespace
 
 fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, double rate_rps,
                           uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
@@ -1205,6 +1311,16 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     }
     resident = p->d_resident;
     src = resident;
+  }
+  // FP_FLAG_SPECULATE (header): sample pass -> its K3 picks a split -> the full
+  // trace pass writes decisions for it -> full K3 -> verify / re-route
+  {
+    const uintptr_t lp = len ? reinterpret_cast<uintptr_t>(len) : 0;
+    const uint64_t hph = (4 - ((lp & 15u) >> 2)) & 3u;
+    const bool spec = (p->flags & FP_FLAG_SPECULATE) && !p->dist && d_decision && len && !is_host_pointer(len) &&
+                      n_local >= (1ull << 26) && p->lut_cells && p->lut_u8 && p->nbins <= 127 &&
+                      p->k3a.shape == kK3Cluster && (reinterpret_cast<uintptr_t>(d_decision + hph) & 3u) == 0;
+    if (spec) return sweep_route_speculative(p, len, n_local, rate_rps, route_model, d_decision, h_best, h_counts, s);
   }
   // pick the split and route on the device: no host round trip in the step.
   // With one rank's grid = the whole grid, K3's last block of route_model
@@ -1372,7 +1488,7 @@ namespace {
 fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double rate_rps,
                      fp_candidate *h_results, void *stream, uint32_t *resident, const TraceArgs *raw,
                      uint8_t *bins, uint32_t *route_out, uint32_t route_model, uint8_t *bins_side,
-                     uint8_t *bins_hi) {
+                     uint8_t *bins_hi, const uint32_t *dec_route, unsigned long long *zero2) {
   if (!p) return FP_ERR_INVALID_ARG;
   if (n_local && !d_len && !raw) return fail(p, FP_ERR_INVALID_ARG, "d_len is NULL");
   if (!(rate_rps > 0.0) || !std::isfinite(rate_rps))
@@ -1419,6 +1535,8 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
       t.bins_hi = bins_hi;
       t.bins_pack = bins_side ? 1u : 0u;
       t.bins_side = bins_side;
+      t.dec_route = dec_route;             // speculative routing: decision bytes into bins_out
+      t.pdl = dec_route ? 1u : 0u;
       LaunchTimer lt(p, FP_KERNEL_TRACE, s);
       // packed bins: the grid the routing pass will use (bins_pack: one piece, n_local)
       cudaError_t e = launch_trace(t, k1_grid_for(p, bins_side ? n_local : n), p->k1_block, p->k1_smem, s);
@@ -1466,6 +1584,7 @@ fp_status sweep_impl(fp_plan *p, const uint32_t *d_len, uint64_t n_local, double
   ea.results = h_results ? p->d_results : nullptr;
   ea.zero_copies = other;
   ea.zero_elems = p->copies_elems;
+  ea.zero_copies2 = zero2;
   ea.route_out = route_out;
   ea.route_model = route_model;
   cudaError_t e;

@@ -1,0 +1,106 @@
+"""FP_FLAG_SPECULATE (speculative routing in sweep_and_route): a sample pass and
+its K3 pick a split, the full trace pass writes the decision bytes for it, the
+full K3 picks the true split, and a verify kernel re-routes from L_total when
+they differ. Whatever the sample says, every output must equal the oracle's:
+best records, route counts, and every decision byte (Alg. 1 for the true best
+split of the whole trace). Covers the hit path, a forced miss (a trace whose
+sampled stripes are unrepresentative), the async form, and the fallbacks."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2604_08075_b200 as fp  # noqa: E402
+from synth import configs  # noqa: E402
+from synth.gen import generate_host  # noqa: E402
+
+N = (1 << 26) + 12_345            # the speculative path needs >= 2^26 requests
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).cuda()
+
+
+def _plan(cfg, flags=fp.FP_FLAG_SPECULATE):
+    return fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=flags)
+
+
+def _check_step(cfg, L, plan, dec, best, counts):
+    _, obest = oracle.sweep(cfg, L, want_all=False)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[0]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    got = dec[:L.size].cpu().numpy()
+    if not np.array_equal(got, odec):
+        bad = np.nonzero(got != odec)[0]
+        raise AssertionError(f"{bad.size} decisions differ, first at {bad[0]}")
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
+
+
+def _sampled_stripes(plan, n):
+    """The request ranges the sample pass reads (white box: grid-wide stripes of
+    the trace pass, every stride-th of them)."""
+    info = fp.fleet_plan_info(plan)
+    S = info["k1_grid"] * info["k1_block"]
+    stripe = S * 4 * 4                                   # requests per grid step (4 uint4 per thread)
+    nsteps = (n // 4 + S * 4 - 1) // (S * 4)
+    stride = max(1, nsteps // 6)
+    return [(k * stripe, min(n, (k + 1) * stripe)) for k in range(0, nsteps, stride)]
+
+
+def test_speculative_hit_equals_oracle():
+    cfg = configs.c5().with_n(N)
+    L = generate_host(cfg.shape, cfg.seed, 0, N)
+    plan = _plan(cfg)
+    dec = torch.full((N,), 0xEE, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(L), cfg.rate_rps, route_model=0, decision=dec)
+    _check_step(cfg, L, plan, dec, best, counts)
+    info = fp.fleet_plan_info(plan)
+    assert info["spec_calls"] == 1 and info["spec_misses"] == 0
+    # steady state: the asynchronous form, twice (the sample's accumulators are re-zeroed by the full K3)
+    d = _dev(L)
+    for _ in range(2):
+        dec.fill_(0xEE)
+        assert fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec, want_best=False) == (None, None)
+    best2 = fp.best_split(plan)
+    _check_step(cfg, L, plan, dec, best2, counts)
+    assert fp.fleet_plan_info(plan)["spec_calls"] == 3
+
+
+def test_speculative_forced_miss_reroutes():
+    """The sampled stripes hold only short requests, so the sample's split is
+    not the whole trace's: the verify kernel must re-route every request."""
+    cfg = configs.c5().with_n(N)
+    L = generate_host(cfg.shape, cfg.seed, 0, N).copy()
+    plan = _plan(cfg)
+    for lo, hi in _sampled_stripes(plan, N):
+        L[lo:hi] = 100
+    dec = torch.full((N,), 0xEE, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(L), cfg.rate_rps, route_model=0, decision=dec)
+    _check_step(cfg, L, plan, dec, best, counts)
+    assert fp.fleet_plan_info(plan)["spec_misses"] == 1
+
+
+@pytest.mark.parametrize("case", ["misaligned_decision", "small_trace", "route_model_1"])
+def test_speculative_fallbacks_and_models(case):
+    n = 1_000_003 if case == "small_trace" else N
+    cfg = configs.c5().with_n(n)
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    plan = _plan(cfg)
+    doff = 1 if case == "misaligned_decision" else 0
+    model = 1 if case == "route_model_1" else 0
+    buf = torch.full((n + 16,), 0xEE, dtype=torch.uint8, device="cuda")
+    dec = buf[doff:doff + n]
+    best, counts = fp.sweep_and_route(plan, _dev(L), cfg.rate_rps, route_model=model, decision=dec)
+    _, obest = oracle.sweep(cfg, L, want_all=False)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[model]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec.cpu().numpy(), odec)
+    expect_spec = case == "route_model_1"
+    assert fp.fleet_plan_info(plan)["spec_calls"] == (1 if expect_spec else 0)

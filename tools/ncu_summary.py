@@ -1,6 +1,7 @@
 """Summarise ncu --set full reports into a markdown table (and the bench's traffic JSON).
 
-usage: python tools/ncu_summary.py OUT.md [--traffic profiles/ncu_traffic.json] name=report.ncu-rep[:units] ...
+usage: python tools/ncu_summary.py OUT.md [--traffic profiles/ncu_traffic.json[@KEY=trace:a,route:b,eval:c]...] name=report.ncu-rep[:units] ...
+(each --traffic spec writes the named launches under workload KEY; default C5 = trace, route, eval)
 `units` (optional) = requests / records / candidates processed by that launch,
 to print instructions and DRAM bytes per unit."""
 import csv
@@ -53,9 +54,10 @@ def raw(rep):
 def main():
     out = sys.argv[1]
     args = sys.argv[2:]
-    traffic_path = None
-    if args and args[0] == "--traffic":
-        traffic_path, args = args[1], args[2:]
+    traffic_specs = []
+    while args and args[0] == "--traffic":
+        traffic_specs.append(args[1])
+        args = args[2:]
     lines = ["| launch | kernel | µs | DRAM read GB | DRAM write GB | DRAM % of peak | occupancy % | issue % | "
              "regs | grid×block | instr/unit | bytes/unit | top stalls (warps per issue) |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
@@ -79,11 +81,16 @@ def main():
     with open(out, "w") as f:
         f.write("\n".join(lines) + "\n")
     print("\n".join(lines))
-    if traffic_path:
-        with open(traffic_path) as f:
+    for spec in traffic_specs:
+        path, _, rest = spec.partition("@")
+        key, mapping = "C5", {"trace": "trace", "route": "route", "eval": "eval"}
+        if rest:
+            key, _, m = rest.partition("=")
+            mapping = dict(kv.split(":") for kv in m.split(","))
+        with open(path) as f:
             t = json.load(f)
-        t.update({"C5": {k: v for k, v in traffic.items() if k in ("trace", "route", "eval")}})
-        with open(traffic_path, "w") as f:
+        t[key] = {k: traffic[v] for k, v in mapping.items() if v in traffic}
+        with open(path, "w") as f:
             json.dump(t, f, indent=1)
 
 
