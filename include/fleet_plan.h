@@ -127,10 +127,11 @@ typedef struct fp_grid {
                                         Every rank must issue the same sequence of
                                         sweeps: a rank's K3 waits on the device for
                                         every peer's K1 of the same step. world <= 64 */
-#define FP_FLAG_SPECULATE 0x80u      /* sweep_and_route, one rank, device trace, |E| < 127,
-                                        >= 2^26 requests: speculative routing. A sample
-                                        pass (every ~6th grid-wide stripe of the trace,
-                                        ~2%) and its K3 pick a split; the full trace pass
+#define FP_FLAG_SPECULATE 0x80u      /* sweep_and_route, device trace, |E| < 127, >= 2^26
+                                        requests on this rank: speculative routing. A
+                                        sample pass (every ~6th grid-wide stripe of this
+                                        rank's trace, ~2%) and its K3 (the whole grid,
+                                        rank-local) pick a split; the full trace pass
                                         then writes Alg. 1's decision bytes for that split
                                         directly into d_decision (no bin round trip:
                                         5 B/request instead of 6.5); the full K3 picks the

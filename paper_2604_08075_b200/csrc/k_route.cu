@@ -787,6 +787,12 @@ __global__ void __launch_bounds__(512) k4_route_verify(const uint32_t *__restric
 
 }  // namespace
 
+cudaError_t launch_pick_route(const fp_candidate *recs, int ranks, uint32_t n_models, uint32_t model,
+                              const uint32_t *edges, uint32_t n_edges, uint32_t *route, cudaStream_t s) {
+  k_pick_route<<<1, 32, 0, s>>>(recs, ranks, n_models, model, edges, n_edges, route);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_route_verify(const uint32_t *len, uint8_t *decision, uint64_t n, const uint32_t *spec,
                                 const uint32_t *route, const uint32_t *edges, unsigned int *misses, int grid,
                                 int block, cudaStream_t s) {

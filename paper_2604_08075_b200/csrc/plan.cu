@@ -1201,15 +1201,25 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
     es.route_model = route_model;
     es.p2p_world = 0;
     es.phase_ts = nullptr;
+    es.cand_first = 0;                   // the whole grid on every rank (its own sample)
+    es.cand_count = p->n_cand;
     cudaError_t e = launch_eval(es, p->k3a, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "sample evaluation launch");
     ++p->launches;
   }
   // 3. + 4. the full trace pass writing decisions for the speculated split, the full K3
+  // (ranks that split the grid: the final split is picked after the all-gather)
   uint32_t *route = reinterpret_cast<uint32_t *>(p->d_rcounts);
-  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, s, nullptr, nullptr, d_decision, route, route_model,
-                            nullptr, nullptr, p->spec_route, p->spec_acc);
+  const bool sliced = p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID);
+  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, s, nullptr, nullptr, d_decision,
+                            sliced ? nullptr : route, route_model, nullptr, nullptr, p->spec_route, p->spec_acc);
   if (st != FP_OK) return st;
+  if (sliced) {
+    cudaError_t e = launch_pick_route(p->d_best, p->world, (uint32_t)M, route_model, p->ta.edges,
+                                      (uint32_t)p->edges.size(), route, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, "route pick launch");
+    ++p->launches;
+  }
   // 5. verify: re-route from L_total when the final split differs
   {
     NvtxRange r("fp:K4v verify");
@@ -1317,7 +1327,7 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
   {
     const uintptr_t lp = len ? reinterpret_cast<uintptr_t>(len) : 0;
     const uint64_t hph = (4 - ((lp & 15u) >> 2)) & 3u;
-    const bool spec = (p->flags & FP_FLAG_SPECULATE) && !p->dist && d_decision && len && !is_host_pointer(len) &&
+    const bool spec = (p->flags & FP_FLAG_SPECULATE) && d_decision && len && !is_host_pointer(len) &&
                       n_local >= (1ull << 26) && p->lut_cells && p->lut_u8 && p->nbins <= 127 &&
                       p->k3a.shape == kK3Cluster && (reinterpret_cast<uintptr_t>(d_decision + hph) & 3u) == 0;
     if (spec) return sweep_route_speculative(p, len, n_local, rate_rps, route_model, d_decision, h_best, h_counts, s);

@@ -146,6 +146,73 @@ def test_two_ranks_one_gpu_match_oracle(name, n, replicated, world):
         assert np.array_equal(got, odec[first:first + got.size])
 
 
+def _spec_rank(rank, world, port, n, flags, q):
+    """FP_FLAG_SPECULATE on a world-2 plan: this rank's shard (>= 2^26 requests)
+    is sampled and routed speculatively; the decisions must be those of the
+    global best split."""
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch.distributed as dist
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        import paper_2604_08075_b200 as fp
+        from synth import configs
+        from synth.gen import generate_device
+        cfg = configs.c5().with_n(n)
+        first, count = fp.fp_shard_range(n, rank, world)
+        d = generate_device(cfg.shape, cfg.seed, first, count)
+        plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), device=0, rank=rank, world=world,
+                                    flags=flags | fp.FP_FLAG_SPECULATE, collectives=GlooCollectives(world))
+        if flags & fp.FP_FLAG_P2P:
+            handles = [None] * world
+            dist.all_gather_object(handles, fp.fp_p2p_export(plan))
+            fp.fp_p2p_import(plan, handles)
+        dec = torch.full((count,), 0xEE, dtype=torch.uint8, device="cuda")
+        sbest, counts = fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec)
+        info = fp.fleet_plan_info(plan)
+        q.put((rank, first, dec.cpu().numpy().tobytes(), sbest.tobytes(), counts, info["spec_calls"], None))
+        dist.barrier()
+        fp.fleet_plan_destroy(plan)
+        dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, 0, None, None, None, 0, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("mode", ["sliced", "replicated", "p2p"])
+def test_ranks_speculative_match_oracle(mode):
+    import oracle
+    import paper_2604_08075_b200 as fp
+    from synth import configs
+    from synth.gen import generate_host
+    world, n = 2, 2 * ((1 << 26) + 4_099)
+    flags = {"sliced": 0, "replicated": fp.FP_FLAG_REPLICATED_GRID, "p2p": fp.FP_FLAG_P2P}[mode]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_spec_rank, args=(r, world, port, n, flags, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=900) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    for o in out:
+        assert o[6] is None, o[6]
+    cfg = configs.c5().with_n(n)
+    L = generate_host(cfg.shape, cfg.seed, 0, n)
+    _, obest = oracle.sweep(cfg, L, want_all=False)
+    b = obest[0]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    for rank, first, dec, sbest, counts, calls, _ in out:
+        assert sbest == obest.tobytes()
+        assert calls == 1, "the speculative path must have run on every rank"
+        got = np.frombuffer(dec, dtype=np.uint8)
+        assert np.array_equal(got, odec[first:first + got.size]), f"rank {rank}"
+        assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
+            [int(x) for x in oc]
+
+
 def _silent_peer(rank, world, port, q):
     """Rank 1 opens the exchange but never sweeps; rank 0's K3 must give up
     waiting (FP_P2P_TIMEOUT_MS) and report FP_ERR_NCCL instead of hanging."""

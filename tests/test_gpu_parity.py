@@ -465,20 +465,23 @@ def test_factored_k3_matches_oracle(tie_mu, monkeypatch):
         assert (feas["cost_dual"] == feas["cost_dual"].min()).sum() > 1      # real ties exercised
 
 
-@pytest.mark.parametrize("variant", ["cs_descending", "cheap_gpu", "huge_hours"])
+@pytest.mark.parametrize("variant", ["cs_descending", "cheap_gpu", "huge_hours", "huge_rate"])
 def test_factored_k3_integer_argmin_fallbacks(variant):
     """k3_factored compares integer GPU counts only when the cost is strictly
     monotone in them and the C_S grid is ascending; these grids take the fp64
     comparison instead (C_S descending; a price below 1/32; hours so large
-    that G * price * hours > 2^44) and must still give the oracle's argmin."""
+    that G * price * hours > 2^44; GPU counts above 2^32) and must still give
+    the oracle's argmin."""
     from dataclasses import replace
     cfg = configs.k3_factored()
     if variant == "cs_descending":
         cfg = replace(cfg, c_short=tuple(reversed(cfg.c_short)))
     elif variant == "cheap_gpu":
         cfg = replace(cfg, gpus=tuple(replace(g, price_per_gpu_hour=0.01) for g in cfg.gpus))
-    else:
+    elif variant == "huge_hours":
         cfg = replace(cfg, hours_per_year=1e12)
+    else:                       # GPU counts above 2^32: the block bound itself disables the integer path
+        cfg = replace(cfg, rate_rps=3e13)
     L = generate_host(cfg.shape, cfg.seed, 0, cfg.n_requests)
     plan = _plan(cfg)
     assert fp.fleet_plan_info(plan)["k3_shape"] == 1                  # factored

@@ -19,6 +19,8 @@ cap() {
   ncu -i $OUT/${TAG}_$1.ncu-rep --page details --csv > $OUT/${TAG}_$1_details.csv 2>/dev/null
   ncu -i $OUT/${TAG}_$1.ncu-rep --page source --csv > $OUT/${TAG}_$1_source.csv 2>/dev/null
 }
+# gpurun copies back at most 64 MiB of gpurun_out/: the reports are summarised
+# below and then removed (the raw/details/source CSV exports stay)
 # per step with speculation: K1 sample, K3 sample, K1 full, K3 full, K4v
 cap sample k1_trace 2 "$MAIN"
 cap trace k1_trace 3 "$MAIN"
@@ -41,4 +43,5 @@ python tools/ncu_summary.py $OUT/${TAG}_summary.md \
   route_ns=$OUT/${TAG}_route_ns.ncu-rep:1000000000 k3_large=$OUT/${TAG}_k3_large.ncu-rep:16777216 \
   c1_maps=$OUT/${TAG}_c1_maps.ncu-rep:1000000000 c3_replay=$OUT/${TAG}_c3_replay.ncu-rep:1000000000 \
   k1w_hist=$OUT/${TAG}_k1w_hist.ncu-rep:1000000000 > $OUT/${TAG}_summary.log 2>&1
+rm -f $OUT/${TAG}_*.ncu-rep $OUT/${TAG}_*_source.csv
 ls -la $OUT | grep $TAG
