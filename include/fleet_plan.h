@@ -140,7 +140,10 @@ typedef struct fp_grid {
                                         are identical to the non-speculative call; only
                                         the time depends on the sample. Difference: when
                                         route_model has no feasible split, d_decision's
-                                        contents are unspecified (not left untouched)  */
+                                        contents are unspecified (not left untouched),
+                                        and `len` must stay unchanged until the call's
+                                        work on `stream` has completed (the verify
+                                        kernel may read it)                            */
 #define FP_FLAG_COLLECTIVES 0x10u    /* run the cross-rank steps even when world == 1
                                         (a one-rank NCCL communicator or the hooks): the
                                         multi-rank code path on a single GPU, for tests  */

@@ -121,6 +121,7 @@ struct fp_plan {
   uint32_t *spec_route = nullptr;
   unsigned int *spec_miss = nullptr;
   uint64_t spec_calls = 0;
+  bool spec_dirty = false;                  // a speculative call failed before its full K3 (which zeroes spec_acc)
   // FP_FLAG_P2P: exchange buffer [2 parities][2][nbins] u64 (each rank's folded
   // histogram) + the arrival flag, the peers' buffers opened by CUDA IPC, and
   // device tables of their addresses
@@ -1168,6 +1169,10 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
     p->spec_miss = reinterpret_cast<unsigned int *>(p->d_spec + acc_b + best_b + 16);
   }
   ++p->spec_calls;
+  // (a failed earlier call left the sample's accumulators dirty: only the
+  // speculation would suffer -- the verify keeps the result exact -- but clear them)
+  if (p->spec_dirty) CUDA_TRY(p, cudaMemsetAsync(p->spec_acc, 0, p->copies_elems * 8, s), "memset sample hist");
+  p->spec_dirty = true;
   // 1. the sample: every stride-th grid-wide stripe of the trace pass (~6 stripes)
   {
     NvtxRange r("fp:K1s sample pass");
@@ -1179,7 +1184,8 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
     const int grid = k1_grid_for(p, n_local);
     const uint64_t stripe = (uint64_t)grid * p->k1_block * 4;        // uint4 per grid step (kUnroll = 4)
     const uint64_t nsteps = (n_local / 4 + stripe - 1) / stripe;
-    t.step_stride = (uint32_t)std::max<uint64_t>(1, nsteps / 6);
+    static const uint64_t stripes = (uint64_t)std::max(1, env_int("FP_SPEC_STRIPES", 6));
+    t.step_stride = (uint32_t)std::max<uint64_t>(1, nsteps / stripes);
     cudaError_t e = launch_trace(t, grid, p->k1_block, p->k1_smem, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "sample pass launch");
     ++p->launches;
@@ -1214,6 +1220,7 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
   fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, s, nullptr, nullptr, d_decision,
                             sliced ? nullptr : route, route_model, nullptr, nullptr, p->spec_route, p->spec_acc);
   if (st != FP_OK) return st;
+  p->spec_dirty = false;                    // the full K3 zeroes the sample's accumulators
   if (sliced) {
     cudaError_t e = launch_pick_route(p->d_best, p->world, (uint32_t)M, route_model, p->ta.edges,
                                       (uint32_t)p->edges.size(), route, s);
