@@ -129,7 +129,7 @@ typedef struct fp_grid {
                                         every peer's K1 of the same step. world <= 64 */
 #define FP_FLAG_SPECULATE 0x80u      /* sweep_and_route, device trace, |E| < 127, >= 2^26
                                         requests on this rank: speculative routing. A
-                                        sample pass (every ~6th grid-wide stripe of this
+                                        sample pass (every ~4th grid-wide stripe of this
                                         rank's trace, ~2%) and its K3 (the whole grid,
                                         rank-local) pick a split; the full trace pass
                                         then writes Alg. 1's decision bytes for that split

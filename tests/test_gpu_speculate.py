@@ -49,7 +49,7 @@ def _sampled_stripes(plan, n):
     S = info["k1_grid"] * info["k1_block"]
     stripe = S * 4 * 4                                   # requests per grid step (4 uint4 per thread)
     nsteps = (n // 4 + S * 4 - 1) // (S * 4)
-    stride = max(1, nsteps // 6)
+    stride = max(1, nsteps // 4)
     return [(k * stripe, min(n, (k + 1) * stripe)) for k in range(0, nsteps, stride)]
 
 
