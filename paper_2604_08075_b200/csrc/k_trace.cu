@@ -299,6 +299,9 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
     // predecessor -- the sample's K3 -- has completed)
     bool store = true;
     DecK dk{0u, 0u, 0u};
+    // a programmatic-dependent launch (the sample pass after the previous
+    // step's verify): nothing of the predecessor's is read before this wait
+    if (a.pdl && !a.dec_route) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (BINS && !PACK && a.dec_route) {
       asm volatile("griddepcontrol.wait;" ::: "memory");
       uint4 rt;

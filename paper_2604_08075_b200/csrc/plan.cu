@@ -1187,6 +1187,7 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
     const uint64_t nsteps = (n_local / 4 + stripe - 1) / stripe;
     static const uint64_t stripes = (uint64_t)std::max(1, env_int("FP_SPEC_STRIPES", 4));
     t.step_stride = (uint32_t)std::max<uint64_t>(1, nsteps / stripes);
+    t.pdl = 1;          // its prologue overlaps the previous kernel's tail (it waits before reading)
     cudaError_t e = launch_trace(t, grid, p->k1_block, p->k1_smem, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "sample pass launch");
     ++p->launches;
