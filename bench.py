@@ -416,7 +416,7 @@ def config_results(fp, names, steps, warmup):
     return out
 
 
-def multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps, warmup):
+def multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps, warmup, spec_flag=0):
     """The multi-GPU step under each exchange / grid mode, weak (n_weak
     requests per rank) and strong (the config's trace split over the ranks):
     NCCL all-reduce with the grid replicated or sliced across ranks (+ the
@@ -436,7 +436,7 @@ def multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps, warmup):
         d = generate_device(c.shape, c.seed, first, n)
         dec = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
         for mode in ("nccl-replicated", "nccl-sliced", "p2p"):
-            flags = fp.FP_FLAG_COLLECTIVES
+            flags = fp.FP_FLAG_COLLECTIVES | spec_flag
             if mode != "nccl-sliced":
                 flags |= fp.FP_FLAG_REPLICATED_GRID
             if mode == "p2p":
@@ -461,9 +461,10 @@ def multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps, warmup):
             dist.barrier(device_ids=[local])       # peers may still read a P2P buffer
             fp.fleet_plan_destroy(plan)
             total = cfg.n_requests if strong else n_weak * world
+            spec = fp.fleet_plan_info(plan)["spec_calls"] > 0
             out.append({"scaling": "strong" if strong else "weak", "exchange": mode, "n_gpus": world,
                         "ms_per_step": ms_step, "requests_per_s": total / (ms_step / 1e3),
-                        "best_index_model0": int(best[0]["index"])})
+                        "best_index_model0": int(best[0]["index"]), "speculative": spec})
         del d, dec
         torch.cuda.empty_cache()
     return out
@@ -640,7 +641,7 @@ def run_ours(args, cfg):
     if multi and args.variants:
         barrier()
         variants = multi_variants(fp, dist, cfg, n_weak, rank, world, local, steps=max(5, args.steps // 2),
-                                  warmup=3)
+                                  warmup=3, spec_flag=spec_flag)
 
     if rank != 0:
         barrier()
