@@ -242,6 +242,25 @@ def next1_fused_estimation(fp, cfg, n, reps=5):
                                          decision=dec)
     k1 = fp.fp_kernel_time(plan, fp.FP_KERNEL_TRACE)
     k4 = fp.fp_kernel_time(plan, fp.FP_KERNEL_ROUTE)
+    # the whole NEXT-1 workflow in one call (sweep_and_route_raw): speculative
+    # (sample, full raw pass writing decisions, verify) vs the three calls
+    step_raw = {}
+    for mode, flags in (("speculative", fp.FP_FLAG_SPECULATE), ("sequential", 0)):
+        pl = fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=flags)
+        for _ in range(2):
+            fp.sweep_and_route_raw(pl, body, mo, cat, cats, cfg.rate_rps, decision=dec, want_best=(flags == 0))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fp.sweep_and_route_raw(pl, body, mo, cat, cats, cfg.rate_rps, decision=dec, want_best=(flags == 0))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        info = fp.fleet_plan_info(pl)
+        step_raw[mode] = {"ms": ms, "requests_per_s": n / (ms / 1e3), "spec_calls": info["spec_calls"],
+                          "spec_misses": info["spec_misses"]}
+        fp.fleet_plan_destroy(pl)
     # NEXT-3: calibration replay of the same stream as feedback (|r|, usage.prompt_tokens, category)
     cal = fp.calibrate_replay(plan, body, tp, cat, [(4.0, 0.5)] * 4)
     torch.cuda.synchronize()
@@ -260,6 +279,9 @@ def next1_fused_estimation(fp, cfg, n, reps=5):
             "k1_raw_requests_per_s": n / (k1ms / 1e3),
             "k4_raw_ms": k4ms, "k4_raw_GBps": 14.0 * n / (k4ms / 1e3) / 1e9,
             "misroute_short_long_at_8K": mis,
+            "step_raw": dict(step_raw, note="sweep_and_route_raw (estimate -> sweep -> argmin -> route) on the raw "
+                             "columns: speculative = 9 B read + 1 B written per request in one full pass (+ ~1% "
+                             "sample); sequential = sweep_thresholds_raw + host argmin + route_batch_raw"),
             "next3_calibration_replay": {"records": n, "ms": cal_ms, "records_per_s": n / (cal_ms / 1e3),
                                          "GBps": 18.0 * n / (cal_ms / 1e3) / 1e9,
                                          "c_hat": [float(x) for x in cal["c_hat"]],

@@ -348,6 +348,26 @@ fp_status route_batch_raw(fp_plan *plan, const fp_raw_trace *trace, uint64_t n_l
                           uint8_t *d_decision, uint32_t *d_l_total, fp_route_counts *h_counts,
                           uint64_t *h_misroute, void *stream);
 
+/* The whole workflow on raw columns: sweep_thresholds_raw, best_split (into
+ * h_best if non-NULL), then route_batch_raw's decisions for model
+ * route_model's best split into d_decision (device; no L_total output, no
+ * mis-route counts), the split's global counts into h_counts. With
+ * FP_FLAG_SPECULATE and the columns in one 16-B phase (category 4-B aligned
+ * at the first vector element), d_decision in that element's 4-B phase, a u8
+ * LUT with |E| < 127 and >= 2^26 requests on the rank: the speculative form
+ * (sample pass, decision bytes written by the full raw trace pass, verify /
+ * re-route from the estimated L_total) -- 9 B read + 1 B written per request
+ * instead of sweep_thresholds_raw's 9 B plus route_batch_raw's 13 B + 1 B;
+ * stream-ordered and asynchronous when h_best and h_counts are NULL. Otherwise
+ * the three calls in sequence (synchronising). Same results either way.
+ * Errors: as the three calls; FP_ERR_STATE if route_model has no feasible
+ * split (the non-speculative form; the speculative one leaves d_decision
+ * unspecified then, like sweep_and_route). */
+fp_status sweep_and_route_raw(fp_plan *plan, const fp_raw_trace *trace, uint64_t n_local,
+                              const fp_estimator *est, double rate_rps, uint32_t route_model,
+                              uint8_t *d_decision, fp_candidate *h_best, fp_route_counts *h_counts,
+                              void *stream);
+
 /* ---- NEXT-2: three pools ---------------------------------------
  * Pools 1, 2, 3 with windows C1 = B1 < C2 = B2 <= C3 = C_L from the B and C_L
  * grids (pairs i < j of B-grid indices). A request goes to the first pool

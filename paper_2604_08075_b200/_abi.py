@@ -33,7 +33,7 @@ EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split"
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
             "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
             "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools", "calibrate_replay",
-            "sweep_peak_windows", "fp_p2p_export", "fp_p2p_import"]
+            "sweep_peak_windows", "fp_p2p_export", "fp_p2p_import", "sweep_and_route_raw"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -177,6 +177,8 @@ def _load():
                                          c_vp, c_vp]),
         "route_batch_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator), c_u32, c_u32,
                                     c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), ctypes.POINTER(c_u64), c_vp]),
+        "sweep_and_route_raw": (c_i32, [c_vp, ctypes.POINTER(fp_raw_trace), c_u64, ctypes.POINTER(fp_estimator),
+                                        c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
         "sweep_three_pools": (c_i32, [c_vp, c_dbl, c_vp, c_vp, c_vp]),
         "sweep_peak_windows": (c_i32, [c_vp, c_vp, c_vp, c_u64, c_u64, c_vp, c_vp, c_vp]),
         "calibrate_replay": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_u64, c_u32, c_dbl, c_vp, c_u64, c_vp, c_vp, c_vp,
@@ -502,6 +504,31 @@ def route_batch_raw(plan, body, max_out, cat, cats, b_short, c_short, c_long, tr
     del keep
     c = {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}
     return c, ([int(mis[0]), int(mis[1])] if true_prompt is not None else None)
+
+
+def sweep_and_route_raw(plan, body, max_out, cat, cats, rate_rps, route_model=0, decision=None, gamma=1.0,
+                        c_floor=0.5, stream=None, want_best=True):
+    """The whole workflow on raw columns; returns (best records, counts dict), or
+    (None, None) with want_best=False (asynchronous in the speculative form)."""
+    tr, n = _raw(body, max_out, cat)
+    est, keep = _estimator(cats, gamma, c_floor)
+    dptr = None
+    if decision is not None:
+        if decision.numel() < n or not decision.is_cuda:
+            raise ValueError("decision must be a CUDA uint8 tensor with >= n elements")
+        dptr = decision.data_ptr()
+    if not want_best:
+        _check(lib.sweep_and_route_raw(plan.handle, ctypes.byref(tr), n, ctypes.byref(est), float(rate_rps),
+                                       route_model, dptr, None, None, _stream_handle(stream, plan.device)), plan)
+        del keep
+        return None, None
+    best = np.zeros(plan.n_models, dtype=FP_CANDIDATE)
+    counts = fp_route_counts()
+    _check(lib.sweep_and_route_raw(plan.handle, ctypes.byref(tr), n, ctypes.byref(est), float(rate_rps), route_model,
+                                   dptr, best.ctypes.data, ctypes.byref(counts),
+                                   _stream_handle(stream, plan.device)), plan)
+    del keep
+    return best, {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}
 
 
 # ---- NEXT-2: three pools ----------------------------------------------------------------

@@ -138,6 +138,10 @@ cudaError_t route_occupancy(int block, int *per_sm);
 // FP_FLAG_SPECULATE: after the full K3 -- if the final split (route) differs
 // from the speculated one (spec), every decision byte is recomputed from
 // L_total (device trace len, decision[i] <-> len[i]) with the final split.
+// the same for raw columns (sweep_and_route_raw): a.decision, a.n, the columns
+// and the estimator fields of `a` are used
+cudaError_t launch_route_verify_raw(const RouteRawArgs &a, const uint32_t *spec, const uint32_t *route,
+                                    const uint32_t *edges, unsigned int *misses, int grid, int block, cudaStream_t s);
 // the routed split {iB, iCS, iCL, ok} from the ranks' gathered best records (sliced grid)
 cudaError_t launch_pick_route(const fp_candidate *recs, int ranks, uint32_t n_models, uint32_t model,
                               const uint32_t *edges, uint32_t n_edges, uint32_t *route, cudaStream_t s);

@@ -785,7 +785,35 @@ __global__ void __launch_bounds__(512) k4_route_verify(const uint32_t *__restric
     dec[i] = (uint8_t)dec_byte(escape_bin(__ldg(len + i), iB, iCS, iCL, edges), iB, iCS, iCL);
 }
 
+// FP_FLAG_SPECULATE, raw columns (sweep_and_route_raw): the same check; a
+// miss re-routes every request from its estimated L_total (Eq. `budget`
+// with the plan's conservative ratios, estimate.cuh -- the trace pass's value)
+__global__ void __launch_bounds__(512) k4_route_verify_raw(RouteRawArgs a, const uint32_t *__restrict__ spec,
+                                                           const uint32_t *__restrict__ route,
+                                                           const uint32_t *__restrict__ edges, unsigned int *misses) {
+  __shared__ double2 cst[kCatTable];
+  setup_cstar(a.calib, a.n_cats, a.gamma, a.c_floor, cst);
+  __syncthreads();
+  asm volatile("griddepcontrol.wait;" ::: "memory");   // the full K3's split (PDL launch)
+  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
+  const uint4 sp = *reinterpret_cast<const uint4 *>(spec);
+  if (!rt.w) return;
+  if (sp.w && sp.x == rt.x && sp.y == rt.y && sp.z == rt.z) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && misses) atomicAdd(misses, 1u);
+  const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
+  const uint64_t S = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += S) {
+    const uint32_t L = estimate_l_total(__ldg(a.body + i), __ldg(a.maxout + i), a.cat[i], cst);
+    a.decision[i] = (uint8_t)dec_byte(escape_bin(L, iB, iCS, iCL, edges), iB, iCS, iCL);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_route_verify_raw(const RouteRawArgs &a, const uint32_t *spec, const uint32_t *route,
+                                    const uint32_t *edges, unsigned int *misses, int grid, int block, cudaStream_t s) {
+  return launch_pdl(k4_route_verify_raw, dim3(grid), dim3(block), 0, s, a, spec, route, edges, misses);
+}
 
 cudaError_t launch_pick_route(const fp_candidate *recs, int ranks, uint32_t n_models, uint32_t model,
                               const uint32_t *edges, uint32_t n_edges, uint32_t *route, cudaStream_t s) {

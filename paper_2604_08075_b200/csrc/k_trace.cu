@@ -496,7 +496,15 @@ void *pick_kernel_bins_w(const Variant &v) {
 
 template <bool PACK>
 void *pick_kernel_bins(const Variant &v) {
-  if (v.raw) return nullptr;
+  if (v.raw) {
+    // raw columns + byte bins / decision bytes (sweep_and_route_raw's
+    // speculative pass): u8 LUT, vector-aligned columns only (raw_vec)
+    if (PACK || v.lutw != 1) return nullptr;
+    if (!v.mass)
+      return v.R == 32 ? kernel_ptr<1, 32, false, false, true, true>() : kernel_ptr<1, 1, false, false, true, true>();
+    if (v.R == 32) return v.split ? kernel_ptr<1, 32, true, true, true, true>() : kernel_ptr<1, 32, false, true, true, true>();
+    return v.split ? kernel_ptr<1, 1, true, true, true, true>() : kernel_ptr<1, 1, false, true, true, true>();
+  }
   if (v.lutw == 1) return pick_kernel_bins_w<1, PACK>(v);
   if (v.lutw == 2 && !PACK) return pick_kernel_bins_w<2, false>(v);
   return nullptr;
@@ -568,6 +576,8 @@ cudaError_t launch_trace(const TraceArgs &a0, int grid, int block, size_t smem, 
       const uint64_t mis = (b & 15u) >> 2, head = mis ? 4 - mis : 0;
       // vector loads need the three columns in the same 16-B phase
       a.raw_vec = ((b & 3u) == 0) && ((m & 15u) == (b & 15u)) && (((k + head) & 3u) == 0);
+      // the scalar raw rounds write no bins: the bin variant needs vector columns
+      if (a.bins_out && !a.raw_vec) return cudaErrorInvalidValue;
     }
     a.n = std::min<uint64_t>(cap, a0.n - off);
     void *args[] = {&a};

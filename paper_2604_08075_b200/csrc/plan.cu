@@ -1155,9 +1155,12 @@ fp_status sweep_thresholds(fp_plan *p, const uint32_t *d_len, uint64_t n_local, 
 
 namespace {
 // FP_FLAG_SPECULATE path of sweep_and_route (preconditions checked by the caller).
+// raw != NULL: the raw-column form (sweep_and_route_raw): *raw is the trace
+// pass's TraceArgs with the columns and estimator set, rr the verify's args.
 fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_local, double rate_rps,
                                   uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
-                                  fp_route_counts *h_counts, cudaStream_t s) {
+                                  fp_route_counts *h_counts, cudaStream_t s, const TraceArgs *raw = nullptr,
+                                  const RouteRawArgs *rr = nullptr) {
   const size_t M = p->models.size();
   if (!p->d_spec) {
     const size_t acc_b = p->copies_elems * 8, best_b = M * sizeof(fp_candidate);
@@ -1177,13 +1180,14 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
   //    6 -> 4 -> 2 stripes: 0.833 -> 0.827 -> 0.823 ms per C5 step, 0 misses each)
   {
     NvtxRange r("fp:K1s sample pass");
-    TraceArgs t = p->ta;
-    t.len = len;
+    TraceArgs t = raw ? *raw : p->ta;
+    t.len = raw ? nullptr : len;
     t.n = n_local;
     t.g_cnt = p->spec_acc;
     t.g_mass = p->spec_acc + p->nbins;
     const int grid = k1_grid_for(p, n_local);
-    const uint64_t stripe = (uint64_t)grid * p->k1_block * 4;        // uint4 per grid step (kUnroll = 4)
+    // uint4 per grid step of k1_trace (kUnroll = 4; raw columns: 2)
+    const uint64_t stripe = (uint64_t)grid * p->k1_block * (raw ? 2 : 4);
     const uint64_t nsteps = (n_local / 4 + stripe - 1) / stripe;
     static const uint64_t stripes = (uint64_t)std::max(1, env_int("FP_SPEC_STRIPES", 4));
     t.step_stride = (uint32_t)std::max<uint64_t>(1, nsteps / stripes);
@@ -1219,8 +1223,16 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
   // (ranks that split the grid: the final split is picked after the all-gather)
   uint32_t *route = reinterpret_cast<uint32_t *>(p->d_rcounts);
   const bool sliced = p->dist && !(p->flags & FP_FLAG_REPLICATED_GRID);
-  fp_status st = sweep_impl(p, len, n_local, rate_rps, nullptr, s, nullptr, nullptr, d_decision,
-                            sliced ? nullptr : route, route_model, nullptr, nullptr, p->spec_route, p->spec_acc);
+  TraceArgs traw;
+  if (raw) {                                 // the raw branch of sweep_impl takes the decision output here
+    traw = *raw;
+    traw.bins_out = d_decision;
+    traw.dec_route = p->spec_route;
+    traw.pdl = 1;
+  }
+  fp_status st = sweep_impl(p, raw ? nullptr : len, n_local, rate_rps, nullptr, s, nullptr, raw ? &traw : nullptr,
+                            d_decision, sliced ? nullptr : route, route_model, nullptr, nullptr, p->spec_route,
+                            p->spec_acc);
   if (st != FP_OK) return st;
   p->spec_dirty = false;                    // the full K3 zeroes the sample's accumulators
   if (sliced) {
@@ -1233,8 +1245,10 @@ fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_lo
   {
     NvtxRange r("fp:K4v verify");
     LaunchTimer lt(p, FP_KERNEL_ROUTE, s);
-    cudaError_t e = launch_route_verify(len, d_decision, n_local, p->spec_route, route, p->ta.edges, p->spec_miss,
-                                        p->k4_grid, p->k4_block, s);
+    cudaError_t e = raw ? launch_route_verify_raw(*rr, p->spec_route, route, p->ta.edges, p->spec_miss, p->k4_grid,
+                                                  p->k4_block, s)
+                        : launch_route_verify(len, d_decision, n_local, p->spec_route, route, p->ta.edges,
+                                              p->spec_miss, p->k4_grid, p->k4_block, s);
     if (e != cudaSuccess) return cuda_fail(p, e, "verify launch");
     ++p->launches;
   }
@@ -1439,6 +1453,66 @@ fp_status sweep_thresholds_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_loc
   a.gamma = est->gamma;
   a.c_floor = est->c_floor;
   return sweep_impl(p, nullptr, n_local, rate_rps, h_results, stream, nullptr, &a);
+}
+
+fp_status sweep_and_route_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, const fp_estimator *est,
+                              double rate_rps, uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
+                              fp_route_counts *h_counts, void *stream) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  fp_status st = check_raw(p, t, n_local, false);
+  if (st != FP_OK) return st;
+  if (route_model >= p->models.size()) return fail(p, FP_ERR_INVALID_ARG, "route_model out of range");
+  if (d_decision && n_local && is_host_pointer(d_decision))
+    return fail(p, FP_ERR_INVALID_ARG, "d_decision must be device memory");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // speculative form: the columns and the decision buffer in the trace pass's
+  // vector phase (k1_trace raw_vec; bins + i in the 4-B phase of body + i)
+  const uintptr_t b = reinterpret_cast<uintptr_t>(t->body_bytes), m = reinterpret_cast<uintptr_t>(t->max_output_tokens),
+                  k = reinterpret_cast<uintptr_t>(t->category);
+  const uint64_t head = ((b & 15u) >> 2) ? 4 - ((b & 15u) >> 2) : 0;
+  const bool vec = ((b & 3u) == 0) && ((m & 15u) == (b & 15u)) && (((k + head) & 3u) == 0);
+  const bool spec = (p->flags & FP_FLAG_SPECULATE) && d_decision && n_local >= (1ull << 26) && vec &&
+                    p->lut_cells && p->lut_u8 && p->nbins <= 127 && p->k3a.shape == kK3Cluster &&
+                    (reinterpret_cast<uintptr_t>(d_decision + head) & 3u) == 0;
+  if (!spec) {
+    // sweep, argmin on the host, route with the split
+    st = sweep_thresholds_raw(p, t, n_local, est, rate_rps, nullptr, stream);
+    if (st != FP_OK) return st;
+    std::vector<fp_candidate> best(p->models.size());
+    st = best_split(p, best.data());
+    if (st != FP_OK) return st;
+    if (h_best) memcpy(h_best, best.data(), best.size() * sizeof(fp_candidate));
+    const fp_candidate &c = best[route_model];
+    if (!(c.flags & FP_CAND_FEASIBLE))
+      return fail(p, FP_ERR_STATE, "model %u has no feasible split to route with", route_model);
+    return route_batch_raw(p, t, n_local, est, c.b_short, c.c_short, c.c_long, d_decision, nullptr, h_counts, nullptr,
+                           stream);
+  }
+  st = upload_estimator(p, est, s);
+  if (st != FP_OK) return st;
+  TraceArgs a = p->ta;
+  a.len = nullptr;
+  a.n = n_local;
+  a.body = t->body_bytes;
+  a.maxout = t->max_output_tokens;
+  a.cat = t->category;
+  a.calib = p->d_calib;
+  a.n_cats = est->n_cats;
+  a.gamma = est->gamma;
+  a.c_floor = est->c_floor;
+  RouteRawArgs rr{};
+  rr.body = t->body_bytes;
+  rr.maxout = t->max_output_tokens;
+  rr.cat = t->category;
+  rr.calib = p->d_calib;
+  rr.n_cats = est->n_cats;
+  rr.gamma = est->gamma;
+  rr.c_floor = est->c_floor;
+  rr.decision = d_decision;
+  rr.n = n_local;
+  return sweep_route_speculative(p, nullptr, n_local, rate_rps, route_model, d_decision, h_best, h_counts, s, &a,
+                                 &rr);
 }
 
 fp_status route_batch_raw(fp_plan *p, const fp_raw_trace *t, uint64_t n_local, const fp_estimator *est,

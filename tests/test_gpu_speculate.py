@@ -42,13 +42,14 @@ def _check_step(cfg, L, plan, dec, best, counts):
     assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
 
 
-def _sampled_stripes(plan, n):
+def _sampled_stripes(plan, n, per_thread=4):
     """The request ranges the sample pass reads (white box: grid-wide stripes of
-    the trace pass, every stride-th of them)."""
+    the trace pass, every stride-th of them; per_thread = uint4 per thread per
+    step: 4, raw columns 2)."""
     info = fp.fleet_plan_info(plan)
     S = info["k1_grid"] * info["k1_block"]
-    stripe = S * 4 * 4                                   # requests per grid step (4 uint4 per thread)
-    nsteps = (n // 4 + S * 4 - 1) // (S * 4)
+    stripe = S * per_thread * 4                          # requests per grid step
+    nsteps = (n // 4 + S * per_thread - 1) // (S * per_thread)
     stride = max(1, nsteps // 4)
     return [(k * stripe, min(n, (k + 1) * stripe)) for k in range(0, nsteps, stride)]
 
@@ -104,3 +105,54 @@ def test_speculative_fallbacks_and_models(case):
     assert np.array_equal(dec.cpu().numpy(), odec)
     expect_spec = case == "route_model_1"
     assert fp.fleet_plan_info(plan)["spec_calls"] == (1 if expect_spec else 0)
+
+
+# ---- the raw-column form (sweep_and_route_raw, NEXT-1) --------------------------------------
+CALIB = [(4.39, 0.45), (3.45, 0.35), (1.97, 0.2), (3.73, 0.38)]   # a calibrated snapshot (stated)
+
+
+def _raw_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32) if a.dtype == np.uint32 else a).cuda()
+
+
+def _raw_check(cfg, body, mo, cat, cats, dec, best, counts, model=0):
+    L = oracle.estimate(body, mo, cat, cats, 1.0, 0.5)
+    _, obest = oracle.sweep(cfg, L, want_all=False)
+    assert best.tobytes() == obest.tobytes()
+    b = obest[model]
+    odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
+    assert np.array_equal(dec[:L.size].cpu().numpy(), odec)
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
+
+
+@pytest.mark.parametrize("flags,n,expect_spec", [("spec", N, True), ("plain", 700_001, False),
+                                                 ("spec", 700_001, False)])
+def test_raw_step_matches_oracle(flags, n, expect_spec):
+    from synth.gen import generate_raw_host
+    cfg = configs.c5().with_n(n)
+    body, mo, cat, _ = generate_raw_host(cfg.shape, cfg.seed, 0, n)
+    plan = _plan(cfg, flags=fp.FP_FLAG_SPECULATE if flags == "spec" else 0)
+    dec = torch.full((n,), 0xEE, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route_raw(plan, _raw_dev(body), _raw_dev(mo), _raw_dev(cat), CALIB, cfg.rate_rps,
+                                          route_model=0, decision=dec)
+    _raw_check(cfg, body, mo, cat, CALIB, dec, best, counts)
+    assert (fp.fleet_plan_info(plan)["spec_calls"] == 1) == expect_spec
+
+
+def test_raw_step_forced_miss():
+    """Sampled stripes of tiny bodies: the sample's split is not the trace's, and
+    the verify kernel re-routes every request from its estimated L_total."""
+    from synth.gen import generate_raw_host
+    cfg = configs.c5().with_n(N)
+    body, mo, cat, _ = generate_raw_host(cfg.shape, cfg.seed, 0, N)
+    body, mo = body.copy(), mo.copy()
+    plan = _plan(cfg)
+    for lo, hi in _sampled_stripes(plan, N, per_thread=2):
+        body[lo:hi] = 10
+        mo[lo:hi] = 1
+    dec = torch.full((N,), 0xEE, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route_raw(plan, _raw_dev(body), _raw_dev(mo), _raw_dev(cat), CALIB, cfg.rate_rps,
+                                          route_model=0, decision=dec)
+    _raw_check(cfg, body, mo, cat, CALIB, dec, best, counts)
+    info = fp.fleet_plan_info(plan)
+    assert info["spec_calls"] == 1 and info["spec_misses"] == 1
