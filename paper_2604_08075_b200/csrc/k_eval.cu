@@ -427,6 +427,10 @@ __device__ __forceinline__ void phase(const EvalArgs &a, int i) {
 // before this sweep's trace pass started: the trace pass is a plain launch).
 __device__ void prologue(const EvalArgs &a, Tab &T, uint32_t m, bool first, unsigned long long *warp_tot) {
   phase(a, 0);
+  // the next kernel (K4p / K4b / K4v, or the speculative full trace pass) may be
+  // scheduled now: each of them waits (griddepcontrol.wait) before it reads
+  // anything this kernel writes
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   load_plan_tables(a, T, m);
   if (first && a.zero_copies) {
     for (size_t i = threadIdx.x; i < a.zero_elems; i += blockDim.x) a.zero_copies[i] = 0ull;
