@@ -499,6 +499,19 @@ cudaError_t launch_route_raw(const RouteRawArgs &a, int grid, int block, cudaStr
 namespace fp {
 namespace {
 
+// A split {iB, iCS, iCL, ok} written by the predecessor kernel (K3 / the pick
+// kernel), read after griddepcontrol.wait. A programmatic dependent starts
+// while its predecessor still runs, so this must be a coherent load that the
+// compiler cannot hoist above the wait: a const __restrict__ (ld.global.nc,
+// "invariant") load was moved above it and read a stale split
+// (test_raw_step_forced_miss caught it once K3 triggered its dependents early).
+__device__ __forceinline__ uint4 ld_split(const uint32_t *p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p)
+               : "memory");
+  return r;
+}
+
 __device__ __forceinline__ uint32_t dec_byte(uint32_t b, uint32_t iB, uint32_t iCS, uint32_t iCL) {
   return (b > iB ? 1u : 0u) + (b > iCS ? 4u : 0u) + (b > iCL ? 9u : 0u);
 }
@@ -630,10 +643,10 @@ __device__ __noinline__ uint4 fix_escapes(uint4 v, uint4 o, const uint32_t *len,
 
 template <bool VEC, bool SWAR>
 __global__ void __launch_bounds__(512) k4_route_bins(const uint8_t *__restrict__ bins, uint8_t *__restrict__ dec,
-                                                      uint64_t n, const uint32_t *__restrict__ route,
+                                                      uint64_t n, const uint32_t *route,
                                                       const uint32_t *__restrict__ len, const uint32_t *__restrict__ edges) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // K3's split (PDL launch)
-  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
+  const uint4 rt = ld_split(route);
   if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
   const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
   const bool esc = len && iCL >= 255u;      // iB <= iCS <= iCL
@@ -701,9 +714,9 @@ template <bool VEC>
 __global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long *__restrict__ lo,
                                                        const uint32_t *__restrict__ hi,
                                                        const uint8_t *__restrict__ side, uint8_t *__restrict__ dec,
-                                                       uint64_t n, uint32_t head, const uint32_t *__restrict__ route) {
+                                                       uint64_t n, uint32_t head, const uint32_t *route) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // K3's split (PDL launch)
-  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
+  const uint4 rt = ld_split(route);
   if (!rt.w) return;                        // no feasible split: nothing to route (the host reports it)
   const uint32_t iB = rt.x, iCS = rt.y, iCL = rt.z;
   const SwarK sk{(0x7Fu - (iB < 0x7Fu ? iB : 0x7Fu)) * 0x01010101u, (0x7Fu - (iCS < 0x7Fu ? iCS : 0x7Fu)) * 0x01010101u,
@@ -770,12 +783,12 @@ __global__ void __launch_bounds__(512) k4_route_packed(const unsigned long long 
 // every request is re-routed from L_total with the final split (escape_bin's
 // stand-in bin has the same order relations to iB <= iCS <= iCL as the bin).
 __global__ void __launch_bounds__(512) k4_route_verify(const uint32_t *__restrict__ len, uint8_t *__restrict__ dec,
-                                                       uint64_t n, const uint32_t *__restrict__ spec,
-                                                       const uint32_t *__restrict__ route,
+                                                       uint64_t n, const uint32_t *spec,
+                                                       const uint32_t *route,
                                                        const uint32_t *__restrict__ edges, unsigned int *misses) {
   asm volatile("griddepcontrol.wait;" ::: "memory");   // the full K3's split (PDL launch)
-  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
-  const uint4 sp = *reinterpret_cast<const uint4 *>(spec);
+  const uint4 rt = ld_split(route);
+  const uint4 sp = ld_split(spec);
   if (!rt.w) return;                           // no feasible split: decisions unspecified (header)
   if (sp.w && sp.x == rt.x && sp.y == rt.y && sp.z == rt.z) return;
   if (blockIdx.x == 0 && threadIdx.x == 0 && misses) atomicAdd(misses, 1u);
@@ -788,15 +801,15 @@ __global__ void __launch_bounds__(512) k4_route_verify(const uint32_t *__restric
 // FP_FLAG_SPECULATE, raw columns (sweep_and_route_raw): the same check; a
 // miss re-routes every request from its estimated L_total (Eq. `budget`
 // with the plan's conservative ratios, estimate.cuh -- the trace pass's value)
-__global__ void __launch_bounds__(512) k4_route_verify_raw(RouteRawArgs a, const uint32_t *__restrict__ spec,
-                                                           const uint32_t *__restrict__ route,
+__global__ void __launch_bounds__(512) k4_route_verify_raw(RouteRawArgs a, const uint32_t *spec,
+                                                           const uint32_t *route,
                                                            const uint32_t *__restrict__ edges, unsigned int *misses) {
   __shared__ double2 cst[kCatTable];
   setup_cstar(a.calib, a.n_cats, a.gamma, a.c_floor, cst);
   __syncthreads();
   asm volatile("griddepcontrol.wait;" ::: "memory");   // the full K3's split (PDL launch)
-  const uint4 rt = *reinterpret_cast<const uint4 *>(route);
-  const uint4 sp = *reinterpret_cast<const uint4 *>(spec);
+  const uint4 rt = ld_split(route);
+  const uint4 sp = ld_split(spec);
   if (!rt.w) return;
   if (sp.w && sp.x == rt.x && sp.y == rt.y && sp.z == rt.z) return;
   if (blockIdx.x == 0 && threadIdx.x == 0 && misses) atomicAdd(misses, 1u);

@@ -121,7 +121,11 @@ def _raw_check(cfg, body, mo, cat, cats, dec, best, counts, model=0):
     assert best.tobytes() == obest.tobytes()
     b = obest[model]
     odec, oc = oracle.route_batch(L, int(b["b_short"]), int(b["c_short"]), int(b["c_long"]))
-    assert np.array_equal(dec[:L.size].cpu().numpy(), odec)
+    got = dec[:L.size].cpu().numpy()
+    if not np.array_equal(got, odec):
+        bad = np.nonzero(got != odec)[0]
+        raise AssertionError(f"{bad.size} decisions differ, first at {bad[:5]}: got {got[bad[:5]]} "
+                             f"expected {odec[bad[:5]]} (L {L[bad[:5]]})")
     assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == [int(x) for x in oc]
 
 
