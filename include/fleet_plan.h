@@ -291,6 +291,8 @@ fp_status best_split(fp_plan *plan, fp_candidate *h_best);
  * holds with clamped bins (min(bin, 255)): the routing pass reads `len` back
  * for requests whose byte is 255 when the split has an edge index >= 255, so
  * `len` must stay unchanged until the call's work has completed on `stream`.
+ * With FP_FLAG_SPECULATE (see the flag) the speculative form runs instead
+ * where its preconditions hold: the same outputs from one full trace pass.
  * Synchronizes -- except in that bin mode with a device trace when h_best and
  * h_counts are both NULL: then the call is stream-ordered and asynchronous,
  * the records stay on the device for a later best_split, and a model without
