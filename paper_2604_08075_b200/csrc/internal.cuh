@@ -296,23 +296,36 @@ struct CalibArgs {
   unsigned long long *snap_block;   // [n_cats] (~0: no snapshot)
   bool vec_bt, vec_c;               // 16-B aligned columns: vector loads
 };
-// one-rank single-pass replay (k_calib.cu c_single): tiles of 4,096 records
-// in ticket order, decoupled look-back over tiles
-struct CalibTileArgs {
+// one rank, n_cats <= 4: the streaming replay (k_calib.cu c_stream), every
+// record read once; a persistent cooperative grid of G CTAs, chunks of G pieces
+struct CalibStreamArgs {
   const uint32_t *bytes, *tokens;
   const uint8_t *cat;
-  uint64_t n, n_tiles;
-  uint32_t n_cats;                  // <= 16
+  uint64_t n;
+  uint32_t n_cats;                  // <= 4
   double beta;
-  const double *c0, *s0;            // device [n_cats] initial state
-  unsigned int *ticket;             // [1] tile ticket (zeroed before the launch)
-  unsigned int *cflag, *sflag;      // [n_tiles] look-back flags (zeroed before the launch)
-  void *cdesc, *sdesc;              // [n_tiles][2][NC] published affine maps (k_calib.cu Aff, 24 B)
+  const double *c0, *s0;            // device [4] initial state
+  uint32_t G, n_chunks;             // CTAs (<= 512), chunks of G pieces of calib_stream_piece() records
+  unsigned int *done, *ready;       // [n_chunks] finished-A counters, [n_chunks + 1] chunk-start flags (zeroed)
+  void *cagg;                       // [n_chunks][G][4] piece c_hat maps (k_calib.cu Aff, 24 B)
+  double *pstate_c;                 // [n_chunks][G][4] c_hat at each piece's start
+  unsigned long long *pstate_n;     // [n_chunks][G][4] observations before each piece
+  double *cstart_c;                 // [n_chunks + 1][4] c_hat at each chunk's start (last: final)
+  unsigned long long *cstart_n;     // [n_chunks + 1][4]
+  double *sig_a, *sig_b;            // [n_chunks * G][4] piece sigma maps
+  unsigned long long *snap_piece;   // [4] piece holding the snap_at-th observation (~0: none; preset)
+  double *snap_v;                   // [4][4] sigma map piece start -> snapshot (a, b), snapshot c_hat
+  void *fin_part, *fin_pre;         // c_stream_final: [4][fin_blocks] range maps, [4] snapshot range prefix (Aff)
+  unsigned int *fin_done, *fin_snapb;   // [4] block counters (zeroed), [4] block holding the snapshot
   uint64_t snap_at;
   double *out;                      // [80]: c_hat[16], sigma[16], n_obs[16] (u64), snap_c[16], snap_s[16]
+  unsigned long long *prof;         // FP_CALIB_PROFILE: [2 n_chunks + 2][8] phase stamps (nullptr: off)
 };
-uint64_t calib_tiles(uint64_t n);
-cudaError_t launch_calib_tile(const CalibTileArgs &a, int sm_count, cudaStream_t s);
+size_t calib_stream_smem();
+uint32_t calib_stream_piece();
+uint32_t calib_stream_fin_blocks();
+int calib_stream_blocks_per_sm();
+cudaError_t launch_calib_stream(const CalibStreamArgs &a, cudaStream_t s);
 size_t calib_scratch_bytes(uint64_t blocks, uint32_t n_cats);
 int calib_blocks_per_sm(uint32_t n_cats);
 cudaError_t launch_calibrate(CalibArgs a, cudaStream_t s);        // C1 C2 C3 C2 C4 (one rank)

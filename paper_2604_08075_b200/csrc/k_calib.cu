@@ -550,366 +550,480 @@ __global__ void c4_snap(CalibArgs a) {
 
 
 // ============================================================================
-// One rank, single pass: every record is read from HBM once.
+// One rank, n_cats <= 4: the streaming replay (c_stream) -- every record is
+// read from HBM once and its c_obs computed once.
 //
-// The stream is cut into tiles of 4,096 records taken in order by a ticket.
-// A block stages its tile in shared memory as c_obs (fp64; dropped feedback
-// has no category) and lists, per category, the positions of its
-// observations in tile order (ballot masks, popcount ranks): a category's
-// observations are then read through that list without per-record category
-// dispatch. The block's 256 threads form per-category worker groups in
-// proportion to the category counts (balanced for any mix); worker j of
-// category k owns the j-th slice of k's list.
-//   pass A  each worker composes the c_hat maps (Eq. `ema`) of its slice; a
-//           scan inside each group gives every worker its exclusive map and
-//           the tile's per-category aggregate
-//   look-back (decoupled single-pass scan over tiles; block-wide: 256
-//           predecessors per round) -> the tile's exact exclusive prefix
-//   pass B  each worker replays its slice from its exact start state (tile
-//           prefix, then group prefix, applied to c_0) -- the sequential
-//           update -- which yields c_hat(before) for every observation and so
-//           the sigma maps (R26); the snapshot at the snap_at-th observation;
-//           group scan and a second look-back for sigma
-// The last tile writes the final state. Reassociation: within 1e-12 of the
-// sequential oracle, like the multi-rank kernels above.
+// A persistent grid of G co-resident CTAs (cooperative launch) walks the
+// stream in chunks of G pieces of 3,584 records; CTA c owns piece c of every
+// chunk. Iteration i of a CTA runs phase A on chunk i, then phase C on chunk
+// i - 2, whose piece is still in the CTA's shared memory (a ring of three):
+// the lag of two leaves a whole iteration for chunk i - 2's scan to land.
+//   A  each warp loads a region of 448 records (coalesced 128-B column loads),
+//      ranks every valid record inside its category with three ballots
+//      (valid, category bit 0, bit 1), and stores c_obs in category order --
+//      each category's run starting on a 16-slot boundary, so lane l's 16
+//      slots hold one category only. Each lane composes the c_hat maps of its
+//      slots (Horner, one FMA per observation: no per-record category
+//      dispatch); a segmented warp scan (lanes of one category are adjacent)
+//      gives every lane its exclusive map in the region and the region
+//      aggregates; 4 threads compose the 8 regions into the piece aggregate.
+//      The CTA that finishes chunk i last (atomic count) scans the chunk's G
+//      piece aggregates, takes the chunk's start state from chunk i - 1's
+//      scanner (flag), and publishes every piece's start state and the next
+//      chunk's (flag) -- the only cross-CTA step on the path, once per chunk.
+//   C  waits for its chunk's flag, then every lane replays its slots from the
+//      exact start state (piece start, region map, lane map): c_hat(before)
+//      for each observation and so the sigma maps (R26), the snap_at-th
+//      observation's state; a segmented warp scan and 4 threads compose the
+//      piece's sigma map (global, [piece][k]).
+// c_stream_final composes the sigma piece maps in stream order and writes the
+// final state and the snapshots.
+// Reassociation: within 1e-12 of the sequential oracle like the kernels above.
+// Opt-in (FP_CALIB_STREAM=1): it reads exactly 9 B/record from HBM (ncu), but
+// each iteration is a chain of latencies -- the column loads (~2 us), the
+// fence and chunk counter, the scanner's hand-off -- that two CTAs per SM
+// (the shared-memory ring of three pieces allows no more) cannot hide: A 6.0,
+// C 2.2, waiting 10.7 us per iteration, 17.5 ms per 1e9 records against the
+// two-pass kernels' 4.7 ms (FP_CALIB_PROFILE=1 prints the phase stamps;
+// profiles/r02/next3_stream_profile.log).
 // ============================================================================
-constexpr uint32_t kTileRecs = 4096;
-constexpr uint32_t kTileWords = kTileRecs / 32;
-constexpr uint32_t kTileThreads = 256;
-constexpr uint32_t kTileWarps = kTileThreads / 32;
+constexpr int kSW = 8;                         // warps per CTA
+constexpr int kSThreads = kSW * 32;
+constexpr int kSWords = 14;                    // 32-record words per warp region
+constexpr int kSRegion = kSWords * 32;         // 448 records
+constexpr int kSSlots = 512;                   // sorted slots per region: 16 per lane (<= 448 + 4 x 15 used)
+constexpr int kSLag = 2;                       // iteration i: phase A of chunk i, phase C of chunk i - kSLag
+constexpr int kSRing = kSLag + 1;              // pieces held in shared memory
+constexpr int kSBeta = kSRegion + 1;           // beta^j, 0 <= j <= 448 (compositions inside a region)
+constexpr uint32_t kIdle = 7u;                 // lane category of an empty lane
+constexpr uint32_t kFinBlocks = 148;           // c_stream_final blocks per category (<= 256)
 
-template <int NC>
-struct TileLayout {
-  static constexpr size_t o = 0;                                          // double [4096]
-  static constexpr size_t mask = o + kTileRecs * 8;                       // u32 [NC][128]
-  static constexpr size_t wpre = mask + (size_t)NC * kTileWords * 4;      // u32 [NC][129]
-  static constexpr size_t pos = wpre + (size_t)NC * (kTileWords + 1) * 4; // u16 [4096]
-  static constexpr size_t cat = pos + kTileRecs * 2;                      // u8 [4096] (0xFF: dropped)
-  static constexpr size_t wmap = (cat + kTileRecs + 15) & ~size_t(15);    // Aff [256]
-  static constexpr size_t bytes = wmap + kTileThreads * sizeof(Aff);
+struct SLayout {
+  static constexpr size_t sorted = 0;                                             // double [ring][w][512]
+  static constexpr size_t lane_b = sorted + (size_t)kSRing * kSW * kSSlots * 8;   // double [ring][w][32]
+  static constexpr size_t lane_m = lane_b + (size_t)kSRing * kSW * 32 * 8;        // u32 [ring][w][32]
+  static constexpr size_t rex = lane_m + (size_t)kSRing * kSW * 32 * 4;           // Aff [ring][w][4]
+  static constexpr size_t bpow = rex + (size_t)kSRing * kSW * 4 * sizeof(Aff);    // double [513]
+  static constexpr size_t bytes = bpow + (size_t)kSBeta * 8;
 };
 
-__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ Aff ld_aff(const Aff *p) {
   return Aff{__ldcg(&p->a), __ldcg(&p->b), __ldcg(&p->n)};
 }
-
-// Per-category exclusive scan of the worker maps wm[g0 .. g0 + P) of each
-// group (one warp per group); the group total -> tot[k].
-__device__ void group_scan(Aff *wm, const uint32_t *gstart, uint32_t n_cats, Aff *tot) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (uint32_t k = warp; k < n_cats; k += kTileWarps) {
-    const uint32_t g0 = gstart[k], P = gstart[k + 1] - g0;
-    const uint32_t q = (P + 31) / 32, lo = min(P, lane * q), hi = min(P, lo + q);
-    Aff run = aff_id();
-    for (uint32_t i = lo; i < hi; ++i) run = compose(run, wm[g0 + i]);
-    const Aff inc = warp_inclusive(run, lane);
-    Aff cur = shfl_up(inc, 1);
-    if (lane == 0) cur = aff_id();
-    for (uint32_t i = lo; i < hi; ++i) {
-      const Aff x = wm[g0 + i];
-      wm[g0 + i] = cur;
-      cur = compose(cur, x);
-    }
-    if (lane == 31) tot[k] = inc;
-  }
+__device__ __forceinline__ void st_release(unsigned int *p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-
-template <int NC>
-struct TileSm {                           // static shared state of one tile
-  Aff tot[NC], excl[NC], sexcl[NC], part[NC];
-  Aff red[NC][kTileWarps];                // look-back: per-warp partial compositions
-  double snapv[NC];
-  uint32_t gstart[NC + 1], cbase[NC + 1], snap_w[NC];
-  uint32_t tile, last[2];
-};
-
-struct TileBuf {
-  double *o;
-  uint32_t *mask, *wpre;
-  uint16_t *pos;
-  uint8_t *cat;
-  Aff *wm;
-};
-
-template <int NC>
-__device__ __forceinline__ TileBuf tile_buf(unsigned char *smem) {
-  using L = TileLayout<NC>;
-  return TileBuf{reinterpret_cast<double *>(smem + L::o), reinterpret_cast<uint32_t *>(smem + L::mask),
-                 reinterpret_cast<uint32_t *>(smem + L::wpre), reinterpret_cast<uint16_t *>(smem + L::pos),
-                 reinterpret_cast<uint8_t *>(smem + L::cat), reinterpret_cast<Aff *>(smem + L::wmap)};
-}
-
-// Stage tile `tile`: c_obs and categories, masks, per-category word prefixes,
-// worker groups, per-category position lists. Returns this thread's slice
-// [r0, r1) of category kw's list (kw == n_cats: no work).
-template <int NC>
-__device__ void stage_tile(const CalibTileArgs &a, const TileBuf &X, TileSm<NC> &S, uint32_t tile, uint32_t &kw,
-                           uint32_t &r0, uint32_t &r1) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t nc = a.n_cats, last_cat = nc - 1;
-  const uint64_t base = (uint64_t)tile * kTileRecs;
-  // warp w stages words 16 w .. 16 w + 15 (coalesced 128-B column loads per word)
-#pragma unroll 1
-  for (uint32_t i0 = 0; i0 < 16; i0 += 4) {
-    uint32_t vb[4], vt[4], vc[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint64_t i = base + (uint64_t)(warp * 16 + i0 + u) * 32 + lane;
-      const bool in = i < a.n;
-      vb[u] = in ? __ldcs(a.bytes + i) : 0u;
-      vt[u] = in ? __ldcs(a.tokens + i) : 0u;
-      vc[u] = in ? (uint32_t)__ldcs(a.cat + i) : 0u;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const uint32_t word = warp * 16 + i0 + u, r = word * 32 + lane;
-      const bool valid = vt[u] != 0u;                           // zero-token feedback is dropped
-      const uint32_t k = vc[u] < last_cat ? vc[u] : last_cat;   // R23
-      X.o[r] = ratio(vb[u], vt[u] | (vt[u] == 0u));
-      X.cat[r] = valid ? (uint8_t)k : (uint8_t)0xFF;
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        if (j < (int)nc) {
-          const unsigned mk = __ballot_sync(0xffffffffu, valid && k == (uint32_t)j);
-          if (lane == (uint32_t)j) X.mask[j * kTileWords + word] = mk;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  // per category: exclusive prefix of the observation counts over words
-  for (uint32_t k = warp; k < nc; k += kTileWarps) {
-    const uint32_t *mk = X.mask + k * kTileWords;
-    uint32_t c[4], run = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { c[u] = __popc(mk[lane * 4 + u]); run += c[u]; }
-    uint32_t inc = run;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, off);
-      if (lane >= (uint32_t)off) inc += y;
-    }
-    uint32_t ex = inc - run;
-    uint32_t *wp = X.wpre + k * (kTileWords + 1);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) { wp[lane * 4 + u] = ex; ex += c[u]; }
-    if (lane == 31) wp[kTileWords] = inc;
-  }
-  __syncthreads();
-  // list offsets and worker groups in proportion to the category counts
-  if (threadIdx.x == 0) {
-    uint32_t total = 0, nonempty = 0, big = 0, bigc = 0;
-    for (uint32_t k = 0; k < nc; ++k) {
-      const uint32_t ck = X.wpre[k * (kTileWords + 1) + kTileWords];
-      S.cbase[k] = total;
-      total += ck;
-      nonempty += ck ? 1u : 0u;
-      if (ck > bigc) { big = k; bigc = ck; }
-    }
-    S.cbase[nc] = total;
-    uint32_t used = 0;
-    for (uint32_t k = 0; k < nc; ++k) {
-      const uint32_t ck = X.wpre[k * (kTileWords + 1) + kTileWords];
-      used += ck ? 1u + (uint32_t)((uint64_t)ck * (kTileThreads - nonempty) / total) : 0u;
-    }
-    const uint32_t extra = total ? kTileThreads - used : 0u;
-    uint32_t g0 = 0;
-    for (uint32_t k = 0; k < nc; ++k) {
-      const uint32_t ck = X.wpre[k * (kTileWords + 1) + kTileWords];
-      S.gstart[k] = g0;
-      g0 += (ck ? 1u + (uint32_t)((uint64_t)ck * (kTileThreads - nonempty) / total) : 0u) + (k == big ? extra : 0u);
-    }
-    S.gstart[nc] = g0;
-  }
-  __syncthreads();
-  // position lists: record r of category k -> pos[cbase[k] + rank of r in k]
-#pragma unroll 4
-  for (uint32_t i = 0; i < 16; ++i) {
-    const uint32_t word = warp * 16 + i, r = word * 32 + lane;
-    const uint32_t k = X.cat[r];
-    if (k != 0xFFu) {
-      const uint32_t below = X.mask[k * kTileWords + word] & ((1u << lane) - 1u);
-      X.pos[S.cbase[k] + X.wpre[k * (kTileWords + 1) + word] + __popc(below)] = (uint16_t)r;
-    }
-  }
-  kw = 0;
-  while (kw < nc && S.gstart[kw + 1] <= threadIdx.x) ++kw;
-  r0 = r1 = 0;
-  if (kw < nc) {
-    const uint32_t P = S.gstart[kw + 1] - S.gstart[kw], j = threadIdx.x - S.gstart[kw];
-    const uint32_t ck = S.cbase[kw + 1] - S.cbase[kw];
-    r0 = S.cbase[kw] + ck * j / P;
-    r1 = S.cbase[kw] + ck * (j + 1) / P;
-  }
-  __syncthreads();
-}
-
-// Decoupled look-back over the whole block (one predecessor per thread, 256
-// per round): publish this tile's aggregates (flag 1), compose the
-// predecessors' aggregates / inclusive prefixes into the exclusive prefix
-// excl[k], publish the inclusive prefix (flag 2). A round covers 256 tiles,
-// so the walk back to the nearest inclusive prefix stays about one round deep
-// at the stream's tile rate. Flags are polled relaxed (no L1 invalidation per
-// poll); one fence after they are seen orders the map reads.
-// desc: [tile][2 (aggregate, inclusive)][NC] maps.
-template <int NC>
-__device__ void look_back_block(uint32_t tile, uint32_t n_cats, unsigned int *flags, Aff *desc, const Aff *agg,
-                                Aff *excl, TileSm<NC> &S) {
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Aff *mine = desc + (size_t)tile * 2 * NC;
-  if (threadIdx.x < n_cats) {
-    mine[threadIdx.x] = agg[threadIdx.x];
-    if (tile == 0) mine[NC + threadIdx.x] = agg[threadIdx.x];
-    excl[threadIdx.x] = aff_id();
-  }
-  if (threadIdx.x == 0) { S.last[0] = 0xffffffffu; S.last[1] = 0u; }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) st_release(flags + tile, tile == 0 ? 2u : 1u);
-  if (tile == 0) return;
-  int64_t top = (int64_t)tile - 1;
+__device__ __forceinline__ void wait_flag(const unsigned int *p) {
+  unsigned int f;
   for (;;) {
-    const int64_t p = top - (int64_t)threadIdx.x;
-    unsigned int f = 0;
-    if (p >= 0) {
-      for (;;) {
-        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flags + p) : "memory");
-        if (f) break;
-        __nanosleep(20);
-      }
-    }
-    __threadfence();                     // acquire: the maps published before the flag
-    // the nearest predecessor with an inclusive prefix (lowest thread), else the oldest valid one
-    const unsigned inc_w = __ballot_sync(0xffffffffu, p >= 0 && f == 2u);
-    const unsigned val_w = __ballot_sync(0xffffffffu, p >= 0);
-    if (lane == 0 && inc_w) atomicMin(&S.last[0], warp * 32 + (uint32_t)__ffs(inc_w) - 1);
-    if (lane == 0 && val_w) atomicMax(&S.last[1], warp * 32 + 31 - (uint32_t)__clz(val_w));
-    __syncthreads();
-    const bool found = S.last[0] != 0xffffffffu;
-    const uint32_t last = found ? S.last[0] : S.last[1];
-    // every category at once: warp-ordered reductions, then one thread per category
-    for (uint32_t k = 0; k < n_cats; ++k) {
-      Aff x = aff_id();
-      if (threadIdx.x <= last)
-        x = ld_aff(desc + ((size_t)p * 2 + ((threadIdx.x == last && f == 2u) ? 1 : 0)) * NC + k);
-      // older predecessors (higher threads) are applied first
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(p) : "memory");
+    if (f) return;
+    __nanosleep(32);
+  }
+}
+
+// physical slot of sorted slot s: lane chunk l = s / 16 owns 8 16-B units,
+// swizzled by l & 7 so that lanes reading their own unit u hit distinct banks
+__device__ __forceinline__ uint32_t sslot(uint32_t s) {
+  const uint32_t l = s >> 4;
+  return (l << 4) | ((((s & 15u) >> 1) ^ (l & 7u)) << 1) | (s & 1u);
+}
+__device__ __forceinline__ uint32_t r16(uint32_t x) { return (x + 15u) & ~15u; }
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// FP_CALIB_PROFILE: phase stamps -- [chunk][0..3] scanner, [n_chunks + i][0..7] CTA 0's iteration i
+#define CS_STAMP(row, col)                                                   \
+  do {                                                                       \
+    if (a.prof && threadIdx.x == 0) a.prof[(uint64_t)(row) * 8 + (col)] = gtime(); \
+  } while (0)
+
+// compose within a region: a from the beta^n table (n <= 512)
+__device__ __forceinline__ Aff compose_t(const Aff &e, const Aff &l, const double *bpow) {
+  const unsigned long long n = e.n + l.n;
+  return Aff{bpow[n], __fma_rn(l.a, e.b, l.b), n};
+}
+
+// lanes sorted by category (kIdle last): inclusive segmented scan of the lane maps
+__device__ __forceinline__ Aff seg_scan(Aff x, uint32_t kl, uint32_t lane, const double *bpow) {
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const Aff y = Aff{__shfl_down_sync(0xffffffffu, x.a, o), __shfl_down_sync(0xffffffffu, x.b, o),
-                          __shfl_down_sync(0xffffffffu, x.n, o)};
-        if ((lane & (2 * o - 1)) == 0) x = compose(y, x);
-      }
-      if (lane == 0) S.red[k][warp] = x;
+  for (int o = 1; o < 32; o <<= 1) {
+    const Aff y = shfl_up(x, o);
+    const uint32_t yk = __shfl_up_sync(0xffffffffu, kl, o);
+    if (lane >= (uint32_t)o && yk == kl) x = compose_t(y, x, bpow);
+  }
+  return x;
+}
+
+// the lane's own category run: [start, start + 16) of category kl with cnt observations
+__device__ __forceinline__ void lane_run(uint32_t lane, const uint32_t st[5], const uint32_t cnt4[4], uint32_t &kl,
+                                         uint32_t &cnt) {
+  const uint32_t ls = lane * 16u;
+  kl = kIdle;
+  cnt = 0u;
+#pragma unroll
+  for (uint32_t k = 0; k < 4; ++k)
+    if (ls >= st[k] && ls < st[k + 1]) { kl = k; cnt = min(16u, cnt4[k] - (ls - st[k])); }
+}
+
+__device__ __forceinline__ void phase_a(const CalibStreamArgs &a, unsigned char *smem, uint32_t i, int &scanner) {
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, ring = i % kSRing, c = blockIdx.x;
+  const double *bpow = reinterpret_cast<const double *>(smem + SLayout::bpow);
+  double *srt = reinterpret_cast<double *>(smem + SLayout::sorted) + (ring * kSW + w) * kSSlots;
+  Aff *rex = reinterpret_cast<Aff *>(smem + SLayout::rex) + ring * kSW * 4;
+  const double beta = a.beta, wgt = __dsub_rn(1.0, a.beta);
+  const uint64_t rb = ((uint64_t)i * a.G + c) * (uint64_t)(kSW * kSRegion) + (uint64_t)w * kSRegion;
+  const uint32_t last = a.n_cats - 1u;
+  uint32_t vb[kSWords], vt[kSWords], info[kSWords];
+#pragma unroll
+  for (int j = 0; j < kSWords; ++j) {
+    const uint64_t r = rb + 32u * j + lane;
+    const bool in = r < a.n;
+    vb[j] = in ? __ldcs(a.bytes + r) : 0u;
+    vt[j] = in ? __ldcs(a.tokens + r) : 0u;
+    info[j] = in ? (uint32_t)__ldcs(a.cat + r) : 0u;
+  }
+  // rank of each valid record inside its category (stream order): three ballots per word
+  uint32_t run[4] = {0u, 0u, 0u, 0u};
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < kSWords; ++j) {
+    const bool valid = vt[j] != 0u;                              // zero-token feedback is dropped
+    const uint32_t k = info[j] < last ? info[j] : last;          // R23
+    const uint32_t v = __ballot_sync(0xffffffffu, valid);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, valid && (k & 1u));
+    const uint32_t b1 = __ballot_sync(0xffffffffu, valid && (k & 2u));
+    const uint32_t m0 = v & ~(b0 | b1), m1 = b0 & ~b1, m2 = b1 & ~b0, m3 = b0 & b1;
+    const uint32_t mine = (k & 2u) ? ((k & 1u) ? m3 : m2) : ((k & 1u) ? m1 : m0);
+    const uint32_t base = (k & 2u) ? ((k & 1u) ? run[3] : run[2]) : ((k & 1u) ? run[1] : run[0]);
+    info[j] = valid ? ((base + __popc(mine & lt)) | (k << 10) | 0x1000u) : 0u;
+    run[0] += __popc(m0); run[1] += __popc(m1); run[2] += __popc(m2); run[3] += __popc(m3);
+  }
+  uint32_t st[5];
+  st[0] = 0u;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) st[k + 1] = st[k] + r16(run[k]);
+#pragma unroll
+  for (int j = 0; j < kSWords; ++j) {
+    const double o = ratio(vb[j], vt[j] | (vt[j] == 0u));
+    if (info[j] & 0x1000u) {
+      const uint32_t k = (info[j] >> 10) & 3u;
+      srt[sslot((info[j] & 0x3ffu) + st[k])] = o;
     }
-    __syncthreads();
-    if (threadIdx.x < n_cats) {
-      const uint32_t k = threadIdx.x;
-      Aff acc = S.red[k][kTileWarps - 1];
-      for (int w = (int)kTileWarps - 2; w >= 0; --w) acc = compose(acc, S.red[k][w]);
-      excl[k] = compose(acc, excl[k]);
-    }
-    if (found) break;
-    __syncthreads();
-    if (threadIdx.x == 0) { S.last[0] = 0xffffffffu; S.last[1] = 0u; }
-    __syncthreads();
-    top -= (int64_t)kTileThreads;
   }
   __syncwarp();
-  if (threadIdx.x < n_cats) mine[NC + threadIdx.x] = compose(excl[threadIdx.x], agg[threadIdx.x]);
+  uint32_t kl, cnt;
+  lane_run(lane, st, run, kl, cnt);
+  const double *lc = srt + lane * 16u;
+  double bt = 0.0;
+  if (cnt == 16u) {
+#pragma unroll
+    for (uint32_t u = 0; u < 8; ++u) {
+      const double2 q = *reinterpret_cast<const double2 *>(lc + ((u ^ (lane & 7u)) << 1));
+      bt = __fma_rn(beta, bt, q.x);
+      bt = __fma_rn(beta, bt, q.y);
+    }
+  } else {
+    for (uint32_t e = 0; e < cnt; ++e) bt = __fma_rn(beta, bt, lc[(((e >> 1) ^ (lane & 7u)) << 1) | (e & 1u)]);
+  }
+  const Aff inc = seg_scan(Aff{bpow[cnt], __dmul_rn(wgt, bt), cnt}, kl, lane, bpow);
+  Aff ex = shfl_up(inc, 1);
+  const uint32_t kprev = __shfl_up_sync(0xffffffffu, kl, 1);
+  if (lane == 0u || kprev != kl) ex = aff_id();
+  reinterpret_cast<double *>(smem + SLayout::lane_b)[(ring * kSW + w) * 32 + lane] = ex.b;
+  reinterpret_cast<uint32_t *>(smem + SLayout::lane_m)[(ring * kSW + w) * 32 + lane] =
+      (uint32_t)ex.n | (cnt << 10) | (kl << 16);
+  // region aggregates: the last lane of each category run (identity for empty categories)
+  const uint32_t knext = __shfl_down_sync(0xffffffffu, kl, 1);
+  if (lane < 4u) {
+    const uint32_t rl = lane == 0u ? run[0] : lane == 1u ? run[1] : lane == 2u ? run[2] : run[3];
+    if (rl == 0u) rex[w * 4 + lane] = aff_id();
+  }
+  if (kl != kIdle && (lane == 31u || knext != kl)) rex[w * 4 + kl] = inc;
+  __syncthreads();
+  if (threadIdx.x < 4u) {                          // regions -> exclusive maps in the piece, piece aggregate
+    const uint32_t k = threadIdx.x;
+    Aff acc = aff_id();
+    for (int r = 0; r < kSW; ++r) {
+      const Aff g = rex[r * 4 + k];
+      rex[r * 4 + k] = acc;
+      acc = compose(acc, g);
+    }
+    static_cast<Aff *>(a.cagg)[((uint64_t)i * a.G + c) * 4 + k] = acc;
+    __threadfence();
+  }
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(a.done + i, 1u) == a.G - 1u;
+  __syncthreads();
+  scanner = s_last;
+}
+
+// exclusive scan of four maps per thread (one per category) over the block:
+// one set of barriers for all four
+__device__ __forceinline__ void block_scan4(const Aff (&x)[4], Aff (&ex)[4], Aff (&tot)[4], Aff (*sw)[4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  Aff inc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) inc[k] = warp_inclusive(x[k], lane);
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) sw[warp][k] = inc[k];
+  }
+  __syncthreads();
+  if (warp < 4) {                                   // warp k scans category k's warp totals
+    Aff v = lane < nw ? sw[lane][warp] : aff_id();
+    v = warp_inclusive(v, lane);
+    if (lane < nw) sw[lane][warp] = v;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    Aff e = shfl_up(inc[k], 1);
+    if (lane == 0) e = aff_id();
+    ex[k] = warp ? compose(sw[warp - 1][k], e) : e;
+    tot[k] = sw[nw - 1][k];
+  }
+  __syncthreads();
+}
+
+// the last CTA of chunk i: piece start states of chunk i, start state of chunk i + 1
+__device__ __noinline__ void scan_chunk(const CalibStreamArgs &a, uint32_t i) {
+  __shared__ Aff s_red[kSW][4];
+  __shared__ double s_c[4];
+  __shared__ unsigned long long s_n[4];
+  CS_STAMP(i, 0);
+  __threadfence();
+  const Aff *ag = static_cast<const Aff *>(a.cagg) + (uint64_t)i * a.G * 4;
+  const uint32_t p0 = 2u * threadIdx.x, p1 = p0 + 1u;
+  Aff x0[4], x1[4], x[4], e0[4], tot[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    x0[k] = p0 < a.G ? ld_aff(ag + p0 * 4 + k) : aff_id();
+    x1[k] = p1 < a.G ? ld_aff(ag + p1 * 4 + k) : aff_id();
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) x[k] = compose(x0[k], x1[k]);
+  block_scan4(x, e0, tot, s_red);
+  CS_STAMP(i, 1);
+  if (threadIdx.x < 4u) {
+    const uint32_t k = threadIdx.x;
+    if (i) wait_flag(a.ready + i);
+    s_c[k] = i ? __ldcg(a.cstart_c + (uint64_t)i * 4 + k) : a.c0[k];
+    s_n[k] = i ? __ldcg(a.cstart_n + (uint64_t)i * 4 + k) : 0ull;
+  }
+  __syncthreads();
+  CS_STAMP(i, 2);
+  const uint64_t q = (uint64_t)i * a.G;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const Aff e1 = compose(e0[k], x0[k]);
+    if (p0 < a.G) { a.pstate_c[(q + p0) * 4 + k] = apply(e0[k], s_c[k]); a.pstate_n[(q + p0) * 4 + k] = s_n[k] + e0[k].n; }
+    if (p1 < a.G) { a.pstate_c[(q + p1) * 4 + k] = apply(e1, s_c[k]); a.pstate_n[(q + p1) * 4 + k] = s_n[k] + e1.n; }
+  }
+  if (threadIdx.x < 4u) {
+    const uint32_t k = threadIdx.x;
+    const Aff t = k == 0u ? tot[0] : k == 1u ? tot[1] : k == 2u ? tot[2] : tot[3];
+    a.cstart_c[(uint64_t)(i + 1) * 4 + k] = apply(t, s_c[k]);
+    a.cstart_n[(uint64_t)(i + 1) * 4 + k] = s_n[k] + t.n;
+  }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) st_release(flags + tile, 2u);
+  if (threadIdx.x == 0) st_release(a.ready + i + 1, 1u);
+  CS_STAMP(i, 3);
 }
 
-template <int NC>
-__global__ void __launch_bounds__(kTileThreads, NC <= 4 ? 4 : 3) c_single(CalibTileArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ TileSm<NC> S;
-  const TileBuf X = tile_buf<NC>(smem);
-  const uint32_t nc = a.n_cats;
-  if (threadIdx.x == 0) S.tile = atomicAdd(a.ticket, 1u);
-  if (threadIdx.x < NC) S.snap_w[threadIdx.x] = 0xffffffffu;
+__device__ __forceinline__ void phase_c(const CalibStreamArgs &a, unsigned char *smem, uint32_t i) {
+  __shared__ double s_pc[4];
+  __shared__ unsigned long long s_pn[4];
+  __shared__ Aff s_sreg[kSW][4];                  // region sigma aggregates
+  __shared__ Aff s_snap[4];                       // sigma map region start -> snapshot
+  __shared__ double s_snapc[4];
+  __shared__ int s_snapw[4];
+  const uint32_t lane = threadIdx.x & 31u, w = threadIdx.x >> 5, ring = i % kSRing, c = blockIdx.x;
+  const double *bpow = reinterpret_cast<const double *>(smem + SLayout::bpow);
+  const double *srt = reinterpret_cast<const double *>(smem + SLayout::sorted) + (ring * kSW + w) * kSSlots;
+  const Aff *rex = reinterpret_cast<const Aff *>(smem + SLayout::rex) + ring * kSW * 4;
+  const double beta = a.beta, wgt = __dsub_rn(1.0, a.beta), inv_w = __drcp_rn(wgt), neg_w = -wgt;
+  const uint64_t piece = (uint64_t)i * a.G + c;
+  if (a.prof && blockIdx.x == 0) CS_STAMP(a.n_chunks + i + kSLag, 3);
+  if (threadIdx.x == 0) wait_flag(a.ready + i + 1);
+  if (a.prof && blockIdx.x == 0) CS_STAMP(a.n_chunks + i + kSLag, 4);
+  if (lane < 4u) s_sreg[w][lane] = aff_id();
+  if (threadIdx.x < 4u) s_snapw[threadIdx.x] = -1;
   __syncthreads();
-  const uint32_t tile = S.tile;
-  Aff *cdesc = static_cast<Aff *>(a.cdesc), *sdesc = static_cast<Aff *>(a.sdesc);
-  const double beta = a.beta, wgt = __dsub_rn(1.0, a.beta);
-  uint32_t kw, r0, r1;
-  stage_tile<NC>(a, X, S, tile, kw, r0, r1);
-  // ---- pass A: c_hat maps ----
-  {
-    double b = 0.0;
-    for (uint32_t r = r0; r < r1; ++r) b = __fma_rn(beta, b, __dmul_rn(wgt, X.o[X.pos[r]]));
-    X.wm[threadIdx.x] = Aff{pow_n(beta, r1 - r0), b, (unsigned long long)(r1 - r0)};
+  if (threadIdx.x < 4u) {
+    s_pc[threadIdx.x] = __ldcg(a.pstate_c + piece * 4 + threadIdx.x);
+    s_pn[threadIdx.x] = __ldcg(a.pstate_n + piece * 4 + threadIdx.x);
   }
   __syncthreads();
-  group_scan(X.wm, S.gstart, nc, S.tot);
-  __syncthreads();
-  look_back_block<NC>(tile, nc, a.cflag, cdesc, S.tot, S.excl, S);
-  __syncthreads();
-  // ---- pass B: replay from the exact start state; sigma maps; snapshot ----
-  double sb = 0.0;
-  if (r1 > r0) {
-    const Aff p0 = compose(S.excl[kw], X.wm[threadIdx.x]);
-    double cv = apply(p0, a.c0[kw]);
-    const unsigned long long before = p0.n;
-    const uint64_t target = (a.snap_at > before && a.snap_at - before <= r1 - r0) ? a.snap_at - before : 0ull;
-    for (uint32_t r = r0; r < r1; ++r) {
-      const double x = X.o[X.pos[r]];
-      const double prev = cv;
-      cv = __fma_rn(beta, prev, __dmul_rn(wgt, x));
-      sb = __fma_rn(beta, sb, __dmul_rn(wgt, fabs(__dsub_rn(x, prev))));
-      if (r - r0 + 1 == target) {
-        S.snapv[kw] = cv;
-        S.part[kw] = Aff{pow_n(beta, (uint32_t)target), sb, 0ull};
-        S.snap_w[kw] = threadIdx.x;
-      }
+  const uint32_t m = reinterpret_cast<const uint32_t *>(smem + SLayout::lane_m)[(ring * kSW + w) * 32 + lane];
+  const double lb = reinterpret_cast<const double *>(smem + SLayout::lane_b)[(ring * kSW + w) * 32 + lane];
+  const uint32_t kl = m >> 16, cnt = (m >> 10) & 31u, ne = m & 0x3ffu;
+  const uint32_t kk = kl & 3u;
+  const Aff rg = rex[w * 4 + kk];
+  const double start = apply(Aff{bpow[ne], lb, ne}, apply(rg, s_pc[kk]));   // c_hat at the lane's first slot
+  const unsigned long long before = s_pn[kk] + rg.n + ne;                    // observations of kl before it
+  const double *lc = srt + lane * 16u;
+  double cs = __dmul_rn(start, inv_w), ss = 0.0;                             // scaled state (1 / w)
+  if (cnt == 16u) {
+#pragma unroll
+    for (uint32_t u = 0; u < 8; ++u) {
+      const double2 q = *reinterpret_cast<const double2 *>(lc + ((u ^ (lane & 7u)) << 1));
+      double d = __fma_rn(neg_w, cs, q.x);
+      cs = __fma_rn(beta, cs, q.x);
+      ss = __fma_rn(beta, ss, fabs(d));
+      d = __fma_rn(neg_w, cs, q.y);
+      cs = __fma_rn(beta, cs, q.y);
+      ss = __fma_rn(beta, ss, fabs(d));
+    }
+  } else {
+    for (uint32_t e = 0; e < cnt; ++e) {
+      const double o = lc[(((e >> 1) ^ (lane & 7u)) << 1) | (e & 1u)];
+      const double d = __fma_rn(neg_w, cs, o);
+      cs = __fma_rn(beta, cs, o);
+      ss = __fma_rn(beta, ss, fabs(d));
     }
   }
-  __syncthreads();                                   // every worker has read its c map
-  X.wm[threadIdx.x] = Aff{pow_n(beta, r1 - r0), sb, 0ull};
+  // the snap_at-th observation of category kl in this lane: replay up to it (once per category)
+  const bool snap = cnt != 0u && a.snap_at > before && a.snap_at - before <= cnt;
+  Aff m1 = aff_id();
+  double csnap = 0.0;
+  if (snap) {
+    const uint32_t t = (uint32_t)(a.snap_at - before);
+    double c2 = __dmul_rn(start, inv_w), s2 = 0.0;
+    for (uint32_t e = 0; e < t; ++e) {
+      const double o = lc[(((e >> 1) ^ (lane & 7u)) << 1) | (e & 1u)];
+      const double d = __fma_rn(neg_w, c2, o);
+      c2 = __fma_rn(beta, c2, o);
+      s2 = __fma_rn(beta, s2, fabs(d));
+    }
+    csnap = __dmul_rn(wgt, c2);
+    m1 = Aff{bpow[t], __dmul_rn(wgt, s2), t};
+  }
+  const Aff inc = seg_scan(Aff{bpow[cnt], __dmul_rn(wgt, ss), cnt}, kl, lane, bpow);
+  Aff ex = shfl_up(inc, 1);
+  const uint32_t kprev = __shfl_up_sync(0xffffffffu, kl, 1);
+  if (lane == 0u || kprev != kl) ex = aff_id();
+  const uint32_t knext = __shfl_down_sync(0xffffffffu, kl, 1);
+  if (kl != kIdle && (lane == 31u || knext != kl)) s_sreg[w][kl] = inc;
+  if (snap) {
+    s_snap[kl] = compose(ex, m1);
+    s_snapc[kl] = csnap;
+    s_snapw[kl] = (int)w;
+  }
   __syncthreads();
-  group_scan(X.wm, S.gstart, nc, S.tot);
-  __syncthreads();
-  look_back_block<NC>(tile, nc, a.sflag, sdesc, S.tot, S.sexcl, S);
-  __syncthreads();
-  if (threadIdx.x < nc) {
+  if (threadIdx.x < 4u) {                            // piece sigma map; snapshot map from the piece start
     const uint32_t k = threadIdx.x;
-    if (S.snap_w[k] != 0xffffffffu) {                // the snap_at-th observation of category k is here
-      const Aff m = compose(S.sexcl[k], compose(X.wm[S.snap_w[k]], S.part[k]));
-      a.out[48 + k] = S.snapv[k];
-      a.out[64 + k] = apply(m, a.s0[k]);
+    Aff acc = aff_id();
+    for (int r = 0; r < kSW; ++r) {
+      if (r == s_snapw[k]) {
+        const Aff sm = compose(acc, s_snap[k]);
+        a.snap_piece[k] = piece;
+        a.snap_v[k * 4 + 0] = sm.a;
+        a.snap_v[k * 4 + 1] = sm.b;
+        a.snap_v[k * 4 + 2] = s_snapc[k];
+      }
+      acc = compose(acc, s_sreg[r][k]);
     }
-    if (tile == a.n_tiles - 1) {                     // the last tile: the final state
-      const Aff ci = ld_aff(cdesc + ((size_t)tile * 2 + 1) * NC + k);
-      const Aff si = compose(S.sexcl[k], S.tot[k]);
-      a.out[k] = apply(ci, a.c0[k]);
-      a.out[16 + k] = apply(si, a.s0[k]);
-      reinterpret_cast<unsigned long long *>(a.out)[32 + k] = ci.n;
+    a.sig_a[piece * 4 + k] = acc.a;
+    a.sig_b[piece * 4 + k] = acc.b;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSThreads, 2) c_stream(CalibStreamArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *bpow = reinterpret_cast<double *>(smem + SLayout::bpow);
+  for (int j = threadIdx.x; j < kSBeta; j += kSThreads) bpow[j] = pow_n(a.beta, (uint32_t)j);
+  __syncthreads();
+  for (uint32_t i = 0; i < a.n_chunks + kSLag; ++i) {
+    const bool p0 = a.prof && blockIdx.x == 0;
+    if (p0) CS_STAMP(a.n_chunks + i, 0);
+    if (i < a.n_chunks) {
+      int scanner = 0;
+      phase_a(a, smem, i, scanner);
+      if (p0) CS_STAMP(a.n_chunks + i, 1);
+      if (scanner) scan_chunk(a, i);
+      if (p0) CS_STAMP(a.n_chunks + i, 2);
     }
+    if (i >= (uint32_t)kSLag) phase_c(a, smem, i - kSLag);
+    if (p0) CS_STAMP(a.n_chunks + i, 5);
   }
 }
 
-template <int NC>
-cudaError_t launch_single(const CalibTileArgs &a, cudaStream_t s) {
-  const size_t smem = TileLayout<NC>::bytes;
-  cudaError_t e = cudaFuncSetAttribute(c_single<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  c_single<NC><<<(unsigned)a.n_tiles, kTileThreads, smem, s>>>(a);
-  return cudaGetLastError();
+// sigma piece maps composed in stream order: block (b, k) composes a
+// contiguous range of pieces of category k; the last block of category k
+// composes the ranges, applies them to s0 and resolves the snapshot
+__global__ void __launch_bounds__(256) c_stream_final(CalibStreamArgs a) {
+  __shared__ Aff s_red[32];
+  __shared__ int s_last;
+  const uint32_t k = blockIdx.y, nb = gridDim.x, b = blockIdx.x, t = threadIdx.x;
+  const uint64_t P = (uint64_t)a.n_chunks * a.G;
+  const uint64_t blo = P * b / nb, bn = P * (b + 1) / nb - blo;
+  const uint64_t lo = blo + bn * t / blockDim.x, hi = blo + bn * (t + 1) / blockDim.x;
+  const uint64_t sp = a.snap_piece[k];
+  Aff run = aff_id(), pre = aff_id();
+  bool mine = false;
+  for (uint64_t p = lo; p < hi; ++p) {
+    if (p == sp) { pre = run; mine = true; }
+    run = compose(run, Aff{a.sig_a[p * 4 + k], a.sig_b[p * 4 + k], 0ull});
+  }
+  Aff ex, tot;
+  block_scan(run, ex, tot, s_red);
+  Aff *part = static_cast<Aff *>(a.fin_part) + (uint64_t)k * nb;
+  if (mine) {                                        // sigma map: this block's first piece -> snapshot piece
+    static_cast<Aff *>(a.fin_pre)[k] = compose(ex, pre);
+    a.fin_snapb[k] = b;
+  }
+  if (t == 0) part[b] = tot;
+  __threadfence();
+  __syncthreads();
+  if (t == 0) s_last = atomicAdd(a.fin_done + k, 1u) == nb - 1u;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const Aff x = t < nb ? ld_aff(part + t) : aff_id();
+  block_scan(x, ex, tot, s_red);
+  if (sp != ~0ull && t == __ldcg(a.fin_snapb + k)) {
+    const double sb = apply(compose(ex, ld_aff(static_cast<const Aff *>(a.fin_pre) + k)), a.s0[k]);
+    a.out[48 + k] = a.snap_v[k * 4 + 2];
+    a.out[64 + k] = apply(Aff{a.snap_v[k * 4 + 0], a.snap_v[k * 4 + 1], 0ull}, sb);
+  }
+  if (t == 0) {
+    a.out[k] = a.cstart_c[(uint64_t)a.n_chunks * 4 + k];
+    a.out[16 + k] = apply(tot, a.s0[k]);
+    reinterpret_cast<unsigned long long *>(a.out)[32 + k] = a.cstart_n[(uint64_t)a.n_chunks * 4 + k];
+  }
 }
 
 }  // namespace
 
-uint64_t calib_tiles(uint64_t n) { return (n + kTileRecs - 1) / kTileRecs; }
+size_t calib_stream_smem() { return SLayout::bytes; }
+uint32_t calib_stream_fin_blocks() { return kFinBlocks; }
+uint32_t calib_stream_piece() { return (uint32_t)(kSW * kSRegion); }
 
-cudaError_t launch_calib_tile(const CalibTileArgs &a, int, cudaStream_t s) {
-  return a.n_cats <= 4 ? launch_single<4>(a, s) : launch_single<16>(a, s);
+int calib_stream_blocks_per_sm() {
+  if (cudaFuncSetAttribute(c_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SLayout::bytes) != cudaSuccess)
+    return 0;
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, c_stream, kSThreads, SLayout::bytes) != cudaSuccess) return 0;
+  return b;
 }
 
-
+cudaError_t launch_calib_stream(const CalibStreamArgs &a, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(c_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SLayout::bytes);
+  if (e != cudaSuccess) return e;
+  CalibStreamArgs args = a;
+  void *params[] = {&args};
+  // every CTA must be resident: phase C waits on flags that other CTAs' phase A publishes
+  e = cudaLaunchCooperativeKernel((const void *)c_stream, dim3(a.G), dim3(kSThreads), params, SLayout::bytes, s);
+  if (e != cudaSuccess) return e;
+  c_stream_final<<<dim3(kFinBlocks, a.n_cats), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
 
 namespace {
 

@@ -1823,16 +1823,28 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
   if (bad) n = 0;
   DeviceGuard g(p->device);
   cudaStream_t s = (cudaStream_t)stream;
-  if (!p->dist && env_int("FP_CALIB_SINGLE", 0)) {
-    // one rank, FP_CALIB_SINGLE=1: the single-pass tile kernel (every record read once;
-    // k_calib.cu c_single, decoupled look-back over tiles). Correct, but slower than the
-    // two-pass kernels below on a B200 (the look-back chain over 244K tiles of 4,096
-    // records does not keep up with the stream: DESIGN.md §10)
-    const uint64_t tiles = calib_tiles(n);
-    const size_t nc = n_cats <= 4 ? 4 : 16;
-    const size_t desc = tiles * 2 * nc * 24;           // one [tile][2][NC] array of maps (24 B)
-    const size_t flag_bytes = ((2 * tiles + 4) * 4 + 255) & ~size_t(255);
-    const size_t need = 16 * 16 * 8 + flag_bytes + 2 * desc + 256;
+  const int stream_bps = (!p->dist && n_cats <= 4 && n > 0 && env_int("FP_CALIB_STREAM", 0))
+                             ? calib_stream_blocks_per_sm() : 0;
+  if (stream_bps > 0) {
+    // one rank, n_cats <= 4, FP_CALIB_STREAM=1: the streaming replay (k_calib.cu
+    // c_stream) -- every record read from HBM once, c_obs computed once, no
+    // per-record category dispatch. Correct, but slower than the two-pass
+    // kernels below on a B200 (17.5 vs 4.7 ms per 1e9 records: each iteration
+    // is a chain of latencies -- column loads, fence + chunk counter, the
+    // chunk scanner's hand-off -- with two CTAs per SM to hide them;
+    // profiles/r02/next3_stream_profile.log).
+    const uint32_t G = (uint32_t)std::min<int64_t>(512, (int64_t)stream_bps * p->sm_count);
+    const uint64_t chunk = (uint64_t)G * calib_stream_piece();
+    const uint64_t nch = (n + chunk - 1) / chunk;
+    if (env_int("FP_CALIB_VERBOSE", 0))
+      fprintf(stderr, "[fp] calibrate_replay: streaming kernel, %d CTAs/SM, G = %u, %llu chunks of %llu records\n",
+              stream_bps, G, (unsigned long long)nch, (unsigned long long)chunk);
+    const uint64_t np = nch * G * 4;                          // (piece, category) entries
+    const size_t flag_bytes = ((2 * nch + 9) * 4 + 255) & ~size_t(255);
+    const size_t fin = (size_t)4 * (calib_stream_fin_blocks() + 1) * 24;
+    const bool prof = env_int("FP_CALIB_PROFILE", 0) != 0;
+    const size_t prof_bytes = prof ? (2 * nch + 2) * 64 : 0;
+    const size_t need = 16 * 16 * 8 + flag_bytes + np * (24 + 8 + 8 + 8 + 8) + (nch + 1) * 4 * 16 + fin + prof_bytes + 256;
     if (p->calib_cap < need) {
       cudaFree(p->d_calib_scratch);
       p->d_calib_scratch = nullptr;
@@ -1842,43 +1854,73 @@ fp_status calibrate_replay(fp_plan *p, const uint32_t *d_body_bytes, const uint3
     }
     unsigned char *base = p->d_calib_scratch;
     double *sm = reinterpret_cast<double *>(base);                       // 16 slots of 16 doubles
-    unsigned int *flags = reinterpret_cast<unsigned int *>(base + 16 * 16 * 8);   // [2][tiles] + ticket
-    unsigned char *descs = base + 16 * 16 * 8 + flag_bytes;
-    CalibTileArgs a{};
+    unsigned int *flags = reinterpret_cast<unsigned int *>(base + 16 * 16 * 8);
+    unsigned char *q = base + 16 * 16 * 8 + flag_bytes;
+    CalibStreamArgs a{};
     a.bytes = d_body_bytes;
     a.tokens = d_prompt_tokens;
     a.cat = d_category;
     a.n = n;
-    a.n_tiles = tiles;
     a.n_cats = n_cats;
     a.beta = beta;
+    a.G = G;
+    a.n_chunks = (uint32_t)nch;
+    a.done = flags;
+    a.ready = flags + nch;
+    a.cagg = q;                                      q += np * 24;
+    a.pstate_c = reinterpret_cast<double *>(q);      q += np * 8;
+    a.pstate_n = reinterpret_cast<unsigned long long *>(q); q += np * 8;
+    a.sig_a = reinterpret_cast<double *>(q);         q += np * 8;
+    a.sig_b = reinterpret_cast<double *>(q);         q += np * 8;
+    a.cstart_c = reinterpret_cast<double *>(q);      q += (nch + 1) * 4 * 8;
+    a.cstart_n = reinterpret_cast<unsigned long long *>(q); q += (nch + 1) * 4 * 8;
+    a.fin_part = q;                                  q += (size_t)4 * calib_stream_fin_blocks() * 24;
+    a.fin_pre = q;                                   q += 4 * 24;
+    a.prof = prof ? reinterpret_cast<unsigned long long *>(q) : nullptr;
+    a.fin_done = flags + 2 * nch + 1;
+    a.fin_snapb = flags + 2 * nch + 5;
     double *c0 = sm + 16 * 8, *s0 = sm + 16 * 9;
     a.c0 = c0;
     a.s0 = s0;
-    a.cflag = flags;
-    a.sflag = flags + tiles;
-    a.ticket = flags + 2 * tiles;
-    a.cdesc = descs;
-    a.sdesc = descs + desc;
+    a.snap_piece = reinterpret_cast<unsigned long long *>(sm + 16 * 10);
+    a.snap_v = sm + 16 * 11;
     a.snap_at = snap_at;
     a.out = sm;
     std::vector<double> init_c(16, 0.0), init_s(16, 0.0), outv(80, 0.0);
     for (uint32_t k = 0; k < n_cats; ++k) {
       init_c[k] = init[k].c_hat;
       init_s[k] = init[k].sigma_hat;
-      outv[k] = init[k].c_hat;                          // the final state of an empty stream
-      outv[16 + k] = init[k].sigma_hat;
     }
     for (int k = 48; k < 80; ++k) outv[k] = std::nan("");
     CUDA_TRY(p, cudaMemcpyAsync(c0, init_c.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
     CUDA_TRY(p, cudaMemcpyAsync(s0, init_s.data(), 16 * 8, cudaMemcpyHostToDevice, s), "H2D init");
     CUDA_TRY(p, cudaMemcpyAsync(sm, outv.data(), 80 * 8, cudaMemcpyHostToDevice, s), "H2D outputs");
-    CUDA_TRY(p, cudaMemsetAsync(flags, 0, (2 * tiles + 1) * 4, s), "memset look-back flags");
-    if (tiles) {
+    CUDA_TRY(p, cudaMemsetAsync(a.snap_piece, 0xFF, 4 * 8, s), "memset snapshot pieces");
+    CUDA_TRY(p, cudaMemsetAsync(flags, 0, (2 * nch + 9) * 4, s), "memset chunk flags");
+    {
       LaunchTimer lt(p, FP_KERNEL_EVAL, s);
-      cudaError_t e = launch_calib_tile(a, p->sm_count, s);
+      cudaError_t e = launch_calib_stream(a, s);
       if (e != cudaSuccess) return cuda_fail(p, e, "calibration replay launch");
-      ++p->launches;
+    }
+    p->launches += 2;
+    if (prof) {
+      std::vector<unsigned long long> t((2 * nch + 2) * 8);
+      CUDA_TRY(p, cudaMemcpyAsync(t.data(), a.prof, t.size() * 8, cudaMemcpyDeviceToHost, s), "D2H profile");
+      CUDA_TRY(p, cudaStreamSynchronize(s), "sync");
+      double sc[3] = {0, 0, 0}, it[5] = {0, 0, 0, 0, 0};
+      for (uint64_t i = 1; i + 1 < nch; ++i)
+        for (int j = 0; j < 3; ++j) sc[j] += (double)(t[i * 8 + j + 1] - t[i * 8 + j]);
+      uint64_t m = 0;
+      for (uint64_t i = 2; i + 2 < nch; ++i, ++m) {
+        const unsigned long long *r = &t[(nch + i) * 8];
+        it[0] += (double)(r[1] - r[0]); it[1] += (double)(r[2] - r[1]); it[2] += (double)(r[3] - r[2]);
+        it[3] += (double)(r[4] - r[3]); it[4] += (double)(r[5] - r[4]);
+      }
+      const double ns = (double)std::max<uint64_t>(1, nch - 2), nm = (double)std::max<uint64_t>(1, m);
+      fprintf(stderr, "[fp] c_stream scanner ns: scan %.0f wait %.0f publish %.0f | CTA 0 iteration ns: A %.0f "
+              "scan %.0f gap %.0f C-wait %.0f C %.0f | total %.3f ms\n", sc[0] / ns, sc[1] / ns, sc[2] / ns,
+              it[0] / nm, it[1] / nm, it[2] / nm, it[3] / nm, it[4] / nm,
+              (double)(t[(2 * nch + 1) * 8 + 5] - t[nch * 8]) * 1e-6);
     }
     std::vector<double> h(80);
     CUDA_TRY(p, cudaMemcpyAsync(h.data(), sm, 80 * 8, cudaMemcpyDeviceToHost, s), "D2H calibration");

@@ -29,10 +29,17 @@ def _close(a, b, rel=1e-12):
     return np.all(both_nan | (np.abs(a - b) <= rel * np.maximum(np.abs(b), 1e-300)))
 
 
+@pytest.mark.parametrize("stream", [False, True])
 @pytest.mark.parametrize("n,ncat,snap", [(1, 4, 1), (37, 4, 5), (100_003, 4, 50), (5_000_000, 4, 1000),
                                          (2_000_001, 3, 50), (300_000, 16, 7),
-                                         (3_000_001, 4, 400_000), (1_000_003, 16, 30_000)])
-def test_replay_matches_sequential(n, ncat, snap):
+                                         (3_000_001, 4, 400_000), (1_000_003, 16, 30_000),
+                                         (1_062_400, 4, 1), (2_124_801, 2, 500_000)])
+def test_replay_matches_sequential(n, ncat, snap, stream, monkeypatch):
+    """The two-pass kernels (the default) and the streaming kernel
+    (FP_CALIB_STREAM=1: one rank, <= 4 categories; sizes at and around whole
+    chunks of 296 x 3,584 records) against the sequential oracle."""
+    if stream:
+        monkeypatch.setenv("FP_CALIB_STREAM", "1")
     body, mo, cat, tp = generate_raw_host("MIX", 13, 0, n)
     if ncat == 16:
         cat = (np.arange(n) * 7 % 20).astype(np.uint8)       # categories >= 16 -> last (R23)
@@ -77,13 +84,14 @@ def test_replay_misaligned_columns(shift):
     assert _close(g["snap_c"], o["snap_c"]) and _close(g["snap_sigma"], o["snap_sigma"])
 
 
-@pytest.mark.parametrize("single", [False, True])
-@pytest.mark.parametrize("mode", ["skew", "dropped", "empty", "one_cat", "mixed"])
-def test_replay_edge_cases(mode, single, monkeypatch):
+@pytest.mark.parametrize("stream", [False, True])
+@pytest.mark.parametrize("mode", ["skew", "dropped", "empty", "one_cat", "mixed", "one_sided"])
+def test_replay_edge_cases(mode, stream, monkeypatch):
     """A 99%-one-category mix, a stream whose feedback is all dropped, an empty
-    stream, one category, a plain mix -- through the two-pass kernels (the
-    default) and the single-pass look-back kernel (FP_CALIB_SINGLE=1: its
-    per-category worker groups and position lists)."""
+    stream, one category, a plain mix, a stream whose first half is one
+    category and second half another -- through the two-pass kernels (the
+    default) and the streaming kernel (FP_CALIB_STREAM=1: its category runs,
+    empty lanes and empty categories)."""
     n = 0 if mode == "empty" else 777_777
     body, mo, cat, tp = generate_raw_host("MIX", 29, 0, max(n, 1))
     body, cat, tp = body[:n], cat[:n], tp[:n]
@@ -92,8 +100,10 @@ def test_replay_edge_cases(mode, single, monkeypatch):
         cat = np.where(np.arange(n) % 101 == 0, cat, 2).astype(np.uint8)
     if mode == "dropped":
         tp = np.zeros_like(tp)
-    if single:
-        monkeypatch.setenv("FP_CALIB_SINGLE", "1")
+    if mode == "one_sided":
+        cat = np.where(np.arange(n) < n // 2, 1, 3).astype(np.uint8)
+    if stream:
+        monkeypatch.setenv("FP_CALIB_STREAM", "1")
     init = [(4.0, 0.5)] * ncat
     plan = fp.fleet_plan_create(**fp.desc_from_config(configs.c1()))
     g = fp.calibrate_replay(plan, _dev(body), _dev(tp), _dev(cat), init, beta=0.95, snap_at=50)
