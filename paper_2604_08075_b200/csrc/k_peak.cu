@@ -104,11 +104,24 @@ __global__ void k0w_bounds_multi(PeakArgs a) {
     mlo = c ? min(lo + c * step - 1, hi - 1) + 1 : lo;
     mhi = c < 32 ? min(lo + (c + 1) * step - 1, hi - 1) : hi;
   }
-  // lower_bound(arrival, t) in [mlo, mhi]: arrival[mlo - 1] < t, arrival[mhi] >= t (or mhi = n)
-  uint64_t n = mhi - mlo;
-  while (n > 0) {
-    const uint64_t half = n >> 1;
-    if (__ldg(a.arrival + mlo + half) < t) { mlo += half + 1; n -= half + 1; } else { n = half; }
+  // lower_bound(arrival, t) in [mlo, mhi]: arrival[mlo - 1] < t, arrival[mhi] >= t (or mhi = n).
+  // Interpolation search on the bracketing values (arrivals of a Poisson trace
+  // grow almost linearly inside an interval: ~4 dependent probes instead of the
+  // ~14 of a binary search over a 1-s window's interval), with a bisection
+  // step whenever an interpolation step kept more than 3/4 of the interval
+  uint64_t vlo = mlo ? __ldg(a.arrival + mlo - 1) : 0ull;
+  uint64_t vhi = mhi < a.n ? __ldg(a.arrival + mhi) : ~0ull;
+  bool bisect = false;
+  while (mhi > mlo) {
+    const uint64_t len = mhi - mlo;
+    uint64_t g = mlo + len / 2;
+    if (!bisect && mhi < a.n && vhi > vlo) {
+      const double f = (double)(t - vlo) / (double)(vhi - vlo);   // vlo < t <= vhi
+      g = mlo + min((uint64_t)(f * (double)len), len - 1);
+    }
+    const uint64_t v = __ldg(a.arrival + g);
+    if (v < t) { mlo = g + 1; vlo = v; } else { mhi = g; vhi = v; }
+    bisect = !bisect && (mhi - mlo) * 4 > len * 3;
   }
   if (w <= a.n_windows) a.start[w] = w == a.n_windows ? a.n : mlo;
 }
