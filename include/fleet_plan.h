@@ -127,8 +127,10 @@ typedef struct fp_grid {
                                         Every rank must issue the same sequence of
                                         sweeps: a rank's K3 waits on the device for
                                         every peer's K1 of the same step. world <= 64 */
-#define FP_FLAG_SPECULATE 0x80u      /* sweep_and_route, device trace, |E| < 127, >= 2^26
-                                        requests on this rank: speculative routing. A
+#define FP_FLAG_SPECULATE 0x80u      /* sweep_and_route, device trace, and a u8 LUT with
+                                        |E| < 127 and >= 2^26 requests on this rank, or a
+                                        u16 LUT (|E| >= 256) and >= 2^28 requests
+                                        (FP_SPEC_MIN_WIDE_LOG2): speculative routing. A
                                         sample pass (every ~4th grid-wide stripe of this
                                         rank's trace, ~2%) and its K3 (the whole grid,
                                         rank-local) pick a split; the full trace pass

@@ -79,8 +79,9 @@ struct TraceArgs {
   // speculative routing (FP_FLAG_SPECULATE, sweep_and_route):
   //  step_stride > 1: a SAMPLE pass -- only the grid steps k = 0, stride, 2 stride, ...
   //    (whole grid-wide stripes spread over the trace), no head / tail elements
-  //  dec_route != NULL (byte bin variant, |E| < 128): bins_out receives DECISION
-  //    bytes for the split {iB, iCS, iCL, ok} at dec_route (read after
+  //  dec_route != NULL (byte bin variant): bins_out receives DECISION bytes
+  //    (SWAR on the bins for a u8 LUT, |E| < 127; for a u16 LUT from L_total
+  //    and the split's edge values) for the split {iB, iCS, iCL, ok} at dec_route (read after
   //    griddepcontrol.wait; ok == 0: nothing is written), pdl: launch as a
   //    programmatic dependent of the previous kernel
   uint32_t step_stride = 1;

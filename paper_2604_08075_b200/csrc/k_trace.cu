@@ -122,6 +122,20 @@ __device__ __forceinline__ uint32_t dec_word(uint32_t w, const DecK &k) {
   return (gB >> 7) + (gS >> 5) + (gL >> 7) * 9u;
 }
 
+// the same decision byte from L_total itself, for edge sets whose bins do not
+// fit the SWAR compare (u16 LUT: |E| >= 256): bin > j <=> e_j < L (E is sorted
+// and unique), so d = [L > B] + 4 [L > C_S] + 9 [L > C_L] with the split's
+// edge values -- dec_word's byte exactly
+struct DecL {
+  uint32_t vB, vCS, vCL;
+};
+__device__ __forceinline__ uint32_t dec_l1(uint32_t L, const DecL &k) {
+  return (L > k.vB ? 1u : 0u) + (L > k.vCS ? 4u : 0u) + (L > k.vCL ? 9u : 0u);
+}
+__device__ __forceinline__ uint32_t dec_l4(const uint4 &v, const DecL &k) {
+  return dec_l1(v.x, k) | (dec_l1(v.y, k) << 8) | (dec_l1(v.z, k) << 16) | (dec_l1(v.w, k) << 24);
+}
+
 // the byte a request's bin is stored as: the bin itself when |E| < 256 (u8
 // LUT), else min(bin, 255) -- 255 then stands for "bin >= 255" (the routing
 // pass reads L_total back for such requests only when the routed split has an
@@ -299,6 +313,10 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
     // predecessor -- the sample's K3 -- has completed)
     bool store = true;
     DecK dk{0u, 0u, 0u};
+    DecL dl{0u, 0u, 0u};
+    // decisions by SWAR on the bin bytes (u8 LUT; the host speculates there
+    // only for |E| < 127) or, for the u16 LUT's clamped bins, from L_total
+    constexpr bool swar = LUTW == 1;
     // a programmatic-dependent launch (the sample pass after the previous
     // step's verify): nothing of the predecessor's is read before this wait
     if (a.pdl && !a.dec_route) asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -309,21 +327,26 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
                    : "=r"(rt.x), "=r"(rt.y), "=r"(rt.z), "=r"(rt.w) : "l"(a.dec_route));
       store = rt.w != 0u;
       dk = dec_k(rt.x, rt.y, rt.z);
+      if (!swar && store) dl = DecL{__ldg(a.edges + rt.x), __ldg(a.edges + rt.y), __ldg(a.edges + rt.z)};
     }
     const bool decm = BINS && !PACK && a.dec_route;
     uint32_t *bins4 = (BINS && !PACK) ? reinterpret_cast<uint32_t *>(a.bins_out + head) : nullptr;
+    auto dec1 = [&](uint32_t b, uint32_t L) { return swar ? dec_word(b, dk) : dec_l1(L, dl); };
     if (a.step_stride == 1u && blockIdx.x == 0 && threadIdx.x < head) {
-      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(threadIdx.x));
+      const uint32_t L = load1(threadIdx.x);
+      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, L);
       if (BINS && store)
-        (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)(decm ? dec_word(b, dk) : bin_byte<LUTW>(b));
+        (PACK ? a.bins_side : a.bins_out)[threadIdx.x] = (uint8_t)(decm ? dec1(b, L) : bin_byte<LUTW>(b));
     }
     if (a.step_stride == 1u && blockIdx.x == gridDim.x - 1 && threadIdx.x < a.n - tail_first) {
-      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, load1(tail_first + threadIdx.x));
+      const uint32_t L = load1(tail_first + threadIdx.x);
+      const uint32_t b = add_one<LUTW, R, SPLIT, MASS>(c, L);
       if (BINS && store) {
         if (PACK) a.bins_side[4 + threadIdx.x] = (uint8_t)b;
-        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)(decm ? dec_word(b, dk) : bin_byte<LUTW>(b));
+        else a.bins_out[tail_first + threadIdx.x] = (uint8_t)(decm ? dec1(b, L) : bin_byte<LUTW>(b));
       }
     }
+    auto dec4 = [&](uint32_t w, const uint4 &v) { return swar ? dec_word(w, dk) : dec_l4(v, dl); };
     const uint4 *body = reinterpret_cast<const uint4 *>(a.len + head);
     // grid-stride stripes: at every step the whole grid reads kUnroll contiguous
     // stripes of gridDim x blockDim x 16 B (measured 7.2 TB/s read-only vs
@@ -344,7 +367,7 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
           const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, v[u]);
           if (BINS && PACK) pw[u & 3] = w;
           else if (BINS && store)
-            asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(decm ? dec_word(w, dk) : w)
+            asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(bins4 + base + u * S), "r"(decm ? dec4(w, v[u]) : w)
                          : "memory");
         }
         if (BINS && PACK) {
@@ -359,9 +382,10 @@ __global__ void __launch_bounds__(512, (RAW || BINS) ? 3 : 1) k1_trace(TraceArgs
         for (int u = 0; u < U; ++u) {
           const uint64_t j = base + u * S;
           if (j < n4) {
-            const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, RAW ? sr.load4(body, j) : sp.load4(body, j));
+            const uint4 vj = RAW ? sr.load4(body, j) : sp.load4(body, j);
+            const uint32_t w = add_four<LUTW, R, SPLIT, MASS>(c, vj);
             if (BINS && PACK) pw[u & 3] = w;
-            else if (BINS && store) bins4[j] = decm ? dec_word(w, dk) : w;
+            else if (BINS && store) bins4[j] = decm ? dec4(w, vj) : w;
           }
         }
         if (BINS && PACK) {

@@ -1157,6 +1157,14 @@ namespace {
 // FP_FLAG_SPECULATE path of sweep_and_route (preconditions checked by the caller).
 // raw != NULL: the raw-column form (sweep_and_route_raw): *raw is the trace
 // pass's TraceArgs with the columns and estimator set, rr the verify's args.
+// the smallest trace (log2 requests per rank) that speculates with a u16 LUT:
+// the wide grids' K3 (~14 us for C3's 30,720 candidates) runs twice per step,
+// which 2 B/request saved pays for only above ~2e8 requests (C3 at 1e8: 0.191
+// ms speculative vs 0.174 ms with the bin pass; profiles/r02/spec_wide/)
+static unsigned spec_min_wide_log2() {
+  return (unsigned)std::min(40, std::max(1, env_int("FP_SPEC_MIN_WIDE_LOG2", 28)));
+}
+
 fp_status sweep_route_speculative(fp_plan *p, const uint32_t *len, uint64_t n_local, double rate_rps,
                                   uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
                                   fp_route_counts *h_counts, cudaStream_t s, const TraceArgs *raw = nullptr,
@@ -1351,7 +1359,8 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     const uintptr_t lp = len ? reinterpret_cast<uintptr_t>(len) : 0;
     const uint64_t hph = (4 - ((lp & 15u) >> 2)) & 3u;
     const bool spec = (p->flags & FP_FLAG_SPECULATE) && d_decision && len && !is_host_pointer(len) &&
-                      n_local >= (1ull << 26) && p->lut_cells && p->lut_u8 && p->nbins <= 127 &&
+                      n_local >= (1ull << (p->lut_u8 ? 26 : spec_min_wide_log2())) && p->lut_cells &&
+                      (!p->lut_u8 || p->nbins <= 127) &&
                       p->k3a.shape == kK3Cluster && (reinterpret_cast<uintptr_t>(d_decision + hph) & 3u) == 0;
     if (spec) return sweep_route_speculative(p, len, n_local, rate_rps, route_model, d_decision, h_best, h_counts, s);
   }

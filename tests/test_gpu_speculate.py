@@ -160,3 +160,30 @@ def test_raw_step_forced_miss():
     _raw_check(cfg, body, mo, cat, CALIB, dec, best, counts)
     info = fp.fleet_plan_info(plan)
     assert info["spec_calls"] == 1 and info["spec_misses"] == 1
+
+
+# ---- speculation for edge sets beyond the SWAR bins (u16 LUT, |E| >= 256) --------------------
+def test_speculative_wide_edge_sets(monkeypatch):
+    """C3's grid (|E| = 258 edges: u16 LUT, clamped byte bins) at the
+    speculative size: the full pass writes decisions from L_total and the
+    split's edge values (the bins no longer fit the SWAR byte compare): hit,
+    then a forced miss."""
+    cfg = configs.c3().with_n(N)
+    L = generate_host(cfg.shape, cfg.seed, 0, N)
+    # (a u16 LUT speculates from 2^28 requests by default)
+    monkeypatch.setenv("FP_SPEC_MIN_WIDE_LOG2", "26")
+    plan = _plan(cfg)
+    info = fp.fleet_plan_info(plan)
+    assert info["n_edges"] >= 256
+    dec = torch.full((N,), 0xEE, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(L), cfg.rate_rps, route_model=0, decision=dec)
+    _check_step(cfg, L, plan, dec, best, counts)
+    info = fp.fleet_plan_info(plan)
+    assert info["spec_calls"] == 1 and info["spec_misses"] == 0
+    L2 = L.copy()
+    for lo, hi in _sampled_stripes(plan, N):
+        L2[lo:hi] = 100
+    dec.fill_(0xEE)
+    best, counts = fp.sweep_and_route(plan, _dev(L2), cfg.rate_rps, route_model=0, decision=dec)
+    _check_step(cfg, L2, plan, dec, best, counts)
+    assert fp.fleet_plan_info(plan)["spec_misses"] == 1
