@@ -387,8 +387,10 @@ def _timed_steps(step, steps, stream, flush=None):
 
 def config_results(fp, names, steps, warmup):
     """BASELINE.json's other configurations (C1-C4) at their full sizes on this
-    GPU, the same step (sweep_and_route, asynchronous) timed per step with CUDA
-    events, the L2 flushed before every step when the trace would fit in it."""
+    GPU, the same step (sweep_and_route, asynchronous, FP_FLAG_SPECULATE like
+    the main step: speculative where its preconditions hold) timed per step
+    with CUDA events, the L2 flushed before every step when the trace would fit
+    in it; then the same step replayed as the plan's captured CUDA graph."""
     import torch
     from synth import configs
     from synth.gen import generate_device
@@ -402,7 +404,7 @@ def config_results(fp, names, steps, warmup):
         n = cfg.n_requests
         d = generate_device(cfg.shape, cfg.seed, 0, n)
         dec = torch.empty(n, dtype=torch.uint8, device="cuda")
-        plan = fp.fleet_plan_create(**fp.desc_from_config(cfg))
+        plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=fp.FP_FLAG_SPECULATE)
         step = lambda: fp.sweep_and_route(plan, d, cfg.rate_rps, route_model=0, decision=dec,  # noqa: E731
                                           stream=stream, want_best=False)
         for _ in range(warmup):
@@ -413,10 +415,21 @@ def config_results(fp, names, steps, warmup):
         launches = fp.fp_kernel_launches(plan) - l0
         best = fp.best_split(plan)
         info = fp.fleet_plan_info(plan)
+        # the same step as the plan's captured CUDA graph (sweep_and_route_graph):
+        # one graph launch per step instead of the kernel launches
+        gstep = lambda: fp.sweep_and_route_graph(plan, d, cfg.rate_rps, dec, stream=stream)  # noqa: E731
+        for _ in range(max(warmup, 2)):
+            gstep()
+        gtotal, gper = _timed_steps(gstep, steps, stream, flush if needs_flush else None)
+        gbest = fp.best_split(plan)
+        assert gbest.tobytes() == best.tobytes(), f"{name}: graph replay differs from the eager step"
         fp.fleet_plan_destroy(plan)
         if per is None:
             per = [total / steps] * steps
+        if gper is None:
+            gper = [gtotal / steps] * steps
         per = sorted(per)
+        gper = sorted(gper)
         med = per[len(per) // 2]
         ms = total / steps
         # the bytes the step must move at least: the trace read once, one decision byte written
@@ -427,6 +440,12 @@ def config_results(fp, names, steps, warmup):
             "step_min_bytes_per_request": 5.0,
             "step_frac_min_bytes": 5.0 * n / (ms / 1e3) / 1e9 / peak,
             "l2": _l2_label(4 * n, l2, needs_flush), "gpu_launches_per_step": launches / steps,
+            "speculative": bool(info["spec_calls"]),
+            "graph": {"ms_per_step": gtotal / steps,
+                      "ms_p10_p50_p90": [gper[int(0.1 * (steps - 1))], gper[len(gper) // 2],
+                                         gper[int(0.9 * (steps - 1))]],
+                      "requests_per_s": n / (gtotal / steps / 1e3),
+                      "note": "sweep_and_route_graph: the same step replayed as the plan's captured CUDA graph"},
             "k3_shape": ["cluster", "factored", "grid"][info["k3_shape"]],
             "best_model0": {"index": int(best[0]["index"]), "b_short": int(best[0]["b_short"]),
                             "c_short": int(best[0]["c_short"]), "c_long": int(best[0]["c_long"]),

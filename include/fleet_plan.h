@@ -305,6 +305,27 @@ fp_status sweep_and_route(fp_plan *plan, const uint32_t *len, uint64_t n_local, 
                           uint32_t route_model, uint8_t *d_decision, fp_candidate *h_best,
                           fp_route_counts *h_counts, void *stream);
 
+/* The step of sweep_and_route in its asynchronous form (device trace, bin
+ * mode, h_best = h_counts = NULL) as a CUDA graph owned by the plan: the first
+ * call with a given (len, n_local, rate_rps, route_model, d_decision) runs the
+ * step once eagerly, then captures it -- once per accumulator parity (each
+ * step's K3 clears the other parity's histogram copies for the next step), on
+ * a plan-owned stream -- and every call launches the parity's graph on
+ * `stream` (any stream, including the legacy default): one cudaGraphLaunch
+ * instead of 3-5 kernel launches (the small traces' steps are launch-bound,
+ * the plan owns the captured graph). Results are those of
+ * sweep_and_route; read them with best_split / sweep_histogram. Same
+ * contract on len and d_decision as the asynchronous call (caller-owned,
+ * unchanged until the stream passes the call). Another argument tuple, or a
+ * scratch reallocation by another call, recaptures. One rank only (world ==
+ * 1, no FP_FLAG_COLLECTIVES / FP_FLAG_P2P) and no FP_FLAG_KERNEL_TIMING /
+ * FP_FLAG_TIME_TRACE (FP_ERR_CONFIG otherwise); FP_ERR_INVALID_ARG for a
+ * host trace, a NULL d_decision or n_local == 0; a step that the
+ * asynchronous form cannot run (host outputs needed: |E| >= 256 with a host
+ * trace, binary-search bins) gives FP_ERR_CONFIG. */
+fp_status sweep_and_route_graph(fp_plan *plan, const uint32_t *len, uint64_t n_local, double rate_rps,
+                                uint32_t route_model, uint8_t *d_decision, void *stream);
+
 /* ---- token-budget estimation (NEXT-1) ----------------------------------------
  * Routing key from raw request columns (Eq. `budget`, with the
  * conservative ratio of Eq. `conservative`, Alg. 1):

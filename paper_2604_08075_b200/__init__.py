@@ -11,7 +11,8 @@ from ._abi import (  # noqa: F401
     FP_KERNEL_EVAL, FP_KERNEL_ROUTE, FP_KERNEL_TRACE, fp_kernel_time, fp_kernel_time_reset, FleetPlan, FleetPlanError, LIB_PATH,
     best_split, desc_from_config, fleet_plan_create, fleet_plan_destroy, fleet_plan_info,
     fp_candidate_range, fp_kernel_launches, fp_merge_best, fp_nccl_get_unique_id,
-    fp_shard_range, fp_status_string, route_batch, route_batch_raw, sweep_and_route, sweep_histogram,
+    fp_shard_range, fp_status_string, route_batch, route_batch_raw, sweep_and_route, sweep_and_route_graph,
+    sweep_histogram,
     sweep_thresholds, sweep_thresholds_raw, sweep_and_route_raw, sweep_three_pools, FP_POOL3, calibrate_replay,
     sweep_peak_windows, FP_PEAK,
 )

@@ -33,7 +33,8 @@ EXPORTED = ["fleet_plan_create", "route_batch", "sweep_thresholds", "best_split"
             "fp_last_error", "fp_shard_range", "fp_candidate_range", "fp_merge_best",
             "fp_nccl_get_unique_id", "fp_kernel_time", "fp_kernel_time_reset", "sweep_and_route",
             "sweep_thresholds_raw", "route_batch_raw", "sweep_three_pools", "calibrate_replay",
-            "sweep_peak_windows", "fp_p2p_export", "fp_p2p_import", "sweep_and_route_raw"]
+            "sweep_peak_windows", "fp_p2p_export", "fp_p2p_import", "sweep_and_route_raw",
+            "sweep_and_route_graph"]
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 
@@ -184,6 +185,7 @@ def _load():
         "calibrate_replay": (c_i32, [c_vp, c_vp, c_vp, c_vp, c_u64, c_u32, c_dbl, c_vp, c_u64, c_vp, c_vp, c_vp,
                                      c_vp]),
         "sweep_and_route": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp, ctypes.POINTER(fp_route_counts), c_vp]),
+        "sweep_and_route_graph": (c_i32, [c_vp, c_vp, c_u64, c_dbl, c_u32, c_vp, c_vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -458,6 +460,18 @@ def sweep_and_route(plan, lengths, rate_rps, route_model=0, decision=None, strea
                                ctypes.byref(counts), _stream_handle(stream, plan.device)), plan)
     del keep
     return best, {k: int(getattr(counts, k)) for k, _ in fp_route_counts._fields_}
+
+
+def sweep_and_route_graph(plan, lengths, rate_rps, decision, route_model=0, stream=None):
+    """sweep_and_route's asynchronous step as the plan's captured CUDA graph
+    (device trace and decision tensor; captured on the first call with these
+    arguments, replayed after). Read the records with best_split()."""
+    if not (hasattr(lengths, "is_cuda") and lengths.is_cuda and lengths.is_contiguous()):
+        raise ValueError("sweep_and_route_graph needs a contiguous CUDA trace")
+    if decision.numel() < lengths.numel() or not decision.is_cuda:
+        raise ValueError("decision must be a CUDA uint8 tensor with >= n elements")
+    _check(lib.sweep_and_route_graph(plan.handle, lengths.data_ptr(), lengths.numel(), float(rate_rps), route_model,
+                                     decision.data_ptr(), _stream_handle(stream, plan.device)), plan)
 
 
 # ---- token-budget estimation (NEXT-1) ------------------------------------------------

@@ -121,6 +121,20 @@ struct fp_plan {
   uint32_t *spec_route = nullptr;
   unsigned int *spec_miss = nullptr;
   uint64_t spec_calls = 0;
+  // sweep_and_route_graph: the captured step per accumulator parity, its key
+  // and the scratch it was captured against
+  struct StepGraph {
+    bool valid = false;
+    const uint32_t *len = nullptr;
+    uint64_t n = 0;
+    double rate = 0.0;
+    uint32_t model = 0;
+    uint8_t *dec = nullptr;
+    const void *bins = nullptr, *spec_buf = nullptr;
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    uint64_t launches[2] = {0, 0}, spec_n[2] = {0, 0};
+  } graph;
+  cudaStream_t graph_stream = nullptr;
   bool spec_dirty = false;                  // a speculative call failed before its full K3 (which zeroes spec_acc)
   // FP_FLAG_P2P: exchange buffer [2 parities][2][nbins] u64 (each rank's folded
   // histogram) + the arrival flag, the peers' buffers opened by CUDA IPC, and
@@ -1002,6 +1016,9 @@ void fleet_plan_destroy(fp_plan *p) {
     cudaFree(p->d_rmu);
     cudaFree(p->d_err);
     if (p->ev_order) cudaEventDestroy(p->ev_order);
+    for (cudaGraphExec_t &x : p->graph.exec)
+      if (x) cudaGraphExecDestroy(x);
+    if (p->graph_stream) cudaStreamDestroy(p->graph_stream);
     cudaFree(p->d_resident);
     cudaFree(p->d_bins);
     cudaFree(p->d_p3);
@@ -1406,6 +1423,92 @@ fp_status sweep_and_route(fp_plan *p, const uint32_t *len, uint64_t n_local, dou
     h_counts->mass_short = b.mass_short;
     h_counts->mass_long = b.mass_long;
   }
+  p->last_stream = s;
+  return FP_OK;
+}
+
+fp_status sweep_and_route_graph(fp_plan *p, const uint32_t *len, uint64_t n_local, double rate_rps,
+                                uint32_t route_model, uint8_t *d_decision, void *stream) {
+  if (!p) return FP_ERR_INVALID_ARG;
+  if (p->dist || (p->flags & (FP_FLAG_COLLECTIVES | FP_FLAG_P2P)))
+    return fail(p, FP_ERR_CONFIG, "sweep_and_route_graph: one rank only");
+  if (p->flags & (FP_FLAG_KERNEL_TIMING | FP_FLAG_TIME_TRACE))
+    return fail(p, FP_ERR_CONFIG, "sweep_and_route_graph: no per-kernel timing inside a graph");
+  if (!len || !d_decision || !n_local || is_host_pointer(len) || is_host_pointer(d_decision))
+    return fail(p, FP_ERR_INVALID_ARG, "sweep_and_route_graph: device trace and decision buffer, n_local > 0");
+  if (route_model >= p->models.size()) return fail(p, FP_ERR_INVALID_ARG, "route_model out of range");
+  if (!p->lut_cells) return fail(p, FP_ERR_CONFIG, "sweep_and_route_graph: bin mode needs the LUT");
+  DeviceGuard g(p->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  auto &G = p->graph;
+  auto drop = [&]() {
+    for (cudaGraphExec_t &x : G.exec)
+      if (x) { cudaGraphExecDestroy(x); x = nullptr; }
+    G.valid = false;
+  };
+  const bool same = G.valid && G.len == len && G.n == n_local && G.rate == rate_rps && G.model == route_model &&
+                    G.dec == d_decision && G.bins == p->d_bins && G.spec_buf == p->d_spec;
+  if (!same) {
+    drop();
+    // one eager step: allocates every scratch buffer the step uses (no
+    // allocation may happen during capture) and leaves the plan in a state
+    // whose bookkeeping (accumulator parity) the graphs reproduce
+    fp_status st = sweep_and_route(p, len, n_local, rate_rps, route_model, d_decision, nullptr, nullptr, s);
+    if (st != FP_OK) return st;
+    if (!p->graph_stream)
+      CUDA_TRY(p, cudaStreamCreateWithFlags(&p->graph_stream, cudaStreamNonBlocking), "graph stream");
+    // the captures read the plan's device state only when replayed; order the
+    // eager step before the first replay on `stream` (it is: same stream)
+    for (int q = 0; q < 2; ++q) {
+      const uint32_t par = (uint32_t)(p->sweep_seq & 1u);
+      const uint64_t l0 = p->launches, s0 = p->spec_calls;
+      CUDA_TRY(p, cudaStreamBeginCapture(p->graph_stream, cudaStreamCaptureModeRelaxed), "begin capture");
+      fp_status st2 = sweep_and_route(p, len, n_local, rate_rps, route_model, d_decision, nullptr, nullptr,
+                                      p->graph_stream);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ec = cudaStreamEndCapture(p->graph_stream, &graph);
+      if (st2 != FP_OK || ec != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        drop();
+        cudaGetLastError();
+        // the captured calls advanced the host bookkeeping without running:
+        // the histogram copies of both parities are cleared before the next step
+        p->parity_clean[0] = p->parity_clean[1] = false;
+        p->spec_dirty = true;
+        return st2 != FP_OK ? st2 : cuda_fail(p, ec, "end capture");
+      }
+      const cudaError_t ei = cudaGraphInstantiate(&G.exec[par], graph, 0);
+      cudaGraphDestroy(graph);
+      if (ei != cudaSuccess) {
+        drop();
+        p->parity_clean[0] = p->parity_clean[1] = false;
+        p->spec_dirty = true;
+        return cuda_fail(p, ei, "graph instantiate");
+      }
+      G.launches[par] = p->launches - l0;
+      G.spec_n[par] = p->spec_calls - s0;
+      p->launches = l0;                 // counted when replayed
+      p->spec_calls = s0;
+    }
+    // the two captures advanced the parity by two: back where the eager step left it
+    G.valid = true;
+    G.len = len;
+    G.n = n_local;
+    G.rate = rate_rps;
+    G.model = route_model;
+    G.dec = d_decision;
+    G.bins = p->d_bins;
+    G.spec_buf = p->d_spec;
+  }
+  const uint32_t par = (uint32_t)(p->sweep_seq & 1u);
+  CUDA_TRY(p, cudaGraphLaunch(G.exec[par], s), "graph launch");
+  // the bookkeeping of the step the graph replays (sweep_impl / sweep_route_speculative)
+  p->parity_clean[par] = false;
+  p->parity_clean[par ^ 1u] = true;
+  ++p->sweep_seq;
+  p->launches += G.launches[par];
+  p->spec_calls += G.spec_n[par];
+  p->have_sweep = true;
   p->last_stream = s;
   return FP_OK;
 }
