@@ -110,3 +110,65 @@ def test_fuzz_whole_path(seed):
             assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
                 [int(x) for x in oc]
     fp.fleet_plan_destroy(plan)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_fuzz_speculative_step(seed, monkeypatch):
+    """The speculative step (FP_FLAG_SPECULATE) on random grids at the
+    speculative size: u8 LUTs with |E| < 127 (decisions by SWAR on the bins)
+    and u16 LUTs (decisions from L_total; FP_SPEC_MIN_WIDE_LOG2=26), random
+    route_model, adversarial values, ragged size -- every decision byte and
+    the best records against the oracle, whether the sample hit or not."""
+    from dataclasses import replace
+    rng = np.random.default_rng(9100 + seed)
+    wide = seed % 2 == 1
+    mult = 256 if wide else int(rng.choice([16, 256]))       # LUT bin mode (not binary search)
+    if wide:
+        b = sorted(set(int(x) * mult for x in rng.integers(1, 512, 400)))[:int(rng.integers(262, 300))]
+    else:
+        b = sorted(set(int(x) * mult for x in rng.integers(1, 65536 // mult, int(rng.integers(3, 110)))))
+        b = b[:118]
+    top = max(b)
+    cl = sorted(set([top] + [((min(int(top * f), 2**31 - mult) + mult - 1) // mult) * mult
+                             for f in rng.uniform(1.0, 4.0, int(rng.integers(1, 4)))]))
+    if not wide:
+        cl = cl[:4]
+    models = list(rng.choice(list(configs.MODELS), int(rng.integers(1, 4)), replace=False))
+    gpus = list(rng.choice(list(configs.GPUS), int(rng.integers(1, 3)), replace=False))
+    n = (1 << 26) + int(rng.integers(0, 5000))
+    cfg = make_config("FZS", str(rng.choice(["AZ", "LM", "MIX"])), 500 + seed, n,
+                      float(rng.choice([1000.0, 1e4])), models, gpus, b, [], cl)
+    if rng.random() < 0.5:
+        vals = {(m.name, g.name, int(w)): float(rng.uniform(0.05, 60.0))
+                for m in cfg.models for g in cfg.gpus for w in cfg.windows()}
+        cfg = replace(cfg, mu_mode="table", mu_values=vals)
+    L = generate_host(cfg.shape, cfg.seed, 0, n).astype(np.uint32)
+    edges = np.array(sorted(set(b) | set(cl)), dtype=np.uint64)
+    k = n // 50
+    pos = rng.integers(0, n, k)
+    e = edges[rng.integers(0, edges.size, k)]
+    pick = rng.integers(0, 4, k)
+    L[pos] = np.minimum(np.select([pick == 0, pick == 1, pick == 2], [e, e + 1, np.maximum(e, 1) - 1],
+                                  default=np.full(k, 2**32 - 1)), 2**32 - 1).astype(np.uint32)
+    if wide:
+        monkeypatch.setenv("FP_SPEC_MIN_WIDE_LOG2", "26")
+    plan = fp.fleet_plan_create(**fp.desc_from_config(cfg), flags=fp.FP_FLAG_SPECULATE)
+    info = fp.fleet_plan_info(plan)
+    assert info["lut_cells"] > 0 and info["k3_shape"] == 0
+    assert (info["n_edges"] >= 256) == wide and (wide or info["n_edges"] < 127)
+    _, obest = oracle.sweep(cfg, L, want_all=False)
+    feas = [m for m in range(len(models)) if obest[m]["flags"] & fp.FP_CAND_FEASIBLE]
+    if not feas:
+        pytest.skip("no model has a feasible split on this random grid")
+    model = int(rng.choice(feas))
+    dec = torch.full((n,), 0xEE, dtype=torch.uint8, device="cuda")
+    best, counts = fp.sweep_and_route(plan, _dev(L), cfg.rate_rps, route_model=model, decision=dec)
+    assert best.tobytes() == obest.tobytes(), f"seed {seed}: best splits differ"
+    bm = obest[model]
+    odec, oc = oracle.route_batch(L, int(bm["b_short"]), int(bm["c_short"]), int(bm["c_long"]))
+    got = dec.cpu().numpy()
+    assert np.array_equal(got, odec), f"seed {seed}: {(got != odec).sum()} decisions differ"
+    assert [counts[k] for k in ("n_short", "n_long", "n_reject", "mass_short", "mass_long")] == \
+        [int(x) for x in oc]
+    assert fp.fleet_plan_info(plan)["spec_calls"] == 1
+    fp.fleet_plan_destroy(plan)
