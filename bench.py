@@ -669,9 +669,24 @@ def run_ours(args, cfg):
         dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         if multi:
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-        e2e = {"value": total_requests * args.e2e_steps / float(dt.item()), "unit": UNIT,
+        e2e_value = total_requests * args.e2e_steps / float(dt.item())
+        # the link's own rate: a plain pinned H2D copy of 1 GB of this trace (device-timed)
+        hb = h_len[: min(n, 1 << 28)]
+        db = torch.empty_like(hb, device=dev)
+        for _ in range(2):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            db.copy_(hb, non_blocking=True)
+            e1.record()
+            e1.synchronize()
+        h2d_gbps = 4 * hb.numel() / (e0.elapsed_time(e1) * 1e6)
+        del db, hb
+        e2e = {"value": e2e_value, "unit": UNIT,
                "h2d_bytes_per_step": 4 * n,   # the pinned trace crosses PCIe once per step
                "d2h_bytes_per_step": best.nbytes + 5 * 8,
+               "h2d_GBps_step": 4 * n * e2e_value / total_requests / 1e9,
+               "h2d_GBps_copy": h2d_gbps,
+               "frac_of_h2d_copy": 4 * n * e2e_value / total_requests / 1e9 / h2d_gbps,
                "note": "sweep_and_route on a pinned host trace: 128 MB chunks DMA'd into the device while K1 "
                        "consumes them (bins written on the device), K4 routes from the bins; best records + "
                        "route counts to host every step"}
