@@ -1501,6 +1501,15 @@ fp_status sweep_and_route_graph(fp_plan *p, const uint32_t *len, uint64_t n_loca
     G.spec_buf = p->d_spec;
   }
   const uint32_t par = (uint32_t)(p->sweep_seq & 1u);
+  // the graphs assume what every completed step leaves behind: this parity's
+  // accumulator copies (and the sample's) cleared by the previous step's K3;
+  // after a step that failed before its K3, clear them here as the eager call would
+  if (!p->parity_clean[par])
+    CUDA_TRY(p, cudaMemsetAsync(p->d_hcopies + par * p->copies_elems, 0, p->copies_elems * 8, s), "memset hist");
+  if (p->spec_dirty && p->spec_acc) {
+    CUDA_TRY(p, cudaMemsetAsync(p->spec_acc, 0, p->copies_elems * 8, s), "memset sample hist");
+    p->spec_dirty = false;
+  }
   CUDA_TRY(p, cudaGraphLaunch(G.exec[par], s), "graph launch");
   // the bookkeeping of the step the graph replays (sweep_impl / sweep_route_speculative)
   p->parity_clean[par] = false;
