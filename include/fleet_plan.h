@@ -39,6 +39,12 @@
  *     predecessor's results); environment FP_NO_PDL=1 issues plain launches.
  *     Either way the results are identical and the calls stay stream-ordered
  *     with respect to the caller's other work on `stream`.
+ *   - Other environment knobs select measured alternatives with identical
+ *     results: FP_SPEC_STRIPES (speculative sample stripes, 4),
+ *     FP_SPEC_MIN_WIDE_LOG2 (u16-LUT speculation threshold, 28),
+ *     FP_CALIB_STREAM=1 (calibrate_replay's single-pass streaming kernel,
+ *     slower on a B200), FP_CALIB_PROFILE=1 (its phase stamps), FP_K3_PHASES=1
+ *     (K3 phase stamps), FP_K4_BLOCK / FP_K4_BLOCKS_PER_SM (routing launch).
  * ======================================================================== */
 #ifndef FLEET_PLAN_H
 #define FLEET_PLAN_H
